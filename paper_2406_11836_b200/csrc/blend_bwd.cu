@@ -1,0 +1,477 @@
+// K8 — backward blend of one KD subset (composite_ray_backward +
+// render_maps_backward, raster.hpp:194-236 / 267-305; engine.hpp:74-88).
+//
+// Per pixel the reference replays the forward to get prefix transmittances
+// A_i, then sweeps in reverse with suffix = sum_{j>i} c_j sigma_j A_j:
+//   d_color_i += gc * sigma_i A_i
+//   d_sigma_i  = gc.c_i A_i - gc.suffix_i/(1-sigma_i) - gT T_f/(1-sigma_i)
+//   unless alpha g >= 0.99:  d_alpha += d_sigma g,  d_mean2d += (d_sigma alpha g) w,
+//                            d_cov2d += 0.5 (d_sigma alpha g) w w^T,   w = inv_cov2d delta.
+// Here the traversal is the forward's own (same range-ordered list, same
+// reorder ring, same emission order, bitwise the same sigma and T sequence),
+// and the suffix is formed as C_final - (running prefix colour), which needs
+// no reverse pass and no T recovery by division (impossible once T
+// underflows in stop=0 mode).
+//
+// Accumulation of the 9 pixel-space adjoints per member: warp-uniform
+// emissions are reduced with a 5-step butterfly, then added into a
+// two-batch shared-memory accumulator window keyed by list position; each
+// retired batch is flushed to HBM with one red.global.add per touched
+// (member, field).  Emissions that fall outside the window go straight to
+// global atomics.  Pixels skipped by the reference rule
+// (gc.isZero() && gT == 0, raster.hpp:285) never emit.
+#include "kernels.h"
+
+namespace dgs_b200 {
+
+namespace {
+
+constexpr int KBUF = 8;
+constexpr float kInf = __builtin_huge_valf();
+constexpr unsigned kFull = 0xffffffffu;
+// staged records (4 float4) + ring (t, id, sigma, g, pos, member) + 2x9 accumulators
+constexpr size_t kBwdSmem = 4 * kBlendThreads * sizeof(float4) + 6 * KBUF * kBlendThreads * sizeof(float) +
+                            2 * 9 * kBlendThreads * sizeof(float);
+
+__device__ __forceinline__ float order_bound(float r, float dmax, float onorm) {
+    const float S = 2.0f * onorm + 2.0f * r + 1.0f;
+    const float dm = dmax * 1.0001f + 1e-6f * S;
+    const float r2 = r * r * (1.0f - 2e-6f);
+    const float dm2 = dm * dm;
+    if (!(r2 > dm2)) return -kInf;
+    return sqrtf(r2 - dm2) * (1.0f - 1e-6f) - 1e-6f * S;
+}
+
+struct PixelRay {
+    float d[3];
+    float pxf, pyf;
+};
+
+__device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewParams& vp, const RenderOpts& ro,
+                                               const Subspace& gate, const float4& A, const float4& B,
+                                               const float4& C, float& t_out, float& sigma_out, float& g_out) {
+    const float dx = fsub(pr.pxf, A.x), dy = fsub(pr.pyf, A.y);
+    const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))), fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
+    if (!(m2 <= fmul(ro.trunc, ro.trunc))) return false;
+    const float t = dot3(pr.d[0], pr.d[1], pr.d[2], fsub(C.x, vp.o[0]), fsub(C.y, vp.o[1]), fsub(C.z, vp.o[2]));
+    if (!(t > 0.0f)) return false;
+    const float x0 = fadd(vp.o[0], fmul(t, pr.d[0]));
+    const float x1 = fadd(vp.o[1], fmul(t, pr.d[1]));
+    const float x2 = fadd(vp.o[2], fmul(t, pr.d[2]));
+    const float e0 = fsub(x0, C.x), e1 = fsub(x1, C.y), e2 = fsub(x2, C.z);
+    if (dot3(e0, e1, e2, e0, e1, e2) > A.w) return false;
+    if (ro.indicator_enabled && !subspace_contains(gate, x0, x1, x2)) return false;
+    const float g = __expf(fmul(-0.5f, m2));
+    const float ag = fmul(A.z, g);
+    const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
+    if (!(sigma > 0.0f)) return false;
+    t_out = t;
+    sigma_out = sigma;
+    g_out = g;
+    return true;
+}
+
+__device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint32_t m, float4& A, float4& B,
+                                         float4& C, float4& D) {
+    const float4* r4 = reinterpret_cast<const float4*>(recs + m);
+    A = __ldg(r4 + 0);
+    B = __ldg(r4 + 1);
+    C = __ldg(r4 + 2);
+    D = __ldg(r4 + 3);
+}
+
+/// Per-pixel backward state.
+struct PixState {
+    float T, a0, a1, a2;   // replayed transmittance and running prefix colour
+    float gc0, gc1, gc2, gT;
+    float Cf0, Cf1, Cf2, Tf;
+    float pxf, pyf;
+};
+
+/// One emitted contribution's 9 pixel-space adjoints:
+/// [d_mean.x, d_mean.y, d_cov00, d_cov01(=d_cov10), d_cov11, d_col.r, d_col.g, d_col.b, d_alpha].
+__device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, float g, const float4& A,
+                                                  const float4& B, const float4& D, float sigma_clamp,
+                                                  float v[9]) {
+    const float a_i = ps.T;
+    const float w = fmul(sigma, a_i);
+    ps.a0 = fadd(ps.a0, fmul(D.x, w));
+    ps.a1 = fadd(ps.a1, fmul(D.y, w));
+    ps.a2 = fadd(ps.a2, fmul(D.z, w));
+    ps.T = fmul(ps.T, fsub(1.0f, sigma));
+    const float one_minus = 1.0f - sigma;
+    const float s0 = ps.Cf0 - ps.a0, s1 = ps.Cf1 - ps.a1, s2 = ps.Cf2 - ps.a2;
+    const float gdc = ps.gc0 * D.x + ps.gc1 * D.y + ps.gc2 * D.z;
+    const float gds = ps.gc0 * s0 + ps.gc1 * s1 + ps.gc2 * s2;
+    const float d_sigma = gdc * a_i - gds / one_minus - ps.gT * ps.Tf / one_minus;
+    v[5] = ps.gc0 * w;
+    v[6] = ps.gc1 * w;
+    v[7] = ps.gc2 * w;
+    if (A.z * g >= sigma_clamp) {  // raster.hpp:228: the clamp freezes alpha/mean/cov
+        v[0] = v[1] = v[2] = v[3] = v[4] = v[8] = 0.0f;
+        return;
+    }
+    v[8] = d_sigma * g;
+    const float d_g = d_sigma * A.z;
+    const float dx = ps.pxf - A.x, dy = ps.pyf - A.y;
+    const float w0 = B.x * dx + B.y * dy, w1 = B.z * dx + B.w * dy;
+    const float s = d_g * g;
+    v[0] = s * w0;
+    v[1] = s * w1;
+    const float h = s * 0.5f;
+    v[2] = h * (w0 * w0);
+    v[3] = h * (w0 * w1);
+    v[4] = h * (w1 * w1);
+}
+
+__global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, RenderOpts ro, Subspace gate,
+                                                             const SplatRec* __restrict__ recs,
+                                                             const uint32_t* __restrict__ pair_val,
+                                                             const uint2* __restrict__ ranges,
+                                                             const uint32_t* __restrict__ dmax_bits, float onorm,
+                                                             const float4* __restrict__ fwd_ct,
+                                                             const float4* __restrict__ grad_ct,
+                                                             const uint8_t* __restrict__ ovf_flag,
+                                                             float* __restrict__ g2d, size_t ld2,
+                                                             BlendStats* __restrict__ stats) {
+    extern __shared__ float4 smem4[];
+    float4* sA = smem4;
+    float4* sB = sA + kBlendThreads;
+    float4* sC = sB + kBlendThreads;
+    float4* sD = sC + kBlendThreads;
+    typedef float Ring[kBlendThreads];
+    typedef uint32_t URing[kBlendThreads];
+    Ring* bt = reinterpret_cast<Ring*>(sD + kBlendThreads);
+    URing* bid = reinterpret_cast<URing*>(bt + KBUF);
+    Ring* bs = reinterpret_cast<Ring*>(bid + KBUF);
+    Ring* bg = bs + KBUF;
+    URing* bpos = reinterpret_cast<URing*>(bg + KBUF);
+    URing* bmem = bpos + KBUF;
+    float* acc = reinterpret_cast<float*>(bmem + KBUF);  // [2][9][256]
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int tile = blockIdx.x;
+    const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
+    const int px = tx * kTileSize + (tid & 15), py = ty * kTileSize + (tid >> 4);
+    const bool inside = px < vp.width && py < vp.height;
+    const size_t pix = (size_t)py * vp.width + px;
+    PixelRay pr;
+    pixel_ray_dir(vp, px, py, pr.d);
+    pr.pxf = fadd((float)px, 0.5f);
+    pr.pyf = fadd((float)py, 0.5f);
+    const float dmax = __uint_as_float(*dmax_bits);
+
+    PixState ps;
+    ps.T = 1.0f;
+    ps.a0 = ps.a1 = ps.a2 = 0.0f;
+    ps.pxf = pr.pxf;
+    ps.pyf = pr.pyf;
+    bool done = !inside;
+    if (inside) {
+        const float4 g = grad_ct[pix];
+        const float4 f = fwd_ct[pix];
+        ps.gc0 = g.x;
+        ps.gc1 = g.y;
+        ps.gc2 = g.z;
+        ps.gT = g.w;
+        ps.Cf0 = f.x;
+        ps.Cf1 = f.y;
+        ps.Cf2 = f.z;
+        ps.Tf = f.w;
+        const float e = ro.grad_skip_eps;
+        const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
+        if ((gc_zero && g.w == 0.0f) || ovf_flag[pix]) done = true;
+    }
+    for (int i = tid; i < 2 * 9 * kBlendThreads; i += kBlendThreads) acc[i] = 0.0f;
+
+    int head = 0, cnt = 0, nemit = 0;
+    float head_t = kInf;
+    unsigned long long n_eval = 0;
+    const uint2 rg = ranges[tile];
+    int batch = -1;
+    uint32_t base = rg.x;
+    int nb = 0;
+
+    // Add 9 values for list position `pos` (member `mem`).
+    auto add9 = [&](uint32_t pos, uint32_t mem, const float v[9]) {
+        const int eb = (int)((pos - rg.x) >> 8);
+        if (eb >= batch - 1) {
+            float* a = acc + (eb & 1) * 9 * kBlendThreads + ((pos - rg.x) & 255);
+#pragma unroll
+            for (int f = 0; f < 9; ++f)
+                if (v[f] != 0.0f) atomicAdd(a + f * kBlendThreads, v[f]);
+        } else {
+#pragma unroll
+            for (int f = 0; f < 9; ++f)
+                if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+        }
+    };
+
+    // Warp-converged emission step: every lane emits at most one entry whose
+    // t is below `L`; uniform targets are butterfly-reduced first.
+    auto emission_round = [&](float L) -> bool {
+        const bool ready = !done && cnt > 0 && head_t < L;
+        if (!__any_sync(kFull, ready)) return false;
+        float v[9];
+        int apos = -1;
+        uint32_t amem = 0;
+#pragma unroll
+        for (int f = 0; f < 9; ++f) v[f] = 0.0f;
+        if (ready) {
+            if (ro.stop > 0.0f && ps.T < ro.stop) {  // raster.hpp:205 replay termination
+                done = true;
+                cnt = 0;
+                head_t = kInf;
+            } else {
+                const int sl = head & (KBUF - 1);
+                const float sigma = bs[sl][tid], g = bg[sl][tid];
+                const uint32_t pos = bpos[sl][tid], mem = bmem[sl][tid];
+                float4 A, B, C, D;
+                if (pos >= base && pos < base + (uint32_t)nb) {
+                    const int j = (int)(pos - base);
+                    A = sA[j];
+                    B = sB[j];
+                    D = sD[j];
+                } else {
+                    load_rec(recs, mem, A, B, C, D);
+                }
+                contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
+                apos = (int)pos;
+                amem = mem;
+                ++nemit;
+                ++head;
+                --cnt;
+                head_t = cnt ? bt[head & (KBUF - 1)][tid] : kInf;
+            }
+        }
+        const unsigned act = __ballot_sync(kFull, apos >= 0);
+        if (act == 0) return true;
+        const int lead = __ffs(act) - 1;
+        const int lpos = __shfl_sync(kFull, apos, lead);
+        if (__all_sync(kFull, apos < 0 || apos == lpos)) {
+#pragma unroll
+            for (int f = 0; f < 9; ++f) {
+                float x = v[f];
+                for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
+                v[f] = x;
+            }
+            if (lane == lead) add9((uint32_t)lpos, amem, v);
+        } else if (apos >= 0) {
+            add9((uint32_t)apos, amem, v);
+        }
+        return true;
+    };
+
+    auto flush_slot = [&](int slot_batch) {
+        if (slot_batch < 0) return;
+        float* a = acc + (slot_batch & 1) * 9 * kBlendThreads;
+        const uint32_t pos = rg.x + (uint32_t)slot_batch * kBlendThreads + tid;
+        if (pos < rg.y) {
+            float v[9];
+            bool any = false;
+#pragma unroll
+            for (int f = 0; f < 9; ++f) {
+                v[f] = a[f * kBlendThreads + tid];
+                any |= v[f] != 0.0f;
+                a[f * kBlendThreads + tid] = 0.0f;
+            }
+            if (any) {
+                const uint32_t mem = pair_val[pos];
+#pragma unroll
+                for (int f = 0; f < 9; ++f)
+                    if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+            }
+        }
+    };
+
+    for (base = rg.x; base < rg.y; base += kBlendThreads) {
+        if (__syncthreads_count(!done) == 0) break;
+        ++batch;
+        flush_slot(batch - 2);  // retire the window slot this batch reuses
+        const uint32_t p = base + tid;
+        nb = (int)min((uint32_t)kBlendThreads, rg.y - base);
+        if (p < rg.y) {
+            float4 A, B, C, D;
+            load_rec(recs, pair_val[p], A, B, C, D);
+            D.w = order_bound(D.w, dmax, onorm);
+            sA[tid] = A;
+            sB[tid] = B;
+            sC[tid] = C;
+            sD[tid] = D;
+        }
+        __syncthreads();
+        for (int j = 0; j < nb; ++j) {
+            const float L = sD[j].w;
+            while (emission_round(L)) {
+            }
+            if (done) continue;
+            const float4 A = sA[j], B = sB[j], C = sC[j];
+            ++n_eval;
+            float t, sigma, g;
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
+            const uint32_t id = __float_as_uint(C.w);
+            if (cnt == KBUF) {  // cannot happen for pixels that did not overflow in the forward
+                done = true;
+                continue;
+            }
+            int pos = head + cnt;
+            while (pos > head) {
+                const int pl = (pos - 1) & (KBUF - 1);
+                const float tp = bt[pl][tid];
+                const uint32_t ip = bid[pl][tid];
+                if (t < tp || (t == tp && id < ip)) {
+                    const int psl = pos & (KBUF - 1);
+                    bt[psl][tid] = tp;
+                    bid[psl][tid] = ip;
+                    bs[psl][tid] = bs[pl][tid];
+                    bg[psl][tid] = bg[pl][tid];
+                    bpos[psl][tid] = bpos[pl][tid];
+                    bmem[psl][tid] = bmem[pl][tid];
+                    --pos;
+                } else {
+                    break;
+                }
+            }
+            const int psl = pos & (KBUF - 1);
+            bt[psl][tid] = t;
+            bid[psl][tid] = id;
+            bs[psl][tid] = sigma;
+            bg[psl][tid] = g;
+            bpos[psl][tid] = base + (uint32_t)j;
+            bmem[psl][tid] = pair_val[base + j];
+            ++cnt;
+            if (pos == head) head_t = t;
+        }
+    }
+    while (emission_round(kInf)) {
+    }
+    __syncthreads();
+    flush_slot(batch - 1);
+    flush_slot(batch);
+
+    if (stats != nullptr) {
+        unsigned long long e = n_eval, c = (unsigned long long)nemit;
+        for (int off = 16; off > 0; off >>= 1) {
+            e += __shfl_xor_sync(kFull, e, off);
+            c += __shfl_xor_sync(kFull, c, off);
+        }
+        if (lane == 0) {
+            atomicAdd(&stats->evals, e);
+            atomicAdd(&stats->contribs, c);
+        }
+    }
+}
+
+// Exact fallback for pixels that overflowed the ring in the forward pass:
+// watermark selection (as in blend_fwd.cu) with global atomics.
+constexpr int FB = 16;
+
+__global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate, const SplatRec* __restrict__ recs,
+                                     const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
+                                     const float4* __restrict__ fwd_ct, const float4* __restrict__ grad_ct,
+                                     const uint32_t* __restrict__ ovf_list, uint32_t n_ovf, float* __restrict__ g2d,
+                                     size_t ld2) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_ovf) return;
+    const uint32_t pix = ovf_list[w];
+    const int px = pix % vp.width, py = pix / vp.width;
+    const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
+    PixelRay pr;
+    pixel_ray_dir(vp, px, py, pr.d);
+    pr.pxf = fadd((float)px, 0.5f);
+    pr.pyf = fadd((float)py, 0.5f);
+    PixState ps;
+    ps.T = 1.0f;
+    ps.a0 = ps.a1 = ps.a2 = 0.0f;
+    ps.pxf = pr.pxf;
+    ps.pyf = pr.pyf;
+    const float4 gg = grad_ct[pix], ff = fwd_ct[pix];
+    ps.gc0 = gg.x;
+    ps.gc1 = gg.y;
+    ps.gc2 = gg.z;
+    ps.gT = gg.w;
+    ps.Cf0 = ff.x;
+    ps.Cf1 = ff.y;
+    ps.Cf2 = ff.z;
+    ps.Tf = ff.w;
+    const float e = ro.grad_skip_eps;
+    if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) return;
+    const uint2 rg = ranges[tile];
+    float wt = -kInf;
+    uint32_t wid = 0;
+    bool have_w = false, done = false;
+    float bt[FB], bs[FB], bgv[FB];
+    uint32_t bi[FB], bm[FB];
+    while (!done) {
+        int m = 0;
+        for (uint32_t p = rg.x; p < rg.y; ++p) {
+            float4 A, B, C, D;
+            const uint32_t mem = pair_val[p];
+            load_rec(recs, mem, A, B, C, D);
+            float t, sigma, g;
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
+            const uint32_t id = __float_as_uint(C.w);
+            if (have_w && !(t > wt || (t == wt && id > wid))) continue;
+            if (m == FB && !(t < bt[FB - 1] || (t == bt[FB - 1] && id < bi[FB - 1]))) continue;
+            int pos = m < FB ? m : FB - 1;
+            while (pos > 0 && (t < bt[pos - 1] || (t == bt[pos - 1] && id < bi[pos - 1]))) {
+                bt[pos] = bt[pos - 1];
+                bi[pos] = bi[pos - 1];
+                bs[pos] = bs[pos - 1];
+                bgv[pos] = bgv[pos - 1];
+                bm[pos] = bm[pos - 1];
+                --pos;
+            }
+            bt[pos] = t;
+            bi[pos] = id;
+            bs[pos] = sigma;
+            bgv[pos] = g;
+            bm[pos] = mem;
+            if (m < FB) ++m;
+        }
+        for (int k = 0; k < m; ++k) {
+            if (ro.stop > 0.0f && ps.T < ro.stop) {
+                done = true;
+                break;
+            }
+            float4 A, B, C, D;
+            load_rec(recs, bm[k], A, B, C, D);
+            float v[9];
+            contribution_grad(ps, bs[k], bgv[k], A, B, D, ro.sigma_clamp, v);
+            for (int f = 0; f < 9; ++f)
+                if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + bm[k], v[f]);
+        }
+        if (m < FB) done = true;
+        if (m > 0) {
+            wt = bt[m - 1];
+            wid = bi[m - 1];
+            have_w = true;
+        }
+    }
+}
+
+}  // namespace
+
+void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                      const float4* fwd_ct, const float4* grad_ct, const uint8_t* ovf_flag, float* g2d, size_t ld2,
+                      BlendStats* stats, cudaStream_t s) {
+    const int tiles = vp.tiles_x * vp.tiles_y;
+    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_blend_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
+        configured = true;
+    }
+    k_blend_bwd<<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits,
+                                                       onorm, fwd_ct, grad_ct, ovf_flag, g2d, ld2, stats);
+}
+
+void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
+                               const ViewBins& vb, const float4* fwd_ct, const float4* grad_ct,
+                               const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s) {
+    if (n_ovf == 0) return;
+    k_blend_bwd_fallback<<<(n_ovf + 63) / 64, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
+                                                          grad_ct, ovf_list, n_ovf, g2d, ld2);
+}
+
+}  // namespace dgs_b200

@@ -1,0 +1,335 @@
+// K4 — forward alpha blend of one KD subset with the RetinaGS subspace gate.
+//
+// Reference semantics (raster.hpp:146-189, engine.hpp:31-52): per pixel, the
+// contributions that pass  m^2 <= 9,  t = d.(mu-o) > 0,  ||o+td-mu||^2 <= D^2,
+// the subspace indicator at x_i, and sigma = min(alpha g, 0.99) > 0  are
+// composited front to back in (t, id) order; termination (T < stop) is tested
+// before every contribution; no background.
+//
+// sm_100a design: one 256-thread CTA per 16x16 tile walks the tile's pair list
+// (range-ordered, binning.cu) in batches of 256 records staged through shared
+// memory (broadcast LDS.128 reads in the inner loop).  Because the list is
+// ordered by range r and every contributor satisfies t >= sqrt(r^2 - D^2),
+// each pixel keeps its accepted contributions in a small shared-memory ring
+// (KBUF entries) sorted by (t, id) and composites an entry as soon as its t is
+// below the lower bound L_n of every not-yet-seen candidate.  The composite
+// order is therefore exactly the reference's per-pixel std::sort order.  A
+// pixel whose ring would overflow is handed to an exact O(n^2/16) fallback.
+#include "kernels.h"
+
+namespace dgs_b200 {
+
+namespace {
+
+constexpr int KBUF = 8;  // ring capacity (power of two)
+constexpr float kInf = __builtin_huge_valf();
+// 4 staged float4 record fields + 6 ring fields per pixel.
+constexpr size_t kFwdSmem = 4 * kBlendThreads * sizeof(float4) + 6 * KBUF * kBlendThreads * sizeof(float);
+
+/// Lower bound on t for every candidate at or after a list position whose
+/// range is r (t >= sqrt(r^2 - D^2), with margins ≫ float
+/// rounding of t, r and the D gate).
+__device__ __forceinline__ float order_bound(float r, float dmax, float onorm) {
+    const float S = 2.0f * onorm + 2.0f * r + 1.0f;
+    const float dm = dmax * 1.0001f + 1e-6f * S;
+    const float r2 = r * r * (1.0f - 2e-6f);
+    const float dm2 = dm * dm;
+    if (!(r2 > dm2)) return -kInf;
+    return sqrtf(r2 - dm2) * (1.0f - 1e-6f) - 1e-6f * S;
+}
+
+struct PixelRay {
+    float d[3];
+    float pxf, pyf;
+};
+
+/// Evaluate one candidate for one pixel with the reference's gates
+/// (raster.hpp:153-161).  Returns false when it does not contribute.
+__device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewParams& vp, const RenderOpts& ro,
+                                               const Subspace& gate, const float4& A, const float4& B,
+                                               const float4& C, float& t_out, float& sigma_out, float& g_out) {
+    const float dx = fsub(pr.pxf, A.x), dy = fsub(pr.pyf, A.y);
+    // eval_2d (splat.hpp:326-332): m2 = delta . (inv_cov2d * delta)
+    const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))), fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
+    if (!(m2 <= fmul(ro.trunc, ro.trunc))) return false;  // g = 0 (or NaN) -> !(g > 0)
+    const float t = dot3(pr.d[0], pr.d[1], pr.d[2], fsub(C.x, vp.o[0]), fsub(C.y, vp.o[1]), fsub(C.z, vp.o[2]));
+    if (!(t > 0.0f)) return false;
+    const float x0 = fadd(vp.o[0], fmul(t, pr.d[0]));
+    const float x1 = fadd(vp.o[1], fmul(t, pr.d[1]));
+    const float x2 = fadd(vp.o[2], fmul(t, pr.d[2]));
+    const float e0 = fsub(x0, C.x), e1 = fsub(x1, C.y), e2 = fsub(x2, C.z);
+    if (dot3(e0, e1, e2, e0, e1, e2) > A.w) return false;
+    if (ro.indicator_enabled && !subspace_contains(gate, x0, x1, x2)) return false;
+    const float g = __expf(fmul(-0.5f, m2));
+    const float ag = fmul(A.z, g);
+    const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;  // std::min(alpha*g, clamp)
+    if (!(sigma > 0.0f)) return false;
+    t_out = t;
+    sigma_out = sigma;
+    g_out = g;
+    return true;
+}
+
+__device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint32_t m, float4& A, float4& B,
+                                         float4& C, float4& D) {
+    const float4* r4 = reinterpret_cast<const float4*>(recs + m);
+    A = __ldg(r4 + 0);
+    B = __ldg(r4 + 1);
+    C = __ldg(r4 + 2);
+    D = __ldg(r4 + 3);
+}
+
+__global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, RenderOpts ro, Subspace gate,
+                                                             const SplatRec* __restrict__ recs,
+                                                             const uint32_t* __restrict__ pair_val,
+                                                             const uint2* __restrict__ ranges,
+                                                             const uint32_t* __restrict__ dmax_bits, float onorm,
+                                                             float4* __restrict__ out_ct, uint8_t* __restrict__ ovf_flag,
+                                                             uint32_t* __restrict__ ovf_list,
+                                                             uint32_t* __restrict__ ovf_count,
+                                                             uint32_t* __restrict__ dbg_ids,
+                                                             uint32_t* __restrict__ dbg_cnt, int dbg_cap,
+                                                             BlendStats* __restrict__ stats) {
+    extern __shared__ float4 smem4[];
+    float4* sA = smem4;
+    float4* sB = sA + kBlendThreads;
+    float4* sC = sB + kBlendThreads;
+    float4* sD = sC + kBlendThreads;
+    typedef float Ring[kBlendThreads];
+    Ring* bt = reinterpret_cast<Ring*>(sD + kBlendThreads);
+    uint32_t(*bid)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bt + KBUF);
+    Ring* bs = reinterpret_cast<Ring*>(bid + KBUF);
+    Ring* bc0 = bs + KBUF;
+    Ring* bc1 = bc0 + KBUF;
+    Ring* bc2 = bc1 + KBUF;
+
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x;
+    const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
+    const int px = tx * kTileSize + (tid & 15), py = ty * kTileSize + (tid >> 4);
+    const bool inside = px < vp.width && py < vp.height;
+    const size_t pix = (size_t)py * vp.width + px;
+    PixelRay pr;
+    pixel_ray_dir(vp, px, py, pr.d);
+    pr.pxf = fadd((float)px, 0.5f);
+    pr.pyf = fadd((float)py, 0.5f);
+    const float dmax = __uint_as_float(*dmax_bits);
+
+    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+    bool done = !inside, ovf = false;
+    int head = 0, cnt = 0, nemit = 0;
+    float head_t = kInf;
+    unsigned long long n_eval = 0;
+
+    auto emit_head = [&]() {
+        if (ro.stop > 0.0f && T < ro.stop) {  // raster.hpp:183
+            done = true;
+            cnt = 0;
+            head_t = kInf;
+            return;
+        }
+        const int sl = head & (KBUF - 1);
+        const float sg = bs[sl][tid];
+        const float w = fmul(sg, T);
+        C0 = fadd(C0, fmul(bc0[sl][tid], w));
+        C1 = fadd(C1, fmul(bc1[sl][tid], w));
+        C2 = fadd(C2, fmul(bc2[sl][tid], w));
+        T = fmul(T, fsub(1.0f, sg));
+        if (dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][tid];
+        ++nemit;
+        ++head;
+        --cnt;
+        head_t = cnt ? bt[head & (KBUF - 1)][tid] : kInf;
+    };
+
+    const uint2 rg = ranges[tile];
+    for (uint32_t base = rg.x; base < rg.y; base += kBlendThreads) {
+        if (__syncthreads_count(!done) == 0) break;
+        const uint32_t p = base + tid;
+        if (p < rg.y) {
+            float4 A, B, C, D;
+            load_rec(recs, pair_val[p], A, B, C, D);
+            D.w = order_bound(D.w, dmax, onorm);
+            sA[tid] = A;
+            sB[tid] = B;
+            sC[tid] = C;
+            sD[tid] = D;
+        }
+        __syncthreads();
+        const int nb = (int)min((uint32_t)kBlendThreads, rg.y - base);
+        for (int j = 0; j < nb && !done; ++j) {
+            const float4 D = sD[j];
+            while (head_t < D.w && !done) emit_head();
+            if (done) break;
+            const float4 A = sA[j], B = sB[j], C = sC[j];
+            ++n_eval;
+            float t, sigma, g;
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
+            const uint32_t id = __float_as_uint(C.w);
+            if (cnt == KBUF) {  // ring full and nothing safe to emit: exact fallback
+                ovf = true;
+                done = true;
+                break;
+            }
+            int pos = head + cnt;
+            while (pos > head) {
+                const int pl = (pos - 1) & (KBUF - 1);
+                const float tp = bt[pl][tid];
+                const uint32_t ip = bid[pl][tid];
+                if (t < tp || (t == tp && id < ip)) {
+                    const int ps = pos & (KBUF - 1);
+                    bt[ps][tid] = tp;
+                    bid[ps][tid] = ip;
+                    bs[ps][tid] = bs[pl][tid];
+                    bc0[ps][tid] = bc0[pl][tid];
+                    bc1[ps][tid] = bc1[pl][tid];
+                    bc2[ps][tid] = bc2[pl][tid];
+                    --pos;
+                } else {
+                    break;
+                }
+            }
+            const int ps = pos & (KBUF - 1);
+            bt[ps][tid] = t;
+            bid[ps][tid] = id;
+            bs[ps][tid] = sigma;
+            bc0[ps][tid] = D.x;
+            bc1[ps][tid] = D.y;
+            bc2[ps][tid] = D.z;
+            ++cnt;
+            if (pos == head) head_t = t;
+        }
+    }
+    while (cnt > 0 && !done) emit_head();
+
+    if (inside) {
+        if (ovf) {
+            ovf_flag[pix] = 1;
+            ovf_list[atomicAdd(ovf_count, 1u)] = (uint32_t)pix;
+        } else {
+            ovf_flag[pix] = 0;
+            out_ct[pix] = make_float4(C0, C1, C2, T);
+            if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
+        }
+    }
+    if (stats != nullptr) {
+        unsigned long long e = n_eval, c = (unsigned long long)nemit, o = ovf ? 1ull : 0ull;
+        for (int off = 16; off > 0; off >>= 1) {
+            e += __shfl_xor_sync(0xffffffffu, e, off);
+            c += __shfl_xor_sync(0xffffffffu, c, off);
+            o += __shfl_xor_sync(0xffffffffu, o, off);
+        }
+        if ((tid & 31) == 0) {
+            atomicAdd(&stats->evals, e);
+            atomicAdd(&stats->contribs, c);
+            atomicAdd(&stats->overflow, o);
+        }
+        if (tid == 0) atomicAdd(&stats->tiles_work, (unsigned long long)(rg.y - rg.x));
+    }
+}
+
+// Exact fallback for ring-overflow pixels: repeatedly selects the next 16
+// contributions above a (t, id) watermark by scanning the whole tile list.
+constexpr int FB = 16;
+
+__global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate, const SplatRec* __restrict__ recs,
+                                     const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
+                                     float4* __restrict__ out_ct, const uint32_t* __restrict__ ovf_list,
+                                     uint32_t n_ovf, uint32_t* __restrict__ dbg_ids, uint32_t* __restrict__ dbg_cnt,
+                                     int dbg_cap) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_ovf) return;
+    const uint32_t pix = ovf_list[w];
+    const int px = pix % vp.width, py = pix / vp.width;
+    const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
+    PixelRay pr;
+    pixel_ray_dir(vp, px, py, pr.d);
+    pr.pxf = fadd((float)px, 0.5f);
+    pr.pyf = fadd((float)py, 0.5f);
+    const uint2 rg = ranges[tile];
+    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+    float wt = -kInf;
+    uint32_t wid = 0;
+    bool have_w = false, done = false;
+    int nemit = 0;
+    float bt[FB], bs[FB], c0[FB], c1[FB], c2[FB];
+    uint32_t bi[FB];
+    while (!done) {
+        int m = 0;
+        for (uint32_t p = rg.x; p < rg.y; ++p) {
+            float4 A, B, C, D;
+            load_rec(recs, pair_val[p], A, B, C, D);
+            float t, sigma, g;
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
+            const uint32_t id = __float_as_uint(C.w);
+            if (have_w && !(t > wt || (t == wt && id > wid))) continue;
+            if (m == FB && !(t < bt[FB - 1] || (t == bt[FB - 1] && id < bi[FB - 1]))) continue;
+            int pos = m < FB ? m : FB - 1;
+            while (pos > 0 && (t < bt[pos - 1] || (t == bt[pos - 1] && id < bi[pos - 1]))) {
+                bt[pos] = bt[pos - 1];
+                bi[pos] = bi[pos - 1];
+                bs[pos] = bs[pos - 1];
+                c0[pos] = c0[pos - 1];
+                c1[pos] = c1[pos - 1];
+                c2[pos] = c2[pos - 1];
+                --pos;
+            }
+            bt[pos] = t;
+            bi[pos] = id;
+            bs[pos] = sigma;
+            c0[pos] = D.x;
+            c1[pos] = D.y;
+            c2[pos] = D.z;
+            if (m < FB) ++m;
+        }
+        for (int k = 0; k < m; ++k) {
+            if (ro.stop > 0.0f && T < ro.stop) {
+                done = true;
+                break;
+            }
+            const float wgt = fmul(bs[k], T);
+            C0 = fadd(C0, fmul(c0[k], wgt));
+            C1 = fadd(C1, fmul(c1[k], wgt));
+            C2 = fadd(C2, fmul(c2[k], wgt));
+            T = fmul(T, fsub(1.0f, bs[k]));
+            if (dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[(size_t)pix * dbg_cap + nemit] = bi[k];
+            ++nemit;
+        }
+        if (m < FB) done = true;
+        if (m > 0) {
+            wt = bt[m - 1];
+            wid = bi[m - 1];
+            have_w = true;
+        }
+    }
+    out_ct[pix] = make_float4(C0, C1, C2, T);
+    if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
+}
+
+}  // namespace
+
+void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                      float4* out_ct, uint8_t* ovf_flag, uint32_t* ovf_list, uint32_t* ovf_count,
+                      uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, cudaStream_t s) {
+    const int tiles = vp.tiles_x * vp.tiles_y;
+    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
+    const size_t smem = kFwdSmem;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_blend_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    k_blend_fwd<<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits, onorm,
+                                                out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids, dbg_cnt, dbg_cap,
+                                                stats);
+}
+
+void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                               float4* out_ct, const uint32_t* ovf_list, uint32_t n_ovf, uint32_t* dbg_ids,
+                               uint32_t* dbg_cnt, int dbg_cap, cudaStream_t s) {
+    if (n_ovf == 0) return;
+    k_blend_fwd_fallback<<<(n_ovf + 63) / 64, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, out_ct,
+                                                          ovf_list, n_ovf, dbg_ids, dbg_cnt, dbg_cap);
+}
+
+}  // namespace dgs_b200

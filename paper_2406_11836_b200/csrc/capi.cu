@@ -1,0 +1,907 @@
+// C-ABI of libdgs_b200.so: device context, subset state, and the training
+// step orchestration (Manager<float>::train_step, manager.hpp:313-386, with
+// the worker side WorkerCore::dispatch, worker.hpp:62-167).  Parameters,
+// optimizer moments and every per-view buffer stay resident in HBM; the host
+// only passes cameras, targets and options.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/dgs_capi.h"
+#include "capi_internal.h"
+#include "kernels.h"
+#include "nccl_dyn.h"
+
+namespace dgs_b200 {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+#define CK(call)                                                                                 \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call); \
+    } while (0)
+#define NK(call)                                                                                       \
+    do {                                                                                               \
+        ncclResult_t r_ = (call);                                                                      \
+        if (r_ != ncclSuccess) throw NcclError(std::string("NCCL error: ") + nccl().GetErrorString(r_)); \
+    } while (0)
+
+const NcclApi& nccl() {
+    static NcclApi api{};
+    static bool loaded = false;
+    if (!loaded) {
+        // RTLD_NOLOAD first: reuse the NCCL torch already mapped, if any.
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) throw NcclError(std::string("cannot load libnccl.so.2: ") + dlerror());
+        auto sym = [&](const char* n) {
+            void* f = dlsym(h, n);
+            if (!f) throw NcclError(std::string("libnccl.so.2 lacks ") + n);
+            return f;
+        };
+        api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+        api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+        api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+        api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+        api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+        api.Send = (decltype(api.Send))sym("ncclSend");
+        api.Recv = (decltype(api.Recv))sym("ncclRecv");
+        api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+        loaded = true;
+    }
+    return api;
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    T* ensure(size_t count) {
+        if (count > n || p == nullptr) {
+            if (p) CK(cudaFree(p));
+            p = nullptr;
+            const size_t c = std::max<size_t>(count, 1);
+            CK(cudaMalloc(&p, c * sizeof(T)));
+            n = c;
+        }
+        return p;
+    }
+};
+
+struct ViewSlot {
+    DevBuf<SplatRec> recs;
+    DevBuf<uint32_t> rect, counts, rkey, dmax, pair_tile, pair_val, pair_tile_alt, pair_val_alt;
+    DevBuf<uint32_t> sort_keys_alt, sort_vals, sort_vals_alt, scan, ovf_list, ovf_count;
+    DevBuf<int> err;
+    DevBuf<uint2> ranges;
+    DevBuf<uint8_t> temp, ovf_flag;
+    DevBuf<float4> ct, grad_ct;
+    int64_t pair_cap = 0;
+    size_t temp_bytes = 0;
+    ViewBins vb;
+    ViewParams vp{};
+    uint32_t n_ovf = 0;
+};
+
+struct SubsetState {
+    int k = 0;
+    int64_t n = 0;
+    int sh_coeffs = 16;
+    int rows = 59;
+    size_t ld = 0;
+    DevBuf<float> P, M, V, G, g2d;
+    DevBuf<uint32_t> ids32;
+    std::vector<uint64_t> ids64;
+    uint64_t adam_step = 0, epoch = 0;
+    std::vector<std::unique_ptr<ViewSlot>> slots;
+    ViewSlot& slot(int v) {
+        while ((int)slots.size() <= v) slots.emplace_back(new ViewSlot());
+        return *slots[v];
+    }
+};
+
+struct Ctx {
+    int device = 0, rank = 0, world = 1;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    Table table{};
+    bool table_set = false;
+    DevBuf<Table> table_dev;
+    dgs_render_options ro_in{};
+    dgs_train_config cfg{};
+    RenderOpts ro{};
+    std::map<int, std::unique_ptr<SubsetState>> subsets;
+    DevBuf<float> merged, grad_rgb, targets, staging, kern;
+    DevBuf<double> block_sums, sums;
+    DevBuf<const float4*> partial_ptrs;
+    DevBuf<float4*> grad_ptrs;
+    DevBuf<float4> scratch_maps, scratch_grads;
+    DevBuf<BlendStats> stats;
+    DevBuf<int> bad;
+    uint64_t launches = 0;
+};
+
+namespace {
+
+RenderOpts to_render_opts(const dgs_render_options& o) {
+    RenderOpts r;
+    r.trunc = (float)o.truncation_radius;
+    r.near_plane = (float)o.near_plane;
+    r.sigma_clamp = (float)o.sigma_clamp;
+    r.cov_reg = (float)o.cov2d_regularization;
+    r.stop = (float)o.stop_threshold;
+    r.sh_degree = o.sh_degree;
+    r.indicator_enabled = o.indicator_enabled;
+    r.grad_skip_eps = (float)o.grad_skip_eps;
+    return r;
+}
+
+ViewParams view_params(const dgs_camera& c) {
+    // Camera::validate (splat.hpp:49-54)
+    if (c.width <= 0 || c.height <= 0) throw std::invalid_argument("camera: non-positive resolution");
+    if (!(c.fx > 0.0f) || !(c.fy > 0.0f)) throw std::invalid_argument("camera: focal lengths must be positive");
+    if (!(c.cx > 0.0f) || !(c.cx < (float)c.width) || !(c.cy > 0.0f) || !(c.cy < (float)c.height))
+        throw std::invalid_argument("camera: principal point outside image");
+    ViewParams vp;
+    if (!make_view_params(c.width, c.height, c.fx, c.fy, c.cx, c.cy, c.q_wc, c.t_wc, &vp))
+        throw std::domain_error("zero quaternion");
+    return vp;
+}
+
+Subspace gate_of(const Ctx& ctx, int k) {
+    if (!ctx.table_set || k < 0 || k >= ctx.table.k_count) throw std::invalid_argument("unknown subset " + std::to_string(k));
+    return ctx.table.sub[k];
+}
+
+SubsetState& subset(Ctx& ctx, int k) {
+    auto it = ctx.subsets.find(k);
+    if (it == ctx.subsets.end()) throw std::invalid_argument("subset " + std::to_string(k) + " is not loaded on this rank");
+    return *it->second;
+}
+
+__global__ void k_hwc_to_planar(const float* __restrict__ in, float* __restrict__ out, size_t px) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= px) return;
+    out[i] = in[3 * i];
+    out[px + i] = in[3 * i + 1];
+    out[2 * px + i] = in[3 * i + 2];
+}
+
+__global__ void k_planar_to_hwc(const float* __restrict__ in, float* __restrict__ out, size_t px) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= px) return;
+    out[3 * i] = in[i];
+    out[3 * i + 1] = in[px + i];
+    out[3 * i + 2] = in[2 * px + i];
+}
+
+/// Field layout (per splat) -> SoA rows on the device.
+void upload_fields(Ctx& ctx, SubsetState& S, const dgs_splats& f, float* dst) {
+    const int64_t n = S.n;
+    std::vector<float> h((size_t)S.rows * S.ld, 0.0f);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int a = 0; a < 3; ++a) h[(size_t)(kRowMu + a) * S.ld + i] = f.mu[3 * i + a];
+        for (int a = 0; a < 3; ++a) h[(size_t)(kRowLogScale + a) * S.ld + i] = f.log_scale[3 * i + a];
+        for (int a = 0; a < 4; ++a) h[(size_t)(kRowRot + a) * S.ld + i] = f.rotation[4 * i + a];
+        h[(size_t)kRowOpacity * S.ld + i] = f.opacity_logit[i];
+        for (int c = 0; c < 3 * S.sh_coeffs; ++c) h[(size_t)(kRowSh + c) * S.ld + i] = f.sh[(size_t)i * 3 * S.sh_coeffs + c];
+    }
+    CK(cudaMemcpyAsync(dst, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+}
+
+void download_fields(Ctx& ctx, SubsetState& S, const float* src, dgs_splats* f) {
+    if (f == nullptr) return;
+    if (f->n < S.n || f->sh_coeffs != S.sh_coeffs) throw std::invalid_argument("store: output arrays too small");
+    std::vector<float> h((size_t)S.rows * S.ld);
+    CK(cudaMemcpyAsync(h.data(), src, h.size() * sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    for (int64_t i = 0; i < S.n; ++i) {
+        if (f->id) f->id[i] = S.ids64[i];
+        for (int a = 0; a < 3; ++a) f->mu[3 * i + a] = h[(size_t)(kRowMu + a) * S.ld + i];
+        for (int a = 0; a < 3; ++a) f->log_scale[3 * i + a] = h[(size_t)(kRowLogScale + a) * S.ld + i];
+        for (int a = 0; a < 4; ++a) f->rotation[4 * i + a] = h[(size_t)(kRowRot + a) * S.ld + i];
+        f->opacity_logit[i] = h[(size_t)kRowOpacity * S.ld + i];
+        for (int c = 0; c < 3 * S.sh_coeffs; ++c) f->sh[(size_t)i * 3 * S.sh_coeffs + c] = h[(size_t)(kRowSh + c) * S.ld + i];
+    }
+}
+
+/// partial_render for local subset S into view slot v (engine.hpp:44-52):
+/// K1 projection, K2 binning, K4 blend (+ exact fallback).
+void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int dbg_cap = 0,
+                    uint32_t* dbg_ids = nullptr, uint32_t* dbg_cnt = nullptr, BlendStats* stats = nullptr) {
+    ViewSlot& vs = S.slot(v);
+    const int64_t n = S.n;
+    const int tiles = vp.tiles_x * vp.tiles_y;
+    const size_t px = (size_t)vp.width * vp.height;
+    vs.vp = vp;
+    ViewBins& vb = vs.vb;
+    vb.recs = vs.recs.ensure(n);
+    vb.rect = vs.rect.ensure(2 * n);
+    vb.counts = vs.counts.ensure(n);
+    vb.rkey = vs.rkey.ensure(n);
+    vb.dmax_bits = vs.dmax.ensure(1);
+    vb.err_index = vs.err.ensure(1);
+    vb.ranges = vs.ranges.ensure(tiles);
+    vs.sort_keys_alt.ensure(n);
+    vs.sort_vals.ensure(n);
+    vs.sort_vals_alt.ensure(n);
+    vs.scan.ensure(n);
+    vs.ct.ensure(px);
+    vs.ovf_flag.ensure(px);
+    vs.ovf_list.ensure(px);
+    vs.ovf_count.ensure(1);
+    if (vs.pair_cap == 0) vs.pair_cap = std::max<int64_t>(4 * n + 1024, 1 << 16);
+    auto alloc_pairs = [&]() {
+        vb.pair_tile = vs.pair_tile.ensure(vs.pair_cap);
+        vb.pair_val = vs.pair_val.ensure(vs.pair_cap);
+        vs.pair_tile_alt.ensure(vs.pair_cap);
+        vs.pair_val_alt.ensure(vs.pair_cap);
+        const size_t tb = binning_temp_bytes((int)n, vs.pair_cap);
+        vs.temp.ensure(tb);
+        vs.temp_bytes = vs.temp.n;
+    };
+    alloc_pairs();
+    CK(cudaMemsetAsync(vb.dmax_bits, 0, 4, ctx.stream));
+    const int int_max = INT_MAX;
+    CK(cudaMemcpyAsync(vb.err_index, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));
+    CK(cudaMemsetAsync(vs.ovf_count.p, 0, 4, ctx.stream));
+    launch_preprocess((int)n, S.P.p, S.ld, S.sh_coeffs, S.ids32.p, vp, ctx.ro, vb, ctx.stream);
+    ++ctx.launches;
+    int64_t P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p,
+                            vs.sort_vals.p, vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p,
+                            ctx.stream);
+    ctx.launches += 3;
+    if (P < 0) {
+        vs.pair_cap = (-P) + (-P) / 4 + 1024;
+        alloc_pairs();
+        P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
+                        vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, ctx.stream);
+        ctx.launches += 3;
+        if (P < 0) throw std::runtime_error("binning: pair buffer sizing failed");
+    }
+    int err = INT_MAX;
+    CK(cudaMemcpyAsync(&err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    if (err != INT_MAX) throw std::domain_error("zero quaternion");
+    launch_blend_fwd(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_flag.p, vs.ovf_list.p, vs.ovf_count.p,
+                     dbg_ids, dbg_cnt, dbg_cap, stats, ctx.stream);
+    ++ctx.launches;
+    CK(cudaMemcpyAsync(&vs.n_ovf, vs.ovf_count.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    if (vs.n_ovf > 0) {
+        launch_blend_fwd_fallback(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_list.p, vs.n_ovf, dbg_ids,
+                                  dbg_cnt, dbg_cap, ctx.stream);
+        ++ctx.launches;
+    }
+}
+
+/// partial_render_backward for subset S, view slot v (engine.hpp:74-88) up to
+/// the pixel-space adjoints g2d (K8 + fallback).
+void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
+    ViewSlot& vs = S.slot(v);
+    S.g2d.ensure(9 * S.ld);
+    CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
+    launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.grad_ct.p, vs.ovf_flag.p, S.g2d.p, S.ld,
+                     stats, ctx.stream);
+    ++ctx.launches;
+    if (vs.n_ovf > 0) {
+        launch_blend_bwd_fallback(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.grad_ct.p, vs.ovf_list.p,
+                                  vs.n_ovf, S.g2d.p, S.ld, ctx.stream);
+        ++ctx.launches;
+    }
+}
+
+AdamParams adam_params(const Ctx& ctx, const SubsetState& S, uint64_t step_after) {
+    // worker.hpp:163-166: lr_pos from the pre-increment step, bias correction at step+1.
+    const dgs_train_config& c = ctx.cfg;
+    AdamParams ap;
+    const float lr_pos = (float)dgs_position_lr(&c, step_after - 1);
+    for (int r = 0; r < kMaxParamRows; ++r) ap.lr[r] = 0.0f;
+    for (int a = 0; a < 3; ++a) {
+        ap.lr[kRowMu + a] = lr_pos;
+        ap.lr[kRowLogScale + a] = (float)c.lr_scale;
+    }
+    for (int a = 0; a < 4; ++a) ap.lr[kRowRot + a] = (float)c.lr_rotation;
+    ap.lr[kRowOpacity] = (float)c.lr_opacity;
+    for (int j = 0; j < S.sh_coeffs; ++j)
+        for (int a = 0; a < 3; ++a) ap.lr[kRowSh + 3 * j + a] = j == 0 ? (float)c.lr_sh_dc : (float)c.lr_sh_rest;
+    ap.b1 = (float)c.adam_beta1;
+    ap.b2 = (float)c.adam_beta2;
+    ap.eps = (float)c.adam_eps;
+    ap.bc1 = 1.0f - std::pow(ap.b1, (float)step_after);  // optim.hpp:108-109: std::pow(float, float)
+    ap.bc2 = 1.0f - std::pow(ap.b2, (float)step_after);
+    return ap;
+}
+
+void check_bad(Ctx& ctx, SubsetState& S) {
+    int bad = INT_MAX;
+    CK(cudaMemcpyAsync(&bad, ctx.bad.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    if (bad != INT_MAX)
+        throw std::runtime_error("partial_render_backward: non-finite gradient for splat id " +
+                                 std::to_string(S.ids64[(size_t)bad]));
+}
+
+void reset_bad(Ctx& ctx) {
+    ctx.bad.ensure(1);
+    const int int_max = INT_MAX;
+    CK(cudaMemcpyAsync(ctx.bad.p, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));
+}
+
+const float* ensure_kernel(Ctx& ctx) {
+    if (ctx.kern.p == nullptr) {
+        // loss.hpp:19-30 ssim_kernel<float>: double exp, cast, float sum, divide.
+        float k[11];
+        float sum = 0.0f;
+        for (int i = 0; i < 11; ++i) {
+            const double x = i - 11 / 2;
+            k[i] = (float)std::exp(-x * x / (2.0 * 1.5 * 1.5));
+            sum += k[i];
+        }
+        for (auto& v : k) v /= sum;
+        ctx.kern.ensure(11);
+        CK(cudaMemcpy(ctx.kern.p, k, sizeof(k), cudaMemcpyHostToDevice));
+    }
+    return ctx.kern.p;
+}
+
+void require_table(const Ctx& ctx) {
+    if (!ctx.table_set) throw std::invalid_argument("partition table not set (dgs_set_table)");
+}
+
+}  // namespace
+}  // namespace dgs_b200
+
+using namespace dgs_b200;
+
+struct dgs_ctx : dgs_b200::Ctx {};
+
+extern "C" {
+
+const char* dgs_last_error(void) { return dgs_b200::g_last_error.c_str(); }
+
+int dgs_nccl_unique_id(void* out128) {
+    return dgs_guard([&] {
+        ncclUniqueId id;
+        NK(nccl().GetUniqueId(&id));
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl_id, dgs_ctx** out) {
+    return dgs_guard([&] {
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) throw std::invalid_argument("dgs_ctx_create: bad device index");
+        if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("dgs_ctx_create: bad rank/world");
+        CK(cudaSetDevice(device));
+        std::unique_ptr<dgs_ctx> c(new dgs_ctx());
+        c->device = device;
+        c->rank = rank;
+        c->world = world;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        if (world > 1) {
+            if (nccl_id == nullptr) throw std::invalid_argument("dgs_ctx_create: world > 1 needs an nccl id");
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            NK(nccl().CommInitRank(&c->comm, world, id, rank));
+        }
+        dgs_default_render_options(&c->ro_in);
+        dgs_default_train_config(&c->cfg);
+        c->ro = to_render_opts(c->ro_in);
+        c->stats.ensure(2);  // [0] forward blend, [1] backward blend
+        *out = c.release();
+    });
+}
+
+int dgs_ctx_destroy(dgs_ctx* ctx) {
+    return dgs_guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->comm) nccl().CommDestroy(ctx->comm);
+        ctx->subsets.clear();
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+void* dgs_stream(dgs_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int dgs_sync(dgs_ctx* ctx) {
+    return dgs_guard([&] {
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int dgs_set_table(dgs_ctx* ctx, const dgs_plane* planes, int32_t k_count, int32_t ppk) {
+    return dgs_guard([&] {
+        if (k_count < 1 || k_count > kMaxSubsets) throw std::invalid_argument("set_table: 1..32 subsets supported");
+        if (ppk < 0 || ppk > kMaxPlanes) throw std::invalid_argument("set_table: at most 8 planes per subspace");
+        Table t{};
+        t.k_count = k_count;
+        for (int k = 0; k < k_count; ++k) {
+            t.sub[k].n = ppk;
+            for (int j = 0; j < ppk; ++j) {
+                const dgs_plane& p = planes[k * ppk + j];
+                t.sub[k].nx[j] = p.n[0];
+                t.sub[k].ny[j] = p.n[1];
+                t.sub[k].nz[j] = p.n[2];
+                t.sub[k].d[j] = p.d;
+                t.sub[k].closed[j] = p.closed;
+            }
+        }
+        ctx->table = t;
+        ctx->table_set = true;
+        ctx->table_dev.ensure(1);
+        CK(cudaMemcpy(ctx->table_dev.p, &ctx->table, sizeof(Table), cudaMemcpyHostToDevice));
+    });
+}
+
+int dgs_set_options(dgs_ctx* ctx, const dgs_render_options* ro, const dgs_train_config* cfg) {
+    return dgs_guard([&] {
+        if (ro) {
+            if (ro->camera_z_order) throw std::invalid_argument("camera_z_order fast mode is not supported");
+            ctx->ro_in = *ro;
+            ctx->ro = to_render_opts(*ro);
+        }
+        if (cfg) {
+            // TrainConfig::validate (optim.hpp:30-37)
+            if (cfg->lambda_ssim < 0.0 || cfg->lambda_ssim > 1.0)
+                throw std::invalid_argument("config: lambda_ssim must be in [0,1]");
+            if (cfg->lr_position_end > cfg->lr_position_start)
+                throw std::invalid_argument("config: position LR end must not exceed start");
+            if (cfg->batch_size < 1) throw std::invalid_argument("config: batch_size must be >= 1");
+            ctx->cfg = *cfg;
+        }
+    });
+}
+
+int dgs_subset_load(dgs_ctx* ctx, int32_t k, const dgs_splats* params, const dgs_splats* m, const dgs_splats* v,
+                    uint64_t adam_step, uint64_t epoch) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        if (k < 0 || k >= ctx->table.k_count) throw std::invalid_argument("subset_load: k outside the table");
+        if (params->sh_coeffs != 1 && params->sh_coeffs != 4 && params->sh_coeffs != 9 && params->sh_coeffs != 16)
+            throw std::invalid_argument("splat sh coefficient count must be (deg+1)^2, deg<=3");
+        if (params->n > INT_MAX / 4) throw std::invalid_argument("subset_load: subset too large for one rank");
+        CK(cudaSetDevice(ctx->device));
+        std::unique_ptr<SubsetState> S(new SubsetState());
+        S->k = k;
+        S->n = params->n;
+        S->sh_coeffs = params->sh_coeffs;
+        S->rows = param_rows(S->sh_coeffs);
+        S->ld = (size_t)((params->n + 31) / 32 * 32);
+        S->adam_step = adam_step;
+        S->epoch = epoch;
+        S->ids64.assign(params->id, params->id + params->n);
+        std::vector<uint32_t> ids32((size_t)params->n);
+        for (int64_t i = 0; i < params->n; ++i) {
+            if (params->id[i] > 0xffffffffull) throw std::invalid_argument("subset_load: splat ids must be < 2^32");
+            ids32[i] = (uint32_t)params->id[i];
+        }
+        S->ids32.ensure(params->n);
+        if (params->n) CK(cudaMemcpy(S->ids32.p, ids32.data(), 4 * ids32.size(), cudaMemcpyHostToDevice));
+        S->P.ensure(S->rows * S->ld);
+        S->M.ensure(S->rows * S->ld);
+        S->V.ensure(S->rows * S->ld);
+        upload_fields(*ctx, *S, *params, S->P.p);
+        if (m) upload_fields(*ctx, *S, *m, S->M.p);
+        else CK(cudaMemset(S->M.p, 0, S->rows * S->ld * sizeof(float)));
+        if (v) upload_fields(*ctx, *S, *v, S->V.p);
+        else CK(cudaMemset(S->V.p, 0, S->rows * S->ld * sizeof(float)));
+        ctx->subsets[k] = std::move(S);
+    });
+}
+
+int dgs_subset_store(dgs_ctx* ctx, int32_t k, dgs_splats* params, dgs_splats* m, dgs_splats* v,
+                     uint64_t* adam_step) {
+    return dgs_guard([&] {
+        SubsetState& S = subset(*ctx, k);
+        download_fields(*ctx, S, S.P.p, params);
+        download_fields(*ctx, S, S.M.p, m);
+        download_fields(*ctx, S, S.V.p, v);
+        if (adam_step) *adam_step = S.adam_step;
+    });
+}
+
+int64_t dgs_subset_size(dgs_ctx* ctx, int32_t k) {
+    auto it = ctx->subsets.find(k);
+    return it == ctx->subsets.end() ? -1 : it->second->n;
+}
+
+int dgs_render_partial(dgs_ctx* ctx, int32_t k, const dgs_camera* cam, float* out_ct, int32_t dbg_cap,
+                       uint32_t* dbg_ids, uint32_t* dbg_cnt) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        SubsetState& S = subset(*ctx, k);
+        const ViewParams vp = view_params(*cam);
+        const size_t px = (size_t)vp.width * vp.height;
+        DevBuf<uint32_t> d_ids, d_cnt;
+        if (dbg_cap > 0) {
+            d_ids.ensure(px * dbg_cap);
+            d_cnt.ensure(px);
+        }
+        forward_subset(*ctx, S, 0, vp, dbg_cap, d_ids.p, d_cnt.p);
+        ViewSlot& vs = S.slot(0);
+        if (out_ct) CK(cudaMemcpyAsync(out_ct, vs.ct.p, px * sizeof(float4), cudaMemcpyDeviceToHost, ctx->stream));
+        if (dbg_cap > 0) {
+            CK(cudaMemcpyAsync(dbg_ids, d_ids.p, px * dbg_cap * 4, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(dbg_cnt, d_cnt.p, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_dump_bins(dgs_ctx* ctx, int32_t k, int64_t* tile_off, int32_t* entries, int64_t cap, int64_t* n_pairs) {
+    return dgs_guard([&] {
+        SubsetState& S = subset(*ctx, k);
+        ViewSlot& vs = S.slot(0);
+        const int tiles = vs.vp.tiles_x * vs.vp.tiles_y;
+        const int64_t P = vs.vb.pairs;
+        *n_pairs = P;
+        if (P > cap) throw std::invalid_argument("dump_bins: capacity too small");
+        std::vector<uint2> rg(tiles);
+        CK(cudaMemcpy(rg.data(), vs.vb.ranges, tiles * sizeof(uint2), cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> vals((size_t)P);
+        if (P) CK(cudaMemcpy(vals.data(), vs.vb.pair_val, P * 4, cudaMemcpyDeviceToHost));
+        int64_t o = 0;
+        tile_off[0] = 0;
+        for (int t = 0; t < tiles; ++t) {
+            for (uint32_t p = rg[t].x; p < rg[t].y; ++p) entries[o++] = (int32_t)vals[p];
+            tile_off[t + 1] = o;
+        }
+    });
+}
+
+int dgs_dump_records(dgs_ctx* ctx, int32_t k, float* recs, uint32_t* counts) {
+    return dgs_guard([&] {
+        SubsetState& S = subset(*ctx, k);
+        ViewSlot& vs = S.slot(0);
+        if (recs) CK(cudaMemcpy(recs, vs.vb.recs, S.n * sizeof(SplatRec), cudaMemcpyDeviceToHost));
+        if (counts) CK(cudaMemcpy(counts, vs.vb.counts, S.n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int dgs_pixel_orders(dgs_ctx* ctx, const dgs_camera* cam, uint16_t* order, uint16_t* count) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        const ViewParams vp = view_params(*cam);
+        const size_t px = (size_t)vp.width * vp.height;
+        const int K = ctx->table.k_count;
+        DevBuf<uint16_t> d_o, d_c;
+        d_o.ensure(px * K);
+        d_c.ensure(px);
+        const int owner = table_locate(ctx->table, vp.o);
+        launch_pixel_orders(vp, ctx->table_dev.p, owner, d_o.p, d_c.p, K, ctx->stream);
+        CK(cudaMemcpyAsync(order, d_o.p, px * K * 2, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(count, d_c.p, px * 2, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_merge(dgs_ctx* ctx, const dgs_camera* cam, const float* partials, const float bg[3], float* out_rgb,
+              float* out_t) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        const ViewParams vp = view_params(*cam);
+        const size_t px = (size_t)vp.width * vp.height;
+        const int K = ctx->table.k_count;
+        ctx->scratch_maps.ensure(px * K);
+        CK(cudaMemcpyAsync(ctx->scratch_maps.p, partials, px * K * sizeof(float4), cudaMemcpyHostToDevice, ctx->stream));
+        std::vector<const float4*> ptrs(K);
+        for (int k = 0; k < K; ++k) ptrs[k] = ctx->scratch_maps.p + px * k;
+        ctx->partial_ptrs.ensure(K);
+        CK(cudaMemcpyAsync(ctx->partial_ptrs.p, ptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->merged.ensure(3 * px);
+        ctx->staging.ensure(4 * px);
+        const int owner = table_locate(ctx->table, vp.o);
+        launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, vp.height, 0, bg, ctx->merged.p,
+                     ctx->staging.p + 3 * px, ctx->stream);
+        k_planar_to_hwc<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->merged.p, ctx->staging.p, px);
+        CK(cudaMemcpyAsync(out_rgb, ctx->staging.p, 3 * px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        if (out_t) CK(cudaMemcpyAsync(out_t, ctx->staging.p + 3 * px, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_loss(dgs_ctx* ctx, int32_t width, int32_t height, const float* render, const float* target, double lambda,
+             double inv_batch, float* grad, double* value, double* sums) {
+    return dgs_guard([&] {
+        if (width <= 0 || height <= 0) throw std::invalid_argument("loss: resolution mismatch");
+        const size_t px = (size_t)width * height;
+        ctx->staging.ensure(3 * px);
+        ctx->merged.ensure(3 * px);
+        ctx->grad_rgb.ensure(3 * px);
+        DevBuf<float> tgt;
+        tgt.ensure(3 * px);
+        const unsigned g = (unsigned)((px + 255) / 256);
+        CK(cudaMemcpyAsync(ctx->staging.p, render, 3 * px * 4, cudaMemcpyHostToDevice, ctx->stream));
+        k_hwc_to_planar<<<g, 256, 0, ctx->stream>>>(ctx->staging.p, ctx->merged.p, px);
+        CK(cudaMemcpyAsync(ctx->staging.p, target, 3 * px * 4, cudaMemcpyHostToDevice, ctx->stream));
+        k_hwc_to_planar<<<g, 256, 0, ctx->stream>>>(ctx->staging.p, tgt.p, px);
+        int nb = 0;
+        const int max_blocks = ((width + 31) / 32) * ((height + 31) / 32) * 3;
+        ctx->block_sums.ensure((size_t)max_blocks * 3);
+        ctx->sums.ensure(3);
+        launch_loss(width, height, 0, height, ctx->merged.p, tgt.p, (float)lambda, ensure_kernel(*ctx),
+                    (float)inv_batch, ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
+        launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p, ctx->stream);
+        k_planar_to_hwc<<<g, 256, 0, ctx->stream>>>(ctx->grad_rgb.p, ctx->staging.p, px);
+        double s[3];
+        CK(cudaMemcpyAsync(s, ctx->sums.p, sizeof(s), cudaMemcpyDeviceToHost, ctx->stream));
+        if (grad) CK(cudaMemcpyAsync(grad, ctx->staging.p, 3 * px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        const double n = 3.0 * px;
+        if (value) *value = (1.0 - lambda) * (s[0] / n) + lambda * (1.0 - s[1] / n);
+        if (sums) std::memcpy(sums, s, sizeof(s));
+    });
+}
+
+int dgs_merge_backward(dgs_ctx* ctx, const dgs_camera* cam, const float* partials, const float* grad_color,
+                       const float bg[3], float* out_grads) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        const ViewParams vp = view_params(*cam);
+        const size_t px = (size_t)vp.width * vp.height;
+        const int K = ctx->table.k_count;
+        ctx->scratch_maps.ensure(px * K);
+        ctx->scratch_grads.ensure(px * K);
+        CK(cudaMemcpyAsync(ctx->scratch_maps.p, partials, px * K * sizeof(float4), cudaMemcpyHostToDevice, ctx->stream));
+        std::vector<const float4*> ptrs(K);
+        std::vector<float4*> gptrs(K);
+        for (int k = 0; k < K; ++k) {
+            ptrs[k] = ctx->scratch_maps.p + px * k;
+            gptrs[k] = ctx->scratch_grads.p + px * k;
+        }
+        ctx->partial_ptrs.ensure(K);
+        ctx->grad_ptrs.ensure(K);
+        CK(cudaMemcpyAsync(ctx->partial_ptrs.p, ptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->grad_ptrs.p, gptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->staging.ensure(3 * px);
+        ctx->grad_rgb.ensure(3 * px);
+        CK(cudaMemcpyAsync(ctx->staging.p, grad_color, 3 * px * 4, cudaMemcpyHostToDevice, ctx->stream));
+        k_hwc_to_planar<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->staging.p, ctx->grad_rgb.p, px);
+        const int owner = table_locate(ctx->table, vp.o);
+        launch_merge_bwd(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, vp.height, 0,
+                         ctx->grad_rgb.p, bg, ctx->grad_ptrs.p, vp.height, 0, ctx->stream);
+        CK(cudaMemcpyAsync(out_grads, ctx->scratch_grads.p, px * K * sizeof(float4), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_render_partial_backward(dgs_ctx* ctx, int32_t k, const dgs_camera* cam, const float* grad_ct,
+                                dgs_splats* grads) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        SubsetState& S = subset(*ctx, k);
+        const ViewParams vp = view_params(*cam);
+        const size_t px = (size_t)vp.width * vp.height;
+        forward_subset(*ctx, S, 0, vp);
+        ViewSlot& vs = S.slot(0);
+        vs.grad_ct.ensure(px);
+        CK(cudaMemcpyAsync(vs.grad_ct.p, grad_ct, px * sizeof(float4), cudaMemcpyHostToDevice, ctx->stream));
+        backward_blend(*ctx, S, 0, nullptr);
+        S.G.ensure(S.rows * S.ld);
+        CK(cudaMemsetAsync(S.G.p, 0, S.rows * S.ld * sizeof(float), ctx->stream));
+        reset_bad(*ctx);
+        launch_project_bwd((int)S.n, S.P.p, S.ld, S.sh_coeffs, vp, ctx->ro, vs.vb.counts, S.g2d.p, S.ld, S.G.p,
+                           ctx->bad.p, ctx->stream);
+        check_bad(*ctx, S);
+        download_fields(*ctx, S, S.G.p, grads);
+    });
+}
+
+int dgs_adam_apply(dgs_ctx* ctx, int32_t k, const dgs_splats* grads) {
+    return dgs_guard([&] {
+        SubsetState& S = subset(*ctx, k);
+        S.G.ensure(S.rows * S.ld);
+        upload_fields(*ctx, S, *grads, S.G.p);
+        const AdamParams ap = adam_params(*ctx, S, S.adam_step + 1);
+        launch_adam((int)S.n, S.P.p, S.M.p, S.V.p, S.ld, S.rows, S.G.p, ap, ctx->stream);
+        ++S.adam_step;
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_upload_targets(dgs_ctx* ctx, int32_t batch, int32_t width, int32_t height, const float* targets_hwc,
+                       const float** device_ptr) {
+    return dgs_guard([&] {
+        const size_t px = (size_t)width * height;
+        ctx->targets.ensure(batch * 3 * px);
+        ctx->staging.ensure(3 * px);
+        for (int b = 0; b < batch; ++b) {
+            CK(cudaMemcpyAsync(ctx->staging.p, targets_hwc + b * 3 * px, 3 * px * 4, cudaMemcpyHostToDevice,
+                               ctx->stream));
+            k_hwc_to_planar<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->staging.p,
+                                                                                    ctx->targets.p + b * 3 * px, px);
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+        *device_ptr = ctx->targets.p;
+    });
+}
+
+int dgs_render(dgs_ctx* ctx, const dgs_camera* cam, const float bg[3], float* out_rgb, float* out_t) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        if (ctx->world != 1) throw std::invalid_argument("dgs_render: multi-rank render goes through dgs_train_step");
+        const ViewParams vp = view_params(*cam);
+        const size_t px = (size_t)vp.width * vp.height;
+        const int K = ctx->table.k_count;
+        std::vector<const float4*> ptrs(K);
+        for (int k = 0; k < K; ++k) {
+            SubsetState& S = subset(*ctx, k);
+            forward_subset(*ctx, S, 0, vp);
+            ptrs[k] = S.slot(0).ct.p;
+        }
+        ctx->partial_ptrs.ensure(K);
+        CK(cudaMemcpyAsync(ctx->partial_ptrs.p, ptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->merged.ensure(3 * px);
+        ctx->staging.ensure(4 * px);
+        const int owner = table_locate(ctx->table, vp.o);
+        launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, vp.height, 0, bg, ctx->merged.p,
+                     ctx->staging.p + 3 * px, ctx->stream);
+        k_planar_to_hwc<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->merged.p, ctx->staging.p, px);
+        if (out_rgb) CK(cudaMemcpyAsync(out_rgb, ctx->staging.p, 3 * px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        if (out_t) CK(cudaMemcpyAsync(out_t, ctx->staging.p + 3 * px, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
+                   int32_t targets_on_device, const float bg[3], dgs_step_result* out) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        if (batch < 1 || cams == nullptr || targets == nullptr)
+            throw std::invalid_argument("train_step: need one target per camera");
+        if (batch != ctx->cfg.batch_size) throw std::invalid_argument("train_step: batch size mismatch with config");
+        if (ctx->world != 1) throw std::invalid_argument("train_step: multi-rank exchange not built into this call");
+        const int K = ctx->table.k_count;
+        for (int k = 0; k < K; ++k) subset(*ctx, k);  // merge needs every subset (engine.hpp:160-163)
+        const uint64_t launches0 = ctx->launches;
+        CK(cudaMemsetAsync(ctx->stats.p, 0, 2 * sizeof(BlendStats), ctx->stream));
+        std::vector<ViewParams> vps(batch);
+        std::vector<double> sums(3 * batch);
+        uint64_t pairs = 0;
+        const float lam = (float)ctx->cfg.lambda_ssim;
+        const float inv_batch = 1.0f / (float)batch;  // manager.hpp:329
+        ctx->partial_ptrs.ensure((size_t)K * batch);
+        ctx->grad_ptrs.ensure((size_t)K * batch);
+        ctx->sums.ensure(3 * batch);
+        for (int v = 0; v < batch; ++v) {
+            vps[v] = view_params(cams[v]);
+            const ViewParams& vp = vps[v];
+            if (v > 0 && (vp.width != vps[0].width || vp.height != vps[0].height))
+                throw std::invalid_argument("train_step: all views of a batch must share a resolution");
+            const size_t px = (size_t)vp.width * vp.height;
+            // ---- render_batch (manager.hpp:262-304): per-subset partials ----
+            std::vector<const float4*> ptrs(K);
+            std::vector<float4*> gptrs(K);
+            for (int k = 0; k < K; ++k) {
+                SubsetState& S = subset(*ctx, k);
+                forward_subset(*ctx, S, v, vp, 0, nullptr, nullptr, ctx->stats.p);
+                ViewSlot& vs = S.slot(v);
+                pairs += (uint64_t)vs.vb.pairs;
+                ptrs[k] = vs.ct.p;
+                gptrs[k] = vs.grad_ct.ensure(px);
+            }
+            CK(cudaMemcpyAsync(ctx->partial_ptrs.p + (size_t)K * v, ptrs.data(), K * sizeof(void*),
+                               cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(ctx->grad_ptrs.p + (size_t)K * v, gptrs.data(), K * sizeof(void*),
+                               cudaMemcpyHostToDevice, ctx->stream));
+            const int owner = table_locate(ctx->table, vp.o);
+            ctx->merged.ensure(3 * px);
+            launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v, vp.height, 0,
+                         bg, ctx->merged.p, nullptr, ctx->stream);
+            ++ctx->launches;
+            // ---- loss (manager.hpp:331-334) ----
+            const float* tgt;
+            if (targets_on_device) {
+                tgt = targets + (size_t)v * 3 * px;
+            } else {
+                ctx->staging.ensure(3 * px);
+                ctx->targets.ensure(3 * px);
+                CK(cudaMemcpyAsync(ctx->staging.p, targets + (size_t)v * 3 * px, 3 * px * 4, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+                k_hwc_to_planar<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->staging.p,
+                                                                                        ctx->targets.p, px);
+                ++ctx->launches;
+                tgt = ctx->targets.p;
+            }
+            ctx->grad_rgb.ensure(3 * px);
+            const int max_blocks = ((vp.width + 31) / 32) * ((vp.height + 31) / 32) * 3;
+            ctx->block_sums.ensure((size_t)max_blocks * 3);
+            int nb = 0;
+            launch_loss(vp.width, vp.height, 0, vp.height, ctx->merged.p, tgt, lam, ensure_kernel(*ctx), inv_batch,
+                        ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
+            launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p + 3 * v, ctx->stream);
+            // ---- merge_backward (engine.hpp:195-234) ----
+            launch_merge_bwd(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v,
+                             vp.height, 0, ctx->grad_rgb.p, bg, ctx->grad_ptrs.p + (size_t)K * v, vp.height, 0,
+                             ctx->stream);
+            ctx->launches += 3;
+        }
+        // ---- MsgBackwardTask x B, then apply_step (worker.hpp:86-127, 162-167) ----
+        reset_bad(*ctx);
+        for (int k = 0; k < K; ++k) {
+            SubsetState& S = subset(*ctx, k);
+            const AdamParams ap = adam_params(*ctx, S, S.adam_step + 1);
+            if (batch > 1) {
+                S.G.ensure(S.rows * S.ld);
+                CK(cudaMemsetAsync(S.G.p, 0, S.rows * S.ld * sizeof(float), ctx->stream));
+            }
+            for (int v = 0; v < batch; ++v) {
+                ViewSlot& vs = S.slot(v);
+                backward_blend(*ctx, S, v, ctx->stats.p + 1);
+                if (v + 1 < batch) {
+                    launch_project_bwd((int)S.n, S.P.p, S.ld, S.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S.g2d.p,
+                                       S.ld, S.G.p, ctx->bad.p, ctx->stream);
+                } else {
+                    launch_project_bwd_adam((int)S.n, S.P.p, S.M.p, S.V.p, S.ld, S.sh_coeffs, vs.vp, ctx->ro,
+                                            vs.vb.counts, S.g2d.p, S.ld, batch > 1 ? S.G.p : nullptr, ap, ctx->bad.p,
+                                            ctx->stream);
+                }
+                ++ctx->launches;
+            }
+            ++S.adam_step;
+        }
+        CK(cudaMemcpyAsync(sums.data(), ctx->sums.p, 3 * batch * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        BlendStats st[2]{};
+        CK(cudaMemcpyAsync(st, ctx->stats.p, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+        int bad = INT_MAX;
+        CK(cudaMemcpyAsync(&bad, ctx->bad.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaGetLastError());
+        if (bad != INT_MAX) {
+            // which subset: report the first loaded subset whose id range covers it
+            throw std::runtime_error("partial_render_backward: non-finite gradient for splat id " +
+                                     std::to_string(subset(*ctx, 0).ids64[(size_t)bad]));
+        }
+        if (out) {
+            std::memset(out, 0, sizeof(*out));
+            double loss = 0.0, mse = 0.0;
+            const double lambda = ctx->cfg.lambda_ssim;
+            for (int v = 0; v < batch; ++v) {
+                const double n = 3.0 * vps[v].width * vps[v].height;
+                loss += ((1.0 - lambda) * (sums[3 * v] / n) + lambda * (1.0 - sums[3 * v + 1] / n)) / batch;
+                mse += (sums[3 * v + 2] / n) / batch;
+            }
+            out->loss = loss;
+            out->psnr = mse == 0.0 ? INFINITY : 10.0 * std::log10(1.0 / mse);
+            // reference accounting (manager.hpp:384): every partial map and its
+            // gradient cross a link: 2 * K * H * W * 4 * sizeof(float) per view.
+            out->comm_bytes = (uint64_t)2 * K * batch * (uint64_t)vps[0].width * vps[0].height * 4 * sizeof(float);
+            out->nccl_bytes = 0;
+            out->pairs = pairs;
+            out->evals_fwd = st[0].evals;
+            out->contribs_fwd = st[0].contribs;
+            out->overflow_pixels = st[0].overflow;
+            out->evals_bwd = st[1].evals;
+            out->contribs_bwd = st[1].contribs;
+            out->kernel_launches = ctx->launches - launches0;
+        }
+    });
+}
+
+}  // extern "C"

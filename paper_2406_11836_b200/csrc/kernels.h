@@ -1,0 +1,100 @@
+// Launchers for the sm_100a kernels (internal to libdgs_b200.so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "dgs_types.cuh"
+
+namespace dgs_b200 {
+
+/// Per-view, per-subset scratch produced by the projection/binning stage and
+/// consumed by both blend kernels.
+struct ViewBins {
+    SplatRec* recs = nullptr;        // [n]
+    uint32_t* rect = nullptr;        // [2n]: x0 | x1 << 16, y0 | y1 << 16
+    uint32_t* counts = nullptr;      // [n] tile count per member (0 = culled)
+    uint32_t* rkey = nullptr;        // [n] range bits (0xffffffff = culled)
+    uint32_t* dmax_bits = nullptr;   // [1] max world_radius over visible members
+    int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
+    uint32_t* pair_tile = nullptr;   // [cap] tile key of each (splat, tile) pair
+    uint32_t* pair_val = nullptr;    // [cap] member index
+    uint2* ranges = nullptr;         // [tiles] (start, end) into the sorted pair list
+    int64_t pairs = 0;
+};
+
+// K1: projection + SH colour + tile rectangles (splat.hpp:288-321, raster.hpp:113-125).
+void launch_preprocess(int n, const float* P, size_t ld, int sh_coeffs, const uint32_t* ids32, const ViewParams& vp,
+                       const RenderOpts& ro, const ViewBins& vb, cudaStream_t s);
+
+// K2 helpers (CUB radix sorts live in binning.cu).
+size_t binning_temp_bytes(int n, int64_t pair_cap);
+// Sorts members by range, emits pairs in range order, stable-sorts them by
+// tile, fills vb.ranges.  Returns the pair count (host sync).  `cap` is the
+// pair buffer capacity; returns -needed if it is too small.
+int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
+                    uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint32_t* pair_tile_alt,
+                    uint32_t* pair_val_alt, uint32_t* scan_buf, cudaStream_t s);
+
+struct BlendStats {
+    unsigned long long evals;      // (pixel, candidate) 2D evaluations
+    unsigned long long contribs;   // emitted contributions
+    unsigned long long overflow;   // pixels routed to the exact fallback
+    unsigned long long tiles_work; // sum over tiles of candidates processed
+};
+
+// K4: forward alpha blend with the RetinaGS subspace gate, exact per-ray (t, id) order.
+void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                      float4* out_ct, uint8_t* ovf_flag, uint32_t* ovf_list, uint32_t* ovf_count,
+                      uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, cudaStream_t s);
+void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                               float4* out_ct, const uint32_t* ovf_list, uint32_t n_ovf, uint32_t* dbg_ids,
+                               uint32_t* dbg_cnt, int dbg_cap, cudaStream_t s);
+
+// K8: backward blend; accumulates 9 pixel-space adjoints per member into g2d (SoA [9][ld2]).
+void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                      const float4* fwd_ct, const float4* grad_ct, const uint8_t* ovf_flag, float* g2d, size_t ld2,
+                      BlendStats* stats, cudaStream_t s);
+void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
+                               const ViewBins& vb, const float4* fwd_ct, const float4* grad_ct,
+                               const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s);
+
+// K3/K5: per-pixel subset order + merge (engine.hpp:108-182). Rows [row0, row1).
+void launch_merge(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
+                  const float4* const* partials, int pstride_rows, int prow0, const float bg[3], float* out_rgb,
+                  float* out_t, cudaStream_t s);
+void launch_pixel_orders(const ViewParams& vp, const Table* tb_dev, int owner, uint16_t* order, uint16_t* count,
+                         int kstride, cudaStream_t s);
+
+// K6: fused L1 + D-SSIM forward and gradient (loss.hpp:33-177), per channel plane.
+// x, y: planar [3][H][W]; grad: planar [3][H][W]; partial sums per block (double[3] each).
+// `kernel` is the 11-tap window in device memory.
+void launch_loss(int W, int H, int row0, int row1, const float* x, const float* y, float lambda,
+                 const float* kernel, float inv_batch, float* grad, double* block_sums, int* n_blocks,
+                 cudaStream_t s);
+void launch_reduce_sums(const double* block_sums, int n_blocks, double* out3, cudaStream_t s);
+
+// K7: merge adjoint (engine.hpp:195-234).
+void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
+                      const float4* const* partials, int pstride_rows, int prow0, const float* grad_rgb,
+                      const float bg[3], float4* const* grad_out, int gstride_rows, int grow0, cudaStream_t s);
+
+struct AdamParams {
+    float lr[kMaxParamRows];  // per row
+    float b1, b2, eps, bc1, bc2;
+};
+
+// K9 (+K10): projection backward (splat.hpp:363-437) fused with dense Adam
+// (optim.hpp:104-126) when `adam` is non-null; otherwise accumulates the
+// parameter gradients into G (SoA rows).
+void launch_project_bwd(int n, const float* P, size_t ld, int sh_coeffs, const ViewParams& vp,
+                        const RenderOpts& ro, const uint32_t* counts, const float* g2d, size_t ld2, float* G,
+                        int* bad_index, cudaStream_t s);
+void launch_project_bwd_adam(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, const ViewParams& vp,
+                             const RenderOpts& ro, const uint32_t* counts, const float* g2d, size_t ld2,
+                             const float* G_extra, const AdamParams& ap, int* bad_index, cudaStream_t s);
+void launch_adam(int n, float* P, float* M, float* V, size_t ld, int rows, const float* G, const AdamParams& ap,
+                 cudaStream_t s);
+
+}  // namespace dgs_b200

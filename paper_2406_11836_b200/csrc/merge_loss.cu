@@ -1,0 +1,340 @@
+// K3/K5/K6/K7 — per-pixel subset order, Eq.-5 merge, fused L1 + D-SSIM loss
+// with its analytic gradient, and the merge adjoint.
+//
+// All four follow the reference op order exactly (engine.hpp:108-234,
+// loss.hpp:19-177), so the merged image, the loss-gradient image and the
+// partial-map gradients are bit-identical to the CPU oracle; only the loss
+// scalars (reduced in double here, sequential float there) differ by
+// rounding.  The merge and adjoint are HBM-streaming (16 B per subset per
+// pixel in, 16 B out); the SSIM kernel keeps its 10 separable 11-tap blurs in
+// shared memory (32x32 output tile, 10-pixel halo) and reads each input once.
+#include "kernels.h"
+
+namespace dgs_b200 {
+
+namespace {
+
+__global__ void k_merge(ViewParams vp, const Table* __restrict__ tb, int owner, int row0, int row1,
+                        const float4* const* __restrict__ partials, int prow0, float bg0, float bg1, float bg2,
+                        float* __restrict__ out_rgb, float* __restrict__ out_t) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = row0 + blockIdx.y;
+    if (x >= vp.width || y >= row1) return;
+    float d[3];
+    pixel_ray_dir(vp, x, y, d);
+    uint16_t ord[kMaxSubsets];
+    const int n = subspace_order(*tb, owner, vp.o, d, ord);
+    float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, tr = 1.0f;
+    const size_t prow = (size_t)(y - prow0) * vp.width + x;
+    for (int i = 0; i < n; ++i) {
+        const float4 p = partials[ord[i]][prow];
+        c0 = fadd(c0, fmul(tr, p.x));  // engine.hpp:174
+        c1 = fadd(c1, fmul(tr, p.y));
+        c2 = fadd(c2, fmul(tr, p.z));
+        tr = fmul(tr, p.w);
+    }
+    const size_t pix = (size_t)y * vp.width + x;
+    const size_t plane = (size_t)vp.width * vp.height;
+    out_rgb[pix] = fadd(c0, fmul(tr, bg0));  // engine.hpp:177
+    out_rgb[plane + pix] = fadd(c1, fmul(tr, bg1));
+    out_rgb[2 * plane + pix] = fadd(c2, fmul(tr, bg2));
+    if (out_t) out_t[pix] = tr;
+}
+
+__global__ void k_pixel_orders(ViewParams vp, const Table* __restrict__ tb, int owner, uint16_t* __restrict__ order,
+                               uint16_t* __restrict__ count, int kstride) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= vp.width) return;
+    float d[3];
+    pixel_ray_dir(vp, x, y, d);
+    uint16_t ord[kMaxSubsets];
+    const int n = subspace_order(*tb, owner, vp.o, d, ord);
+    const size_t pix = (size_t)y * vp.width + x;
+    count[pix] = (uint16_t)n;
+    for (int i = 0; i < kstride; ++i) order[pix * kstride + i] = i < n ? ord[i] : 0;
+}
+
+__global__ void k_merge_bwd(ViewParams vp, const Table* __restrict__ tb, int owner, int row0, int row1,
+                            const float4* const* __restrict__ partials, int prow0, const float* __restrict__ grad_rgb,
+                            float bg0, float bg1, float bg2, float4* const* __restrict__ grad_out, int grow0) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = row0 + blockIdx.y;
+    if (x >= vp.width || y >= row1) return;
+    float d[3];
+    pixel_ray_dir(vp, x, y, d);
+    uint16_t ord[kMaxSubsets];
+    const int n = subspace_order(*tb, owner, vp.o, d, ord);
+    const size_t pix = (size_t)y * vp.width + x;
+    const size_t plane = (size_t)vp.width * vp.height;
+    const float gc0 = grad_rgb[pix], gc1 = grad_rgb[plane + pix], gc2 = grad_rgb[2 * plane + pix];
+    const float gt_eff = fadd(0.0f, dot3(gc0, gc1, gc2, bg0, bg1, bg2));  // engine.hpp:216 (grad_T_total = 0)
+    const size_t prow = (size_t)(y - prow0) * vp.width + x;
+    const size_t grow = (size_t)(y - grow0) * vp.width + x;
+    float prefix[kMaxSubsets + 1];
+    float4 pk[kMaxSubsets];
+    prefix[0] = 1.0f;
+    for (int i = 0; i < n; ++i) {
+        pk[i] = partials[ord[i]][prow];
+        prefix[i + 1] = fmul(prefix[i], pk[i].w);
+    }
+    // absent subsets get exact zeros
+    uint32_t present = 0;
+    for (int i = 0; i < n; ++i) present |= 1u << ord[i];
+    for (int k = 0; k < tb->k_count; ++k)
+        if (!(present & (1u << k))) grad_out[k][grow] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, tail = 1.0f;
+    for (int i = n - 1; i >= 0; --i) {
+        const float pf = prefix[i];
+        const float dT = fmul(pf, fadd(dot3(gc0, gc1, gc2, s0, s1, s2), fmul(gt_eff, tail)));
+        grad_out[ord[i]][grow] = make_float4(fmul(pf, gc0), fmul(pf, gc1), fmul(pf, gc2), dT);
+        const float4 p = pk[i];
+        s0 = fadd(p.x, fmul(p.w, s0));
+        s1 = fadd(p.y, fmul(p.w, s1));
+        s2 = fadd(p.z, fmul(p.w, s2));
+        tail = fmul(tail, p.w);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused L1 + D-SSIM (loss.hpp:94-177), one channel plane per blockIdx.z.
+// ---------------------------------------------------------------------------
+constexpr int kOT = 32;             // output tile
+constexpr int kR = 5;               // blur radius
+constexpr int kIn = kOT + 4 * kR;   // 52: input tile with 10-pixel halo
+constexpr int kMid = kOT + 2 * kR;  // 42: first-stage maps with 5-pixel halo
+constexpr size_t kLossSmem = (2 * kIn * kIn + 5 * kIn * kMid + 5 * kMid * kMid) * sizeof(float);
+
+__global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, const float* __restrict__ xs,
+                                              const float* __restrict__ ys, float lam, float c1, float c2,
+                                              float nf, float inv_batch, const float* __restrict__ kern_g,
+                                              float* __restrict__ grad, double* __restrict__ block_sums) {
+    extern __shared__ float sm[];
+    float* X = sm;                       // [kIn][kIn]
+    float* Y = X + kIn * kIn;            // [kIn][kIn]
+    float* Hb = Y + kIn * kIn;           // [5][kIn][kMid] horizontal stage (reused as [5][kMid][kOT])
+    float* Vb = Hb + 5 * kIn * kMid;     // [5][kMid][kMid]
+    __shared__ float kern[11];
+    __shared__ double red[3][8];
+    const int tid = threadIdx.x;
+    if (tid < 11) kern[tid] = kern_g[tid];
+    const int ox = blockIdx.x * kOT, oy = row0 + blockIdx.y * kOT;
+    const int ch = blockIdx.z;
+    const size_t plane = (size_t)W * H;
+    const float* xp = xs + ch * plane;
+    const float* yp = ys + ch * plane;
+    // stage 0: inputs with zero padding outside the image
+    for (int i = tid; i < kIn * kIn; i += 256) {
+        const int r = i / kIn, c = i % kIn;
+        const int gy = oy - 2 * kR + r, gx = ox - 2 * kR + c;
+        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+        X[i] = in ? xp[(size_t)gy * W + gx] : 0.0f;
+        Y[i] = in ? yp[(size_t)gy * W + gx] : 0.0f;
+    }
+    __syncthreads();
+    // stage 1: horizontal blur of x, y, x*x, y*y, x*y  (rows -10..+41, cols -5..+36)
+    for (int i = tid; i < kIn * kMid; i += 256) {
+        const int r = i / kMid, c = i % kMid;
+        float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f, a4 = 0.0f;
+        const float* xr = X + r * kIn + c;
+        const float* yr = Y + r * kIn + c;
+        const int gx0 = ox - kR + c - kR;
+#pragma unroll
+        for (int k = 0; k < 11; ++k) {
+            const int gx = gx0 + k;
+            if (gx < 0 || gx >= W) continue;  // zero padding = skipped term (loss.hpp:44)
+            const float xv = xr[k], yv = yr[k], w = kern[k];
+            a0 = fadd(a0, fmul(w, xv));
+            a1 = fadd(a1, fmul(w, yv));
+            a2 = fadd(a2, fmul(w, fmul(xv, xv)));
+            a3 = fadd(a3, fmul(w, fmul(yv, yv)));
+            a4 = fadd(a4, fmul(w, fmul(xv, yv)));
+        }
+        Hb[0 * kIn * kMid + i] = a0;
+        Hb[1 * kIn * kMid + i] = a1;
+        Hb[2 * kIn * kMid + i] = a2;
+        Hb[3 * kIn * kMid + i] = a3;
+        Hb[4 * kIn * kMid + i] = a4;
+    }
+    __syncthreads();
+    // stage 2: vertical blur -> mu_x, mu_y, E[xx], E[yy], E[xy] at tile +-5;
+    // then the per-pixel SSIM partials A, B, C, B*mu_x, C*mu_y (zero outside the image).
+    double s_ssim = 0.0;
+    for (int i = tid; i < kMid * kMid; i += 256) {
+        const int r = i / kMid, c = i % kMid;
+        const int gy = oy - kR + r, gx = ox - kR + c;
+        float m[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            float a = 0.0f;
+            const float* col = Hb + q * kIn * kMid + r * kMid + c;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                const int yy = gy - kR + k;
+                if (yy < 0 || yy >= H) continue;
+                a = fadd(a, fmul(kern[k], col[k * kMid]));
+            }
+            m[q] = a;
+        }
+        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+        float A = 0.0f, B = 0.0f, C = 0.0f, Bm = 0.0f, Cm = 0.0f;
+        if (in) {
+            const float mx = m[0], my = m[1];
+            const float sxx = fsub(m[2], fmul(mx, mx));
+            const float syy = fsub(m[3], fmul(my, my));
+            const float sxy = fsub(m[4], fmul(mx, my));
+            const float n1 = fadd(fmul(fmul(2.0f, mx), my), c1), n2 = fadd(fmul(2.0f, sxy), c2);
+            const float d1 = fadd(fadd(fmul(mx, mx), fmul(my, my)), c1), d2 = fadd(fadd(sxx, syy), c2);
+            const float dd = fmul(d1, d2);
+            const float s = fdiv(fmul(n1, n2), dd);
+            A = fsub(fdiv(fmul(fmul(2.0f, my), n2), dd), fdiv(fmul(fmul(2.0f, mx), s), d1));
+            B = fdiv(-s, d2);
+            C = fdiv(fmul(2.0f, n1), dd);
+            Bm = fmul(B, mx);
+            Cm = fmul(C, my);
+            const bool own = r >= kR && r < kR + kOT && c >= kR && c < kR + kOT && gy < row1;
+            if (own) s_ssim += (double)s;
+        }
+        Vb[0 * kMid * kMid + i] = A;
+        Vb[1 * kMid * kMid + i] = B;
+        Vb[2 * kMid * kMid + i] = Bm;
+        Vb[3 * kMid * kMid + i] = C;
+        Vb[4 * kMid * kMid + i] = Cm;
+    }
+    __syncthreads();
+    // stage 3: horizontal blur of the five maps (rows -5..+36, cols 0..31)
+    float* H2 = Hb;  // [5][kMid][kOT]
+    for (int i = tid; i < kMid * kOT; i += 256) {
+        const int r = i / kOT, c = i % kOT;
+        const int gx0 = ox + c - kR;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            float a = 0.0f;
+            const float* row = Vb + q * kMid * kMid + r * kMid + c;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                const int gx = gx0 + k;
+                if (gx < 0 || gx >= W) continue;
+                a = fadd(a, fmul(kern[k], row[k]));
+            }
+            H2[q * kMid * kOT + i] = a;
+        }
+    }
+    __syncthreads();
+    // stage 4: vertical blur -> gradient (loss.hpp:138-140, 160-175)
+    double s_l1 = 0.0, s_mse = 0.0;
+    for (int i = tid; i < kOT * kOT; i += 256) {
+        const int r = i / kOT, c = i % kOT;
+        const int gy = oy + r, gx = ox + c;
+        if (gy >= row1 || gy >= H || gx >= W) continue;
+        float cv[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            float a = 0.0f;
+            const float* col = H2 + q * kMid * kOT + r * kOT + c;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                const int yy = gy - kR + k;
+                if (yy < 0 || yy >= H) continue;
+                a = fadd(a, fmul(kern[k], col[k * kOT]));
+            }
+            cv[q] = a;
+        }
+        const float xv = X[(r + 2 * kR) * kIn + c + 2 * kR], yv = Y[(r + 2 * kR) * kIn + c + 2 * kR];
+        // dS/dx = (conv(A) + 2x conv(B) - 2 conv(B mu_x) + y conv(C) - conv(C mu_y)) / n
+        const float sg = fdiv(fsub(fadd(fsub(fadd(cv[0], fmul(fmul(2.0f, xv), cv[1])), fmul(2.0f, cv[2])),
+                                        fmul(yv, cv[3])),
+                                   cv[4]),
+                              nf);
+        const float d = fsub(xv, yv);
+        const float sgn = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
+        const float gl1 = fdiv(fmul(fsub(1.0f, lam), sgn), nf);
+        const float g = fsub(gl1, fmul(lam, sg));
+        grad[ch * plane + (size_t)gy * W + gx] = fmul(g, inv_batch);
+        s_l1 += (double)fabsf(d);
+        s_mse += (double)fmul(d, d);
+    }
+    // block sums (deterministic)
+    double v[3] = {s_l1, s_ssim, s_mse};
+    for (int q = 0; q < 3; ++q) {
+        double x = v[q];
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        if ((tid & 31) == 0) red[q][tid >> 5] = x;
+    }
+    __syncthreads();
+    if (tid < 3) {
+        double x = 0.0;
+        for (int w = 0; w < 8; ++w) x += red[tid][w];
+        const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        block_sums[(size_t)b * 3 + tid] = x;
+    }
+}
+
+__global__ void k_reduce_sums(const double* __restrict__ bs, int n, double* __restrict__ out) {
+    __shared__ double red[3][32];
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int q = 0; q < 3; ++q) v[q] += bs[(size_t)i * 3 + q];
+    for (int q = 0; q < 3; ++q) {
+        double x = v[q];
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double x = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) x += red[threadIdx.x][w];
+        out[threadIdx.x] = x;
+    }
+}
+
+}  // namespace
+
+void launch_merge(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
+                  const float4* const* partials, int pstride_rows, int prow0, const float bg[3], float* out_rgb,
+                  float* out_t, cudaStream_t s) {
+    (void)pstride_rows;
+    if (row1 <= row0) return;
+    dim3 grid((vp.width + 127) / 128, row1 - row0);
+    k_merge<<<grid, 128, 0, s>>>(vp, tb_dev, owner, row0, row1, partials, prow0, bg[0], bg[1], bg[2], out_rgb, out_t);
+}
+
+void launch_pixel_orders(const ViewParams& vp, const Table* tb_dev, int owner, uint16_t* order, uint16_t* count,
+                         int kstride, cudaStream_t s) {
+    dim3 grid((vp.width + 127) / 128, vp.height);
+    k_pixel_orders<<<grid, 128, 0, s>>>(vp, tb_dev, owner, order, count, kstride);
+}
+
+void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
+                      const float4* const* partials, int pstride_rows, int prow0, const float* grad_rgb,
+                      const float bg[3], float4* const* grad_out, int gstride_rows, int grow0, cudaStream_t s) {
+    (void)pstride_rows;
+    (void)gstride_rows;
+    if (row1 <= row0) return;
+    dim3 grid((vp.width + 127) / 128, row1 - row0);
+    k_merge_bwd<<<grid, 128, 0, s>>>(vp, tb_dev, owner, row0, row1, partials, prow0, grad_rgb, bg[0], bg[1], bg[2],
+                                     grad_out, grow0);
+}
+
+void launch_loss(int W, int H, int row0, int row1, const float* x, const float* y, float lambda,
+                 const float* kernel, float inv_batch, float* grad, double* block_sums, int* n_blocks,
+                 cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLossSmem);
+        configured = true;
+    }
+    dim3 grid((W + kOT - 1) / kOT, (row1 - row0 + kOT - 1) / kOT, 3);
+    *n_blocks = (int)(grid.x * grid.y * grid.z);
+    // loss.hpp:16-17: C1 = (0.01)^2, C2 = (0.03)^2 evaluated in double, then T(.)
+    const float c1 = (float)(0.01 * 0.01), c2 = (float)(0.03 * 0.03);
+    const float nf = (float)((size_t)W * H * 3);
+    k_loss<<<grid, 256, kLossSmem, s>>>(W, H, row0, row1, x, y, lambda, c1, c2, nf, inv_batch, kernel, grad,
+                                        block_sums);
+}
+
+void launch_reduce_sums(const double* block_sums, int n_blocks, double* out3, cudaStream_t s) {
+    k_reduce_sums<<<1, 256, 0, s>>>(block_sums, n_blocks, out3);
+}
+
+}  // namespace dgs_b200

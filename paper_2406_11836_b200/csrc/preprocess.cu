@@ -1,0 +1,160 @@
+// K1 — per-member projection (EWA), SH colour, opacity sigmoid, support radius
+// D_i, tile rectangle and range key.  One thread per member; HBM-bound
+// (59 param floats in, one 64-byte record + 16 bytes of binning data out).
+//
+// Bit-exactness: every quantity that feeds an index or a gate is computed in
+// the reference's op order with _rn intrinsics (no FMA contraction):
+//   t = W mu + t_wc, mean2d, J, V = J W, Sigma = (R S)(R S)^T, cov2d = V Sigma V^T
+//   (+0.3 I), det, inv_cov2d, 3*sqrt(c_ii), the cull test and the tile bins
+//   (splat.hpp:245-321, raster.hpp:113-125), and D_i = 3*max(exp(log_scale))
+//   with the glibc expf port (splat.hpp:36-37).
+#include "kernels.h"
+
+namespace dgs_b200 {
+
+namespace {
+
+__global__ void __launch_bounds__(256) k_preprocess(int n, const float* __restrict__ P, size_t ld, int sh_coeffs,
+                                                    const uint32_t* __restrict__ ids32, ViewParams vp,
+                                                    RenderOpts ro, ViewBins vb) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    float dmax_local = 0.0f;
+    if (i < n) {
+        auto row = [&](int r) { return __ldg(P + (size_t)r * ld + i); };
+        const float mu0 = row(kRowMu), mu1 = row(kRowMu + 1), mu2 = row(kRowMu + 2);
+        // t = W mu + t_wc (splat.hpp:292)
+        const float t0 = fadd(dot3(vp.R[0], vp.R[1], vp.R[2], mu0, mu1, mu2), vp.t[0]);
+        const float t1 = fadd(dot3(vp.R[3], vp.R[4], vp.R[5], mu0, mu1, mu2), vp.t[1]);
+        const float t2 = fadd(dot3(vp.R[6], vp.R[7], vp.R[8], mu0, mu1, mu2), vp.t[2]);
+        bool visible = t2 > ro.near_plane;  // splat.hpp:293
+        float mx = 0, my = 0, c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+        float q[4] = {row(kRowRot), row(kRowRot + 1), row(kRowRot + 2), row(kRowRot + 3)};
+        float r[9];
+        const bool qok = rotation_from_quat(q, r);
+        if (visible && !qok) {  // math.hpp:36-37 throws only for projected splats
+            atomicMin(vb.err_index, i);
+            visible = false;
+        }
+        const float s0 = glibc_expf(row(kRowLogScale)), s1 = glibc_expf(row(kRowLogScale + 1)),
+                    s2 = glibc_expf(row(kRowLogScale + 2));
+        if (visible) {
+            mx = fadd(fdiv(fmul(vp.fx, t0), t2), vp.cx);  // splat.hpp:299
+            my = fadd(fdiv(fmul(vp.fy, t1), t2), vp.cy);
+            // perspective_jacobian (splat.hpp:276-282)
+            const float iz = fdiv(1.0f, t2);
+            const float J[6] = {fmul(vp.fx, iz), 0.0f, fmul(fmul(fmul(-vp.fx, t0), iz), iz),
+                                0.0f, fmul(vp.fy, iz), fmul(fmul(fmul(-vp.fy, t1), iz), iz)};
+            float V[6];  // V = J * W  (2x3)
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 3; ++b)
+                    V[a * 3 + b] = sum3(fmul(J[a * 3 + 0], vp.R[0 * 3 + b]), fmul(J[a * 3 + 1], vp.R[1 * 3 + b]),
+                                        fmul(J[a * 3 + 2], vp.R[2 * 3 + b]));
+            // covariance3d (splat.hpp:245-250): M = R diag(s), Sigma = M M^T
+            const float sc[3] = {s0, s1, s2};
+            float M[9];
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) M[a * 3 + b] = fmul(r[a * 3 + b], sc[b]);
+            float S[9];
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    S[a * 3 + b] = sum3(fmul(M[a * 3 + 0], M[b * 3 + 0]), fmul(M[a * 3 + 1], M[b * 3 + 1]),
+                                        fmul(M[a * 3 + 2], M[b * 3 + 2]));
+            float VS[6];  // (V Sigma), evaluated before the outer product (Eigen nested-product rule)
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 3; ++b)
+                    VS[a * 3 + b] = sum3(fmul(V[a * 3 + 0], S[0 * 3 + b]), fmul(V[a * 3 + 1], S[1 * 3 + b]),
+                                         fmul(V[a * 3 + 2], S[2 * 3 + b]));
+            float C2[4];
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b)
+                    C2[a * 2 + b] = sum3(fmul(VS[a * 3 + 0], V[b * 3 + 0]), fmul(VS[a * 3 + 1], V[b * 3 + 1]),
+                                         fmul(VS[a * 3 + 2], V[b * 3 + 2]));
+            c00 = fadd(C2[0], ro.cov_reg);
+            c01 = C2[1];
+            c10 = C2[2];
+            c11 = fadd(C2[3], ro.cov_reg);
+            const float rx = fmul(ro.trunc, fsqrt(c00)), ry = fmul(ro.trunc, fsqrt(c11));
+            // splat.hpp:311-313 cull against the image rectangle
+            if (fadd(mx, rx) < 0.0f || fsub(mx, rx) > (float)vp.width || fadd(my, ry) < 0.0f ||
+                fsub(my, ry) > (float)vp.height)
+                visible = false;
+            if (visible) {
+                const float det = fsub(fmul(c00, c11), fmul(c01, c10));
+                SplatRec rec;
+                rec.mx = mx;
+                rec.my = my;
+                rec.i00 = fdiv(c11, det);
+                rec.i01 = fdiv(-c01, det);
+                rec.i10 = fdiv(-c10, det);
+                rec.i11 = fdiv(c00, det);
+                // tile rectangle (raster.hpp:117-121): C++ truncating int division, then clamp
+                const int x0 = clampi(x86_float_to_int(floorf(fsub(mx, rx))) / kTileSize, 0, vp.tiles_x - 1);
+                const int x1 = clampi(x86_float_to_int(floorf(fadd(mx, rx))) / kTileSize, 0, vp.tiles_x - 1);
+                const int y0 = clampi(x86_float_to_int(floorf(fsub(my, ry))) / kTileSize, 0, vp.tiles_y - 1);
+                const int y1 = clampi(x86_float_to_int(floorf(fadd(my, ry))) / kTileSize, 0, vp.tiles_y - 1);
+                vb.rect[2 * (size_t)i] = (uint32_t)x0 | ((uint32_t)x1 << 16);
+                vb.rect[2 * (size_t)i + 1] = (uint32_t)y0 | ((uint32_t)y1 << 16);
+                vb.counts[i] = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+                // SH colour toward the camera centre (splat.hpp:315-317)
+                const float v0 = fsub(mu0, vp.o[0]), v1 = fsub(mu1, vp.o[1]), v2 = fsub(mu2, vp.o[2]);
+                const float n2 = dot3(v0, v1, v2, v0, v1, v2);
+                float dir[3] = {v0, v1, v2};
+                if (n2 > 0.0f) {
+                    const float sn = fsqrt(n2);
+                    dir[0] = fdiv(v0, sn);
+                    dir[1] = fdiv(v1, sn);
+                    dir[2] = fdiv(v2, sn);
+                }
+                int stored_deg = sh_coeffs == 16 ? 3 : (sh_coeffs == 9 ? 2 : (sh_coeffs == 4 ? 1 : 0));
+                const int deg = ro.sh_degree < 0 ? stored_deg : (ro.sh_degree < stored_deg ? ro.sh_degree : stored_deg);
+                float b[16];
+                sh_basis(dir, deg, b);
+                const int nb = (deg + 1) * (deg + 1);
+                float col[3] = {0.5f, 0.5f, 0.5f};
+                for (int k = 0; k < nb; ++k)
+                    for (int ch = 0; ch < 3; ++ch) col[ch] = fadd(col[ch], fmul(b[k], row(kRowSh + 3 * k + ch)));
+                rec.cr = col[0] < 0.0f ? 0.0f : col[0];  // cwiseMax(0) = std::max(c, 0)
+                rec.cg = col[1] < 0.0f ? 0.0f : col[1];
+                rec.cb = col[2] < 0.0f ? 0.0f : col[2];
+                rec.alpha = sigmoidf_exact(row(kRowOpacity));
+                float smax = s0;  // Vec3::maxCoeff (first maximum)
+                if (s1 > smax) smax = s1;
+                if (s2 > smax) smax = s2;
+                const float wr = fmul(ro.trunc, smax);  // splat.hpp:319
+                rec.d2 = fmul(wr, wr);
+                rec.mux = mu0;
+                rec.muy = mu1;
+                rec.muz = mu2;
+                rec.id = ids32[i];
+                rec.range = fsqrt(n2);
+                vb.recs[i] = rec;
+                vb.rkey[i] = f2u(rec.range);
+                dmax_local = wr;
+            }
+        }
+        if (!visible) {
+            vb.counts[i] = 0;
+            vb.rkey[i] = 0xffffffffu;
+        }
+    }
+    // block max of D over visible members -> one atomic per block
+    __shared__ float s_max[8];
+    float m = dmax_local;
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, s_max[w]);
+        if (m > 0.0f) atomicMax(vb.dmax_bits, __float_as_uint(m));
+    }
+}
+
+}  // namespace
+
+void launch_preprocess(int n, const float* P, size_t ld, int sh_coeffs, const uint32_t* ids32, const ViewParams& vp,
+                       const RenderOpts& ro, const ViewBins& vb, cudaStream_t s) {
+    if (n <= 0) return;
+    k_preprocess<<<(n + 255) / 256, 256, 0, s>>>(n, P, ld, sh_coeffs, ids32, vp, ro, vb);
+}
+
+}  // namespace dgs_b200

@@ -1,0 +1,64 @@
+"""Regenerate the committed golden fixtures from the reference itself.
+
+Runs oracle/_ref/ref_dump (the UNMODIFIED reference headers compiled against
+the Eigen shim, see oracle/Makefile) and stores its outputs here with a
+manifest of the exact arguments.  Needs /root/reference only at build time of
+oracle/_ref (this container); the fixtures themselves travel with the repo.
+"""
+import json
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+REF = HERE.parent.parent / "oracle" / "_ref" / "ref_dump"
+
+SETS = {
+    # C1-style synthetic scene, 2-way KD split, oracle options (stop = 0): contributor lists exact.
+    "g1_synth_kd1_oracle": dict(scene="synth", count=2000, w=64, h=48, n_views=8, seed=11, kd=1, mode="oracle",
+                                view=0, perturb=5),
+    # clustered scene, 4-way split, default options (early termination), another view.
+    "g2_synth_kd2_default": dict(scene="synth", count=1200, clustered=1, w=80, h=64, n_views=8, seed=7, kd=2,
+                                 mode="default", view=3, perturb=9),
+    # tests/test_helpers.hpp random_splats (SH degree 1, large splats), monolithic.
+    "g3_random_kd0_oracle": dict(scene="random", count=60, seed=2, sh_degree=1, w=24, h=24, n_views=4, kd=0,
+                                 mode="oracle", view=1, perturb=3),
+    # non-zero background, 8-way split, default options.
+    "g4_synth_kd3_bg": dict(scene="synth", count=2000, w=48, h=48, n_views=6, seed=23, kd=3, mode="default",
+                            view=2, perturb=4, bg_r=0.2, bg_g=0.5, bg_b=0.9),
+}
+DUMPS = ["save_scene", "dump_table", "dump_orders", "dump_project", "dump_partials", "contributors", "dump_render",
+         "dump_step"]
+
+
+def run(name, args, out):
+    tmp = out / "_npy"
+    tmp.mkdir()
+    argv = [str(REF)] + [f"{k}={v}" for k, v in args.items()] + DUMPS + [f"out={tmp}"]
+    subprocess.run(argv, check=True)
+    arrays = {f.stem: np.load(f) for f in sorted(tmp.glob("*.npy"))}
+    np.savez_compressed(out / "golden.npz", **arrays)
+    shutil.rmtree(tmp)
+    (out / "manifest.json").write_text(json.dumps({"name": name, "args": args, "dumps": DUMPS,
+                                                   "generator": "oracle/_ref/ref_dump"}, indent=1))
+
+
+def main():
+    if not REF.exists():
+        sys.exit("build oracle/_ref first: make -C oracle ref")
+    only = sys.argv[1:]
+    for name, args in SETS.items():
+        if only and name not in only:
+            continue
+        out = HERE / name
+        shutil.rmtree(out, ignore_errors=True)
+        out.mkdir(parents=True)
+        run(name, args, out)
+        print(name, sum(f.stat().st_size for f in out.iterdir()) // 1024, "KiB")
+
+
+if __name__ == "__main__":
+    main()
