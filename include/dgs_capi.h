@@ -184,6 +184,10 @@ int dgs_merge_backward(dgs_ctx* ctx, const dgs_camera* cam, const float* partial
  * into `grads` (arrays of the dgs_splats layout; id may be NULL). */
 int dgs_render_partial_backward(dgs_ctx* ctx, int32_t k, const dgs_camera* cam, const float* grad_ct,
                                 dgs_splats* grads);
+/* Pixel-space adjoints (Splat2DGrad, splat.hpp:341-347) of the last
+ * dgs_render_partial_backward: n x 9 = d_mean2d(2), d_cov2d(00, 01, 11),
+ * d_color(3), d_alpha (debug / parity). */
+int dgs_dump_pixel_grads(dgs_ctx* ctx, int32_t k, float* out);
 /* apply_step (worker.hpp:162-167) with the given gradients (GradBuffers
  * layout); advances the subset's Adam step. */
 int dgs_adam_apply(dgs_ctx* ctx, int32_t k, const dgs_splats* grads);

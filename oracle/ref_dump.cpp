@@ -547,6 +547,33 @@ int main(int argc, char** argv) {
                 save_npy(t + "dT", per[k].d_transmittance.data, {std::size_t(cam.height), std::size_t(cam.width)});
                 GradBuffers<Real> g = partial_render_backward<Real>(members[k], table.subspaces[k], cam,
                                                                     per[k].d_color, per[k].d_transmittance, opts);
+                if (has("dump_g2d")) {
+                    // Pixel-space adjoints per projected splat, accumulated in plain
+                    // pixel order (raster.hpp:267-305 without the 16-chunk split).
+                    const auto scene = detail::project_scene<Real>(members[k], cam, opts);
+                    std::vector<Splat2DGrad<Real>> pg(scene.splats2d.size());
+                    std::vector<detail::Contribution<Real>> contribs;
+                    std::vector<Real> prefix;
+                    const detail::SubspaceGate<Real> gate{&table.subspaces[k], opts.indicator_enabled};
+                    for (int y = 0; y < cam.height; ++y)
+                        for (int x = 0; x < cam.width; ++x) {
+                            const Vec3<Real> gc = per[k].d_color.rgb(y, x);
+                            const Real gtv = per[k].d_transmittance.at(y, x, 0);
+                            if (gc.isZero() && gtv == Real(0)) continue;
+                            const Ray<Real> ray = pixel_ray(cam, x, y);
+                            const Vec2<Real> pix{Real(x) + Real(0.5), Real(y) + Real(0.5)};
+                            detail::collect_contributions(scene, scene.candidates(x, y), ray, pix, opts, gate, contribs);
+                            detail::composite_ray_backward<Real>(contribs, scene, opts, pix, gc, gtv, pg, prefix);
+                        }
+                    std::vector<Real> g2(pg.size() * 9);
+                    for (std::size_t p = 0; p < pg.size(); ++p) {
+                        const auto& q = pg[p];
+                        const Real v[9] = {q.d_mean2d[0], q.d_mean2d[1], q.d_cov2d(0, 0), q.d_cov2d(0, 1), q.d_cov2d(1, 1),
+                                           q.d_color[0], q.d_color[1], q.d_color[2], q.d_alpha};
+                        for (int f = 0; f < 9; ++f) g2[p * 9 + f] = v[f];
+                    }
+                    save_npy(t + "g2d", g2, {pg.size(), 9});
+                }
                 save_grads(t + "grad_", g);
                 // worker.hpp:162-167 apply_step with fresh moments.
                 std::vector<Splat<Real>> upd = members[k];

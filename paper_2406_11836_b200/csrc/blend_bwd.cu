@@ -82,9 +82,11 @@ __device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint
 
 /// Per-pixel backward state.
 struct PixState {
-    float T, a0, a1, a2;   // replayed transmittance and running prefix colour
+    float T;                 // replayed transmittance (bitwise the forward's sequence)
+    double a0, a1, a2;       // running prefix sum of c*sigma*A (double, as the forward's D)
     float gc0, gc1, gc2, gT;
-    float Cf0, Cf1, Cf2, Tf;
+    double Cf0, Cf1, Cf2;    // total sum from the forward (double)
+    float Tf;
     float pxf, pyf;
 };
 
@@ -95,15 +97,18 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
                                                   float v[9]) {
     const float a_i = ps.T;
     const float w = fmul(sigma, a_i);
-    ps.a0 = fadd(ps.a0, fmul(D.x, w));
-    ps.a1 = fadd(ps.a1, fmul(D.y, w));
-    ps.a2 = fadd(ps.a2, fmul(D.z, w));
+    const double wd = (double)sigma * (double)a_i;
+    ps.a0 += (double)D.x * wd;
+    ps.a1 += (double)D.y * wd;
+    ps.a2 += (double)D.z * wd;
     ps.T = fmul(ps.T, fsub(1.0f, sigma));
-    const float one_minus = 1.0f - sigma;
-    const float s0 = ps.Cf0 - ps.a0, s1 = ps.Cf1 - ps.a1, s2 = ps.Cf2 - ps.a2;
-    const float gdc = ps.gc0 * D.x + ps.gc1 * D.y + ps.gc2 * D.z;
-    const float gds = ps.gc0 * s0 + ps.gc1 * s1 + ps.gc2 * s2;
-    const float d_sigma = gdc * a_i - gds / one_minus - ps.gT * ps.Tf / one_minus;
+    // suffix_i = sum_{j>i} c_j sigma_j A_j = C - prefix_i, evaluated in double so
+    // the difference keeps full relative accuracy (raster.hpp:212-224).
+    const double one_minus = 1.0 - (double)sigma;
+    const double s0 = ps.Cf0 - ps.a0, s1 = ps.Cf1 - ps.a1, s2 = ps.Cf2 - ps.a2;
+    const double gdc = (double)ps.gc0 * D.x + (double)ps.gc1 * D.y + (double)ps.gc2 * D.z;
+    const double gds = (double)ps.gc0 * s0 + (double)ps.gc1 * s1 + (double)ps.gc2 * s2;
+    const float d_sigma = (float)(gdc * a_i - gds / one_minus - (double)ps.gT * (double)ps.Tf / one_minus);
     v[5] = ps.gc0 * w;
     v[6] = ps.gc1 * w;
     v[7] = ps.gc2 * w;
@@ -130,6 +135,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
                                                              const uint2* __restrict__ ranges,
                                                              const uint32_t* __restrict__ dmax_bits, float onorm,
                                                              const float4* __restrict__ fwd_ct,
+                                                             const double* __restrict__ fwd_cd,
                                                              const float4* __restrict__ grad_ct,
                                                              const uint8_t* __restrict__ ovf_flag,
                                                              float* __restrict__ g2d, size_t ld2,
@@ -163,7 +169,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
 
     PixState ps;
     ps.T = 1.0f;
-    ps.a0 = ps.a1 = ps.a2 = 0.0f;
+    ps.a0 = ps.a1 = ps.a2 = 0.0;
     ps.pxf = pr.pxf;
     ps.pyf = pr.pyf;
     bool done = !inside;
@@ -174,9 +180,9 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
         ps.gc1 = g.y;
         ps.gc2 = g.z;
         ps.gT = g.w;
-        ps.Cf0 = f.x;
-        ps.Cf1 = f.y;
-        ps.Cf2 = f.z;
+        ps.Cf0 = fwd_cd[3 * pix];
+        ps.Cf1 = fwd_cd[3 * pix + 1];
+        ps.Cf2 = fwd_cd[3 * pix + 2];
         ps.Tf = f.w;
         const float e = ro.grad_skip_eps;
         const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
@@ -368,9 +374,9 @@ constexpr int FB = 16;
 
 __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate, const SplatRec* __restrict__ recs,
                                      const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
-                                     const float4* __restrict__ fwd_ct, const float4* __restrict__ grad_ct,
-                                     const uint32_t* __restrict__ ovf_list, uint32_t n_ovf, float* __restrict__ g2d,
-                                     size_t ld2) {
+                                     const float4* __restrict__ fwd_ct, const double* __restrict__ fwd_cd,
+                                     const float4* __restrict__ grad_ct, const uint32_t* __restrict__ ovf_list,
+                                     uint32_t n_ovf, float* __restrict__ g2d, size_t ld2) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= n_ovf) return;
     const uint32_t pix = ovf_list[w];
@@ -382,7 +388,7 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
     pr.pyf = fadd((float)py, 0.5f);
     PixState ps;
     ps.T = 1.0f;
-    ps.a0 = ps.a1 = ps.a2 = 0.0f;
+    ps.a0 = ps.a1 = ps.a2 = 0.0;
     ps.pxf = pr.pxf;
     ps.pyf = pr.pyf;
     const float4 gg = grad_ct[pix], ff = fwd_ct[pix];
@@ -390,9 +396,9 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
     ps.gc1 = gg.y;
     ps.gc2 = gg.z;
     ps.gT = gg.w;
-    ps.Cf0 = ff.x;
-    ps.Cf1 = ff.y;
-    ps.Cf2 = ff.z;
+    ps.Cf0 = fwd_cd[3 * (size_t)pix];
+    ps.Cf1 = fwd_cd[3 * (size_t)pix + 1];
+    ps.Cf2 = fwd_cd[3 * (size_t)pix + 2];
     ps.Tf = ff.w;
     const float e = ro.grad_skip_eps;
     if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) return;
@@ -453,8 +459,8 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
 }  // namespace
 
 void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
-                      const float4* fwd_ct, const float4* grad_ct, const uint8_t* ovf_flag, float* g2d, size_t ld2,
-                      BlendStats* stats, cudaStream_t s) {
+                      const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
+                      float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
     static bool configured = false;
@@ -463,15 +469,15 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
         configured = true;
     }
     k_blend_bwd<<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits,
-                                                       onorm, fwd_ct, grad_ct, ovf_flag, g2d, ld2, stats);
+                                                       onorm, fwd_ct, fwd_cd, grad_ct, ovf_flag, g2d, ld2, stats);
 }
 
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
-                               const ViewBins& vb, const float4* fwd_ct, const float4* grad_ct,
+                               const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
                                const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s) {
     if (n_ovf == 0) return;
     k_blend_bwd_fallback<<<(n_ovf + 63) / 64, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
-                                                          grad_ct, ovf_list, n_ovf, g2d, ld2);
+                                                          fwd_cd, grad_ct, ovf_list, n_ovf, g2d, ld2);
 }
 
 }  // namespace dgs_b200

@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                                                              uint32_t* __restrict__ ovf_count,
                                                              uint32_t* __restrict__ dbg_ids,
                                                              uint32_t* __restrict__ dbg_cnt, int dbg_cap,
-                                                             BlendStats* __restrict__ stats) {
+                                                             BlendStats* __restrict__ stats,
+                                                             double* __restrict__ out_cd) {
     extern __shared__ float4 smem4[];
     float4* sA = smem4;
     float4* sB = sA + kBlendThreads;
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     const float dmax = __uint_as_float(*dmax_bits);
 
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+    double D0 = 0.0, D1 = 0.0, D2 = 0.0;  // exact-ish sum of c*sigma*A for the backward suffix
     bool done = !inside, ovf = false;
     int head = 0, cnt = 0, nemit = 0;
     float head_t = kInf;
@@ -134,6 +136,12 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         C0 = fadd(C0, fmul(bc0[sl][tid], w));
         C1 = fadd(C1, fmul(bc1[sl][tid], w));
         C2 = fadd(C2, fmul(bc2[sl][tid], w));
+        if (out_cd != nullptr) {
+            const double wd = (double)sg * (double)T;
+            D0 += (double)bc0[sl][tid] * wd;
+            D1 += (double)bc1[sl][tid] * wd;
+            D2 += (double)bc2[sl][tid] * wd;
+        }
         T = fmul(T, fsub(1.0f, sg));
         if (dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][tid];
         ++nemit;
@@ -209,6 +217,11 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         } else {
             ovf_flag[pix] = 0;
             out_ct[pix] = make_float4(C0, C1, C2, T);
+            if (out_cd != nullptr) {
+                out_cd[3 * pix] = D0;
+                out_cd[3 * pix + 1] = D1;
+                out_cd[3 * pix + 2] = D2;
+            }
             if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
         }
     }
@@ -236,7 +249,7 @@ __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
                                      const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
                                      float4* __restrict__ out_ct, const uint32_t* __restrict__ ovf_list,
                                      uint32_t n_ovf, uint32_t* __restrict__ dbg_ids, uint32_t* __restrict__ dbg_cnt,
-                                     int dbg_cap) {
+                                     int dbg_cap, double* __restrict__ out_cd) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= n_ovf) return;
     const uint32_t pix = ovf_list[w];
@@ -248,6 +261,7 @@ __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
     pr.pyf = fadd((float)py, 0.5f);
     const uint2 rg = ranges[tile];
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+    double D0 = 0.0, D1 = 0.0, D2 = 0.0;
     float wt = -kInf;
     uint32_t wid = 0;
     bool have_w = false, done = false;
@@ -291,6 +305,10 @@ __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
             C0 = fadd(C0, fmul(c0[k], wgt));
             C1 = fadd(C1, fmul(c1[k], wgt));
             C2 = fadd(C2, fmul(c2[k], wgt));
+            const double wd = (double)bs[k] * (double)T;
+            D0 += (double)c0[k] * wd;
+            D1 += (double)c1[k] * wd;
+            D2 += (double)c2[k] * wd;
             T = fmul(T, fsub(1.0f, bs[k]));
             if (dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[(size_t)pix * dbg_cap + nemit] = bi[k];
             ++nemit;
@@ -303,6 +321,11 @@ __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
         }
     }
     out_ct[pix] = make_float4(C0, C1, C2, T);
+    if (out_cd != nullptr) {
+        out_cd[3 * (size_t)pix] = D0;
+        out_cd[3 * (size_t)pix + 1] = D1;
+        out_cd[3 * (size_t)pix + 2] = D2;
+    }
     if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
 }
 
@@ -310,7 +333,8 @@ __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
 
 void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       float4* out_ct, uint8_t* ovf_flag, uint32_t* ovf_list, uint32_t* ovf_count,
-                      uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, cudaStream_t s) {
+                      uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, double* out_cd,
+                      cudaStream_t s) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
     const size_t smem = kFwdSmem;
@@ -321,15 +345,15 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
     }
     k_blend_fwd<<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits, onorm,
                                                 out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids, dbg_cnt, dbg_cap,
-                                                stats);
+                                                stats, out_cd);
 }
 
 void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                                float4* out_ct, const uint32_t* ovf_list, uint32_t n_ovf, uint32_t* dbg_ids,
-                               uint32_t* dbg_cnt, int dbg_cap, cudaStream_t s) {
+                               uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s) {
     if (n_ovf == 0) return;
     k_blend_fwd_fallback<<<(n_ovf + 63) / 64, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, out_ct,
-                                                          ovf_list, n_ovf, dbg_ids, dbg_cnt, dbg_cap);
+                                                          ovf_list, n_ovf, dbg_ids, dbg_cnt, dbg_cap, out_cd);
 }
 
 }  // namespace dgs_b200

@@ -95,6 +95,7 @@ struct ViewSlot {
     DevBuf<uint2> ranges;
     DevBuf<uint8_t> temp, ovf_flag;
     DevBuf<float4> ct, grad_ct;
+    DevBuf<double> cd;  // double colour sums for the backward suffix
     int64_t pair_cap = 0;
     size_t temp_bytes = 0;
     ViewBins vb;
@@ -247,6 +248,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vs.sort_vals_alt.ensure(n);
     vs.scan.ensure(n);
     vs.ct.ensure(px);
+    vs.cd.ensure(3 * px);
     vs.ovf_flag.ensure(px);
     vs.ovf_list.ensure(px);
     vs.ovf_count.ensure(1);
@@ -284,13 +286,13 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     CK(cudaStreamSynchronize(ctx.stream));
     if (err != INT_MAX) throw std::domain_error("zero quaternion");
     launch_blend_fwd(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_flag.p, vs.ovf_list.p, vs.ovf_count.p,
-                     dbg_ids, dbg_cnt, dbg_cap, stats, ctx.stream);
+                     dbg_ids, dbg_cnt, dbg_cap, stats, vs.cd.p, ctx.stream);
     ++ctx.launches;
     CK(cudaMemcpyAsync(&vs.n_ovf, vs.ovf_count.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
     CK(cudaStreamSynchronize(ctx.stream));
     if (vs.n_ovf > 0) {
         launch_blend_fwd_fallback(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_list.p, vs.n_ovf, dbg_ids,
-                                  dbg_cnt, dbg_cap, ctx.stream);
+                                  dbg_cnt, dbg_cap, vs.cd.p, ctx.stream);
         ++ctx.launches;
     }
 }
@@ -301,12 +303,12 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     ViewSlot& vs = S.slot(v);
     S.g2d.ensure(9 * S.ld);
     CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
-    launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.grad_ct.p, vs.ovf_flag.p, S.g2d.p, S.ld,
-                     stats, ctx.stream);
+    launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, S.g2d.p,
+                     S.ld, stats, ctx.stream);
     ++ctx.launches;
     if (vs.n_ovf > 0) {
-        launch_blend_bwd_fallback(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.grad_ct.p, vs.ovf_list.p,
-                                  vs.n_ovf, S.g2d.p, S.ld, ctx.stream);
+        launch_blend_bwd_fallback(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p,
+                                  vs.ovf_list.p, vs.n_ovf, S.g2d.p, S.ld, ctx.stream);
         ++ctx.launches;
     }
 }
@@ -710,6 +712,17 @@ int dgs_render_partial_backward(dgs_ctx* ctx, int32_t k, const dgs_camera* cam, 
                            ctx->bad.p, ctx->stream);
         check_bad(*ctx, S);
         download_fields(*ctx, S, S.G.p, grads);
+    });
+}
+
+int dgs_dump_pixel_grads(dgs_ctx* ctx, int32_t k, float* out) {
+    return dgs_guard([&] {
+        SubsetState& S = subset(*ctx, k);
+        if (S.g2d.p == nullptr) throw std::invalid_argument("no backward has run for this subset");
+        std::vector<float> h(9 * S.ld);
+        CK(cudaMemcpy(h.data(), S.g2d.p, h.size() * 4, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < S.n; ++i)
+            for (int f = 0; f < 9; ++f) out[i * 9 + f] = h[(size_t)f * S.ld + i];
     });
 }
 

@@ -47,17 +47,19 @@ struct BlendStats {
 // K4: forward alpha blend with the RetinaGS subspace gate, exact per-ray (t, id) order.
 void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       float4* out_ct, uint8_t* ovf_flag, uint32_t* ovf_list, uint32_t* ovf_count,
-                      uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, cudaStream_t s);
+                      uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, double* out_cd,
+                      cudaStream_t s);
 void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                                float4* out_ct, const uint32_t* ovf_list, uint32_t n_ovf, uint32_t* dbg_ids,
-                               uint32_t* dbg_cnt, int dbg_cap, cudaStream_t s);
+                               uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s);
 
 // K8: backward blend; accumulates 9 pixel-space adjoints per member into g2d (SoA [9][ld2]).
+// fwd_cd: the forward's double-precision colour sums (suffix = C - prefix without cancellation loss).
 void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
-                      const float4* fwd_ct, const float4* grad_ct, const uint8_t* ovf_flag, float* g2d, size_t ld2,
-                      BlendStats* stats, cudaStream_t s);
+                      const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
+                      float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s);
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
-                               const ViewBins& vb, const float4* fwd_ct, const float4* grad_ct,
+                               const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
                                const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s);
 
 // K3/K5: per-pixel subset order + merge (engine.hpp:108-182). Rows [row0, row1).

@@ -285,6 +285,12 @@ class Context:
         check(lib().dgs_render_partial_backward(self._h, k, C.byref(cam), ptr(grad_ct), C.byref(gc)))
         return g
 
+    def dump_pixel_grads(self, k: int) -> np.ndarray:
+        n = lib().dgs_subset_size(self._h, k)
+        out = np.zeros((n, 9), np.float32)
+        check(lib().dgs_dump_pixel_grads(self._h, k, ptr(out)))
+        return out
+
     def adam_apply(self, k: int, grads: Splats):
         gc = grads.c()
         check(lib().dgs_adam_apply(self._h, k, C.byref(gc)))

@@ -74,3 +74,40 @@ def rel_err(got, want, floor=1e-8):
     got = np.asarray(got, np.float64)
     want = np.asarray(want, np.float64)
     return np.abs(got - want) / np.maximum(np.maximum(np.abs(got), np.abs(want)), floor)
+
+
+# Float-atomic accumulation order differs from the reference's chunked
+# sequential sums: gradient entries whose magnitude is below
+# NOISE_FLOOR x (max |g| of that field in that subset) are cancellation-
+# dominated and are compared absolutely at that floor instead of relatively.
+NOISE_FLOOR = 1e-3
+GRAD_RTOL = 1e-3
+
+
+def grad_errors(got, want, floor_frac=NOISE_FLOOR):
+    want = np.asarray(want, np.float64)
+    scale = float(np.abs(want).max()) if want.size else 0.0
+    return rel_err(got, want, floor=max(floor_frac * scale, 1e-30))
+
+
+def adam_lr_rows(cfg, sh_coeffs):
+    """Per-parameter learning rates in GradBuffers field order (optim.hpp:104-126) at step 1."""
+    return {"mu": cfg.lr_position_start, "log_scale": cfg.lr_scale, "rotation": cfg.lr_rotation,
+            "opacity_logit": cfg.lr_opacity,
+            "sh": np.array([cfg.lr_sh_dc] + [cfg.lr_sh_rest] * (sh_coeffs - 1))[:, None]}
+
+
+def post_adam_ok(got, want, grad_ref, lr, rtol=GRAD_RTOL, floor_frac=NOISE_FLOOR):
+    """Post-Adam parameters: rel_err <= rtol where the reference gradient is above
+    the noise floor; elsewhere Adam's normalised step may take the other sign,
+    so |delta| <= 2 lr + rtol |want| (optim.hpp:90-97: the first step is +-lr)."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    g = np.abs(np.asarray(grad_ref, np.float64))
+    scale = g.max() if g.size else 0.0
+    noisy = g <= floor_frac * scale
+    lr = np.broadcast_to(np.asarray(lr, np.float64), want.shape)
+    e = rel_err(got, want)
+    ok_strict = (e <= rtol) | noisy
+    ok_noisy = (~noisy) | (np.abs(got - want) <= 2.0 * lr * (1 + 1e-3) + rtol * np.abs(want))
+    return ok_strict & ok_noisy, e, noisy

@@ -31,7 +31,7 @@ SETS = {
                             view=2, perturb=4, bg_r=0.2, bg_g=0.5, bg_b=0.9),
 }
 DUMPS = ["save_scene", "dump_table", "dump_orders", "dump_project", "dump_partials", "contributors", "dump_render",
-         "dump_step"]
+         "dump_step", "dump_g2d"]
 
 
 def run(name, args, out):

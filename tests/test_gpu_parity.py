@@ -14,7 +14,7 @@ compared bit for bit.
 import numpy as np
 import pytest
 
-from conftest import Golden, rel_err
+from conftest import GRAD_RTOL, Golden, adam_lr_rows, grad_errors, post_adam_ok, rel_err
 from paper_2406_11836_b200 import engine
 
 pytestmark = pytest.mark.gpu
@@ -143,8 +143,8 @@ def test_partial_backward_gradients(golden):
         for f in GRAD_FIELDS:
             want = g[f"k{k}_grad_{f}"]
             a = getattr(got, f[2:]).reshape(want.shape)
-            e = rel_err(a, want)
-            assert e.max() <= 1e-3, (k, f, float(e.max()), np.unravel_index(e.argmax(), e.shape))
+            e = grad_errors(a, want)
+            assert e.max() <= GRAD_RTOL, (k, f, float(e.max()), np.unravel_index(e.argmax(), e.shape))
     ctx.close()
 
 
@@ -174,11 +174,12 @@ def test_full_train_step_matches_reference(golden):
     cam = g.camera()
     res = mgr.train_step([cam], g["step_target"][None], g.bg)
     assert abs(res["loss"] - float(g["step_loss"][0])) <= 1e-4 * max(1.0, abs(float(g["step_loss"][0])))
+    lrs = adam_lr_rows(cfg, s.sh_coeffs)
     for k in range(g.subsets()):
         p, _, _, step = mgr.ctx.store_subset(k, s.sh_coeffs)
         assert step == 1
         for f in PARAM_FIELDS:
             want = g[f"k{k}_adam_{f}"]
-            e = rel_err(getattr(p, f).reshape(want.shape), want)
-            assert e.max() <= 1e-3, (k, f, float(e.max()))
+            ok, e, noisy = post_adam_ok(getattr(p, f).reshape(want.shape), want, g[f"k{k}_grad_d_{f}"], lrs[f])
+            assert ok.all(), (k, f, float(e[~noisy].max()) if (~noisy).any() else 0.0, int((~ok).sum()))
     mgr.close()
