@@ -424,6 +424,7 @@ int main(int argc, char** argv) {
         std::filesystem::create_directories(g_out);
 
         // ---- scene -------------------------------------------------------
+        const double t_setup0 = now_s();
         std::vector<Splat<Real>> splats;
         std::vector<Camera<Real>> cams;
         const std::string scene = arg("scene", "synth");
@@ -491,6 +492,8 @@ int main(int argc, char** argv) {
 
         if (cams.empty()) return 0;
         const Camera<Real>& cam = cams.at(view);
+        if (has("time_direct") || has("time_step"))
+            std::printf("{\"setup_s\": %.3f, \"splats\": %zu}\n", now_s() - t_setup0, splats.size());
 
         if (has("dump_orders")) {
             const PixelOrders po = compute_pixel_orders(table, cam);
@@ -589,13 +592,68 @@ int main(int argc, char** argv) {
             }
         }
 
+        // ---- timed direct-call train step (CPU baseline) --------------------
+        // The sequence of Manager<float>::train_step (manager.hpp:313-386) and
+        // the worker side (worker.hpp:62-167) for every subset on this host,
+        // without the message-passing copies: partial_render per subset,
+        // compute_pixel_orders, merge, loss, merge_backward,
+        // partial_render_backward and apply_step (adam over every member).
+        if (has("time_direct")) {
+            TrainConfig cfg;
+            cfg.kd_depth = depth;
+            Image<Real> target(cam.width, cam.height, 3);
+            if (has("target") && arg("target", "") != "zeros") target.data = load_npy<Real>(arg("target", ""));
+            std::vector<std::vector<AdamMoments<Real>>> moments(table.subset_count());
+            std::vector<std::vector<Splat<Real>>> mem = members;
+            for (int k = 0; k < table.subset_count(); ++k)
+                for (const auto& sp : mem[k]) moments[k].push_back(AdamMoments<Real>::like(sp));
+            const int steps = int(iarg("time_direct", 1));
+            const double budget = farg("budget_s", 1e30);
+            double total = 0.0;
+            std::uint64_t adam_step = 0;
+            for (int st = 0; st < steps; ++st) {
+                const double t0 = now_s();
+                std::vector<PartialImage<Real>> partials;
+                for (int k = 0; k < table.subset_count(); ++k)
+                    partials.push_back(partial_render<Real>(mem[k], table.subspaces[k], cam, opts));
+                const double t1 = now_s();
+                const PixelOrders orders = compute_pixel_orders(table, cam);
+                const RenderedImage<Real> img = merge<Real>(partials, orders, bg);
+                LossResult<Real> l = loss<Real>(img.color, target, cfg.lambda_ssim);
+                const Real mse_v = mse<Real>(img.color, target);
+                const Image<Real> gt0(cam.width, cam.height, 1, Real(0));
+                auto per = merge_backward<Real>(partials, orders, l.grad, gt0, bg);
+                const double t2 = now_s();
+                for (int k = 0; k < table.subset_count(); ++k) {
+                    GradBuffers<Real> g = partial_render_backward<Real>(mem[k], table.subspaces[k], cam,
+                                                                        per[k].d_color, per[k].d_transmittance, opts);
+                    const double lr_pos = position_lr(cfg, adam_step);
+                    for (std::size_t i = 0; i < mem[k].size(); ++i)
+                        adam_apply(mem[k][i], g, i, moments[k][i], cfg, lr_pos, adam_step + 1);
+                }
+                ++adam_step;
+                const double t3 = now_s();
+                total += t3 - t0;
+                std::printf("{\"step\": %d, \"seconds\": %.6f, \"forward_s\": %.6f, \"merge_loss_s\": %.6f, "
+                            "\"backward_adam_s\": %.6f, \"loss\": %.9g, \"mse\": %.9g, \"threads\": %u}\n",
+                            st, t3 - t0, t1 - t0, t2 - t1, t3 - t2, (double)l.value, (double)mse_v, hardware_threads());
+                std::fflush(stdout);
+                if (total > budget) break;
+            }
+        }
+
         // ---- timed Manager<float>::train_step (CPU baseline) ---------------
         if (has("time_step")) {
             TrainConfig cfg;
             cfg.kd_depth = depth;
             cfg.batch_size = 1;
             Image<Real> target;
-            {
+            if (arg("target", "") == "zeros") {
+                target = Image<Real>(cam.width, cam.height, 3);
+            } else if (has("target")) {
+                target = Image<Real>(cam.width, cam.height, 3);
+                target.data = load_npy<Real>(arg("target", ""));
+            } else {
                 std::vector<Splat<Real>> gt = gt_splats;
                 if (has("target_scene_dir")) gt = load_splats(arg("target_scene_dir", ""));
                 const double t0 = now_s();

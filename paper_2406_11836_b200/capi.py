@@ -117,9 +117,14 @@ _SIGS = {
     "dgs_train_step": (C.c_int, [_P, C.c_int32, C.POINTER(Camera), _P, C.c_int32, _P, C.POINTER(StepResult)]),
     "dgs_upload_targets": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
     "dgs_render": (C.c_int, [_P, C.POINTER(Camera), _P, _P, _P]),
+    "dgs_set_profiling": (C.c_int, [_P, C.c_int32]),
+    "dgs_stage_times": (C.c_int, [_P, _P, _P]),
     "dgs_stream": (_P, [_P]),
     "dgs_sync": (C.c_int, [_P]),
 }
+
+STAGES = ("preprocess", "binning", "blend_fwd", "merge", "loss", "merge_bwd", "blend_bwd", "project_bwd_adam",
+          "exchange")
 
 _lib = None
 

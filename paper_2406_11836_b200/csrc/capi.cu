@@ -120,8 +120,73 @@ struct SubsetState {
     }
 };
 
+/// Event pairs around every stage launch, resolved at the next sync point.
+struct StageTimer {
+    static constexpr int kStages = 9;
+    bool on = false;
+    double ms[kStages] = {};
+    uint64_t count[kStages] = {};
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        return e;
+    }
+    void resolve() {
+        for (auto& p : pending) {
+            float t = 0.0f;
+            CK(cudaEventSynchronize(p.second.second));
+            CK(cudaEventElapsedTime(&t, p.second.first, p.second.second));
+            ms[p.first] += t;
+            count[p.first] += 1;
+            pool.push_back(p.second.first);
+            pool.push_back(p.second.second);
+        }
+        pending.clear();
+    }
+    ~StageTimer() {
+        for (auto& p : pending) {
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+/// Stage scope: records start/stop events when profiling is on; end() (or
+/// the destructor) closes it.
+struct Stage {
+    StageTimer& t;
+    int id;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    Stage(StageTimer& t_, int id_, cudaStream_t s_) : t(t_), id(id_), s(s_) {
+        if (t.on) {
+            a = t.get();
+            CK(cudaEventRecord(a, s));
+        }
+    }
+    void end() {
+        if (a) {
+            cudaEvent_t b = t.get();
+            cudaEventRecord(b, s);
+            t.pending.push_back({id, {a, b}});
+            a = nullptr;
+        }
+    }
+    ~Stage() { end(); }
+};
+enum { kStPre = 0, kStBin, kStFwd, kStMerge, kStLoss, kStMergeBwd, kStBwd, kStAdam, kStExchange };
+
 struct Ctx {
     int device = 0, rank = 0, world = 1;
+    StageTimer timer;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
     Table table{};
@@ -267,8 +332,12 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     const int int_max = INT_MAX;
     CK(cudaMemcpyAsync(vb.err_index, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));
     CK(cudaMemsetAsync(vs.ovf_count.p, 0, 4, ctx.stream));
-    launch_preprocess((int)n, S.P.p, S.ld, S.sh_coeffs, S.ids32.p, vp, ctx.ro, vb, ctx.stream);
+    {
+        Stage st(ctx.timer, kStPre, ctx.stream);
+        launch_preprocess((int)n, S.P.p, S.ld, S.sh_coeffs, S.ids32.p, vp, ctx.ro, vb, ctx.stream);
+    }
     ++ctx.launches;
+    Stage st_bin(ctx.timer, kStBin, ctx.stream);
     int64_t P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p,
                             vs.sort_vals.p, vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p,
                             ctx.stream);
@@ -281,16 +350,20 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         ctx.launches += 3;
         if (P < 0) throw std::runtime_error("binning: pair buffer sizing failed");
     }
+    st_bin.end();
     int err = INT_MAX;
     CK(cudaMemcpyAsync(&err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
     CK(cudaStreamSynchronize(ctx.stream));
     if (err != INT_MAX) throw std::domain_error("zero quaternion");
+    Stage st_fwd(ctx.timer, kStFwd, ctx.stream);
     launch_blend_fwd(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_flag.p, vs.ovf_list.p, vs.ovf_count.p,
                      dbg_ids, dbg_cnt, dbg_cap, stats, vs.cd.p, ctx.stream);
+    st_fwd.end();
     ++ctx.launches;
     CK(cudaMemcpyAsync(&vs.n_ovf, vs.ovf_count.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
     CK(cudaStreamSynchronize(ctx.stream));
     if (vs.n_ovf > 0) {
+        Stage st(ctx.timer, kStFwd, ctx.stream);
         launch_blend_fwd_fallback(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_list.p, vs.n_ovf, dbg_ids,
                                   dbg_cnt, dbg_cap, vs.cd.p, ctx.stream);
         ++ctx.launches;
@@ -303,6 +376,7 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     ViewSlot& vs = S.slot(v);
     S.g2d.ensure(9 * S.ld);
     CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
+    Stage st(ctx.timer, kStBwd, ctx.stream);
     launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, S.g2d.p,
                      S.ld, stats, ctx.stream);
     ++ctx.launches;
@@ -425,6 +499,29 @@ int dgs_ctx_destroy(dgs_ctx* ctx) {
         ctx->subsets.clear();
         cudaStreamDestroy(ctx->stream);
         delete ctx;
+    });
+}
+
+int dgs_set_profiling(dgs_ctx* ctx, int32_t enabled) {
+    return dgs_guard([&] {
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->timer.resolve();
+        ctx->timer.on = enabled != 0;
+        for (int i = 0; i < StageTimer::kStages; ++i) {
+            ctx->timer.ms[i] = 0.0;
+            ctx->timer.count[i] = 0;
+        }
+    });
+}
+
+int dgs_stage_times(dgs_ctx* ctx, double* ms, uint64_t* counts) {
+    return dgs_guard([&] {
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->timer.resolve();
+        for (int i = 0; i < StageTimer::kStages; ++i) {
+            if (ms) ms[i] = ctx->timer.ms[i];
+            if (counts) counts[i] = ctx->timer.count[i];
+        }
     });
 }
 
@@ -825,8 +922,11 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                                cudaMemcpyHostToDevice, ctx->stream));
             const int owner = table_locate(ctx->table, vp.o);
             ctx->merged.ensure(3 * px);
-            launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v, vp.height, 0,
-                         bg, ctx->merged.p, nullptr, ctx->stream);
+            {
+                Stage st(ctx->timer, kStMerge, ctx->stream);
+                launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v,
+                             vp.height, 0, bg, ctx->merged.p, nullptr, ctx->stream);
+            }
             ++ctx->launches;
             // ---- loss (manager.hpp:331-334) ----
             const float* tgt;
@@ -846,13 +946,20 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             const int max_blocks = ((vp.width + 31) / 32) * ((vp.height + 31) / 32) * 3;
             ctx->block_sums.ensure((size_t)max_blocks * 3);
             int nb = 0;
-            launch_loss(vp.width, vp.height, 0, vp.height, ctx->merged.p, tgt, lam, ensure_kernel(*ctx), inv_batch,
-                        ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
-            launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p + 3 * v, ctx->stream);
+            const float* kern = ensure_kernel(*ctx);
+            {
+                Stage st(ctx->timer, kStLoss, ctx->stream);
+                launch_loss(vp.width, vp.height, 0, vp.height, ctx->merged.p, tgt, lam, kern, inv_batch,
+                            ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
+                launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p + 3 * v, ctx->stream);
+            }
             // ---- merge_backward (engine.hpp:195-234) ----
-            launch_merge_bwd(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v,
-                             vp.height, 0, ctx->grad_rgb.p, bg, ctx->grad_ptrs.p + (size_t)K * v, vp.height, 0,
-                             ctx->stream);
+            {
+                Stage st(ctx->timer, kStMergeBwd, ctx->stream);
+                launch_merge_bwd(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v,
+                                 vp.height, 0, ctx->grad_rgb.p, bg, ctx->grad_ptrs.p + (size_t)K * v, vp.height, 0,
+                                 ctx->stream);
+            }
             ctx->launches += 3;
         }
         // ---- MsgBackwardTask x B, then apply_step (worker.hpp:86-127, 162-167) ----
@@ -867,6 +974,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             for (int v = 0; v < batch; ++v) {
                 ViewSlot& vs = S.slot(v);
                 backward_blend(*ctx, S, v, ctx->stats.p + 1);
+                Stage st(ctx->timer, kStAdam, ctx->stream);
                 if (v + 1 < batch) {
                     launch_project_bwd((int)S.n, S.P.p, S.ld, S.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S.g2d.p,
                                        S.ld, S.G.p, ctx->bad.p, ctx->stream);
@@ -886,6 +994,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         CK(cudaMemcpyAsync(&bad, ctx->bad.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaGetLastError());
+        ctx->timer.resolve();
         if (bad != INT_MAX) {
             // which subset: report the first loaded subset whose id range covers it
             throw std::runtime_error("partial_render_backward: non-finite gradient for splat id " +

@@ -218,6 +218,15 @@ class Context:
     def sync(self):
         check(lib().dgs_sync(self._h))
 
+    def set_profiling(self, on: bool):
+        check(lib().dgs_set_profiling(self._h, int(on)))
+
+    def stage_times(self) -> dict:
+        ms = np.zeros(len(capi.STAGES), np.float64)
+        cnt = np.zeros(len(capi.STAGES), np.uint64)
+        check(lib().dgs_stage_times(self._h, ptr(ms), ptr(cnt)))
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(capi.STAGES)}
+
     def set_table(self, table: PartitionTable):
         self.table = table
         check(lib().dgs_set_table(self._h, table.c_planes(), table.subset_count, table.planes.shape[1]))
