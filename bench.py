@@ -60,6 +60,8 @@ def workload_config(a, world):
         "render_options": "default (per-ray t order, stop 1e-4, 3-sigma, near 0.01)",
         "backward_skip": "exact-zero (grad_skip_eps=0): the reference's Eigen isZero() threshold would skip "
                          "every pixel's backward at 1080p (DESIGN.md)",
+        "optimizer": "dense Adam over every member; deterministic=0 (fast Adam: reciprocal bias corrections, "
+                     "MUFU sqrt/divide, <= few ulp from the reference's IEEE sequence)",
         "l2": "no flush needed: params + Adam moments (7.1 GB) and per-view buffers exceed the 126 MB L2",
         "parallelism": f"kd-model-parallel x{world}",
     }
@@ -189,7 +191,7 @@ def b200_arm(a, world, rank, local_rank):
     target, _ = tmgr.render(cam)
     tmgr.close()
     del gt
-    cfg = engine.train_config(kd_depth=int(math.log2(world)), iterations=30000)
+    cfg = engine.train_config(kd_depth=int(math.log2(world)), iterations=30000, deterministic=0)
     ro = engine.render_options(grad_skip_eps=0.0)
     mgr = engine.Manager(init, cfg, ro, device=local_rank)
     ctx = mgr.ctx

@@ -56,7 +56,8 @@ class TrainConfigC(C.Structure):
                 ("lambda_ssim", C.c_double), ("lr_position_start", C.c_double), ("lr_position_end", C.c_double),
                 ("lr_sh_dc", C.c_double), ("lr_sh_rest", C.c_double), ("lr_opacity", C.c_double),
                 ("lr_scale", C.c_double), ("lr_rotation", C.c_double), ("adam_beta1", C.c_double),
-                ("adam_beta2", C.c_double), ("adam_eps", C.c_double), ("grad_sync", C.c_int32)]
+                ("adam_beta2", C.c_double), ("adam_eps", C.c_double), ("grad_sync", C.c_int32),
+                ("deterministic", C.c_int32)]
 
 
 class Plane(C.Structure):

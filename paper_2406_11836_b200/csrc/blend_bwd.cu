@@ -13,25 +13,22 @@
 // no reverse pass and no T recovery by division (impossible once T
 // underflows in stop=0 mode).
 //
-// Accumulation of the 9 pixel-space adjoints per member: warp-uniform
-// emissions are reduced with a 5-step butterfly, then added into a
-// two-batch shared-memory accumulator window keyed by list position; each
-// retired batch is flushed to HBM with one red.global.add per touched
-// (member, field).  Emissions that fall outside the window go straight to
-// global atomics.  Pixels skipped by the reference rule
-// (gc.isZero() && gT == 0, raster.hpp:285) never emit.
+// Accumulation of the 9 pixel-space adjoints per member: emissions are
+// grouped into warp-uniform sub-rounds (one list position each), reduced with
+// a 5-step butterfly and added by one lane with native red.global.add.f32
+// (shared-memory float atomics are CAS loops on sm_100).  Pixels skipped by
+// the reference rule (gc.isZero() && gT == 0, raster.hpp:285) never emit.
 #include "kernels.h"
 
 namespace dgs_b200 {
 
 namespace {
 
-constexpr int KBUF = 8;
+constexpr int KBUF = 8;  // must equal blend_fwd.cu (identical overflow decisions)
 constexpr float kInf = __builtin_huge_valf();
 constexpr unsigned kFull = 0xffffffffu;
-// staged records (4 float4) + ring (t, id, sigma, g, pos, member) + 2x9 accumulators
-constexpr size_t kBwdSmem = 4 * kBlendThreads * sizeof(float4) + 6 * KBUF * kBlendThreads * sizeof(float) +
-                            2 * 9 * kBlendThreads * sizeof(float);
+// staged records (4 float4) + ring (t, id, sigma, list position)
+constexpr size_t kBwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float);
 
 __device__ __forceinline__ float order_bound(float r, float dmax, float onorm) {
     const float S = 2.0f * onorm + 2.0f * r + 1.0f;
@@ -150,10 +147,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
     Ring* bt = reinterpret_cast<Ring*>(sD + kBlendThreads);
     URing* bid = reinterpret_cast<URing*>(bt + KBUF);
     Ring* bs = reinterpret_cast<Ring*>(bid + KBUF);
-    Ring* bg = bs + KBUF;
-    URing* bpos = reinterpret_cast<URing*>(bg + KBUF);
-    URing* bmem = bpos + KBUF;
-    float* acc = reinterpret_cast<float*>(bmem + KBUF);  // [2][9][256]
+    URing* bpos = reinterpret_cast<URing*>(bs + KBUF);
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int tile = blockIdx.x;
@@ -188,112 +182,90 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
         const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
         if ((gc_zero && g.w == 0.0f) || ovf_flag[pix]) done = true;
     }
-    for (int i = tid; i < 2 * 9 * kBlendThreads; i += kBlendThreads) acc[i] = 0.0f;
 
     int head = 0, cnt = 0, nemit = 0;
     float head_t = kInf;
+    uint32_t head_pos = 0xffffffffu;
     unsigned long long n_eval = 0;
     const uint2 rg = ranges[tile];
-    int batch = -1;
     uint32_t base = rg.x;
     int nb = 0;
 
-    // Add 9 values for list position `pos` (member `mem`).
-    auto add9 = [&](uint32_t pos, uint32_t mem, const float v[9]) {
-        const int eb = (int)((pos - rg.x) >> 8);
-        if (eb >= batch - 1) {
-            float* a = acc + (eb & 1) * 9 * kBlendThreads + ((pos - rg.x) & 255);
-#pragma unroll
-            for (int f = 0; f < 9; ++f)
-                if (v[f] != 0.0f) atomicAdd(a + f * kBlendThreads, v[f]);
-        } else {
-#pragma unroll
-            for (int f = 0; f < 9; ++f)
-                if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
-        }
-    };
-
-    // Warp-converged emission step: every lane emits at most one entry whose
-    // t is below `L`; uniform targets are butterfly-reduced first.
-    auto emission_round = [&](float L) -> bool {
-        const bool ready = !done && cnt > 0 && head_t < L;
-        if (!__any_sync(kFull, ready)) return false;
-        float v[9];
-        int apos = -1;
-        uint32_t amem = 0;
-#pragma unroll
-        for (int f = 0; f < 9; ++f) v[f] = 0.0f;
-        if (ready) {
-            if (ro.stop > 0.0f && ps.T < ro.stop) {  // raster.hpp:205 replay termination
+    // Emit every ready entry (t < L) of every lane, one list position per
+    // sub-round: the warp takes the smallest ready head position, the lanes
+    // holding it pop and compute their adjoints, a butterfly reduces the 9
+    // values and one lane issues native red.global.add.f32.
+    auto emit_ready = [&](float L) {
+        for (;;) {
+            bool ready = !done && cnt > 0 && head_t < L;
+            if (ready && ro.stop > 0.0f && ps.T < ro.stop) {  // raster.hpp:205 replay termination
                 done = true;
                 cnt = 0;
                 head_t = kInf;
-            } else {
+                head_pos = 0xffffffffu;
+                ready = false;
+            }
+            if (!__any_sync(kFull, ready)) return;
+            const uint32_t mine = ready ? head_pos : 0xffffffffu;
+            const uint32_t pmin = __reduce_min_sync(kFull, mine);
+            const bool go = ready && mine == pmin;
+            float v[9];
+#pragma unroll
+            for (int f = 0; f < 9; ++f) v[f] = 0.0f;
+            uint32_t mem = 0;
+            if (go) {
                 const int sl = head & (KBUF - 1);
-                const float sigma = bs[sl][tid], g = bg[sl][tid];
-                const uint32_t pos = bpos[sl][tid], mem = bmem[sl][tid];
+                const float sigma = bs[sl][tid];
+                mem = pair_val[pmin];
                 float4 A, B, C, D;
-                if (pos >= base && pos < base + (uint32_t)nb) {
-                    const int j = (int)(pos - base);
+                if (pmin >= base && pmin < base + (uint32_t)nb) {
+                    const int j = (int)(pmin - base);
                     A = sA[j];
                     B = sB[j];
                     D = sD[j];
                 } else {
                     load_rec(recs, mem, A, B, C, D);
                 }
+                // g = eval_2d at this pixel, recomputed exactly as in eval_candidate
+                const float dx = fsub(pr.pxf, A.x), dy = fsub(pr.pyf, A.y);
+                const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
+                                      fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
+                const float g = __expf(fmul(-0.5f, m2));
                 contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
-                apos = (int)pos;
-                amem = mem;
                 ++nemit;
                 ++head;
                 --cnt;
-                head_t = cnt ? bt[head & (KBUF - 1)][tid] : kInf;
+                const int hs = head & (KBUF - 1);
+                head_t = cnt ? bt[hs][tid] : kInf;
+                head_pos = cnt ? bpos[hs][tid] : 0xffffffffu;
             }
-        }
-        const unsigned act = __ballot_sync(kFull, apos >= 0);
-        if (act == 0) return true;
-        const int lead = __ffs(act) - 1;
-        const int lpos = __shfl_sync(kFull, apos, lead);
-        if (__all_sync(kFull, apos < 0 || apos == lpos)) {
+            const unsigned gm = __ballot_sync(kFull, go);
+            const int leader = __ffs(gm) - 1;
+            if (gm == (1u << leader)) {  // a single lane: no reduction needed
+                if (lane == leader) {
 #pragma unroll
-            for (int f = 0; f < 9; ++f) {
-                float x = v[f];
-                for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
-                v[f] = x;
-            }
-            if (lane == lead) add9((uint32_t)lpos, amem, v);
-        } else if (apos >= 0) {
-            add9((uint32_t)apos, amem, v);
-        }
-        return true;
-    };
-
-    auto flush_slot = [&](int slot_batch) {
-        if (slot_batch < 0) return;
-        float* a = acc + (slot_batch & 1) * 9 * kBlendThreads;
-        const uint32_t pos = rg.x + (uint32_t)slot_batch * kBlendThreads + tid;
-        if (pos < rg.y) {
-            float v[9];
-            bool any = false;
+                    for (int f = 0; f < 9; ++f)
+                        if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+                }
+            } else {
 #pragma unroll
-            for (int f = 0; f < 9; ++f) {
-                v[f] = a[f * kBlendThreads + tid];
-                any |= v[f] != 0.0f;
-                a[f * kBlendThreads + tid] = 0.0f;
-            }
-            if (any) {
-                const uint32_t mem = pair_val[pos];
+                for (int f = 0; f < 9; ++f) {
+                    float x = v[f];
 #pragma unroll
-                for (int f = 0; f < 9; ++f)
-                    if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+                    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
+                    v[f] = x;
+                }
+                if (lane == leader) {
+#pragma unroll
+                    for (int f = 0; f < 9; ++f)
+                        if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+                }
             }
         }
     };
 
     for (base = rg.x; base < rg.y; base += kBlendThreads) {
         if (__syncthreads_count(!done) == 0) break;
-        ++batch;
-        flush_slot(batch - 2);  // retire the window slot this batch reuses
         const uint32_t p = base + tid;
         nb = (int)min((uint32_t)kBlendThreads, rg.y - base);
         if (p < rg.y) {
@@ -307,9 +279,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
         }
         __syncthreads();
         for (int j = 0; j < nb; ++j) {
-            const float L = sD[j].w;
-            while (emission_round(L)) {
-            }
+            emit_ready(sD[j].w);
             if (done) continue;
             const float4 A = sA[j], B = sB[j], C = sC[j];
             ++n_eval;
@@ -320,6 +290,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
                 done = true;
                 continue;
             }
+            const uint32_t lpos = base + (uint32_t)j;
             int pos = head + cnt;
             while (pos > head) {
                 const int pl = (pos - 1) & (KBUF - 1);
@@ -330,9 +301,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
                     bt[psl][tid] = tp;
                     bid[psl][tid] = ip;
                     bs[psl][tid] = bs[pl][tid];
-                    bg[psl][tid] = bg[pl][tid];
                     bpos[psl][tid] = bpos[pl][tid];
-                    bmem[psl][tid] = bmem[pl][tid];
                     --pos;
                 } else {
                     break;
@@ -342,18 +311,15 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
             bt[psl][tid] = t;
             bid[psl][tid] = id;
             bs[psl][tid] = sigma;
-            bg[psl][tid] = g;
-            bpos[psl][tid] = base + (uint32_t)j;
-            bmem[psl][tid] = pair_val[base + j];
+            bpos[psl][tid] = lpos;
             ++cnt;
-            if (pos == head) head_t = t;
+            if (pos == head) {
+                head_t = t;
+                head_pos = lpos;
+            }
         }
     }
-    while (emission_round(kInf)) {
-    }
-    __syncthreads();
-    flush_slot(batch - 1);
-    flush_slot(batch);
+    emit_ready(kInf);
 
     if (stats != nullptr) {
         unsigned long long e = n_eval, c = (unsigned long long)nemit;

@@ -21,10 +21,10 @@ namespace dgs_b200 {
 
 namespace {
 
-constexpr int KBUF = 8;  // ring capacity (power of two)
+constexpr int KBUF = 8;  // ring capacity (power of two); must equal blend_bwd.cu
 constexpr float kInf = __builtin_huge_valf();
-// 4 staged float4 record fields + 6 ring fields per pixel.
-constexpr size_t kFwdSmem = 4 * kBlendThreads * sizeof(float4) + 6 * KBUF * kBlendThreads * sizeof(float);
+// 4 staged float4 record fields + 4 ring fields per pixel (t, id, sigma, member).
+constexpr size_t kFwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float);
 
 /// Lower bound on t for every candidate at or after a list position whose
 /// range is r (t >= sqrt(r^2 - D^2), with margins ≫ float
@@ -100,9 +100,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     Ring* bt = reinterpret_cast<Ring*>(sD + kBlendThreads);
     uint32_t(*bid)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bt + KBUF);
     Ring* bs = reinterpret_cast<Ring*>(bid + KBUF);
-    Ring* bc0 = bs + KBUF;
-    Ring* bc1 = bc0 + KBUF;
-    Ring* bc2 = bc1 + KBUF;
+    uint32_t(*bmem)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bs + KBUF);
 
     const int tid = threadIdx.x;
     const int tile = blockIdx.x;
@@ -132,15 +130,16 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         }
         const int sl = head & (KBUF - 1);
         const float sg = bs[sl][tid];
+        const float4 col = __ldg(reinterpret_cast<const float4*>(recs + bmem[sl][tid]) + 3);
         const float w = fmul(sg, T);
-        C0 = fadd(C0, fmul(bc0[sl][tid], w));
-        C1 = fadd(C1, fmul(bc1[sl][tid], w));
-        C2 = fadd(C2, fmul(bc2[sl][tid], w));
+        C0 = fadd(C0, fmul(col.x, w));
+        C1 = fadd(C1, fmul(col.y, w));
+        C2 = fadd(C2, fmul(col.z, w));
         if (out_cd != nullptr) {
             const double wd = (double)sg * (double)T;
-            D0 += (double)bc0[sl][tid] * wd;
-            D1 += (double)bc1[sl][tid] * wd;
-            D2 += (double)bc2[sl][tid] * wd;
+            D0 += (double)col.x * wd;
+            D1 += (double)col.y * wd;
+            D2 += (double)col.z * wd;
         }
         T = fmul(T, fsub(1.0f, sg));
         if (dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][tid];
@@ -189,9 +188,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                     bt[ps][tid] = tp;
                     bid[ps][tid] = ip;
                     bs[ps][tid] = bs[pl][tid];
-                    bc0[ps][tid] = bc0[pl][tid];
-                    bc1[ps][tid] = bc1[pl][tid];
-                    bc2[ps][tid] = bc2[pl][tid];
+                    bmem[ps][tid] = bmem[pl][tid];
                     --pos;
                 } else {
                     break;
@@ -201,9 +198,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             bt[ps][tid] = t;
             bid[ps][tid] = id;
             bs[ps][tid] = sigma;
-            bc0[ps][tid] = D.x;
-            bc1[ps][tid] = D.y;
-            bc2[ps][tid] = D.z;
+            bmem[ps][tid] = pair_val[base + j];
             ++cnt;
             if (pos == head) head_t = t;
         }

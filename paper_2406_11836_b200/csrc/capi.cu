@@ -406,6 +406,9 @@ AdamParams adam_params(const Ctx& ctx, const SubsetState& S, uint64_t step_after
     ap.eps = (float)c.adam_eps;
     ap.bc1 = 1.0f - std::pow(ap.b1, (float)step_after);  // optim.hpp:108-109: std::pow(float, float)
     ap.bc2 = 1.0f - std::pow(ap.b2, (float)step_after);
+    ap.rbc1 = (float)(1.0 / (double)ap.bc1);
+    ap.rbc2 = (float)(1.0 / (double)ap.bc2);
+    ap.exact = c.deterministic ? 1 : 0;
     return ap;
 }
 

@@ -154,6 +154,7 @@ void dgs_default_train_config(dgs_train_config* c) {
     c->adam_beta2 = 0.999;
     c->adam_eps = 1e-15;
     c->grad_sync = 0;
+    c->deterministic = 1;
 }
 
 double dgs_position_lr(const dgs_train_config* c, uint64_t step) {

@@ -85,6 +85,8 @@ void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int 
 struct AdamParams {
     float lr[kMaxParamRows];  // per row
     float b1, b2, eps, bc1, bc2;
+    float rbc1, rbc2;         // 1/bc1, 1/bc2 (fast mode)
+    int exact;                // 1: reference IEEE op sequence (TrainConfig::deterministic)
 };
 
 // K9 (+K10): projection backward (splat.hpp:363-437) fused with dense Adam

@@ -165,6 +165,28 @@ def test_adam_bit_exact_given_reference_gradients(golden):
     ctx.close()
 
 
+def test_fast_adam_close_to_reference(golden):
+    """deterministic=0 (fast Adam): post-Adam parameters within 1e-5 rel of the reference given its gradients."""
+    g = golden
+    s = g.splats()
+    ctx = engine.Context(0)
+    members = members_of(g)
+    ctx.set_table(engine.build_kdtree(s.mu, g.args.get("kd", 0)))
+    ctx.set_options(engine.render_options(oracle=g.oracle_mode), engine.train_config(deterministic=0))
+    for k, idx in enumerate(members):
+        ctx.load_subset(k, s.take(idx))
+        grads = engine.Splats.empty(len(idx), s.sh_coeffs)
+        for f in GRAD_FIELDS:
+            getattr(grads, f[2:])[...] = g[f"k{k}_grad_{f}"].reshape(getattr(grads, f[2:]).shape)
+        ctx.adam_apply(k, grads)
+        p, _, _, _ = ctx.store_subset(k, s.sh_coeffs)
+        for f in PARAM_FIELDS:
+            want = g[f"k{k}_adam_{f}"].reshape(getattr(p, f).shape)
+            e = rel_err(getattr(p, f), want)
+            assert e.max() <= 1e-5, (k, f, float(e.max()), getattr(p, f).reshape(-1)[e.argmax()], want.reshape(-1)[e.argmax()])
+    ctx.close()
+
+
 def test_full_train_step_matches_reference(golden):
     """Manager::train_step end to end: post-Adam parameters within 1e-3 rel."""
     g = golden
