@@ -1,0 +1,1011 @@
+/*
+ * dgs_oracle.c — CPU restatement of the reference's training-step algorithm
+ * (float instantiation).  TEST INFRASTRUCTURE ONLY (see dgs_oracle.h).
+ *
+ * Every function cites the reference file:line it restates
+ * (/root/reference/proj/include/dgs/...).  Floating-point expressions follow
+ * the reference's evaluation order under the Eigen rules documented in
+ * oracle/eigen_shim/Eigen/Core (products: a0+(a1+a2) over inner dimension 3,
+ * a0+a1 over 2; contiguous Vec4 reductions (a0+a2)+(a1+a3)); compiled with
+ * -ffp-contract=off, so results are bit-identical to oracle/_ref (pinned by
+ * tests/test_oracle_cpu.py).  Single-threaded; the reference's 16-chunk
+ * reduction order (parallel.hpp:25, raster.hpp:272-305) is reproduced.
+ */
+#include "dgs_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------------------
+ * Eigen-order helpers
+ * ------------------------------------------------------------------------- */
+static inline float sum3(float a, float b, float c) { return a + (b + c); }
+static inline float dot3(const float* a, const float* b) { return sum3(a[0] * b[0], a[1] * b[1], a[2] * b[2]); }
+static inline float dot4(const float* a, const float* b) {
+    return (a[0] * b[0] + a[2] * b[2]) + (a[1] * b[1] + a[3] * b[3]);
+}
+static inline float fmaxf_std(float a, float b) { return (a < b) ? b : a; } /* std::max */
+static inline float fminf_std(float a, float b) { return (b < a) ? b : a; } /* std::min */
+
+/* math.hpp:21-24 */
+static inline float sigmoidf_ref(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+/* math.hpp:33-45 rotation_from_quat; returns 0 for a zero quaternion (throws there). */
+static int rotation_from_quat(const float q[4], float r[9]) {
+    const float n = sqrtf(dot4(q, q));
+    if (n <= 0.0f) return 0;
+    const float w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+    r[0] = 1.0f - 2.0f * (y * y + z * z);
+    r[1] = 2.0f * (x * y - w * z);
+    r[2] = 2.0f * (x * z + w * y);
+    r[3] = 2.0f * (x * y + w * z);
+    r[4] = 1.0f - 2.0f * (x * x + z * z);
+    r[5] = 2.0f * (y * z - w * x);
+    r[6] = 2.0f * (x * z - w * y);
+    r[7] = 2.0f * (y * z + w * x);
+    r[8] = 1.0f - 2.0f * (x * x + y * y);
+    return 1;
+}
+
+typedef struct {
+    float R[9], t[3], o[3];
+    float fx, fy, cx, cy;
+    int w, h, tx, ty;
+} view_t;
+
+/* Camera::rotation/center (splat.hpp:56-57). */
+static int make_view(const orc_camera* c, view_t* v) {
+    if (!rotation_from_quat(c->q, v->R)) return 0;
+    for (int i = 0; i < 3; ++i) {
+        v->t[i] = c->t[i];
+        const float col[3] = {v->R[0 * 3 + i], v->R[1 * 3 + i], v->R[2 * 3 + i]};
+        v->o[i] = -dot3(col, c->t);
+    }
+    v->fx = c->fx;
+    v->fy = c->fy;
+    v->cx = c->cx;
+    v->cy = c->cy;
+    v->w = c->width;
+    v->h = c->height;
+    v->tx = (c->width + 15) / 16;
+    v->ty = (c->height + 15) / 16;
+    return 1;
+}
+
+/* pixel_ray (splat.hpp:82-95). */
+static void pixel_ray(const view_t* v, int ix, int iy, float d[3]) {
+    const float px = (float)ix + 0.5f, py = (float)iy + 0.5f;
+    const float dc[3] = {(px - v->cx) / v->fx, (py - v->cy) / v->fy, 1.0f};
+    float u[3];
+    for (int i = 0; i < 3; ++i) {
+        const float col[3] = {v->R[0 * 3 + i], v->R[1 * 3 + i], v->R[2 * 3 + i]};
+        u[i] = dot3(col, dc);
+    }
+    const float n2 = dot3(u, u);
+    if (n2 > 0.0f) {
+        const float s = sqrtf(n2);
+        for (int i = 0; i < 3; ++i) d[i] = u[i] / s;
+    } else {
+        for (int i = 0; i < 3; ++i) d[i] = u[i];
+    }
+}
+
+/* sh::basis (splat.hpp:150-176). */
+static void sh_basis(const float d[3], int deg, float b[16]) {
+    memset(b, 0, 16 * sizeof(float));
+    b[0] = (float)0.28209479177387814;
+    if (deg < 1) return;
+    const float x = d[0], y = d[1], z = d[2];
+    b[1] = (float)(-0.4886025119029199) * y;
+    b[2] = (float)(0.4886025119029199) * z;
+    b[3] = (float)(-0.4886025119029199) * x;
+    if (deg < 2) return;
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    b[4] = (float)1.0925484305920792 * xy;
+    b[5] = (float)-1.0925484305920792 * yz;
+    b[6] = (float)0.31539156525252005 * (2.0f * zz - xx - yy);
+    b[7] = (float)-1.0925484305920792 * xz;
+    b[8] = (float)0.5462742152960396 * (xx - yy);
+    if (deg < 3) return;
+    b[9] = (float)-0.5900435899266435 * y * (3.0f * xx - yy);
+    b[10] = (float)2.890611442640554 * xy * z;
+    b[11] = (float)-0.4570457994644657 * y * (4.0f * zz - xx - yy);
+    b[12] = (float)0.3731763325901154 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = (float)-0.4570457994644657 * x * (4.0f * zz - xx - yy);
+    b[14] = (float)1.445305721320277 * z * (xx - yy);
+    b[15] = (float)-0.5900435899266435 * x * (xx - 3.0f * yy);
+}
+
+/* sh::basis_jacobian (splat.hpp:179-204), row-major j[16][3]. */
+static void sh_basis_jac(const float d[3], int deg, float j[16][3]) {
+    memset(j, 0, 16 * 3 * sizeof(float));
+    if (deg < 1) return;
+    const double C1 = 0.4886025119029199;
+    const double C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
+                          0.5462742152960396};
+    const double C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644657, 0.3731763325901154,
+                          -0.4570457994644657, 1.445305721320277, -0.5900435899266435};
+    const float x = d[0], y = d[1], z = d[2];
+    j[1][1] = (float)-C1;
+    j[2][2] = (float)C1;
+    j[3][0] = (float)-C1;
+    if (deg < 2) return;
+    j[4][0] = (float)C2[0] * y; j[4][1] = (float)C2[0] * x;
+    j[5][1] = (float)C2[1] * z; j[5][2] = (float)C2[1] * y;
+    j[6][0] = (float)(-2 * C2[2]) * x; j[6][1] = (float)(-2 * C2[2]) * y; j[6][2] = (float)(4 * C2[2]) * z;
+    j[7][0] = (float)C2[3] * z; j[7][2] = (float)C2[3] * x;
+    j[8][0] = (float)(2 * C2[4]) * x; j[8][1] = (float)(-2 * C2[4]) * y;
+    if (deg < 3) return;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    j[9][0] = (float)(6 * C3[0]) * x * y; j[9][1] = (float)C3[0] * (3.0f * xx - 3.0f * yy);
+    j[10][0] = (float)C3[1] * y * z; j[10][1] = (float)C3[1] * x * z; j[10][2] = (float)C3[1] * x * y;
+    j[11][0] = (float)(-2 * C3[2]) * x * y; j[11][1] = (float)C3[2] * (4.0f * zz - xx - 3.0f * yy);
+    j[11][2] = (float)(8 * C3[2]) * y * z;
+    j[12][0] = (float)(-6 * C3[3]) * x * z; j[12][1] = (float)(-6 * C3[3]) * y * z;
+    j[12][2] = (float)C3[3] * (6.0f * zz - 3.0f * xx - 3.0f * yy);
+    j[13][0] = (float)C3[4] * (4.0f * zz - 3.0f * xx - yy); j[13][1] = (float)(-2 * C3[4]) * x * y;
+    j[13][2] = (float)(8 * C3[4]) * x * z;
+    j[14][0] = (float)(2 * C3[5]) * x * z; j[14][1] = (float)(-2 * C3[5]) * y * z; j[14][2] = (float)C3[5] * (xx - yy);
+    j[15][0] = (float)C3[6] * (3.0f * xx - 3.0f * yy); j[15][1] = (float)(-6 * C3[6]) * x * y;
+}
+
+static int stored_degree(int c) { return c == 16 ? 3 : (c == 9 ? 2 : (c == 4 ? 1 : 0)); }
+static int eval_degree(const orc_opts* o, int c) {
+    const int s = stored_degree(c);
+    return o->sh_degree < 0 ? s : (o->sh_degree < s ? o->sh_degree : s);
+}
+
+/* Splat2D (splat.hpp:102-113). */
+typedef struct {
+    float mx, my;
+    float c[4], inv[4]; /* row-major 2x2 */
+    float depth, col[3], alpha, mu[3], radius;
+} splat2d_t;
+
+/* project_splat (splat.hpp:288-321); returns 1 if projected. */
+static int project_splat(const orc_splats* s, int64_t i, const view_t* v, const orc_opts* o, splat2d_t* out) {
+    const float* mu = s->mu + 3 * i;
+    float t[3];
+    for (int a = 0; a < 3; ++a) t[a] = dot3(v->R + 3 * a, mu) + v->t[a];
+    if (!(t[2] > o->near_plane)) return 0;
+    out->depth = t[2];
+    out->mx = v->fx * t[0] / t[2] + v->cx;
+    out->my = v->fy * t[1] / t[2] + v->cy;
+    const float iz = 1.0f / t[2];
+    const float J[6] = {v->fx * iz, 0.0f, -v->fx * t[0] * iz * iz, 0.0f, v->fy * iz, -v->fy * t[1] * iz * iz};
+    float V[6];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+            V[a * 3 + b] = sum3(J[a * 3] * v->R[b], J[a * 3 + 1] * v->R[3 + b], J[a * 3 + 2] * v->R[6 + b]);
+    float r[9];
+    if (!rotation_from_quat(s->rotation + 4 * i, r)) return -1;
+    const float* ls = s->log_scale + 3 * i;
+    const float sc[3] = {expf(ls[0]), expf(ls[1]), expf(ls[2])};
+    float M[9], S[9], VS[6];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) M[a * 3 + b] = r[a * 3 + b] * sc[b];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) S[a * 3 + b] = sum3(M[a * 3] * M[b * 3], M[a * 3 + 1] * M[b * 3 + 1], M[a * 3 + 2] * M[b * 3 + 2]);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+            VS[a * 3 + b] = sum3(V[a * 3] * S[b], V[a * 3 + 1] * S[3 + b], V[a * 3 + 2] * S[6 + b]);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            out->c[a * 2 + b] = sum3(VS[a * 3] * V[b * 3], VS[a * 3 + 1] * V[b * 3 + 1], VS[a * 3 + 2] * V[b * 3 + 2]);
+    out->c[0] += o->cov_reg;
+    out->c[3] += o->cov_reg;
+    const float det = out->c[0] * out->c[3] - out->c[1] * out->c[2];
+    out->inv[0] = out->c[3] / det;
+    out->inv[1] = -out->c[1] / det;
+    out->inv[2] = -out->c[2] / det;
+    out->inv[3] = out->c[0] / det;
+    const float rx = o->trunc * sqrtf(out->c[0]), ry = o->trunc * sqrtf(out->c[3]);
+    if (out->mx + rx < 0.0f || out->mx - rx > (float)v->w || out->my + ry < 0.0f || out->my - ry > (float)v->h)
+        return 0;
+    const int deg = eval_degree(o, s->sh_coeffs);
+    float dir[3] = {mu[0] - v->o[0], mu[1] - v->o[1], mu[2] - v->o[2]};
+    const float n2 = dot3(dir, dir);
+    if (n2 > 0.0f) {
+        const float q = sqrtf(n2);
+        for (int a = 0; a < 3; ++a) dir[a] = dir[a] / q;
+    }
+    float b[16];
+    sh_basis(dir, deg, b);
+    const float* sh = s->sh + (size_t)i * s->sh_coeffs * 3;
+    float col[3] = {0.5f, 0.5f, 0.5f};
+    for (int k = 0; k < (deg + 1) * (deg + 1); ++k)
+        for (int ch = 0; ch < 3; ++ch) col[ch] = col[ch] + b[k] * sh[k * 3 + ch];
+    for (int ch = 0; ch < 3; ++ch) out->col[ch] = fmaxf_std(col[ch], 0.0f);
+    out->alpha = sigmoidf_ref(s->opacity_logit[i]);
+    float smax = sc[0];
+    if (sc[1] > smax) smax = sc[1];
+    if (sc[2] > smax) smax = sc[2];
+    out->radius = o->trunc * smax;
+    for (int a = 0; a < 3; ++a) out->mu[a] = mu[a];
+    return 1;
+}
+
+/* x86 cvttss2si semantics for static_cast<int>(float) (raster.hpp:118-121). */
+static int to_int_x86(float f) {
+    if (!(f > -2147483904.0f && f < 2147483648.0f)) return (int)0x80000000u;
+    return (int)f;
+}
+static int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+typedef struct {
+    int64_t np;
+    splat2d_t* sp;
+    int64_t* src;
+    int64_t* off;  /* tiles + 1 */
+    int64_t* ent;  /* projected indices, projected order per tile */
+} scene_t;
+
+static void scene_free(scene_t* sc) {
+    free(sc->sp);
+    free(sc->src);
+    free(sc->off);
+    free(sc->ent);
+}
+
+/* project_scene (raster.hpp:91-127). Returns 0 on success, -1 on zero quaternion. */
+static int project_scene(const orc_splats* s, const view_t* v, const orc_opts* o, scene_t* sc) {
+    sc->sp = (splat2d_t*)malloc(sizeof(splat2d_t) * (s->n ? s->n : 1));
+    sc->src = (int64_t*)malloc(sizeof(int64_t) * (s->n ? s->n : 1));
+    sc->np = 0;
+    for (int64_t i = 0; i < s->n; ++i) {
+        const int r = project_splat(s, i, v, o, &sc->sp[sc->np]);
+        if (r < 0) return -1;
+        if (r) sc->src[sc->np++] = i;
+    }
+    const int tiles = v->tx * v->ty;
+    int64_t* cnt = (int64_t*)calloc(tiles + 1, sizeof(int64_t));
+    int* rect = (int*)malloc(sizeof(int) * 4 * (sc->np ? sc->np : 1));
+    for (int64_t p = 0; p < sc->np; ++p) {
+        const splat2d_t* q = &sc->sp[p];
+        const float rx = o->trunc * sqrtf(q->c[0]), ry = o->trunc * sqrtf(q->c[3]);
+        int* R = rect + 4 * p;
+        R[0] = clampi(to_int_x86(floorf(q->mx - rx)) / 16, 0, v->tx - 1);
+        R[1] = clampi(to_int_x86(floorf(q->mx + rx)) / 16, 0, v->tx - 1);
+        R[2] = clampi(to_int_x86(floorf(q->my - ry)) / 16, 0, v->ty - 1);
+        R[3] = clampi(to_int_x86(floorf(q->my + ry)) / 16, 0, v->ty - 1);
+        for (int ty = R[2]; ty <= R[3]; ++ty)
+            for (int tx = R[0]; tx <= R[1]; ++tx) cnt[ty * v->tx + tx + 1]++;
+    }
+    sc->off = (int64_t*)malloc(sizeof(int64_t) * (tiles + 1));
+    sc->off[0] = 0;
+    for (int t = 0; t < tiles; ++t) sc->off[t + 1] = sc->off[t] + cnt[t + 1];
+    sc->ent = (int64_t*)malloc(sizeof(int64_t) * (sc->off[tiles] ? sc->off[tiles] : 1));
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * tiles);
+    for (int t = 0; t < tiles; ++t) fill[t] = sc->off[t];
+    for (int64_t p = 0; p < sc->np; ++p) {
+        const int* R = rect + 4 * p;
+        for (int ty = R[2]; ty <= R[3]; ++ty)
+            for (int tx = R[0]; tx <= R[1]; ++tx) sc->ent[fill[ty * v->tx + tx]++] = p;
+    }
+    free(cnt);
+    free(rect);
+    free(fill);
+    return 0;
+}
+
+/* partition.hpp:25-28, 58-63 */
+static int indicator(const orc_subspace* s, const float x[3]) {
+    for (int p = 0; p < s->n; ++p) {
+        const float n[3] = {s->nx[p], s->ny[p], s->nz[p]};
+        const float val = dot3(n, x) + s->d[p];
+        if (s->closed[p] ? !(val <= 0.0f) : !(val < 0.0f)) return 0;
+    }
+    return 1;
+}
+
+/* eval_2d (splat.hpp:325-332) */
+static float eval_2d(const splat2d_t* q, float px, float py, const orc_opts* o) {
+    const float d0 = px - q->mx, d1 = py - q->my;
+    const float w0 = q->inv[0] * d0 + q->inv[1] * d1, w1 = q->inv[2] * d0 + q->inv[3] * d1;
+    const float m2 = d0 * w0 + d1 * w1;
+    if (m2 > o->trunc * o->trunc) return 0.0f;
+    return expf(-0.5f * m2);
+}
+
+typedef struct {
+    float key;
+    uint64_t id;
+    int64_t proj;
+    float sigma;
+} contrib_t;
+
+static int contrib_cmp(const void* a, const void* b) {
+    const contrib_t* x = (const contrib_t*)a;
+    const contrib_t* y = (const contrib_t*)b;
+    if (x->key < y->key) return -1;
+    if (y->key < x->key) return 1;
+    return x->id < y->id ? -1 : (x->id > y->id ? 1 : 0);
+}
+
+/* collect_contributions (raster.hpp:146-167) */
+static int64_t collect(const scene_t* sc, const uint64_t* ids, int64_t tile, const view_t* v, const float d[3],
+                       float px, float py, const orc_opts* o, const orc_subspace* gate, contrib_t* out) {
+    int64_t n = 0;
+    for (int64_t e = sc->off[tile]; e < sc->off[tile + 1]; ++e) {
+        const int64_t p = sc->ent[e];
+        const splat2d_t* q = &sc->sp[p];
+        const float g = eval_2d(q, px, py, o);
+        if (!(g > 0.0f)) continue;
+        const float rel[3] = {q->mu[0] - v->o[0], q->mu[1] - v->o[1], q->mu[2] - v->o[2]};
+        const float t = dot3(d, rel);
+        if (!(t > 0.0f)) continue;
+        const float xi[3] = {v->o[0] + t * d[0], v->o[1] + t * d[1], v->o[2] + t * d[2]};
+        const float e3[3] = {xi[0] - q->mu[0], xi[1] - q->mu[1], xi[2] - q->mu[2]};
+        if (dot3(e3, e3) > q->radius * q->radius) continue;
+        if (gate && o->indicator_enabled && !indicator(gate, xi)) continue;
+        const float sigma = fminf_std(q->alpha * g, o->sigma_clamp);
+        if (!(sigma > 0.0f)) continue;
+        out[n].key = t;
+        out[n].id = ids[sc->src[p]];
+        out[n].proj = p;
+        out[n].sigma = sigma;
+        ++n;
+    }
+    qsort(out, (size_t)n, sizeof(contrib_t), contrib_cmp);
+    return n;
+}
+
+int64_t orc_project(const orc_splats* s, const orc_camera* cam, const orc_opts* o, float* rec19, uint8_t* visible,
+                    int64_t* bins_off, int32_t* bins_ent, int64_t cap) {
+    view_t v;
+    if (!make_view(cam, &v)) return -1;
+    scene_t sc;
+    if (project_scene(s, &v, o, &sc) < 0) {
+        scene_free(&sc);
+        return -1;
+    }
+    const int tiles = v.tx * v.ty;
+    const int64_t P = sc.off[tiles];
+    if (rec19) memset(rec19, 0, sizeof(float) * 19 * s->n);
+    if (visible) memset(visible, 0, (size_t)s->n);
+    for (int64_t p = 0; p < sc.np; ++p) {
+        const int64_t i = sc.src[p];
+        if (visible) visible[i] = 1;
+        if (rec19) {
+            float* r = rec19 + 19 * i;
+            const splat2d_t* q = &sc.sp[p];
+            r[0] = q->mx; r[1] = q->my;
+            for (int a = 0; a < 4; ++a) { r[2 + a] = q->c[a]; r[6 + a] = q->inv[a]; }
+            r[10] = q->depth;
+            for (int a = 0; a < 3; ++a) r[11 + a] = q->col[a];
+            r[14] = q->alpha;
+            for (int a = 0; a < 3; ++a) r[15 + a] = q->mu[a];
+            r[18] = q->radius;
+        }
+    }
+    if (bins_off && P <= cap) {
+        for (int t = 0; t <= tiles; ++t) bins_off[t] = sc.off[t];
+        for (int64_t e = 0; e < P; ++e) bins_ent[e] = (int32_t)sc.src[sc.ent[e]];
+    }
+    scene_free(&sc);
+    return P <= cap ? P : -P;
+}
+
+/* render_maps with the subspace gate (raster.hpp:241-263, engine.hpp:31-52) */
+int orc_partial_render(const orc_splats* s, const orc_subspace* sub, const orc_camera* cam, const orc_opts* o,
+                       float* out_ct, int32_t dbg_cap, uint32_t* dbg_ids, uint32_t* dbg_cnt) {
+    view_t v;
+    if (!make_view(cam, &v)) return -1;
+    scene_t sc;
+    if (project_scene(s, &v, o, &sc) < 0) {
+        scene_free(&sc);
+        return -1;
+    }
+    int64_t maxlen = 1;
+    for (int t = 0; t < v.tx * v.ty; ++t)
+        if (sc.off[t + 1] - sc.off[t] > maxlen) maxlen = sc.off[t + 1] - sc.off[t];
+    contrib_t* buf = (contrib_t*)malloc(sizeof(contrib_t) * maxlen);
+    const float stop = o->stop;
+    for (int y = 0; y < v.h; ++y)
+        for (int x = 0; x < v.w; ++x) {
+            float d[3];
+            pixel_ray(&v, x, y, d);
+            const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+            const int64_t tile = (int64_t)(y / 16) * v.tx + x / 16;
+            const int64_t n = collect(&sc, s->id, tile, &v, d, px, py, o, sub, buf);
+            float C[3] = {0.0f, 0.0f, 0.0f}, T = 1.0f;
+            int32_t ne = 0;
+            const size_t pix = (size_t)y * v.w + x;
+            for (int64_t k = 0; k < n; ++k) { /* composite_ray (raster.hpp:177-189) */
+                if (stop > 0.0f && T < stop) break;
+                const splat2d_t* q = &sc.sp[buf[k].proj];
+                const float wgt = buf[k].sigma * T;
+                for (int ch = 0; ch < 3; ++ch) C[ch] = C[ch] + q->col[ch] * wgt;
+                T = T * (1.0f - buf[k].sigma);
+                if (dbg_ids && ne < dbg_cap) dbg_ids[pix * dbg_cap + ne] = (uint32_t)buf[k].id;
+                ++ne;
+            }
+            if (out_ct) {
+                out_ct[4 * pix] = C[0];
+                out_ct[4 * pix + 1] = C[1];
+                out_ct[4 * pix + 2] = C[2];
+                out_ct[4 * pix + 3] = T;
+            }
+            if (dbg_cnt) dbg_cnt[pix] = (uint32_t)ne;
+        }
+    free(buf);
+    scene_free(&sc);
+    return 0;
+}
+
+/* subspace_order (partition.hpp:265-300) + compute_pixel_orders (engine.hpp:108-131) */
+int orc_pixel_orders(const orc_subspace* subs, int32_t K, const orc_camera* cam, uint16_t* order, uint16_t* count) {
+    view_t v;
+    if (!make_view(cam, &v)) return -1;
+    int owner = -1;
+    for (int k = 0; k < K && owner < 0; ++k)
+        if (indicator(&subs[k], v.o)) owner = k;
+    float* te = (float*)malloc(sizeof(float) * K);
+    int* ks = (int*)malloc(sizeof(int) * K);
+    for (int y = 0; y < v.h; ++y)
+        for (int x = 0; x < v.w; ++x) {
+            float d[3];
+            pixel_ray(&v, x, y, d);
+            int n = 0;
+            for (int k = 0; k < K; ++k) {
+                const orc_subspace* s = &subs[k];
+                float lo = -INFINITY, hi = INFINITY;
+                int empty = 0;
+                for (int p = 0; p < s->n; ++p) {
+                    const float nn[3] = {s->nx[p], s->ny[p], s->nz[p]};
+                    const float a = dot3(nn, d);
+                    const float b = dot3(nn, v.o) + s->d[p];
+                    if (a == 0.0f) {
+                        if (b > 0.0f) { empty = 1; break; }
+                    } else {
+                        const float ts = -b / a;
+                        if (a > 0.0f) hi = fminf_std(hi, ts);
+                        else lo = fmaxf_std(lo, ts);
+                    }
+                }
+                if (empty || lo > hi || !(hi > 0.0f)) continue;
+                const float ten = fmaxf_std(lo, 0.0f);
+                int pos = n;
+                while (pos > 0) {
+                    const int kp = ks[pos - 1];
+                    int less;
+                    if ((k == owner) != (kp == owner)) less = (k == owner);
+                    else less = ten < te[pos - 1] || (ten == te[pos - 1] && k < kp);
+                    if (!less) break;
+                    te[pos] = te[pos - 1];
+                    ks[pos] = ks[pos - 1];
+                    --pos;
+                }
+                te[pos] = ten;
+                ks[pos] = k;
+                ++n;
+            }
+            const size_t pix = (size_t)y * v.w + x;
+            count[pix] = (uint16_t)n;
+            for (int i = 0; i < K; ++i) order[pix * K + i] = (uint16_t)(i < n ? ks[i] : 0);
+        }
+    free(te);
+    free(ks);
+    return 0;
+}
+
+/* merge (engine.hpp:152-182) */
+int orc_merge(const float* partials, const uint16_t* order, const uint16_t* count, int32_t K, int32_t w, int32_t h,
+              const float bg[3], float* out_rgb, float* out_t) {
+    const size_t px = (size_t)w * h;
+    for (size_t p = 0; p < px; ++p) {
+        float c[3] = {0.0f, 0.0f, 0.0f}, tr = 1.0f;
+        for (int i = 0; i < count[p]; ++i) {
+            const float* q = partials + ((size_t)order[p * K + i] * px + p) * 4;
+            for (int ch = 0; ch < 3; ++ch) c[ch] = c[ch] + tr * q[ch];
+            tr = tr * q[3];
+        }
+        for (int ch = 0; ch < 3; ++ch) out_rgb[3 * p + ch] = c[ch] + tr * bg[ch];
+        if (out_t) out_t[p] = tr;
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Loss (loss.hpp:19-177)
+ * ------------------------------------------------------------------------- */
+static void ssim_kernel(float k[11]) { /* loss.hpp:19-30 */
+    float sum = 0.0f;
+    for (int i = 0; i < 11; ++i) {
+        const double x = i - 11 / 2;
+        k[i] = (float)exp(-x * x / (2.0 * 1.5 * 1.5));
+        sum += k[i];
+    }
+    for (int i = 0; i < 11; ++i) k[i] /= sum;
+}
+
+static void gauss_blur(const float* img, int w, int h, const float k[11], float* tmp, float* out) { /* loss.hpp:33-62 */
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < 3; ++c) {
+                float acc = 0.0f;
+                for (int i = -5; i <= 5; ++i) {
+                    const int xx = x + i;
+                    if (xx < 0 || xx >= w) continue;
+                    acc += k[i + 5] * img[((size_t)y * w + xx) * 3 + c];
+                }
+                tmp[((size_t)y * w + x) * 3 + c] = acc;
+            }
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < 3; ++c) {
+                float acc = 0.0f;
+                for (int i = -5; i <= 5; ++i) {
+                    const int yy = y + i;
+                    if (yy < 0 || yy >= h) continue;
+                    acc += k[i + 5] * tmp[((size_t)yy * w + x) * 3 + c];
+                }
+                out[((size_t)y * w + x) * 3 + c] = acc;
+            }
+}
+
+float orc_loss(const float* render, const float* target, int32_t w, int32_t h, float lam, float* grad,
+               float* means3) {
+    const size_t n = (size_t)w * h * 3;
+    float k[11];
+    ssim_kernel(k);
+    float* buf = (float*)malloc(sizeof(float) * n * 13);
+    float *mx = buf, *my = buf + n, *xx = buf + 2 * n, *yy = buf + 3 * n, *xy = buf + 4 * n, *tmp = buf + 5 * n;
+    float *am = buf + 6 * n, *bm = buf + 7 * n, *cm = buf + 8 * n, *prod = buf + 9 * n, *o1 = buf + 10 * n,
+          *o2 = buf + 11 * n, *o3 = buf + 12 * n;
+    /* L1 part (loss.hpp:161-167) */
+    float l1 = 0.0f, mse_acc = 0.0f;
+    for (size_t i = 0; i < n; ++i) {
+        const float d = render[i] - target[i];
+        l1 += fabsf(d);
+        mse_acc += d * d;
+        if (grad) grad[i] = (1.0f - lam) * (d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f)) / (float)n;
+    }
+    l1 /= (float)n;
+    /* ssim (loss.hpp:94-143) */
+    const float c1 = (float)(0.01 * 0.01), c2 = (float)(0.03 * 0.03);
+    gauss_blur(render, w, h, k, tmp, mx);
+    gauss_blur(target, w, h, k, tmp, my);
+    for (size_t i = 0; i < n; ++i) prod[i] = render[i] * render[i];
+    gauss_blur(prod, w, h, k, tmp, xx);
+    for (size_t i = 0; i < n; ++i) prod[i] = target[i] * target[i];
+    gauss_blur(prod, w, h, k, tmp, yy);
+    for (size_t i = 0; i < n; ++i) prod[i] = render[i] * target[i];
+    gauss_blur(prod, w, h, k, tmp, xy);
+    float total = 0.0f;
+    for (size_t i = 0; i < n; ++i) {
+        const float a = mx[i], b = my[i];
+        const float sxx = xx[i] - a * a, syy = yy[i] - b * b, sxy = xy[i] - a * b;
+        const float n1 = 2 * a * b + c1, n2 = 2 * sxy + c2;
+        const float d1 = a * a + b * b + c1, d2 = sxx + syy + c2;
+        const float s = (n1 * n2) / (d1 * d2);
+        total += s;
+        am[i] = 2 * b * n2 / (d1 * d2) - 2 * a * s / d1;
+        bm[i] = -s / d2;
+        cm[i] = 2 * n1 / (d1 * d2);
+    }
+    const float ssim_v = total / (float)n;
+    if (grad && lam > 0.0f) {
+        gauss_blur(am, w, h, k, tmp, o1);             /* ca */
+        gauss_blur(bm, w, h, k, tmp, o2);             /* cb */
+        for (size_t i = 0; i < n; ++i) prod[i] = bm[i] * mx[i];
+        gauss_blur(prod, w, h, k, tmp, o3);           /* cbmx */
+        /* reuse am/xx for cc, ccmy */
+        gauss_blur(cm, w, h, k, tmp, am);             /* cc */
+        for (size_t i = 0; i < n; ++i) prod[i] = cm[i] * my[i];
+        gauss_blur(prod, w, h, k, tmp, xx);           /* ccmy */
+        for (size_t i = 0; i < n; ++i) {
+            const float sg = (o1[i] + 2 * render[i] * o2[i] - 2 * o3[i] + target[i] * am[i] - xx[i]) / (float)n;
+            grad[i] -= lam * sg;
+        }
+    }
+    if (means3) {
+        means3[0] = l1;
+        means3[1] = ssim_v;
+        means3[2] = mse_acc / (float)n;
+    }
+    free(buf);
+    return (1.0f - lam) * l1 + lam * (1.0f - ssim_v);
+}
+
+/* merge_backward (engine.hpp:195-234), grad_trans_total = 0 */
+int orc_merge_backward(const float* partials, const uint16_t* order, const uint16_t* count, int32_t K, int32_t w,
+                       int32_t h, const float* gcol, const float bg[3], float* out) {
+    const size_t px = (size_t)w * h;
+    memset(out, 0, sizeof(float) * 4 * px * K);
+    float* prefix = (float*)malloc(sizeof(float) * (K + 1));
+    for (size_t p = 0; p < px; ++p) {
+        const float gc[3] = {gcol[3 * p], gcol[3 * p + 1], gcol[3 * p + 2]};
+        const float gt_eff = 0.0f + dot3(gc, bg);
+        const int n = count[p];
+        prefix[0] = 1.0f;
+        for (int i = 0; i < n; ++i) prefix[i + 1] = prefix[i] * partials[((size_t)order[p * K + i] * px + p) * 4 + 3];
+        float suffix[3] = {0.0f, 0.0f, 0.0f}, tail = 1.0f;
+        for (int i = n - 1; i >= 0; --i) {
+            const int k = order[p * K + i];
+            const float* q = partials + ((size_t)k * px + p) * 4;
+            float* o = out + ((size_t)k * px + p) * 4;
+            for (int ch = 0; ch < 3; ++ch) o[ch] = prefix[i] * gc[ch];
+            o[3] = prefix[i] * (dot3(gc, suffix) + gt_eff * tail);
+            for (int ch = 0; ch < 3; ++ch) suffix[ch] = q[ch] + q[3] * suffix[ch];
+            tail *= q[3];
+        }
+    }
+    free(prefix);
+    return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Backward (raster.hpp:194-317, splat.hpp:223-239, 363-437)
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    float dm[2], dc[4], dcol[3], da;
+} g2d_t; /* Splat2DGrad (splat.hpp:341-347) */
+
+/* composite_ray_backward (raster.hpp:194-236) */
+static void composite_backward(const contrib_t* cb, int64_t n, const scene_t* sc, const orc_opts* o, float px,
+                               float py, const float gc[3], float gt, g2d_t* pg, float* prefix) {
+    const float stop = o->stop;
+    float trans = 1.0f;
+    int64_t done = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        if (stop > 0.0f && trans < stop) break;
+        prefix[done++] = trans;
+        trans *= (1.0f - cb[k].sigma);
+    }
+    const float t_final = trans;
+    float suffix[3] = {0.0f, 0.0f, 0.0f};
+    for (int64_t k = done; k-- > 0;) {
+        const splat2d_t* s = &sc->sp[cb[k].proj];
+        const float a_i = prefix[k], sig = cb[k].sigma, one_minus = 1.0f - sig;
+        g2d_t* g = &pg[cb[k].proj];
+        const float ws = sig * a_i;
+        for (int ch = 0; ch < 3; ++ch) g->dcol[ch] = g->dcol[ch] + gc[ch] * ws;
+        const float d_sigma = dot3(gc, s->col) * a_i - dot3(gc, suffix) / one_minus - gt * t_final / one_minus;
+        for (int ch = 0; ch < 3; ++ch) suffix[ch] = suffix[ch] + s->col[ch] * ws;
+        const float gval = eval_2d(s, px, py, o);
+        if (s->alpha * gval >= o->sigma_clamp) continue;
+        g->da += d_sigma * gval;
+        const float d_g = d_sigma * s->alpha;
+        const float d0 = px - s->mx, d1 = py - s->my;
+        const float w0 = s->inv[0] * d0 + s->inv[1] * d1, w1 = s->inv[2] * d0 + s->inv[3] * d1;
+        const float m = d_g * gval;
+        g->dm[0] = g->dm[0] + m * w0;
+        g->dm[1] = g->dm[1] + m * w1;
+        const float hh = d_g * gval * 0.5f;
+        const float ww[4] = {w0 * w0, w0 * w1, w1 * w0, w1 * w1};
+        for (int a = 0; a < 4; ++a) g->dc[a] = g->dc[a] + hh * ww[a];
+    }
+}
+
+/* project_splat_backward (splat.hpp:363-437) into the GradBuffers slot of member i */
+static void project_backward(const orc_splats* sp, int64_t i, const view_t* v, const orc_opts* o, const g2d_t* g,
+                             orc_grads* out) {
+    const float* W = v->R;
+    const float* mu = sp->mu + 3 * i;
+    float t[3];
+    for (int a = 0; a < 3; ++a) t[a] = dot3(W + 3 * a, mu) + v->t[a];
+    const float iz = 1.0f / t[2];
+    const float J[6] = {v->fx * iz, 0.0f, -v->fx * t[0] * iz * iz, 0.0f, v->fy * iz, -v->fy * t[1] * iz * iz};
+    float d_t[3];
+    for (int a = 0; a < 3; ++a) d_t[a] = J[a] * g->dm[0] + J[3 + a] * g->dm[1];
+    float r[9];
+    rotation_from_quat(sp->rotation + 4 * i, r);
+    const float* ls = sp->log_scale + 3 * i;
+    const float sc[3] = {expf(ls[0]), expf(ls[1]), expf(ls[2])};
+    float m[9], sigma[9], V[6];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) m[a * 3 + b] = r[a * 3 + b] * sc[b];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) sigma[a * 3 + b] = sum3(m[a * 3] * m[b * 3], m[a * 3 + 1] * m[b * 3 + 1], m[a * 3 + 2] * m[b * 3 + 2]);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b) V[a * 3 + b] = sum3(J[a * 3] * W[b], J[a * 3 + 1] * W[3 + b], J[a * 3 + 2] * W[6 + b]);
+    float g2[4];
+    g2[0] = 0.5f * (g->dc[0] + g->dc[0]);
+    g2[1] = 0.5f * (g->dc[1] + g->dc[2]);
+    g2[2] = 0.5f * (g->dc[2] + g->dc[1]);
+    g2[3] = 0.5f * (g->dc[3] + g->dc[3]);
+    /* d_sigma = (V^T g2) V */
+    float vtg[6]; /* 3x2 */
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 2; ++b) vtg[a * 2 + b] = V[a] * g2[b] + V[3 + a] * g2[2 + b];
+    float dS[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dS[a * 3 + b] = vtg[a * 2] * V[b] + vtg[a * 2 + 1] * V[3 + b];
+    /* d_v = ((g2 + g2^T) V) Sigma */
+    float gs[4] = {g2[0] + g2[0], g2[1] + g2[2], g2[2] + g2[1], g2[3] + g2[3]};
+    float gv[6];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b) gv[a * 3 + b] = gs[a * 2] * V[b] + gs[a * 2 + 1] * V[3 + b];
+    float dv[6];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b) dv[a * 3 + b] = sum3(gv[a * 3] * sigma[b], gv[a * 3 + 1] * sigma[3 + b], gv[a * 3 + 2] * sigma[6 + b]);
+    /* d_j = d_v W^T */
+    float dj[6];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b) dj[a * 3 + b] = sum3(dv[a * 3] * W[b * 3], dv[a * 3 + 1] * W[b * 3 + 1], dv[a * 3 + 2] * W[b * 3 + 2]);
+    d_t[0] += dj[2] * (-v->fx * iz * iz);
+    d_t[1] += dj[5] * (-v->fy * iz * iz);
+    d_t[2] += dj[0] * (-v->fx * iz * iz) + dj[2] * (2.0f * v->fx * t[0] * iz * iz * iz) + dj[4] * (-v->fy * iz * iz) +
+              dj[5] * (2.0f * v->fy * t[1] * iz * iz * iz);
+    float* dmu = out->d_mu + 3 * i;
+    for (int a = 0; a < 3; ++a) {
+        const float col[3] = {W[a], W[3 + a], W[6 + a]};
+        dmu[a] += dot3(col, d_t);
+    }
+    /* d_m = (dS + dS^T) m */
+    float dsym[9], dm[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dsym[a * 3 + b] = dS[a * 3 + b] + dS[b * 3 + a];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dm[a * 3 + b] = sum3(dsym[a * 3] * m[b], dsym[a * 3 + 1] * m[3 + b], dsym[a * 3 + 2] * m[6 + b]);
+    float dr[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dr[a * 3 + b] = dm[a * 3 + b] * sc[b];
+    float* dls = out->d_log_scale + 3 * i;
+    for (int a = 0; a < 3; ++a) {
+        const float rc[3] = {r[a], r[3 + a], r[6 + a]}, mc[3] = {dm[a], dm[3 + a], dm[6 + a]};
+        dls[a] += dot3(rc, mc) * sc[a];
+    }
+    const float* q = sp->rotation + 4 * i;
+    const float n = sqrtf(dot4(q, q));
+    const float qn[4] = {q[0] / n, q[1] / n, q[2] / n, q[3] / n};
+    const float qw = qn[0], qx = qn[1], qy = qn[2], qz = qn[3];
+    float dq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#define ADDQ(rr, cc, a, b, c, d)             \
+    do {                                     \
+        const float gg_ = dr[(rr) * 3 + (cc)]; \
+        dq[0] += gg_ * (a);                  \
+        dq[1] += gg_ * (b);                  \
+        dq[2] += gg_ * (c);                  \
+        dq[3] += gg_ * (d);                  \
+    } while (0)
+    ADDQ(0, 0, 0.0f, 0.0f, -4.0f * qy, -4.0f * qz);
+    ADDQ(0, 1, -2.0f * qz, 2.0f * qy, 2.0f * qx, -2.0f * qw);
+    ADDQ(0, 2, 2.0f * qy, 2.0f * qz, 2.0f * qw, 2.0f * qx);
+    ADDQ(1, 0, 2.0f * qz, 2.0f * qy, 2.0f * qx, 2.0f * qw);
+    ADDQ(1, 1, 0.0f, -4.0f * qx, 0.0f, -4.0f * qz);
+    ADDQ(1, 2, -2.0f * qx, -2.0f * qw, 2.0f * qz, 2.0f * qy);
+    ADDQ(2, 0, -2.0f * qy, 2.0f * qz, -2.0f * qw, 2.0f * qx);
+    ADDQ(2, 1, 2.0f * qx, 2.0f * qw, 2.0f * qz, 2.0f * qy);
+    ADDQ(2, 2, 0.0f, -4.0f * qx, -4.0f * qy, 0.0f);
+#undef ADDQ
+    const float qd = dot4(qn, dq);
+    float* drot = out->d_rotation + 4 * i;
+    for (int a = 0; a < 4; ++a) drot[a] += (dq[a] - qn[a] * qd) / n;
+    /* SH colour chain (eval_sh_backward) */
+    const int deg = eval_degree(o, sp->sh_coeffs);
+    const float rel[3] = {mu[0] - v->o[0], mu[1] - v->o[1], mu[2] - v->o[2]};
+    const float dist = sqrtf(dot3(rel, rel));
+    const float dir[3] = {rel[0] / dist, rel[1] / dist, rel[2] / dist};
+    float b[16], jb[16][3];
+    sh_basis(dir, deg, b);
+    sh_basis_jac(dir, deg, jb);
+    const int nb = (deg + 1) * (deg + 1);
+    const float* co = sp->sh + (size_t)i * sp->sh_coeffs * 3;
+    float pre[3] = {0.5f, 0.5f, 0.5f};
+    for (int k = 0; k < nb; ++k)
+        for (int ch = 0; ch < 3; ++ch) pre[ch] = pre[ch] + b[k] * co[k * 3 + ch];
+    float gg[3] = {g->dcol[0], g->dcol[1], g->dcol[2]};
+    for (int ch = 0; ch < 3; ++ch)
+        if (pre[ch] < 0.0f) gg[ch] = 0.0f;
+    float ddir[3] = {0.0f, 0.0f, 0.0f};
+    float* dsh = out->d_sh + (size_t)i * sp->sh_coeffs * 3;
+    for (int k = 0; k < nb; ++k) {
+        for (int ch = 0; ch < 3; ++ch) dsh[k * 3 + ch] = dsh[k * 3 + ch] + b[k] * gg[ch];
+        const float gd = dot3(gg, co + k * 3);
+        for (int a = 0; a < 3; ++a) ddir[a] = ddir[a] + jb[k][a] * gd;
+    }
+    const float dd = dot3(dir, ddir);
+    for (int a = 0; a < 3; ++a) dmu[a] += (ddir[a] - dir[a] * dd) / dist;
+    const float al = sigmoidf_ref(sp->opacity_logit[i]);
+    out->d_opacity_logit[i] += g->da * al * (1.0f - al);
+}
+
+int orc_partial_backward(const orc_splats* s, const orc_subspace* sub, const orc_camera* cam, const orc_opts* o,
+                         const float* grad_ct, orc_grads* out) {
+    view_t v;
+    if (!make_view(cam, &v)) return -1;
+    scene_t sc;
+    if (project_scene(s, &v, o, &sc) < 0) {
+        scene_free(&sc);
+        return -1;
+    }
+    const int64_t np = sc.np;
+    int64_t maxlen = 1;
+    for (int t = 0; t < v.tx * v.ty; ++t)
+        if (sc.off[t + 1] - sc.off[t] > maxlen) maxlen = sc.off[t + 1] - sc.off[t];
+    contrib_t* buf = (contrib_t*)malloc(sizeof(contrib_t) * maxlen);
+    float* prefix = (float*)malloc(sizeof(float) * maxlen);
+    g2d_t* merged = (g2d_t*)calloc(np ? np : 1, sizeof(g2d_t));
+    g2d_t* pg = (g2d_t*)malloc(sizeof(g2d_t) * (np ? np : 1));
+    /* parallel_chunks(H, 16) decomposition (parallel.hpp:30-55), merged in chunk order */
+    const int chunks = v.h < 16 ? v.h : 16;
+    const int per = (v.h + chunks - 1) / chunks;
+    for (int c = 0; c < chunks; ++c) {
+        const int y0 = c * per, y1 = (y0 + per < v.h) ? y0 + per : v.h;
+        if (y0 >= y1) continue;
+        memset(pg, 0, sizeof(g2d_t) * (np ? np : 1));
+        for (int y = y0; y < y1; ++y)
+            for (int x = 0; x < v.w; ++x) {
+                const size_t pix = (size_t)y * v.w + x;
+                const float gc[3] = {grad_ct[4 * pix], grad_ct[4 * pix + 1], grad_ct[4 * pix + 2]};
+                const float gt = grad_ct[4 * pix + 3];
+                const float e = o->grad_skip_eps; /* gc.isZero() && gt == 0 (raster.hpp:285) */
+                if (fabsf(gc[0]) <= e && fabsf(gc[1]) <= e && fabsf(gc[2]) <= e && gt == 0.0f) continue;
+                float d[3];
+                pixel_ray(&v, x, y, d);
+                const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+                const int64_t tile = (int64_t)(y / 16) * v.tx + x / 16;
+                const int64_t n = collect(&sc, s->id, tile, &v, d, px, py, o, sub, buf);
+                composite_backward(buf, n, &sc, o, px, py, gc, gt, pg, prefix);
+            }
+        for (int64_t p = 0; p < np; ++p) {
+            for (int a = 0; a < 2; ++a) merged[p].dm[a] += pg[p].dm[a];
+            for (int a = 0; a < 4; ++a) merged[p].dc[a] += pg[p].dc[a];
+            for (int a = 0; a < 3; ++a) merged[p].dcol[a] += pg[p].dcol[a];
+            merged[p].da += pg[p].da;
+        }
+    }
+    const size_t nsh = (size_t)s->n * s->sh_coeffs * 3;
+    memset(out->d_mu, 0, sizeof(float) * 3 * s->n);
+    memset(out->d_log_scale, 0, sizeof(float) * 3 * s->n);
+    memset(out->d_rotation, 0, sizeof(float) * 4 * s->n);
+    memset(out->d_opacity_logit, 0, sizeof(float) * s->n);
+    memset(out->d_sh, 0, sizeof(float) * nsh);
+    for (int64_t p = 0; p < np; ++p) project_backward(s, sc.src[p], &v, o, &merged[p], out);
+    free(buf);
+    free(prefix);
+    free(merged);
+    free(pg);
+    scene_free(&sc);
+    return 0;
+}
+
+/* adam_apply (optim.hpp:90-126) for every member, step = 1-based count */
+static void adam_scalar(float* th, float* m, float* v, float g, float lr, float b1, float b2, float eps, float bc1,
+                        float bc2) {
+    *m = b1 * *m + (1.0f - b1) * g;
+    *v = b2 * *v + (1.0f - b2) * g * g;
+    const float mhat = *m / bc1, vhat = *v / bc2;
+    *th -= lr * mhat / (sqrtf(vhat) + eps);
+}
+
+int orc_adam(int64_t n, int32_t C, float* mu, float* ls, float* rot, float* op, float* sh, float* m_all,
+             float* v_all, const orc_grads* g, double lr_pos, double lr_scale, double lr_rot, double lr_op,
+             double lr_dc, double lr_rest, double b1d, double b2d, double epsd, uint64_t step) {
+    const float b1 = (float)b1d, b2 = (float)b2d, eps = (float)epsd;
+    const float bc1 = 1.0f - powf(b1, (float)step), bc2 = 1.0f - powf(b2, (float)step);
+    const int rows = 11 + 3 * C;
+    for (int64_t i = 0; i < n; ++i) {
+        float* m = m_all + (size_t)i * rows;
+        float* v = v_all + (size_t)i * rows;
+        for (int a = 0; a < 3; ++a) {
+            adam_scalar(&mu[3 * i + a], &m[a], &v[a], g->d_mu[3 * i + a], (float)lr_pos, b1, b2, eps, bc1, bc2);
+            adam_scalar(&ls[3 * i + a], &m[3 + a], &v[3 + a], g->d_log_scale[3 * i + a], (float)lr_scale, b1, b2, eps,
+                        bc1, bc2);
+        }
+        for (int a = 0; a < 4; ++a)
+            adam_scalar(&rot[4 * i + a], &m[6 + a], &v[6 + a], g->d_rotation[4 * i + a], (float)lr_rot, b1, b2, eps,
+                        bc1, bc2);
+        adam_scalar(&op[i], &m[10], &v[10], g->d_opacity_logit[i], (float)lr_op, b1, b2, eps, bc1, bc2);
+        for (int j = 0; j < C; ++j)
+            for (int a = 0; a < 3; ++a)
+                adam_scalar(&sh[((size_t)i * C + j) * 3 + a], &m[11 + 3 * j + a], &v[11 + 3 * j + a],
+                            g->d_sh[((size_t)i * C + j) * 3 + a], j == 0 ? (float)lr_dc : (float)lr_rest, b1, b2, eps,
+                            bc1, bc2);
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Partition (partition.hpp:93-251)
+ * ------------------------------------------------------------------------- */
+static int fcmp(const void* a, const void* b) {
+    const float x = *(const float*)a, y = *(const float*)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+typedef struct {
+    float planes[16][5];
+    int np;
+    float lo[3], hi[3];
+} region_t;
+
+static void kd_split(float* pts, size_t b, size_t e, int depth, int target, region_t reg, float* out, int* leaf,
+                     int L) {
+    if (depth == target) {
+        for (int i = 0; i < L; ++i)
+            for (int c = 0; c < 5; ++c) out[((size_t)*leaf * L + i) * 5 + c] = reg.planes[i][c];
+        (*leaf)++;
+        return;
+    }
+    int axis = 0;
+    float plane = 0.0f;
+    if (b < e) {
+        float lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = pts[3 * b + a];
+        for (size_t i = b + 1; i < e; ++i)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = fminf_std(lo[a], pts[3 * i + a]);
+                hi[a] = fmaxf_std(hi[a], pts[3 * i + a]);
+            }
+        const float ext[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+        float mx = ext[0];
+        for (int a = 1; a < 3; ++a)
+            if (ext[a] > mx) {
+                mx = ext[a];
+                axis = a;
+            }
+        const size_t n = e - b;
+        float* c = (float*)malloc(sizeof(float) * n);
+        for (size_t i = 0; i < n; ++i) c[i] = pts[3 * (b + i) + axis];
+        qsort(c, n, sizeof(float), fcmp);
+        plane = (n % 2 == 0) ? (c[n / 2 - 1] + c[n / 2]) / 2.0f : c[n / 2];
+        free(c);
+    } else {
+        const float lo = reg.lo[axis], hi = reg.hi[axis];
+        plane = (isfinite(lo) && isfinite(hi)) ? (lo + hi) / 2.0f : isfinite(lo) ? lo + 1.0f : isfinite(hi) ? hi - 1.0f : 0.0f;
+    }
+    size_t mid = b;
+    for (size_t i = b; i < e; ++i)
+        if (pts[3 * i + axis] < plane) {
+            float t[3];
+            memcpy(t, pts + 3 * i, sizeof(t));
+            memcpy(pts + 3 * i, pts + 3 * mid, sizeof(t));
+            memcpy(pts + 3 * mid, t, sizeof(t));
+            ++mid;
+        }
+    region_t left = reg, right = reg;
+    float* lp = left.planes[left.np++];
+    lp[0] = lp[1] = lp[2] = 0.0f;
+    lp[axis] = 1.0f;
+    lp[3] = -plane;
+    lp[4] = 0.0f;
+    left.hi[axis] = fminf_std(left.hi[axis], plane);
+    float* rp = right.planes[right.np++];
+    rp[0] = rp[1] = rp[2] = 0.0f;
+    rp[axis] = -1.0f;
+    rp[3] = plane;
+    rp[4] = 1.0f;
+    right.lo[axis] = fmaxf_std(right.lo[axis], plane);
+    kd_split(pts, b, mid, depth + 1, target, left, out, leaf, L);
+    kd_split(pts, mid, e, depth + 1, target, right, out, leaf, L);
+}
+
+int orc_kdtree(const float* centers, int64_t n, int32_t depth, float* planes5) {
+    if (n <= 0 || depth < 0 || depth > 16) return -1;
+    float* pts = (float*)malloc(sizeof(float) * 3 * n);
+    memcpy(pts, centers, sizeof(float) * 3 * n);
+    region_t root;
+    memset(&root, 0, sizeof(root));
+    for (int a = 0; a < 3; ++a) {
+        root.lo[a] = -INFINITY;
+        root.hi[a] = INFINITY;
+    }
+    int leaf = 0;
+    kd_split(pts, 0, (size_t)n, 0, depth, root, planes5, &leaf, depth);
+    free(pts);
+    return 0;
+}
+
+int orc_assign(const float* planes5, int32_t K, int32_t L, const float* mu, const float* ls, int64_t n, float dm,
+               uint8_t* mask) {
+    for (int64_t i = 0; i < n; ++i) {
+        const float s0 = expf(ls[3 * i]), s1 = expf(ls[3 * i + 1]), s2 = expf(ls[3 * i + 2]);
+        float smax = s0;
+        if (s1 > smax) smax = s1;
+        if (s2 > smax) smax = s2;
+        const float di = dm * smax;
+        for (int k = 0; k < K; ++k) {
+            int member = 1;
+            for (int j = 0; j < L && member; ++j) {
+                const float* p = planes5 + ((size_t)k * L + j) * 5;
+                if (dot3(p, mu + 3 * i) + p[3] > di) member = 0;
+            }
+            mask[i * K + k] = (uint8_t)member;
+        }
+    }
+    return 0;
+}
