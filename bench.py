@@ -252,13 +252,15 @@ def b200_arm(a, world, rank, local_rank):
     n_all = init.n
     rows = 59
     alg_bytes = {
-        # K9+K10: read p, m, v + tile count, write p, m, v for every member (dense Adam)
-        "project_bwd_adam": n_all * (6 * rows * 4 + 4),
+        # K10 streaming Adam: read p, m, v + the 17-float gradient record, write p, m, v (every member)
+        "adam": n_all * (6 * rows * 4 + 17 * 4),
         # K1: 59 params in, 64-B record + 16 B binning data out (lower bound: all visible)
         "preprocess": n_all * (rows * 4 + 4 + 64 + 16),
     }
     launches_per_step = {k: v[1] / max(1, a.steps) for k, v in stages.items()}
-    roof_kernel = dom if dom in alg_bytes else "project_bwd_adam"
+    # the blend kernels are FP32-issue bound (no HBM roofline); report the
+    # dominant HBM-bound kernel, the dense Adam stream
+    roof_kernel = dom if dom in alg_bytes else "adam"
     t_kernel_ms = per_stage[roof_kernel] / max(1.0, launches_per_step.get(roof_kernel, 1.0))
     achieved = alg_bytes[roof_kernel] / (t_kernel_ms / 1e3) / 1e9
     traffic = None

@@ -215,9 +215,10 @@ int dgs_render(dgs_ctx* ctx, const dgs_camera* cam, const float bg[3], float* ou
 /* Per-stage device timing with CUDA events on the context's stream.  Stages:
  * 0 preprocess (K1), 1 binning (K2, incl. CUB sorts), 2 blend_fwd (K4),
  * 3 merge (K5), 4 loss (K6), 5 merge_bwd (K7), 6 blend_bwd (K8),
- * 7 project_bwd_adam (K9+K10), 8 exchange (NCCL).  Accumulated over calls
- * while enabled; dgs_stage_times returns total ms and launch counts. */
-#define DGS_NUM_STAGES 9
+ * 7 project_bwd (K9, gradient record), 8 adam (K10, streaming), 9 exchange
+ * (NCCL).  Accumulated over calls while enabled; dgs_stage_times returns
+ * total ms and launch counts. */
+#define DGS_NUM_STAGES 10
 int dgs_set_profiling(dgs_ctx* ctx, int32_t enabled);
 int dgs_stage_times(dgs_ctx* ctx, double* ms, uint64_t* counts);
 /* CUDA stream the context launches on (cudaStream_t as void*), for timing. */

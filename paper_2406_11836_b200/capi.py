@@ -124,7 +124,7 @@ _SIGS = {
     "dgs_sync": (C.c_int, [_P]),
 }
 
-STAGES = ("preprocess", "binning", "blend_fwd", "merge", "loss", "merge_bwd", "blend_bwd", "project_bwd_adam",
+STAGES = ("preprocess", "binning", "blend_fwd", "merge", "loss", "merge_bwd", "blend_bwd", "project_bwd", "adam",
           "exchange")
 
 _lib = None

@@ -101,11 +101,11 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     ps.T = fmul(ps.T, fsub(1.0f, sigma));
     // suffix_i = sum_{j>i} c_j sigma_j A_j = C - prefix_i, evaluated in double so
     // the difference keeps full relative accuracy (raster.hpp:212-224).
-    const double one_minus = 1.0 - (double)sigma;
     const double s0 = ps.Cf0 - ps.a0, s1 = ps.Cf1 - ps.a1, s2 = ps.Cf2 - ps.a2;
     const double gdc = (double)ps.gc0 * D.x + (double)ps.gc1 * D.y + (double)ps.gc2 * D.z;
-    const double gds = (double)ps.gc0 * s0 + (double)ps.gc1 * s1 + (double)ps.gc2 * s2;
-    const float d_sigma = (float)(gdc * a_i - gds / one_minus - (double)ps.gT * (double)ps.Tf / one_minus);
+    const double num = (double)ps.gc0 * s0 + (double)ps.gc1 * s1 + (double)ps.gc2 * s2 + (double)ps.gT * (double)ps.Tf;
+    const float inv_om = __frcp_rn(1.0f - sigma);  // 1/(1-sigma), sigma <= 0.99
+    const float d_sigma = (float)(gdc * a_i - num * (double)inv_om);
     v[5] = ps.gc0 * w;
     v[6] = ps.gc1 * w;
     v[7] = ps.gc2 * w;
@@ -126,7 +126,7 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     v[4] = h * (w1 * w1);
 }
 
-__global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, RenderOpts ro, Subspace gate,
+__global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, RenderOpts ro, Subspace gate,
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
                                                              const uint2* __restrict__ ranges,
@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(ViewParams vp, Rend
             }
             const unsigned gm = __ballot_sync(kFull, go);
             const int leader = __ffs(gm) - 1;
-            if (gm == (1u << leader)) {  // a single lane: no reduction needed
-                if (lane == leader) {
+            if (__popc(gm) <= 2) {  // one or two lanes: direct atomics beat a 45-shuffle butterfly
+                if (go) {
 #pragma unroll
                     for (int f = 0; f < 9; ++f)
                         if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);

@@ -109,7 +109,7 @@ struct SubsetState {
     int sh_coeffs = 16;
     int rows = 59;
     size_t ld = 0;
-    DevBuf<float> P, M, V, G, g2d;
+    DevBuf<float> P, M, V, G, g2d, rec;
     DevBuf<uint32_t> ids32;
     std::vector<uint64_t> ids64;
     uint64_t adam_step = 0, epoch = 0;
@@ -122,7 +122,7 @@ struct SubsetState {
 
 /// Event pairs around every stage launch, resolved at the next sync point.
 struct StageTimer {
-    static constexpr int kStages = 9;
+    static constexpr int kStages = 10;
     bool on = false;
     double ms[kStages] = {};
     uint64_t count[kStages] = {};
@@ -182,7 +182,7 @@ struct Stage {
     }
     ~Stage() { end(); }
 };
-enum { kStPre = 0, kStBin, kStFwd, kStMerge, kStLoss, kStMergeBwd, kStBwd, kStAdam, kStExchange };
+enum { kStPre = 0, kStBin, kStFwd, kStMerge, kStLoss, kStMergeBwd, kStBwd, kStProjBwd, kStAdam, kStExchange };
 
 struct Ctx {
     int device = 0, rank = 0, world = 1;
@@ -977,16 +977,31 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             for (int v = 0; v < batch; ++v) {
                 ViewSlot& vs = S.slot(v);
                 backward_blend(*ctx, S, v, ctx->stats.p + 1);
-                Stage st(ctx->timer, kStAdam, ctx->stream);
                 if (v + 1 < batch) {
+                    Stage st(ctx->timer, kStProjBwd, ctx->stream);
                     launch_project_bwd((int)S.n, S.P.p, S.ld, S.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S.g2d.p,
                                        S.ld, S.G.p, ctx->bad.p, ctx->stream);
+                    ++ctx->launches;
                 } else {
+                    // K9 (gradient record) + K10 (streaming Adam) with a split event between them
+                    S.rec.ensure((size_t)kGradRecordRows * S.ld);
+                    cudaEvent_t a = nullptr, mid = nullptr, b = nullptr;
+                    if (ctx->timer.on) {
+                        a = ctx->timer.get();
+                        mid = ctx->timer.get();
+                        CK(cudaEventRecord(a, ctx->stream));
+                    }
                     launch_project_bwd_adam((int)S.n, S.P.p, S.M.p, S.V.p, S.ld, S.sh_coeffs, vs.vp, ctx->ro,
                                             vs.vb.counts, S.g2d.p, S.ld, batch > 1 ? S.G.p : nullptr, ap, ctx->bad.p,
-                                            ctx->stream);
+                                            S.rec.p, mid, ctx->stream);
+                    if (ctx->timer.on) {
+                        b = ctx->timer.get();
+                        CK(cudaEventRecord(b, ctx->stream));
+                        ctx->timer.pending.push_back({kStProjBwd, {a, mid}});
+                        ctx->timer.pending.push_back({kStAdam, {mid, b}});
+                    }
+                    ctx->launches += 2;
                 }
-                ++ctx->launches;
             }
             ++S.adam_step;
         }
