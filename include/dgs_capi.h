@@ -200,10 +200,27 @@ int dgs_adam_apply(dgs_ctx* ctx, int32_t k, const dgs_splats* grads);
 
 /* ---- The hot path: Manager<float>::train_step (manager.hpp:313-386) ----------- */
 /* One barrier-synchronised training step over a batch of B views.
+ * Multi-rank (world > 1): every rank calls it with the same cameras; rank r
+ * must hold exactly the subsets k with dgs_subset_owner(k, K, world) == r;
+ * partial rows are exchanged with NCCL all-to-all (grouped send/recv),
+ * loss sums are all-reduced.
  * targets: B x H x W x 3 floats (Image<float> layout).  targets_on_device = 0:
  * host pointer, copied in; 1: device pointer to B planar [3][H][W] images. */
 int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
                    int32_t targets_on_device, const float bg[3], dgs_step_result* out);
+/* Multi-rank plan: rank j owns pixel rows [r0, r1) of every
+ * view for merge + loss, with a 10-row SSIM halo [h0, h1); subset k lives on
+ * rank dgs_subset_owner(k, K, world).  rows4 = {r0, r1, h0, h1}. */
+int dgs_slice_plan(int32_t height, int32_t slices, int32_t s, int32_t* rows4);
+int32_t dgs_subset_owner(int32_t k, int32_t k_count, int32_t world);
+/* Single-rank test mode: run the multi-rank manager path (halo windows,
+ * exchange buffers, per-slice loss sums) over `slices` virtual slices with
+ * device copies in place of NCCL.  Default 1 (whole image, zero-copy). */
+int dgs_set_virtual_slices(dgs_ctx* ctx, int32_t slices);
+/* Partial map (C_k, T_k) and its gradient (dL/dC_k, dL/dT_k) of local
+ * subset k for view slot v of the last dgs_train_step (debug / parity):
+ * H*W*4 floats each (either may be NULL). */
+int dgs_dump_grad_maps(dgs_ctx* ctx, int32_t k, int32_t view, float* partial_ct, float* grad_ct);
 /* Upload B targets (HWC host) once into a device planar buffer owned by ctx;
  * returns the device pointer for dgs_train_step(targets_on_device = 1). */
 int dgs_upload_targets(dgs_ctx* ctx, int32_t batch, int32_t width, int32_t height, const float* targets_hwc,

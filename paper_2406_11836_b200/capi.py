@@ -120,6 +120,10 @@ _SIGS = {
     "dgs_render": (C.c_int, [_P, C.POINTER(Camera), _P, _P, _P]),
     "dgs_set_profiling": (C.c_int, [_P, C.c_int32]),
     "dgs_stage_times": (C.c_int, [_P, _P, _P]),
+    "dgs_set_virtual_slices": (C.c_int, [_P, C.c_int32]),
+    "dgs_slice_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P]),
+    "dgs_subset_owner": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32]),
+    "dgs_dump_grad_maps": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
     "dgs_stream": (_P, [_P]),
     "dgs_sync": (C.c_int, [_P]),
 }

@@ -201,6 +201,9 @@ struct Ctx {
     DevBuf<const float4*> partial_ptrs;
     DevBuf<float4*> grad_ptrs;
     DevBuf<float4> scratch_maps, scratch_grads;
+    DevBuf<float4> xrecv, xgrad;   // sliced exchange buffers (K x halo rows, K x owned rows)
+    DevBuf<float> targets_win;
+    int virtual_slices = 1;        // single-rank sliced mode (tests the multi-rank manager path)
     DevBuf<BlendStats> stats;
     DevBuf<int> bad;
     uint64_t launches = 0;
@@ -442,6 +445,92 @@ const float* ensure_kernel(Ctx& ctx) {
         CK(cudaMemcpy(ctx.kern.p, k, sizeof(k), cudaMemcpyHostToDevice));
     }
     return ctx.kern.p;
+}
+
+/// Pixel-row slice owned by slice s of S (contiguous, balanced) and its
+/// SSIM halo: the loss gradient at row y reads merged rows y-10..y+10
+/// (two 5-row blur stages, loss.hpp:130-140).
+struct SliceRows {
+    int r0, r1, h0, h1;
+};
+constexpr int kSsimHalo = 10;
+SliceRows slice_rows(int H, int S, int s) {
+    SliceRows R;
+    R.r0 = (int)((int64_t)H * s / S);
+    R.r1 = (int)((int64_t)H * (s + 1) / S);
+    R.h0 = std::max(0, R.r0 - kSsimHalo);
+    R.h1 = std::min(H, R.r1 + kSsimHalo);
+    return R;
+}
+/// Rank that owns KD subset k (contiguous blocks of subsets per rank).
+int subset_owner(int k, int K, int W) { return (int)((int64_t)k * W / K); }
+
+/// Forward exchange for slice `sl`: rows [h0, h1) of every subset's partial
+/// map land in ctx.xrecv[k].  Multi-rank: one NCCL group of send/recv (the
+/// all-to-all of manager.hpp:280-293's gather, sliced); single rank
+/// (virtual slices): device copies with the same layout.  Returns bytes sent
+/// over NCCL.
+uint64_t exchange_forward(Ctx& ctx, int v, const std::vector<int>& local, int Wd, int H, int S, int sl) {
+    const int K = ctx.table.k_count, W = ctx.world, rank = ctx.rank;
+    const SliceRows me = slice_rows(H, S, sl);
+    const size_t hr = (size_t)(me.h1 - me.h0);
+    uint64_t sent = 0;
+    if (W > 1) {
+        NK(nccl().GroupStart());
+        for (int k : local) {
+            const float4* src = subset(ctx, k).slot(v).ct.p;
+            for (int j = 0; j < W; ++j) {
+                if (j == rank) continue;
+                const SliceRows R = slice_rows(H, S, j);
+                const size_t cnt = (size_t)(R.h1 - R.h0) * Wd * 4;
+                NK(nccl().Send(src + (size_t)R.h0 * Wd, cnt, ncclFloat, j, ctx.comm, ctx.stream));
+                sent += cnt * 4;
+            }
+        }
+        for (int k = 0; k < K; ++k) {
+            const int o = subset_owner(k, K, W);
+            if (o == rank) continue;
+            NK(nccl().Recv(ctx.xrecv.p + (size_t)k * hr * Wd, hr * Wd * 4, ncclFloat, o, ctx.comm, ctx.stream));
+        }
+        NK(nccl().GroupEnd());
+    }
+    for (int k : local)  // own subsets: local copy
+        CK(cudaMemcpyAsync(ctx.xrecv.p + (size_t)k * hr * Wd, subset(ctx, k).slot(v).ct.p + (size_t)me.h0 * Wd,
+                           hr * Wd * sizeof(float4), cudaMemcpyDeviceToDevice, ctx.stream));
+    return sent;
+}
+
+/// Backward exchange for slice `sl`: (dL/dC_k, dL/dT_k) rows [r0, r1) from
+/// ctx.xgrad[k] to the rank holding subset k (manager.hpp:336-343's
+/// scatter, sliced).
+uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int Wd, int H, int S, int sl) {
+    const int K = ctx.table.k_count, W = ctx.world, rank = ctx.rank;
+    const SliceRows me = slice_rows(H, S, sl);
+    const size_t orows = (size_t)(me.r1 - me.r0);
+    uint64_t sent = 0;
+    if (W > 1) {
+        NK(nccl().GroupStart());
+        for (int k = 0; k < K; ++k) {
+            const int o = subset_owner(k, K, W);
+            if (o == rank) continue;
+            NK(nccl().Send(ctx.xgrad.p + (size_t)k * orows * Wd, orows * Wd * 4, ncclFloat, o, ctx.comm, ctx.stream));
+            sent += orows * Wd * 16;
+        }
+        for (int k : local) {
+            float4* dst = subset(ctx, k).slot(v).grad_ct.p;
+            for (int j = 0; j < W; ++j) {
+                if (j == rank) continue;
+                const SliceRows R = slice_rows(H, S, j);
+                NK(nccl().Recv(dst + (size_t)R.r0 * Wd, (size_t)(R.r1 - R.r0) * Wd * 4, ncclFloat, j, ctx.comm,
+                               ctx.stream));
+            }
+        }
+        NK(nccl().GroupEnd());
+    }
+    for (int k : local)
+        CK(cudaMemcpyAsync(subset(ctx, k).slot(v).grad_ct.p + (size_t)me.r0 * Wd, ctx.xgrad.p + (size_t)k * orows * Wd,
+                           orows * Wd * sizeof(float4), cudaMemcpyDeviceToDevice, ctx.stream));
+    return sent;
 }
 
 void require_table(const Ctx& ctx) {
@@ -719,8 +808,8 @@ int dgs_merge(dgs_ctx* ctx, const dgs_camera* cam, const float* partials, const 
         ctx->merged.ensure(3 * px);
         ctx->staging.ensure(4 * px);
         const int owner = table_locate(ctx->table, vp.o);
-        launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, vp.height, 0, bg, ctx->merged.p,
-                     ctx->staging.p + 3 * px, ctx->stream);
+        launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, 0, bg, ctx->merged.p,
+                     ctx->staging.p + 3 * px, 0, vp.height, ctx->stream);
         k_planar_to_hwc<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->merged.p, ctx->staging.p, px);
         CK(cudaMemcpyAsync(out_rgb, ctx->staging.p, 3 * px * 4, cudaMemcpyDeviceToHost, ctx->stream));
         if (out_t) CK(cudaMemcpyAsync(out_t, ctx->staging.p + 3 * px, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -747,7 +836,7 @@ int dgs_loss(dgs_ctx* ctx, int32_t width, int32_t height, const float* render, c
         const int max_blocks = ((width + 31) / 32) * ((height + 31) / 32) * 3;
         ctx->block_sums.ensure((size_t)max_blocks * 3);
         ctx->sums.ensure(3);
-        launch_loss(width, height, 0, height, ctx->merged.p, tgt.p, (float)lambda, ensure_kernel(*ctx),
+        launch_loss(width, height, 0, height, 0, height, ctx->merged.p, tgt.p, (float)lambda, ensure_kernel(*ctx),
                     (float)inv_batch, ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
         launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p, ctx->stream);
         k_planar_to_hwc<<<g, 256, 0, ctx->stream>>>(ctx->grad_rgb.p, ctx->staging.p, px);
@@ -786,8 +875,8 @@ int dgs_merge_backward(dgs_ctx* ctx, const dgs_camera* cam, const float* partial
         CK(cudaMemcpyAsync(ctx->staging.p, grad_color, 3 * px * 4, cudaMemcpyHostToDevice, ctx->stream));
         k_hwc_to_planar<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->staging.p, ctx->grad_rgb.p, px);
         const int owner = table_locate(ctx->table, vp.o);
-        launch_merge_bwd(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, vp.height, 0,
-                         ctx->grad_rgb.p, bg, ctx->grad_ptrs.p, vp.height, 0, ctx->stream);
+        launch_merge_bwd(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, 0, ctx->grad_rgb.p, 0,
+                         vp.height, bg, ctx->grad_ptrs.p, 0, ctx->stream);
         CK(cudaMemcpyAsync(out_grads, ctx->scratch_grads.p, px * K * sizeof(float4), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     });
@@ -873,8 +962,8 @@ int dgs_render(dgs_ctx* ctx, const dgs_camera* cam, const float bg[3], float* ou
         ctx->merged.ensure(3 * px);
         ctx->staging.ensure(4 * px);
         const int owner = table_locate(ctx->table, vp.o);
-        launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, vp.height, 0, bg, ctx->merged.p,
-                     ctx->staging.p + 3 * px, ctx->stream);
+        launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p, 0, bg, ctx->merged.p,
+                     ctx->staging.p + 3 * px, 0, vp.height, ctx->stream);
         k_planar_to_hwc<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->merged.p, ctx->staging.p, px);
         if (out_rgb) CK(cudaMemcpyAsync(out_rgb, ctx->staging.p, 3 * px * 4, cudaMemcpyDeviceToHost, ctx->stream));
         if (out_t) CK(cudaMemcpyAsync(out_t, ctx->staging.p + 3 * px, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -889,111 +978,159 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         if (batch < 1 || cams == nullptr || targets == nullptr)
             throw std::invalid_argument("train_step: need one target per camera");
         if (batch != ctx->cfg.batch_size) throw std::invalid_argument("train_step: batch size mismatch with config");
-        if (ctx->world != 1) throw std::invalid_argument("train_step: multi-rank exchange not built into this call");
-        const int K = ctx->table.k_count;
-        for (int k = 0; k < K; ++k) subset(*ctx, k);  // merge needs every subset (engine.hpp:160-163)
+        const int K = ctx->table.k_count, W = ctx->world, rank = ctx->rank;
+        std::vector<int> local;
+        for (int k = 0; k < K; ++k) {
+            const int o = subset_owner(k, K, W);
+            const bool here = ctx->subsets.count(k) != 0;
+            if (W == 1 && !here) throw std::invalid_argument("merge: missing subset partials: " + std::to_string(k));
+            if (W > 1 && (o == rank) != here)
+                throw std::invalid_argument("train_step: subset " + std::to_string(k) + " must live on rank " +
+                                            std::to_string(o));
+            if (here) local.push_back(k);
+        }
         const uint64_t launches0 = ctx->launches;
+        uint64_t nccl_bytes = 0;
         CK(cudaMemsetAsync(ctx->stats.p, 0, 2 * sizeof(BlendStats), ctx->stream));
         std::vector<ViewParams> vps(batch);
-        std::vector<double> sums(3 * batch);
         uint64_t pairs = 0;
         const float lam = (float)ctx->cfg.lambda_ssim;
         const float inv_batch = 1.0f / (float)batch;  // manager.hpp:329
-        ctx->partial_ptrs.ensure((size_t)K * batch);
-        ctx->grad_ptrs.ensure((size_t)K * batch);
-        ctx->sums.ensure(3 * batch);
+        const int S = W > 1 ? W : std::max(1, ctx->virtual_slices);
+        const bool zero_copy = (W == 1 && S == 1);
+        ctx->partial_ptrs.ensure((size_t)K);
+        ctx->grad_ptrs.ensure((size_t)K);
+        ctx->sums.ensure((size_t)3 * batch * S);
         for (int v = 0; v < batch; ++v) {
             vps[v] = view_params(cams[v]);
             const ViewParams& vp = vps[v];
             if (v > 0 && (vp.width != vps[0].width || vp.height != vps[0].height))
                 throw std::invalid_argument("train_step: all views of a batch must share a resolution");
-            const size_t px = (size_t)vp.width * vp.height;
+            const int Wd = vp.width, H = vp.height;
+            const size_t px = (size_t)Wd * H;
             // ---- render_batch (manager.hpp:262-304): per-subset partials ----
-            std::vector<const float4*> ptrs(K);
-            std::vector<float4*> gptrs(K);
-            for (int k = 0; k < K; ++k) {
-                SubsetState& S = subset(*ctx, k);
-                forward_subset(*ctx, S, v, vp, 0, nullptr, nullptr, ctx->stats.p);
-                ViewSlot& vs = S.slot(v);
-                pairs += (uint64_t)vs.vb.pairs;
-                ptrs[k] = vs.ct.p;
-                gptrs[k] = vs.grad_ct.ensure(px);
+            for (int k : local) {
+                SubsetState& S_ = subset(*ctx, k);
+                forward_subset(*ctx, S_, v, vp, 0, nullptr, nullptr, ctx->stats.p);
+                pairs += (uint64_t)S_.slot(v).vb.pairs;
+                S_.slot(v).grad_ct.ensure(px);
             }
-            CK(cudaMemcpyAsync(ctx->partial_ptrs.p + (size_t)K * v, ptrs.data(), K * sizeof(void*),
-                               cudaMemcpyHostToDevice, ctx->stream));
-            CK(cudaMemcpyAsync(ctx->grad_ptrs.p + (size_t)K * v, gptrs.data(), K * sizeof(void*),
-                               cudaMemcpyHostToDevice, ctx->stream));
             const int owner = table_locate(ctx->table, vp.o);
-            ctx->merged.ensure(3 * px);
-            {
-                Stage st(ctx->timer, kStMerge, ctx->stream);
-                launch_merge(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v,
-                             vp.height, 0, bg, ctx->merged.p, nullptr, ctx->stream);
-            }
-            ++ctx->launches;
-            // ---- loss (manager.hpp:331-334) ----
-            const float* tgt;
-            if (targets_on_device) {
-                tgt = targets + (size_t)v * 3 * px;
-            } else {
-                ctx->staging.ensure(3 * px);
-                ctx->targets.ensure(3 * px);
-                CK(cudaMemcpyAsync(ctx->staging.p, targets + (size_t)v * 3 * px, 3 * px * 4, cudaMemcpyHostToDevice,
-                                   ctx->stream));
-                k_hwc_to_planar<<<(unsigned)((px + 255) / 256), 256, 0, ctx->stream>>>(ctx->staging.p,
-                                                                                        ctx->targets.p, px);
-                ++ctx->launches;
-                tgt = ctx->targets.p;
-            }
-            ctx->grad_rgb.ensure(3 * px);
-            const int max_blocks = ((vp.width + 31) / 32) * ((vp.height + 31) / 32) * 3;
-            ctx->block_sums.ensure((size_t)max_blocks * 3);
-            int nb = 0;
             const float* kern = ensure_kernel(*ctx);
-            {
-                Stage st(ctx->timer, kStLoss, ctx->stream);
-                launch_loss(vp.width, vp.height, 0, vp.height, ctx->merged.p, tgt, lam, kern, inv_batch,
-                            ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
-                launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p + 3 * v, ctx->stream);
+            const std::vector<int> slices = W > 1 ? std::vector<int>{rank} : [&] {
+                std::vector<int> a(S);
+                for (int i = 0; i < S; ++i) a[i] = i;
+                return a;
+            }();
+            for (int sl : slices) {
+                const SliceRows R = slice_rows(H, S, sl);
+                const int hr = R.h1 - R.h0, orows = R.r1 - R.r0;
+                // ---- forward exchange: partial rows [h0, h1) of every subset -> this slice ----
+                std::vector<const float4*> ptrs(K);
+                std::vector<float4*> gptrs(K);
+                int prow0 = 0, grow0 = 0;
+                if (zero_copy) {
+                    for (int k = 0; k < K; ++k) {
+                        ptrs[k] = subset(*ctx, k).slot(v).ct.p;
+                        gptrs[k] = subset(*ctx, k).slot(v).grad_ct.p;
+                    }
+                } else {
+                    ctx->xrecv.ensure((size_t)K * hr * Wd);
+                    ctx->xgrad.ensure((size_t)K * orows * Wd);
+                    for (int k = 0; k < K; ++k) {
+                        ptrs[k] = ctx->xrecv.p + (size_t)k * hr * Wd;
+                        gptrs[k] = ctx->xgrad.p + (size_t)k * orows * Wd;
+                    }
+                    prow0 = R.h0;
+                    grow0 = R.r0;
+                    Stage st(ctx->timer, kStExchange, ctx->stream);
+                    nccl_bytes += exchange_forward(*ctx, v, local, Wd, H, S, sl);
+                }
+                CK(cudaMemcpyAsync(ctx->partial_ptrs.p, ptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+                CK(cudaMemcpyAsync(ctx->grad_ptrs.p, gptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+                // ---- merge (engine.hpp:152-182) over rows [h0, h1) ----
+                ctx->merged.ensure((size_t)3 * hr * Wd);
+                {
+                    Stage st(ctx->timer, kStMerge, ctx->stream);
+                    launch_merge(vp, ctx->table_dev.p, owner, R.h0, R.h1, ctx->partial_ptrs.p, prow0, bg,
+                                 ctx->merged.p, nullptr, R.h0, hr, ctx->stream);
+                }
+                // ---- target window ----
+                ctx->targets_win.ensure((size_t)3 * hr * Wd);
+                const float* tgt;
+                if (targets_on_device && zero_copy) {
+                    tgt = targets + (size_t)v * 3 * px;
+                } else if (targets_on_device) {
+                    for (int c = 0; c < 3; ++c)
+                        CK(cudaMemcpyAsync(ctx->targets_win.p + (size_t)c * hr * Wd,
+                                           targets + (size_t)v * 3 * px + (size_t)c * px + (size_t)R.h0 * Wd,
+                                           (size_t)hr * Wd * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+                    tgt = ctx->targets_win.p;
+                } else {
+                    ctx->staging.ensure((size_t)3 * hr * Wd);
+                    CK(cudaMemcpyAsync(ctx->staging.p, targets + (size_t)v * 3 * px + (size_t)R.h0 * Wd * 3,
+                                       (size_t)hr * Wd * 12, cudaMemcpyHostToDevice, ctx->stream));
+                    k_hwc_to_planar<<<(unsigned)(((size_t)hr * Wd + 255) / 256), 256, 0, ctx->stream>>>(
+                        ctx->staging.p, ctx->targets_win.p, (size_t)hr * Wd);
+                    ++ctx->launches;
+                    tgt = ctx->targets_win.p;
+                }
+                // ---- loss (manager.hpp:331-334) on owned rows [r0, r1) ----
+                ctx->grad_rgb.ensure((size_t)3 * hr * Wd);
+                const int max_blocks = ((Wd + 31) / 32) * ((orows + 31) / 32) * 3;
+                ctx->block_sums.ensure((size_t)max_blocks * 3);
+                int nb = 0;
+                {
+                    Stage st(ctx->timer, kStLoss, ctx->stream);
+                    launch_loss(Wd, H, R.r0, R.r1, R.h0, hr, ctx->merged.p, tgt, lam, kern, inv_batch,
+                                ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
+                    launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p + (size_t)3 * (v * S + sl), ctx->stream);
+                }
+                // ---- merge_backward (engine.hpp:195-234) on owned rows ----
+                {
+                    Stage st(ctx->timer, kStMergeBwd, ctx->stream);
+                    launch_merge_bwd(vp, ctx->table_dev.p, owner, R.r0, R.r1, ctx->partial_ptrs.p, prow0,
+                                     ctx->grad_rgb.p, R.h0, hr, bg, ctx->grad_ptrs.p, grow0, ctx->stream);
+                }
+                ctx->launches += 4;
+                // ---- backward exchange: (dL/dC_k, dL/dT_k) rows [r0, r1) -> subset owners ----
+                if (!zero_copy) {
+                    Stage st(ctx->timer, kStExchange, ctx->stream);
+                    nccl_bytes += exchange_backward(*ctx, v, local, Wd, H, S, sl);
+                }
             }
-            // ---- merge_backward (engine.hpp:195-234) ----
-            {
-                Stage st(ctx->timer, kStMergeBwd, ctx->stream);
-                launch_merge_bwd(vp, ctx->table_dev.p, owner, 0, vp.height, ctx->partial_ptrs.p + (size_t)K * v,
-                                 vp.height, 0, ctx->grad_rgb.p, bg, ctx->grad_ptrs.p + (size_t)K * v, vp.height, 0,
-                                 ctx->stream);
-            }
-            ctx->launches += 3;
         }
         // ---- MsgBackwardTask x B, then apply_step (worker.hpp:86-127, 162-167) ----
         reset_bad(*ctx);
-        for (int k = 0; k < K; ++k) {
-            SubsetState& S = subset(*ctx, k);
-            const AdamParams ap = adam_params(*ctx, S, S.adam_step + 1);
+        for (int k : local) {
+            SubsetState& S_ = subset(*ctx, k);
+            const AdamParams ap = adam_params(*ctx, S_, S_.adam_step + 1);
             if (batch > 1) {
-                S.G.ensure(S.rows * S.ld);
-                CK(cudaMemsetAsync(S.G.p, 0, S.rows * S.ld * sizeof(float), ctx->stream));
+                S_.G.ensure(S_.rows * S_.ld);
+                CK(cudaMemsetAsync(S_.G.p, 0, S_.rows * S_.ld * sizeof(float), ctx->stream));
             }
             for (int v = 0; v < batch; ++v) {
-                ViewSlot& vs = S.slot(v);
-                backward_blend(*ctx, S, v, ctx->stats.p + 1);
+                ViewSlot& vs = S_.slot(v);
+                backward_blend(*ctx, S_, v, ctx->stats.p + 1);
                 if (v + 1 < batch) {
                     Stage st(ctx->timer, kStProjBwd, ctx->stream);
-                    launch_project_bwd((int)S.n, S.P.p, S.ld, S.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S.g2d.p,
-                                       S.ld, S.G.p, ctx->bad.p, ctx->stream);
+                    launch_project_bwd((int)S_.n, S_.P.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S_.g2d.p,
+                                       S_.ld, S_.G.p, ctx->bad.p, ctx->stream);
                     ++ctx->launches;
                 } else {
                     // K9 (gradient record) + K10 (streaming Adam) with a split event between them
-                    S.rec.ensure((size_t)kGradRecordRows * S.ld);
+                    S_.rec.ensure((size_t)kGradRecordRows * S_.ld);
                     cudaEvent_t a = nullptr, mid = nullptr, b = nullptr;
                     if (ctx->timer.on) {
                         a = ctx->timer.get();
                         mid = ctx->timer.get();
                         CK(cudaEventRecord(a, ctx->stream));
                     }
-                    launch_project_bwd_adam((int)S.n, S.P.p, S.M.p, S.V.p, S.ld, S.sh_coeffs, vs.vp, ctx->ro,
-                                            vs.vb.counts, S.g2d.p, S.ld, batch > 1 ? S.G.p : nullptr, ap, ctx->bad.p,
-                                            S.rec.p, mid, ctx->stream);
+                    launch_project_bwd_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro,
+                                            vs.vb.counts, S_.g2d.p, S_.ld, batch > 1 ? S_.G.p : nullptr, ap,
+                                            ctx->bad.p, S_.rec.p, mid, ctx->stream);
                     if (ctx->timer.on) {
                         b = ctx->timer.get();
                         CK(cudaEventRecord(b, ctx->stream));
@@ -1003,9 +1140,24 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                     ctx->launches += 2;
                 }
             }
-            ++S.adam_step;
+            ++S_.adam_step;
         }
-        CK(cudaMemcpyAsync(sums.data(), ctx->sums.p, 3 * batch * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        // loss sums: slices of this rank (fixed order), then across ranks
+        std::vector<double> sums((size_t)3 * batch * S);
+        if (W > 1) {
+            // every rank wrote only its own slice entry; zero the others and sum across ranks
+            std::vector<double> mine((size_t)3 * batch * S, 0.0);
+            CK(cudaMemcpyAsync(sums.data(), ctx->sums.p, sums.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            for (int v = 0; v < batch; ++v)
+                for (int q = 0; q < 3; ++q) mine[(size_t)3 * (v * S + rank) + q] = sums[(size_t)3 * (v * S + rank) + q];
+            CK(cudaMemcpyAsync(ctx->sums.p, mine.data(), mine.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            {
+                Stage st(ctx->timer, kStExchange, ctx->stream);
+                NK(nccl().AllReduce(ctx->sums.p, ctx->sums.p, mine.size(), ncclDouble, ncclSum, ctx->comm, ctx->stream));
+            }
+        }
+        CK(cudaMemcpyAsync(sums.data(), ctx->sums.p, sums.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         BlendStats st[2]{};
         CK(cudaMemcpyAsync(st, ctx->stats.p, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
         int bad = INT_MAX;
@@ -1014,25 +1166,27 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         CK(cudaGetLastError());
         ctx->timer.resolve();
         if (bad != INT_MAX) {
-            // which subset: report the first loaded subset whose id range covers it
             throw std::runtime_error("partial_render_backward: non-finite gradient for splat id " +
-                                     std::to_string(subset(*ctx, 0).ids64[(size_t)bad]));
+                                     std::to_string(subset(*ctx, local[0]).ids64[(size_t)bad]));
         }
         if (out) {
             std::memset(out, 0, sizeof(*out));
             double loss = 0.0, mse = 0.0;
             const double lambda = ctx->cfg.lambda_ssim;
             for (int v = 0; v < batch; ++v) {
+                double s3[3] = {0.0, 0.0, 0.0};
+                for (int sl = 0; sl < S; ++sl)
+                    for (int q = 0; q < 3; ++q) s3[q] += sums[(size_t)3 * (v * S + sl) + q];
                 const double n = 3.0 * vps[v].width * vps[v].height;
-                loss += ((1.0 - lambda) * (sums[3 * v] / n) + lambda * (1.0 - sums[3 * v + 1] / n)) / batch;
-                mse += (sums[3 * v + 2] / n) / batch;
+                loss += ((1.0 - lambda) * (s3[0] / n) + lambda * (1.0 - s3[1] / n)) / batch;
+                mse += (s3[2] / n) / batch;
             }
             out->loss = loss;
             out->psnr = mse == 0.0 ? INFINITY : 10.0 * std::log10(1.0 / mse);
             // reference accounting (manager.hpp:384): every partial map and its
             // gradient cross a link: 2 * K * H * W * 4 * sizeof(float) per view.
             out->comm_bytes = (uint64_t)2 * K * batch * (uint64_t)vps[0].width * vps[0].height * 4 * sizeof(float);
-            out->nccl_bytes = 0;
+            out->nccl_bytes = nccl_bytes;
             out->pairs = pairs;
             out->evals_fwd = st[0].evals;
             out->contribs_fwd = st[0].contribs;
@@ -1043,5 +1197,40 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         }
     });
 }
+
+int dgs_dump_grad_maps(dgs_ctx* ctx, int32_t k, int32_t view, float* partial_ct, float* grad_ct) {
+    return dgs_guard([&] {
+        SubsetState& S = subset(*ctx, k);
+        if (view < 0 || view >= (int)S.slots.size()) throw std::invalid_argument("dump_grad_maps: no such view slot");
+        ViewSlot& vs = S.slot(view);
+        const size_t px = (size_t)vs.vp.width * vs.vp.height;
+        if (partial_ct) CK(cudaMemcpy(partial_ct, vs.ct.p, px * sizeof(float4), cudaMemcpyDeviceToHost));
+        if (grad_ct) {
+            if (!vs.grad_ct.p) throw std::invalid_argument("dump_grad_maps: no backward has run");
+            CK(cudaMemcpy(grad_ct, vs.grad_ct.p, px * sizeof(float4), cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+int dgs_set_virtual_slices(dgs_ctx* ctx, int32_t slices) {
+    return dgs_guard([&] {
+        if (slices < 1) throw std::invalid_argument("virtual slices must be >= 1");
+        if (ctx->world > 1 && slices != 1) throw std::invalid_argument("virtual slices are a single-rank mode");
+        ctx->virtual_slices = slices;
+    });
+}
+
+int dgs_slice_plan(int32_t height, int32_t slices, int32_t s, int32_t* rows4) {
+    return dgs_guard([&] {
+        if (height < 1 || slices < 1 || s < 0 || s >= slices) throw std::invalid_argument("slice_plan: bad arguments");
+        const SliceRows R = slice_rows(height, slices, s);
+        rows4[0] = R.r0;
+        rows4[1] = R.r1;
+        rows4[2] = R.h0;
+        rows4[3] = R.h1;
+    });
+}
+
+int32_t dgs_subset_owner(int32_t k, int32_t k_count, int32_t world) { return subset_owner(k, k_count, world); }
 
 }  // extern "C"

@@ -62,25 +62,29 @@ void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
                                const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
                                const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s);
 
-// K3/K5: per-pixel subset order + merge (engine.hpp:108-182). Rows [row0, row1).
+// Row windows: an array "with base b and rows r" holds image rows [b, b + r)
+// (planar arrays: plane = r * W).  partials[k] / grad_out[k] hold float4
+// rows starting at prow0 / grow0.
+// K3/K5: per-pixel subset order + merge (engine.hpp:108-182) for rows [row0, row1).
 void launch_merge(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
-                  const float4* const* partials, int pstride_rows, int prow0, const float bg[3], float* out_rgb,
-                  float* out_t, cudaStream_t s);
+                  const float4* const* partials, int prow0, const float bg[3], float* out_rgb, float* out_t,
+                  int out_base, int out_rows, cudaStream_t s);
 void launch_pixel_orders(const ViewParams& vp, const Table* tb_dev, int owner, uint16_t* order, uint16_t* count,
                          int kstride, cudaStream_t s);
 
-// K6: fused L1 + D-SSIM forward and gradient (loss.hpp:33-177), per channel plane.
-// x, y: planar [3][H][W]; grad: planar [3][H][W]; partial sums per block (double[3] each).
-// `kernel` is the 11-tap window in device memory.
-void launch_loss(int W, int H, int row0, int row1, const float* x, const float* y, float lambda,
-                 const float* kernel, float inv_batch, float* grad, double* block_sums, int* n_blocks,
+// K6: fused L1 + D-SSIM forward and gradient (loss.hpp:33-177), per channel plane,
+// outputs for rows [row0, row1); x, y, grad: planar windows (in_base, in_rows)
+// that must cover [row0 - 10, row1 + 10) clipped to the image.
+// Partial sums per block (double[3] each).  `kernel`: 11 taps in device memory.
+void launch_loss(int W, int H, int row0, int row1, int in_base, int in_rows, const float* x, const float* y,
+                 float lambda, const float* kernel, float inv_batch, float* grad, double* block_sums, int* n_blocks,
                  cudaStream_t s);
 void launch_reduce_sums(const double* block_sums, int n_blocks, double* out3, cudaStream_t s);
 
-// K7: merge adjoint (engine.hpp:195-234).
+// K7: merge adjoint (engine.hpp:195-234) for rows [row0, row1); grad_rgb window (g_base, g_rows).
 void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
-                      const float4* const* partials, int pstride_rows, int prow0, const float* grad_rgb,
-                      const float bg[3], float4* const* grad_out, int gstride_rows, int grow0, cudaStream_t s);
+                      const float4* const* partials, int prow0, const float* grad_rgb, int g_base, int g_rows,
+                      const float bg[3], float4* const* grad_out, int grow0, cudaStream_t s);
 
 struct AdamParams {
     float lr[kMaxParamRows];  // per row

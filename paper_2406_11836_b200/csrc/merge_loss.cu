@@ -16,7 +16,7 @@ namespace {
 
 __global__ void k_merge(ViewParams vp, const Table* __restrict__ tb, int owner, int row0, int row1,
                         const float4* const* __restrict__ partials, int prow0, float bg0, float bg1, float bg2,
-                        float* __restrict__ out_rgb, float* __restrict__ out_t) {
+                        float* __restrict__ out_rgb, float* __restrict__ out_t, int out_base, int out_rows) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = row0 + blockIdx.y;
     if (x >= vp.width || y >= row1) return;
@@ -33,8 +33,8 @@ __global__ void k_merge(ViewParams vp, const Table* __restrict__ tb, int owner, 
         c2 = fadd(c2, fmul(tr, p.z));
         tr = fmul(tr, p.w);
     }
-    const size_t pix = (size_t)y * vp.width + x;
-    const size_t plane = (size_t)vp.width * vp.height;
+    const size_t pix = (size_t)(y - out_base) * vp.width + x;
+    const size_t plane = (size_t)vp.width * out_rows;
     out_rgb[pix] = fadd(c0, fmul(tr, bg0));  // engine.hpp:177
     out_rgb[plane + pix] = fadd(c1, fmul(tr, bg1));
     out_rgb[2 * plane + pix] = fadd(c2, fmul(tr, bg2));
@@ -57,7 +57,8 @@ __global__ void k_pixel_orders(ViewParams vp, const Table* __restrict__ tb, int 
 
 __global__ void k_merge_bwd(ViewParams vp, const Table* __restrict__ tb, int owner, int row0, int row1,
                             const float4* const* __restrict__ partials, int prow0, const float* __restrict__ grad_rgb,
-                            float bg0, float bg1, float bg2, float4* const* __restrict__ grad_out, int grow0) {
+                            int g_base, int g_rows, float bg0, float bg1, float bg2,
+                            float4* const* __restrict__ grad_out, int grow0) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = row0 + blockIdx.y;
     if (x >= vp.width || y >= row1) return;
@@ -65,8 +66,8 @@ __global__ void k_merge_bwd(ViewParams vp, const Table* __restrict__ tb, int own
     pixel_ray_dir(vp, x, y, d);
     uint16_t ord[kMaxSubsets];
     const int n = subspace_order(*tb, owner, vp.o, d, ord);
-    const size_t pix = (size_t)y * vp.width + x;
-    const size_t plane = (size_t)vp.width * vp.height;
+    const size_t pix = (size_t)(y - g_base) * vp.width + x;
+    const size_t plane = (size_t)vp.width * g_rows;
     const float gc0 = grad_rgb[pix], gc1 = grad_rgb[plane + pix], gc2 = grad_rgb[2 * plane + pix];
     const float gt_eff = fadd(0.0f, dot3(gc0, gc1, gc2, bg0, bg1, bg2));  // engine.hpp:216 (grad_T_total = 0)
     const size_t prow = (size_t)(y - prow0) * vp.width + x;
@@ -105,10 +106,13 @@ constexpr int kIn = kOT + 4 * kR;   // 52: input tile with 10-pixel halo
 constexpr int kMid = kOT + 2 * kR;  // 42: first-stage maps with 5-pixel halo
 constexpr size_t kLossSmem = (2 * kIn * kIn + 5 * kIn * kMid + 5 * kMid * kMid) * sizeof(float);
 
-__global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, const float* __restrict__ xs,
-                                              const float* __restrict__ ys, float lam, float c1, float c2,
-                                              float nf, float inv_batch, const float* __restrict__ kern_g,
-                                              float* __restrict__ grad, double* __restrict__ block_sums) {
+__global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, int in_base, int in_rows,
+                                              const float* __restrict__ xs, const float* __restrict__ ys, float lam,
+                                              float c1, float c2, float nf, float inv_batch,
+                                              const float* __restrict__ kern_g, float* __restrict__ grad,
+                                              double* __restrict__ block_sums) {
+    // x, y, grad: planar [3][in_rows][W] covering image rows [in_base, in_base + in_rows);
+    // outputs for rows [row0, row1) need inputs within +-10 rows, which the caller provides.
     extern __shared__ float sm[];
     float* X = sm;                       // [kIn][kIn]
     float* Y = X + kIn * kIn;            // [kIn][kIn]
@@ -120,16 +124,17 @@ __global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, 
     if (tid < 11) kern[tid] = kern_g[tid];
     const int ox = blockIdx.x * kOT, oy = row0 + blockIdx.y * kOT;
     const int ch = blockIdx.z;
-    const size_t plane = (size_t)W * H;
+    const size_t plane = (size_t)W * in_rows;
     const float* xp = xs + ch * plane;
     const float* yp = ys + ch * plane;
-    // stage 0: inputs with zero padding outside the image
+    // stage 0: inputs with zero padding outside the image (rows outside the
+    // provided window only feed outputs beyond [row0, row1), which are dropped)
     for (int i = tid; i < kIn * kIn; i += 256) {
         const int r = i / kIn, c = i % kIn;
         const int gy = oy - 2 * kR + r, gx = ox - 2 * kR + c;
-        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-        X[i] = in ? xp[(size_t)gy * W + gx] : 0.0f;
-        Y[i] = in ? yp[(size_t)gy * W + gx] : 0.0f;
+        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= in_base && gy < in_base + in_rows;
+        X[i] = in ? xp[(size_t)(gy - in_base) * W + gx] : 0.0f;
+        Y[i] = in ? yp[(size_t)(gy - in_base) * W + gx] : 0.0f;
     }
     __syncthreads();
     // stage 1: horizontal blur of x, y, x*x, y*y, x*y  (rows -10..+41, cols -5..+36)
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, 
         const float sgn = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
         const float gl1 = fdiv(fmul(fsub(1.0f, lam), sgn), nf);
         const float g = fsub(gl1, fmul(lam, sg));
-        grad[ch * plane + (size_t)gy * W + gx] = fmul(g, inv_batch);
+        grad[ch * plane + (size_t)(gy - in_base) * W + gx] = fmul(g, inv_batch);
         s_l1 += (double)fabsf(d);
         s_mse += (double)fmul(d, d);
     }
@@ -291,12 +296,12 @@ __global__ void k_reduce_sums(const double* __restrict__ bs, int n, double* __re
 }  // namespace
 
 void launch_merge(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
-                  const float4* const* partials, int pstride_rows, int prow0, const float bg[3], float* out_rgb,
-                  float* out_t, cudaStream_t s) {
-    (void)pstride_rows;
+                  const float4* const* partials, int prow0, const float bg[3], float* out_rgb, float* out_t,
+                  int out_base, int out_rows, cudaStream_t s) {
     if (row1 <= row0) return;
     dim3 grid((vp.width + 127) / 128, row1 - row0);
-    k_merge<<<grid, 128, 0, s>>>(vp, tb_dev, owner, row0, row1, partials, prow0, bg[0], bg[1], bg[2], out_rgb, out_t);
+    k_merge<<<grid, 128, 0, s>>>(vp, tb_dev, owner, row0, row1, partials, prow0, bg[0], bg[1], bg[2], out_rgb, out_t,
+                                 out_base, out_rows);
 }
 
 void launch_pixel_orders(const ViewParams& vp, const Table* tb_dev, int owner, uint16_t* order, uint16_t* count,
@@ -306,18 +311,16 @@ void launch_pixel_orders(const ViewParams& vp, const Table* tb_dev, int owner, u
 }
 
 void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
-                      const float4* const* partials, int pstride_rows, int prow0, const float* grad_rgb,
-                      const float bg[3], float4* const* grad_out, int gstride_rows, int grow0, cudaStream_t s) {
-    (void)pstride_rows;
-    (void)gstride_rows;
+                      const float4* const* partials, int prow0, const float* grad_rgb, int g_base, int g_rows,
+                      const float bg[3], float4* const* grad_out, int grow0, cudaStream_t s) {
     if (row1 <= row0) return;
     dim3 grid((vp.width + 127) / 128, row1 - row0);
-    k_merge_bwd<<<grid, 128, 0, s>>>(vp, tb_dev, owner, row0, row1, partials, prow0, grad_rgb, bg[0], bg[1], bg[2],
-                                     grad_out, grow0);
+    k_merge_bwd<<<grid, 128, 0, s>>>(vp, tb_dev, owner, row0, row1, partials, prow0, grad_rgb, g_base, g_rows, bg[0],
+                                     bg[1], bg[2], grad_out, grow0);
 }
 
-void launch_loss(int W, int H, int row0, int row1, const float* x, const float* y, float lambda,
-                 const float* kernel, float inv_batch, float* grad, double* block_sums, int* n_blocks,
+void launch_loss(int W, int H, int row0, int row1, int in_base, int in_rows, const float* x, const float* y,
+                 float lambda, const float* kernel, float inv_batch, float* grad, double* block_sums, int* n_blocks,
                  cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
@@ -329,8 +332,8 @@ void launch_loss(int W, int H, int row0, int row1, const float* x, const float* 
     // loss.hpp:16-17: C1 = (0.01)^2, C2 = (0.03)^2 evaluated in double, then T(.)
     const float c1 = (float)(0.01 * 0.01), c2 = (float)(0.03 * 0.03);
     const float nf = (float)((size_t)W * H * 3);
-    k_loss<<<grid, 256, kLossSmem, s>>>(W, H, row0, row1, x, y, lambda, c1, c2, nf, inv_batch, kernel, grad,
-                                        block_sums);
+    k_loss<<<grid, 256, kLossSmem, s>>>(W, H, row0, row1, in_base, in_rows, x, y, lambda, c1, c2, nf, inv_batch,
+                                        kernel, grad, block_sums);
 }
 
 void launch_reduce_sums(const double* block_sums, int n_blocks, double* out3, cudaStream_t s) {

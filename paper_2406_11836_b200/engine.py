@@ -163,6 +163,17 @@ class PartitionTable:
         return out
 
 
+def slice_plan(height: int, slices: int, s: int) -> tuple[int, int, int, int]:
+    """(r0, r1, h0, h1): owned pixel rows and the 10-row SSIM halo of slice s."""
+    out = np.zeros(4, np.int32)
+    check(lib().dgs_slice_plan(height, slices, s, ptr(out)))
+    return tuple(int(x) for x in out)
+
+
+def subset_owner(k: int, k_count: int, world: int) -> int:
+    return int(lib().dgs_subset_owner(k, k_count, world))
+
+
 def build_kdtree(centers: np.ndarray, depth: int) -> PartitionTable:
     centers = np.ascontiguousarray(centers, dtype=np.float32)
     K = 1 << depth
@@ -347,6 +358,15 @@ class Context:
         t = np.zeros((cam.height, cam.width), np.float32)
         check(lib().dgs_render(self._h, C.byref(cam), ptr(bga), ptr(rgb), ptr(t)))
         return rgb, t
+
+    def set_virtual_slices(self, slices: int):
+        check(lib().dgs_set_virtual_slices(self._h, slices))
+
+    def dump_grad_maps(self, k: int, view: int, cam: Camera):
+        ct = np.zeros((cam.height, cam.width, 4), np.float32)
+        g = np.zeros((cam.height, cam.width, 4), np.float32)
+        check(lib().dgs_dump_grad_maps(self._h, k, view, ptr(ct), ptr(g)))
+        return ct, g
 
     def upload_targets(self, targets: np.ndarray) -> int:
         targets = np.ascontiguousarray(targets, np.float32)
