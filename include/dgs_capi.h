@@ -237,6 +237,9 @@ int dgs_render(dgs_ctx* ctx, const dgs_camera* cam, const float bg[3], float* ou
  * total ms and launch counts. */
 #define DGS_NUM_STAGES 10
 int dgs_set_profiling(dgs_ctx* ctx, int32_t enabled);
+/* Blend evaluation / contribution / overflow counters in dgs_step_result
+ * (off by default: they cost a few percent in the blend kernels). */
+int dgs_set_collect_stats(dgs_ctx* ctx, int32_t enabled);
 int dgs_stage_times(dgs_ctx* ctx, double* ms, uint64_t* counts);
 /* CUDA stream the context launches on (cudaStream_t as void*), for timing. */
 void* dgs_stream(dgs_ctx* ctx);

@@ -119,6 +119,7 @@ _SIGS = {
     "dgs_upload_targets": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
     "dgs_render": (C.c_int, [_P, C.POINTER(Camera), _P, _P, _P]),
     "dgs_set_profiling": (C.c_int, [_P, C.c_int32]),
+    "dgs_set_collect_stats": (C.c_int, [_P, C.c_int32]),
     "dgs_stage_times": (C.c_int, [_P, _P, _P]),
     "dgs_set_virtual_slices": (C.c_int, [_P, C.c_int32]),
     "dgs_slice_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P]),

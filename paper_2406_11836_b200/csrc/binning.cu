@@ -29,31 +29,81 @@ __global__ void k_gather_counts(const uint32_t* __restrict__ sorted_idx, const u
     if (j < n) out[j] = counts[sorted_idx[j]];
 }
 
+/// Pair emission, warp-cooperative: the warp's 32 members (in range order)
+/// own a contiguous run of output slots; lane l writes slots l, l+32, ...
+/// of that run, finding its member by a search over the warp's prefix sums,
+/// so every store instruction writes 32 consecutive words.
 __global__ void k_emit_pairs(const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ offsets,
                              const uint32_t* __restrict__ counts, const uint32_t* __restrict__ rect, int tiles_x,
                              int n, uint32_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_val) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const uint32_t i = sorted_idx[j];
-    if (counts[i] == 0) return;
-    const uint32_t rx = rect[2 * (size_t)i], ry = rect[2 * (size_t)i + 1];
-    const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
-    uint32_t o = offsets[j];
-    for (int ty = y0; ty <= y1; ++ty)
-        for (int tx = x0; tx <= x1; ++tx) {
-            pair_tile[o] = (uint32_t)(ty * tiles_x + tx);
-            pair_val[o] = i;
-            ++o;
+    const int lane = threadIdx.x & 31;
+    uint32_t i = 0, c = 0, off = 0, x0 = 0, w = 1, y0 = 0;
+    if (j < n) {
+        i = sorted_idx[j];
+        c = counts[i];
+        off = offsets[j];
+        if (c) {
+            const uint32_t rx = rect[2 * (size_t)i], ry = rect[2 * (size_t)i + 1];
+            x0 = rx & 0xffff;
+            w = (rx >> 16) - x0 + 1;
+            y0 = ry & 0xffff;
         }
+    }
+    // inclusive prefix of counts within the warp
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    // offsets[] holds inclusive ends: lane 0's start is its end minus its count
+    const uint32_t base = __shfl_sync(0xffffffffu, off - c, 0);
+    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        // owner lane: first lane whose inclusive prefix exceeds q
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, inc, lo + step - 1);
+            if (v <= q) lo += step;
+        }
+        const uint32_t ex = __shfl_sync(0xffffffffu, inc - c, lo);
+        const uint32_t mi = __shfl_sync(0xffffffffu, i, lo);
+        const uint32_t mx0 = __shfl_sync(0xffffffffu, x0, lo);
+        const uint32_t mw = __shfl_sync(0xffffffffu, w, lo);
+        const uint32_t my0 = __shfl_sync(0xffffffffu, y0, lo);
+        if (q < total) {
+            const uint32_t r = q - ex;
+            const uint32_t ty = my0 + r / mw, tx = mx0 + r % mw;
+            pair_tile[base + q] = ty * (uint32_t)tiles_x + tx;
+            pair_val[base + q] = mi;
+        }
+    }
 }
 
-__global__ void k_tile_ranges(const uint32_t* __restrict__ tile, int64_t P, uint2* __restrict__ ranges) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    const uint32_t t = tile[p];
-    if (p == 0 || tile[p - 1] != t) ranges[t].x = (uint32_t)p;
-    if (p == P - 1 || tile[p + 1] != t) ranges[t].y = (uint32_t)(p + 1);
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__ a, uint32_t n, uint32_t key) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
+
+/// Per-tile [start, end) by binary search over the sorted tile keys (one thread per tile).
+__global__ void k_tile_ranges(const uint32_t* __restrict__ tile, uint32_t P, int tiles, uint2* __restrict__ ranges) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= tiles) return;
+    ranges[t] = make_uint2(lower_bound_u32(tile, P, (uint32_t)t), lower_bound_u32(tile, P, (uint32_t)t + 1));
+}
+
+struct CountOf {
+    const uint32_t* counts;
+    __host__ __device__ uint32_t operator()(uint32_t i) const { return counts[i]; }
+};
 
 int bits_for(uint32_t v) {
     int b = 1;
@@ -69,7 +119,8 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
                                     (uint32_t*)nullptr, n);
     cub::DoubleBuffer<uint32_t> dk, dv;
     cub::DeviceRadixSort::SortPairs(nullptr, b, dk, dv, (int)pair_cap, 0, 32);
-    cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, n);
+    cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it((const uint32_t*)nullptr, CountOf{nullptr});
+    cub::DeviceScan::InclusiveSum(nullptr, c, it, (uint32_t*)nullptr, n);
     size_t m = a > b ? a : b;
     return (m > c ? m : c) + 256;
 }
@@ -86,21 +137,21 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     size_t tb = temp_bytes;
     // 1) members by range (culled members carry 0xffffffff and sort last)
     cub::DeviceRadixSort::SortPairs(temp, tb, vb.rkey, sort_keys_alt, sort_vals, sort_vals_alt, n, 0, 32, s);
-    // 2) tile counts in range order -> exclusive scan -> pair offsets
-    k_gather_counts<<<grid, blk, 0, s>>>(sort_vals_alt, vb.counts, sort_keys_alt, n);
+    // 2) tile counts in range order -> inclusive scan -> pair end offsets
+    //    (the gather is fused into the scan through a transform iterator)
+    cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> cnt_it(sort_vals_alt, CountOf{vb.counts});
     tb = temp_bytes;
-    cub::DeviceScan::ExclusiveSum(temp, tb, sort_keys_alt, scan_buf, n, s);
-    uint32_t last_off = 0, last_cnt = 0;
-    cudaMemcpyAsync(&last_off, scan_buf + (n - 1), 4, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&last_cnt, sort_keys_alt + (n - 1), 4, cudaMemcpyDeviceToHost, s);
+    cub::DeviceScan::InclusiveSum(temp, tb, cnt_it, scan_buf, n, s);
+    uint32_t last_end = 0;
+    cudaMemcpyAsync(&last_end, scan_buf + (n - 1), 4, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    const int64_t P = (int64_t)last_off + last_cnt;
+    const int64_t P = (int64_t)last_end;
     if (P > cap) return -P;
     vb.pairs = P;
     if (P == 0) return 0;
     // 3) emit (tile, member) pairs, range-ordered within every tile
     k_emit_pairs<<<grid, blk, 0, s>>>(sort_vals_alt, scan_buf, vb.counts, vb.rect, vp.tiles_x, n, vb.pair_tile,
-                                      vb.pair_val);
+                                      vb.pair_val);  // scan_buf holds inclusive ends: start = end - count
     // 4) stable LSD radix sort by tile id only
     cub::DoubleBuffer<uint32_t> dk(vb.pair_tile, pair_tile_alt), dv(vb.pair_val, pair_val_alt);
     tb = temp_bytes;
@@ -110,7 +161,7 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
         cudaMemcpyAsync(vb.pair_val, dv.Current(), 4 * (size_t)P, cudaMemcpyDeviceToDevice, s);
     }
     // 5) per-tile [start, end)
-    k_tile_ranges<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(vb.pair_tile, P, vb.ranges);
+    k_tile_ranges<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(vb.pair_tile, (uint32_t)P, tiles, vb.ranges);
     return P;
 }
 

@@ -126,6 +126,7 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     v[4] = h * (w1 * w1);
 }
 
+template <bool STATS>
 __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, RenderOpts ro, Subspace gate,
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                                       fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
                 const float g = __expf(fmul(-0.5f, m2));
                 contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
-                ++nemit;
+                if (STATS) ++nemit;
                 ++head;
                 --cnt;
                 const int hs = head & (KBUF - 1);
@@ -240,14 +241,14 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                 head_pos = cnt ? bpos[hs][tid] : 0xffffffffu;
             }
             const unsigned gm = __ballot_sync(kFull, go);
-            const int leader = __ffs(gm) - 1;
-            if (__popc(gm) <= 2) {  // one or two lanes: direct atomics beat a 45-shuffle butterfly
+            if (__popc(gm) <= 2) {  // one or two lanes: direct atomics
                 if (go) {
 #pragma unroll
                     for (int f = 0; f < 9; ++f)
                         if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
                 }
             } else {
+                const int leader = __ffs(gm) - 1;
 #pragma unroll
                 for (int f = 0; f < 9; ++f) {
                     float x = v[f];
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
             emit_ready(sD[j].w);
             if (done) continue;
             const float4 A = sA[j], B = sB[j], C = sC[j];
-            ++n_eval;
+            if (STATS) ++n_eval;
             float t, sigma, g;
             if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
             const uint32_t id = __float_as_uint(C.w);
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
     }
     emit_ready(kInf);
 
-    if (stats != nullptr) {
+    if (STATS && stats != nullptr) {
         unsigned long long e = n_eval, c = (unsigned long long)nemit;
         for (int off = 16; off > 0; off >>= 1) {
             e += __shfl_xor_sync(kFull, e, off);
@@ -431,11 +432,18 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
     const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_blend_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
+        cudaFuncSetAttribute(k_blend_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
+        cudaFuncSetAttribute(k_blend_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
         configured = true;
     }
-    k_blend_bwd<<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits,
-                                                       onorm, fwd_ct, fwd_cd, grad_ct, ovf_flag, g2d, ld2, stats);
+    if (stats)
+        k_blend_bwd<true><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
+                                                                 vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
+                                                                 ovf_flag, g2d, ld2, stats);
+    else
+        k_blend_bwd<false><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
+                                                                  vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
+                                                                  ovf_flag, g2d, ld2, stats);
 }
 
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,

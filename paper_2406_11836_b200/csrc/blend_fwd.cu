@@ -79,6 +79,7 @@ __device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint
     D = __ldg(r4 + 3);
 }
 
+template <bool DBG, bool STATS>
 __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, RenderOpts ro, Subspace gate,
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
@@ -142,8 +143,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             D2 += (double)col.z * wd;
         }
         T = fmul(T, fsub(1.0f, sg));
-        if (dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][tid];
-        ++nemit;
+        if (DBG && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][tid];
+        if (DBG || STATS) ++nemit;
         ++head;
         --cnt;
         head_t = cnt ? bt[head & (KBUF - 1)][tid] : kInf;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             while (head_t < D.w && !done) emit_head();
             if (done) break;
             const float4 A = sA[j], B = sB[j], C = sC[j];
-            ++n_eval;
+            if (STATS) ++n_eval;
             float t, sigma, g;
             if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
             const uint32_t id = __float_as_uint(C.w);
@@ -217,10 +218,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                 out_cd[3 * pix + 1] = D1;
                 out_cd[3 * pix + 2] = D2;
             }
-            if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
+            if (DBG) dbg_cnt[pix] = (uint32_t)nemit;
         }
     }
-    if (stats != nullptr) {
+    if (STATS && stats != nullptr) {
         unsigned long long e = n_eval, c = (unsigned long long)nemit, o = ovf ? 1ull : 0ull;
         for (int off = 16; off > 0; off >>= 1) {
             e += __shfl_xor_sync(0xffffffffu, e, off);
@@ -335,12 +336,19 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
     const size_t smem = kFwdSmem;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_blend_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_fwd<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_fwd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_fwd<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    k_blend_fwd<<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits, onorm,
-                                                out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids, dbg_cnt, dbg_cap,
-                                                stats, out_cd);
+#define DGS_FWD(D, S)                                                                                              \
+    k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits, \
+                                                         onorm, out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids,       \
+                                                         dbg_cnt, dbg_cap, stats, out_cd)
+    if (dbg_ids != nullptr && dbg_cnt != nullptr) DGS_FWD(true, true);
+    else if (stats != nullptr) DGS_FWD(false, true);
+    else DGS_FWD(false, false);
+#undef DGS_FWD
 }
 
 void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,

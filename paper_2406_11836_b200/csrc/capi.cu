@@ -204,6 +204,7 @@ struct Ctx {
     DevBuf<float4> xrecv, xgrad;   // sliced exchange buffers (K x halo rows, K x owned rows)
     DevBuf<float> targets_win;
     int virtual_slices = 1;        // single-rank sliced mode (tests the multi-rank manager path)
+    bool collect_stats = false;    // blend evaluation/contribution counters (costs ~5% in the blends)
     DevBuf<BlendStats> stats;
     DevBuf<int> bad;
     uint64_t launches = 0;
@@ -1011,7 +1012,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             // ---- render_batch (manager.hpp:262-304): per-subset partials ----
             for (int k : local) {
                 SubsetState& S_ = subset(*ctx, k);
-                forward_subset(*ctx, S_, v, vp, 0, nullptr, nullptr, ctx->stats.p);
+                forward_subset(*ctx, S_, v, vp, 0, nullptr, nullptr, ctx->collect_stats ? ctx->stats.p : nullptr);
                 pairs += (uint64_t)S_.slot(v).vb.pairs;
                 S_.slot(v).grad_ct.ensure(px);
             }
@@ -1113,7 +1114,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             }
             for (int v = 0; v < batch; ++v) {
                 ViewSlot& vs = S_.slot(v);
-                backward_blend(*ctx, S_, v, ctx->stats.p + 1);
+                backward_blend(*ctx, S_, v, ctx->collect_stats ? ctx->stats.p + 1 : nullptr);
                 if (v + 1 < batch) {
                     Stage st(ctx->timer, kStProjBwd, ctx->stream);
                     launch_project_bwd((int)S_.n, S_.P.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S_.g2d.p,
@@ -1122,20 +1123,21 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                 } else {
                     // K9 (gradient record) + K10 (streaming Adam) with a split event between them
                     S_.rec.ensure((size_t)kGradRecordRows * S_.ld);
-                    cudaEvent_t a = nullptr, mid = nullptr, b = nullptr;
+                    cudaEvent_t a = nullptr, m1 = nullptr, m2 = nullptr, b = nullptr;
                     if (ctx->timer.on) {
                         a = ctx->timer.get();
-                        mid = ctx->timer.get();
+                        m1 = ctx->timer.get();
+                        m2 = ctx->timer.get();
                         CK(cudaEventRecord(a, ctx->stream));
                     }
                     launch_project_bwd_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro,
                                             vs.vb.counts, S_.g2d.p, S_.ld, batch > 1 ? S_.G.p : nullptr, ap,
-                                            ctx->bad.p, S_.rec.p, mid, ctx->stream);
+                                            ctx->bad.p, S_.rec.p, m1, m2, ctx->stream);
                     if (ctx->timer.on) {
                         b = ctx->timer.get();
                         CK(cudaEventRecord(b, ctx->stream));
-                        ctx->timer.pending.push_back({kStProjBwd, {a, mid}});
-                        ctx->timer.pending.push_back({kStAdam, {mid, b}});
+                        ctx->timer.pending.push_back({kStProjBwd, {a, m1}});
+                        ctx->timer.pending.push_back({kStAdam, {m2, b}});
                     }
                     ctx->launches += 2;
                 }
@@ -1210,6 +1212,10 @@ int dgs_dump_grad_maps(dgs_ctx* ctx, int32_t k, int32_t view, float* partial_ct,
             CK(cudaMemcpy(grad_ct, vs.grad_ct.p, px * sizeof(float4), cudaMemcpyDeviceToHost));
         }
     });
+}
+
+int dgs_set_collect_stats(dgs_ctx* ctx, int32_t enabled) {
+    return dgs_guard([&] { ctx->collect_stats = enabled != 0; });
 }
 
 int dgs_set_virtual_slices(dgs_ctx* ctx, int32_t slices) {

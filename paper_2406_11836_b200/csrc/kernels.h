@@ -103,7 +103,7 @@ void launch_project_bwd(int n, const float* P, size_t ld, int sh_coeffs, const V
 void launch_project_bwd_adam(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, const ViewParams& vp,
                              const RenderOpts& ro, const uint32_t* counts, const float* g2d, size_t ld2,
                              const float* G_extra, const AdamParams& ap, int* bad_index, float* g_rec,
-                             cudaEvent_t mid_event, cudaStream_t s);
+                             cudaEvent_t mid_end, cudaEvent_t mid_begin, cudaStream_t s);
 constexpr int kGradRecordRows = 17;
 void launch_adam(int n, float* P, float* M, float* V, size_t ld, int rows, const float* G, const AdamParams& ap,
                  cudaStream_t s);

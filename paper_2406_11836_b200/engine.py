@@ -229,6 +229,9 @@ class Context:
     def sync(self):
         check(lib().dgs_sync(self._h))
 
+    def set_collect_stats(self, on: bool):
+        check(lib().dgs_set_collect_stats(self._h, int(on)))
+
     def set_profiling(self, on: bool):
         check(lib().dgs_set_profiling(self._h, int(on)))
 
