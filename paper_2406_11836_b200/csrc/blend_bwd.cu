@@ -28,7 +28,8 @@ constexpr int KBUF = 8;  // must equal blend_fwd.cu (identical overflow decision
 constexpr float kInf = __builtin_huge_valf();
 constexpr unsigned kFull = 0xffffffffu;
 // staged records (4 float4) + ring (t, id, sigma, list position)
-constexpr size_t kBwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float);
+constexpr size_t kBwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float) +
+                            kBlendThreads + (kBlendThreads / 32) * kBlendThreads * sizeof(uint16_t);
 
 __device__ __forceinline__ float order_bound(float r, float dmax, float onorm) {
     const float S = 2.0f * onorm + 2.0f * r + 1.0f;
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
                                                              const uint2* __restrict__ ranges,
+                                                             const float* __restrict__ ext_y,
                                                              const uint32_t* __restrict__ dmax_bits, float onorm,
                                                              const float4* __restrict__ fwd_ct,
                                                              const double* __restrict__ fwd_cd,
@@ -149,6 +151,9 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
     URing* bid = reinterpret_cast<URing*>(bt + KBUF);
     Ring* bs = reinterpret_cast<Ring*>(bid + KBUF);
     URing* bpos = reinterpret_cast<URing*>(bs + KBUF);
+    uint16_t* wlist = reinterpret_cast<uint16_t*>(bpos + KBUF) + (threadIdx.x >> 5) * kBlendThreads;
+    uint8_t* smask = reinterpret_cast<uint8_t*>(reinterpret_cast<uint16_t*>(bpos + KBUF) +
+                                                (kBlendThreads / 32) * kBlendThreads);
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int tile = blockIdx.x;
@@ -271,15 +276,43 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
         nb = (int)min((uint32_t)kBlendThreads, rg.y - base);
         if (p < rg.y) {
             float4 A, B, C, D;
-            load_rec(recs, pair_val[p], A, B, C, D);
+            const uint32_t m = pair_val[p];
+            load_rec(recs, m, A, B, C, D);
             D.w = order_bound(D.w, dmax, onorm);
             sA[tid] = A;
             sB[tid] = B;
             sC[tid] = C;
             sD[tid] = D;
+            // which warps (pixel row pairs of this tile) can see m^2 <= 9: a warp is
+            // skipped only if |dy| > ext_y on both of its rows (same float dy as eval)
+            const float ey = __ldg(ext_y + m);
+            uint32_t wm = 0;
+#pragma unroll
+            for (int w = 0; w < kBlendThreads / 32; ++w) {
+                const float y0 = fadd((float)(ty * kTileSize + 2 * w), 0.5f);
+                const float y1 = fadd((float)(ty * kTileSize + 2 * w + 1), 0.5f);
+                const float d0 = fabsf(fsub(y0, A.y)), d1 = fabsf(fsub(y1, A.y));
+                if (!(fminf(d0, d1) > ey)) wm |= 1u << w;
+            }
+            smask[tid] = (uint8_t)wm;
         }
         __syncthreads();
-        for (int j = 0; j < nb; ++j) {
+        // this warp's candidates of the batch, in list order
+        int nlist = 0;
+        {
+            const int wid = tid >> 5, lane = tid & 31;
+            const int nbb = (int)min((uint32_t)kBlendThreads, rg.y - base);
+            for (int c0 = 0; c0 < nbb; c0 += 32) {
+                const int jj = c0 + lane;
+                const bool hit = jj < nbb && ((smask[jj] >> wid) & 1u);
+                const unsigned bm = __ballot_sync(0xffffffffu, hit);
+                if (hit) wlist[nlist + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)jj;
+                nlist += __popc(bm);
+            }
+            __syncwarp();
+        }
+        for (int q = 0; q < nlist; ++q) {
+            const int j = wlist[q];
             emit_ready(sD[j].w);
             if (done) continue;
             const float4 A = sA[j], B = sB[j], C = sC[j];
@@ -438,11 +471,11 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
     }
     if (stats)
         k_blend_bwd<true><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
-                                                                 vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
+                                                                 vb.ext_y, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
                                                                  ovf_flag, g2d, ld2, stats);
     else
         k_blend_bwd<false><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
-                                                                  vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
+                                                                  vb.ext_y, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
                                                                   ovf_flag, g2d, ld2, stats);
 }
 

@@ -24,7 +24,8 @@ namespace {
 constexpr int KBUF = 8;  // ring capacity (power of two); must equal blend_bwd.cu
 constexpr float kInf = __builtin_huge_valf();
 // 4 staged float4 record fields + 4 ring fields per pixel (t, id, sigma, member).
-constexpr size_t kFwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float);
+constexpr size_t kFwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float) +
+                            kBlendThreads + (kBlendThreads / 32) * kBlendThreads * sizeof(uint16_t);
 
 /// Lower bound on t for every candidate at or after a list position whose
 /// range is r (t >= sqrt(r^2 - D^2), with margins ≫ float
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
                                                              const uint2* __restrict__ ranges,
+                                                             const float* __restrict__ ext_y,
                                                              const uint32_t* __restrict__ dmax_bits, float onorm,
                                                              float4* __restrict__ out_ct, uint8_t* __restrict__ ovf_flag,
                                                              uint32_t* __restrict__ ovf_list,
@@ -102,6 +104,9 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     uint32_t(*bid)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bt + KBUF);
     Ring* bs = reinterpret_cast<Ring*>(bid + KBUF);
     uint32_t(*bmem)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bs + KBUF);
+    uint16_t* wlist = reinterpret_cast<uint16_t*>(bmem + KBUF) + (threadIdx.x >> 5) * kBlendThreads;
+    uint8_t* smask = reinterpret_cast<uint8_t*>(reinterpret_cast<uint16_t*>(bmem + KBUF) +
+                                                (kBlendThreads / 32) * kBlendThreads);
 
     const int tid = threadIdx.x;
     const int tile = blockIdx.x;
@@ -156,16 +161,44 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         const uint32_t p = base + tid;
         if (p < rg.y) {
             float4 A, B, C, D;
-            load_rec(recs, pair_val[p], A, B, C, D);
+            const uint32_t m = pair_val[p];
+            load_rec(recs, m, A, B, C, D);
             D.w = order_bound(D.w, dmax, onorm);
             sA[tid] = A;
             sB[tid] = B;
             sC[tid] = C;
             sD[tid] = D;
+            // which warps (pixel row pairs of this tile) can see m^2 <= 9: a warp is
+            // skipped only if |dy| > ext_y on both of its rows (same float dy as eval)
+            const float ey = __ldg(ext_y + m);
+            uint32_t wm = 0;
+#pragma unroll
+            for (int w = 0; w < kBlendThreads / 32; ++w) {
+                const float y0 = fadd((float)(ty * kTileSize + 2 * w), 0.5f);
+                const float y1 = fadd((float)(ty * kTileSize + 2 * w + 1), 0.5f);
+                const float d0 = fabsf(fsub(y0, A.y)), d1 = fabsf(fsub(y1, A.y));
+                if (!(fminf(d0, d1) > ey)) wm |= 1u << w;
+            }
+            smask[tid] = (uint8_t)wm;
         }
         __syncthreads();
+        // this warp's candidates of the batch, in list order
+        int nlist = 0;
+        {
+            const int wid = tid >> 5, lane = tid & 31;
+            const int nbb = (int)min((uint32_t)kBlendThreads, rg.y - base);
+            for (int c0 = 0; c0 < nbb; c0 += 32) {
+                const int jj = c0 + lane;
+                const bool hit = jj < nbb && ((smask[jj] >> wid) & 1u);
+                const unsigned bm = __ballot_sync(0xffffffffu, hit);
+                if (hit) wlist[nlist + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)jj;
+                nlist += __popc(bm);
+            }
+            __syncwarp();
+        }
         const int nb = (int)min((uint32_t)kBlendThreads, rg.y - base);
-        for (int j = 0; j < nb && !done; ++j) {
+        for (int q = 0; q < nlist && !done; ++q) {
+            const int j = wlist[q];
             const float4 D = sD[j];
             while (head_t < D.w && !done) emit_head();
             if (done) break;
@@ -342,7 +375,7 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
         configured = true;
     }
 #define DGS_FWD(D, S)                                                                                              \
-    k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.dmax_bits, \
+    k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext_y, vb.dmax_bits, \
                                                          onorm, out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids,       \
                                                          dbg_cnt, dbg_cap, stats, out_cd)
     if (dbg_ids != nullptr && dbg_cnt != nullptr) DGS_FWD(true, true);

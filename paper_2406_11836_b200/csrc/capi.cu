@@ -90,6 +90,7 @@ struct DevBuf {
 struct ViewSlot {
     DevBuf<SplatRec> recs;
     DevBuf<uint32_t> rect, counts, rkey, dmax, pair_tile, pair_val, pair_tile_alt, pair_val_alt;
+    DevBuf<float> ext_y;
     DevBuf<uint32_t> sort_keys_alt, sort_vals, sort_vals_alt, scan, ovf_list, ovf_count;
     DevBuf<int> err;
     DevBuf<uint2> ranges;
@@ -309,6 +310,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vb.rect = vs.rect.ensure(2 * n);
     vb.counts = vs.counts.ensure(n);
     vb.rkey = vs.rkey.ensure(n);
+    vb.ext_y = vs.ext_y.ensure(n);
     vb.dmax_bits = vs.dmax.ensure(1);
     vb.err_index = vs.err.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);

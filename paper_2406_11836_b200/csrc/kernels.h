@@ -16,6 +16,7 @@ struct ViewBins {
     uint32_t* rect = nullptr;        // [2n]: x0 | x1 << 16, y0 | y1 << 16
     uint32_t* counts = nullptr;      // [n] tile count per member (0 = culled)
     uint32_t* rkey = nullptr;        // [n] range bits (0xffffffff = culled)
+    float* ext_y = nullptr;          // [n] conservative row half-extent of the m^2 <= 9 region (warp culling)
     uint32_t* dmax_bits = nullptr;   // [1] max world_radius over visible members
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
     uint32_t* pair_tile = nullptr;   // [cap] tile key of each (splat, tile) pair

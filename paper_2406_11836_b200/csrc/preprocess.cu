@@ -14,13 +14,38 @@ namespace dgs_b200 {
 
 namespace {
 
-__global__ void __launch_bounds__(256) k_preprocess(int n, const float* __restrict__ P, size_t ld, int sh_coeffs,
-                                                    const uint32_t* __restrict__ ids32, ViewParams vp,
-                                                    RenderOpts ro, ViewBins vb) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+/// Members are staged per CTA: one elected thread issues a bulk copy
+/// (cp.async.bulk, the TMA engine) of each parameter row segment into shared
+/// memory on one mbarrier, so all 11 + 3C rows of the CTA are in flight at
+/// once; the per-member math then reads shared memory.
+constexpr int kPreTB = 128;
+
+template <int SHC>
+__global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __restrict__ P, size_t ld,
+                                                       const uint32_t* __restrict__ ids32, ViewParams vp,
+                                                       RenderOpts ro, ViewBins vb) {
+    constexpr int ROWS = kRowSh + 3 * SHC;
+    constexpr int sh_coeffs = SHC;
+    __shared__ __align__(128) float tile[ROWS * kPreTB];
+    __shared__ uint64_t bar;
+    const int tid = threadIdx.x;
+    const int i0 = blockIdx.x * kPreTB;
+    const int i = i0 + tid;
+    const int cnt = min(kPreTB, n - i0);
+    const uint32_t bytes = (uint32_t)((cnt + 3) / 4) * 16u;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&bar, (uint32_t)ROWS * bytes);
+        for (int r = 0; r < ROWS; ++r) bulk_g2s(tile + r * kPreTB, P + (size_t)r * ld + i0, bytes, &bar);
+    }
+    mbar_wait(&bar, 0);
     float dmax_local = 0.0f;
     if (i < n) {
-        auto row = [&](int r) { return __ldg(P + (size_t)r * ld + i); };
+        auto row = [&](int r) { return tile[r * kPreTB + tid]; };
         const float mu0 = row(kRowMu), mu1 = row(kRowMu + 1), mu2 = row(kRowMu + 2);
         // t = W mu + t_wc (splat.hpp:292)
         const float t0 = fadd(dot3(vp.R[0], vp.R[1], vp.R[2], mu0, mu1, mu2), vp.t[0]);
@@ -87,6 +112,24 @@ __global__ void __launch_bounds__(256) k_preprocess(int n, const float* __restri
                 rec.i01 = fdiv(-c01, det);
                 rec.i10 = fdiv(-c10, det);
                 rec.i11 = fdiv(c00, det);
+                {
+                    // Conservative |dy| bound of the reference's computed m^2 <= trunc^2
+                    // region (eval_2d, splat.hpp:326-332): every term of the float m^2
+                    // carries <= 4 roundings, so m2_float <= 9 implies
+                    // a' dx^2 - 2h|dx dy| + d' dy^2 <= 9 with a' = a(1-g), d' = d(1-g),
+                    // h = (|b+c| + g(|b|+|c|))/2, g = 1e-6 > gamma_4.  Minimising over dx
+                    // gives |dy| <= trunc * sqrt(a' / (a'd' - h^2)).
+                    const double a = rec.i00, b = rec.i01, c = rec.i10, d = rec.i11, g = 1e-6;
+                    const double ap = a * (1.0 - g), dp = d * (1.0 - g);
+                    const double h = 0.5 * (fabs(b + c) + g * (fabs(b) + fabs(c)));
+                    float ey = __int_as_float(0x7f800000);
+                    if (a > 0.0 && d > 0.0 && ap * dp > h * h * (1.0 + 1e-9)) {
+                        const double t2 = (double)fmul(ro.trunc, ro.trunc);
+                        const double e = sqrt(t2 * ap / (ap * dp - h * h));
+                        ey = (float)(e * (1.0 + 1e-6) + 1e-5);
+                    }
+                    vb.ext_y[i] = ey;
+                }
                 // tile rectangle (raster.hpp:117-121): C++ truncating int division, then clamp
                 const int x0 = clampi(x86_float_to_int(floorf(fsub(mx, rx))) / kTileSize, 0, vp.tiles_x - 1);
                 const int x1 = clampi(x86_float_to_int(floorf(fadd(mx, rx))) / kTileSize, 0, vp.tiles_x - 1);
@@ -138,7 +181,7 @@ __global__ void __launch_bounds__(256) k_preprocess(int n, const float* __restri
         }
     }
     // block max of D over visible members -> one atomic per block
-    __shared__ float s_max[8];
+    __shared__ float s_max[kPreTB / 32];
     float m = dmax_local;
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
     if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
@@ -154,7 +197,13 @@ __global__ void __launch_bounds__(256) k_preprocess(int n, const float* __restri
 void launch_preprocess(int n, const float* P, size_t ld, int sh_coeffs, const uint32_t* ids32, const ViewParams& vp,
                        const RenderOpts& ro, const ViewBins& vb, cudaStream_t s) {
     if (n <= 0) return;
-    k_preprocess<<<(n + 255) / 256, 256, 0, s>>>(n, P, ld, sh_coeffs, ids32, vp, ro, vb);
+    const unsigned grid = (unsigned)((n + kPreTB - 1) / kPreTB);
+    switch (sh_coeffs) {
+        case 1: k_preprocess<1><<<grid, kPreTB, 0, s>>>(n, P, ld, ids32, vp, ro, vb); break;
+        case 4: k_preprocess<4><<<grid, kPreTB, 0, s>>>(n, P, ld, ids32, vp, ro, vb); break;
+        case 9: k_preprocess<9><<<grid, kPreTB, 0, s>>>(n, P, ld, ids32, vp, ro, vb); break;
+        default: k_preprocess<16><<<grid, kPreTB, 0, s>>>(n, P, ld, ids32, vp, ro, vb); break;
+    }
 }
 
 }  // namespace dgs_b200
