@@ -291,7 +291,8 @@ def b200_arm(a, world, rank, local_rank):
             cpu = {"value": None, "unit": "Mpixel/s", "cores": 0, "kind": "reference", "sample": err}
 
     last = dict(results[-1])
-    for key in ("evals_fwd", "contribs_fwd", "evals_bwd", "contribs_bwd", "overflow_pixels"):
+    for key in ("evals_fwd", "contribs_fwd", "evals_bwd", "contribs_bwd", "overflow_pixels", "subrounds_bwd",
+                "small_subrounds_bwd", "tiles_work_fwd"):
         last[key] = results_stats[-1][key]
     line = {
         "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": a.steps,
@@ -312,7 +313,9 @@ def b200_arm(a, world, rank, local_rank):
         "step_stats": {"loss_first": results[0]["loss"], "loss_last": last["loss"], "psnr_last": last["psnr"],
                        "pairs": last["pairs"], "evals_fwd": last["evals_fwd"], "contribs_fwd": last["contribs_fwd"],
                        "evals_bwd": last["evals_bwd"], "contribs_bwd": last["contribs_bwd"],
-                       "overflow_pixels": last["overflow_pixels"], "comm_bytes_reference_accounting":
+                       "overflow_pixels": last["overflow_pixels"], "subrounds_bwd": last["subrounds_bwd"],
+                       "small_subrounds_bwd": last["small_subrounds_bwd"], "tiles_work_fwd": last["tiles_work_fwd"],
+                       "comm_bytes_reference_accounting":
                            last["comm_bytes"]},
         "setup_s": setup_s,
     }

@@ -111,6 +111,7 @@ typedef struct dgs_step_result {
     uint64_t pairs;           /* (splat, tile) pairs over all local subsets and views */
     uint64_t evals_fwd, contribs_fwd, evals_bwd, contribs_bwd, overflow_pixels;
     uint64_t kernel_launches; /* kernels this call launched */
+    uint64_t subrounds_bwd, small_subrounds_bwd, tiles_work_fwd; /* blend work counters (stats mode) */
 } dgs_step_result;
 
 const char* dgs_last_error(void);

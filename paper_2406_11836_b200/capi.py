@@ -75,7 +75,8 @@ class StepResult(C.Structure):
     _fields_ = [("loss", C.c_double), ("psnr", C.c_double), ("comm_bytes", C.c_uint64), ("nccl_bytes", C.c_uint64),
                 ("pairs", C.c_uint64), ("evals_fwd", C.c_uint64), ("contribs_fwd", C.c_uint64),
                 ("evals_bwd", C.c_uint64), ("contribs_bwd", C.c_uint64), ("overflow_pixels", C.c_uint64),
-                ("kernel_launches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("subrounds_bwd", C.c_uint64),
+                ("small_subrounds_bwd", C.c_uint64), ("tiles_work_fwd", C.c_uint64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
     int head = 0, cnt = 0, nemit = 0;
     float head_t = kInf;
     uint32_t head_pos = 0xffffffffu;
-    unsigned long long n_eval = 0;
+    unsigned long long n_eval = 0, n_rounds = 0, n_small = 0;
     const uint2 rg = ranges[tile];
     uint32_t base = rg.x;
     int nb = 0;
@@ -246,6 +246,10 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                 head_pos = cnt ? bpos[hs][tid] : 0xffffffffu;
             }
             const unsigned gm = __ballot_sync(kFull, go);
+            if (STATS) {
+                ++n_rounds;
+                if (__popc(gm) <= 2) ++n_small;
+            }
             if (__popc(gm) <= 2) {  // one or two lanes: direct atomics
                 if (go) {
 #pragma unroll
@@ -312,6 +316,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
             __syncwarp();
         }
         for (int q = 0; q < nlist; ++q) {
+            if (__all_sync(kFull, done)) break;  // warp finished: no lane can emit again
             const int j = wlist[q];
             emit_ready(sD[j].w);
             if (done) continue;
@@ -364,6 +369,8 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
         if (lane == 0) {
             atomicAdd(&stats->evals, e);
             atomicAdd(&stats->contribs, c);
+            atomicAdd(&stats->subrounds, n_rounds);
+            atomicAdd(&stats->small_rounds, n_small);
         }
     }
 }

@@ -1197,6 +1197,9 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             out->overflow_pixels = st[0].overflow;
             out->evals_bwd = st[1].evals;
             out->contribs_bwd = st[1].contribs;
+            out->subrounds_bwd = st[1].subrounds;
+            out->small_subrounds_bwd = st[1].small_rounds;
+            out->tiles_work_fwd = st[0].tiles_work;
             out->kernel_launches = ctx->launches - launches0;
         }
     });

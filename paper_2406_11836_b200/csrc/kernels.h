@@ -43,6 +43,8 @@ struct BlendStats {
     unsigned long long contribs;   // emitted contributions
     unsigned long long overflow;   // pixels routed to the exact fallback
     unsigned long long tiles_work; // sum over tiles of candidates processed
+    unsigned long long subrounds;  // backward: warp emission sub-rounds
+    unsigned long long small_rounds; // backward: sub-rounds with <= 2 lanes
 };
 
 // K4: forward alpha blend with the RetinaGS subspace gate, exact per-ray (t, id) order.
