@@ -185,6 +185,20 @@ int dgs_loss(dgs_ctx* ctx, int32_t width, int32_t height, const float* render, c
 int dgs_merge_backward(dgs_ctx* ctx, const dgs_camera* cam, const float* partials, const float* grad_color,
                        const float bg[3], float* out_grads);
 
+/* merge / merge_backward on caller-supplied PixelOrders (engine.hpp:97-106
+ * layout: order[px][k_stride], count[px]), exactly the reference signatures
+ * merge(partials, orders, background) (engine.hpp:152-182) and
+ * merge_backward(partials, orders, grad_color, grad_trans_total, background)
+ * (engine.hpp:195-234).  No partition table needed.  grad_trans_total may be
+ * NULL (zero). */
+int dgs_merge_ordered(dgs_ctx* ctx, int32_t width, int32_t height, int32_t k_count, int32_t k_stride,
+                      const uint16_t* order, const uint16_t* count, const float* partials, const float bg[3],
+                      float* out_rgb, float* out_t);
+int dgs_merge_backward_ordered(dgs_ctx* ctx, int32_t width, int32_t height, int32_t k_count, int32_t k_stride,
+                               const uint16_t* order, const uint16_t* count, const float* partials,
+                               const float* grad_color, const float* grad_trans_total, const float bg[3],
+                               float* out_grads);
+
 /* ---- Per-subset backward (engine.hpp:74-88) + optimizer ------------------------ */
 /* partial_render_backward: grad_ct = H*W*4 (dL/dC_k rgb, dL/dT_k).  Writes the
  * parameter gradients (GradBuffers layout, index-aligned with the members)

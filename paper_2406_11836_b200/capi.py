@@ -113,6 +113,9 @@ _SIGS = {
     "dgs_merge": (C.c_int, [_P, C.POINTER(Camera), _P, _P, _P, _P]),
     "dgs_loss": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, C.c_double, C.c_double, _P, C.POINTER(C.c_double), _P]),
     "dgs_merge_backward": (C.c_int, [_P, C.POINTER(Camera), _P, _P, _P, _P]),
+    "dgs_merge_ordered": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
+    "dgs_merge_backward_ordered": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P,
+                                             _P, _P]),
     "dgs_render_partial_backward": (C.c_int, [_P, C.c_int32, C.POINTER(Camera), _P, C.POINTER(SplatsC)]),
     "dgs_dump_pixel_grads": (C.c_int, [_P, C.c_int32, _P]),
     "dgs_adam_apply": (C.c_int, [_P, C.c_int32, C.POINTER(SplatsC)]),

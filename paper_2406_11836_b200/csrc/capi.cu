@@ -885,6 +885,72 @@ int dgs_merge_backward(dgs_ctx* ctx, const dgs_camera* cam, const float* partial
     });
 }
 
+static void check_orders(int32_t width, int32_t height, int32_t k_count, int32_t k_stride, const uint16_t* order,
+                         const uint16_t* count) {
+    if (width <= 0 || height <= 0) throw std::invalid_argument("merge: non-positive resolution");
+    if (k_count <= 0 || k_count > kMaxSubsets || k_stride < k_count)
+        throw std::invalid_argument("merge: subset count out of range");
+    const size_t px = (size_t)width * height;
+    for (size_t p = 0; p < px; ++p) {
+        if (count[p] > k_count) throw std::invalid_argument("merge: order count exceeds subset count");
+        for (int i = 0; i < count[p]; ++i)
+            if (order[p * k_stride + i] >= k_count) throw std::invalid_argument("merge: order names unknown subset");
+    }
+}
+
+int dgs_merge_ordered(dgs_ctx* ctx, int32_t width, int32_t height, int32_t k_count, int32_t k_stride,
+                      const uint16_t* order, const uint16_t* count, const float* partials, const float bg[3],
+                      float* out_rgb, float* out_t) {
+    return dgs_guard([&] {
+        check_orders(width, height, k_count, k_stride, order, count);
+        const size_t px = (size_t)width * height;
+        DevBuf<uint16_t> d_o, d_c;
+        d_o.ensure(px * k_stride);
+        d_c.ensure(px);
+        ctx->scratch_maps.ensure(px * k_count);
+        ctx->staging.ensure(4 * px);
+        CK(cudaMemcpyAsync(d_o.p, order, px * k_stride * 2, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d_c.p, count, px * 2, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->scratch_maps.p, partials, px * k_count * sizeof(float4), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        launch_merge_ordered((int)px, k_stride, d_o.p, d_c.p, ctx->scratch_maps.p, bg, ctx->staging.p,
+                             ctx->staging.p + 3 * px, ctx->stream);
+        CK(cudaMemcpyAsync(out_rgb, ctx->staging.p, 3 * px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        if (out_t) CK(cudaMemcpyAsync(out_t, ctx->staging.p + 3 * px, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_merge_backward_ordered(dgs_ctx* ctx, int32_t width, int32_t height, int32_t k_count, int32_t k_stride,
+                               const uint16_t* order, const uint16_t* count, const float* partials,
+                               const float* grad_color, const float* grad_trans_total, const float bg[3],
+                               float* out_grads) {
+    return dgs_guard([&] {
+        check_orders(width, height, k_count, k_stride, order, count);
+        const size_t px = (size_t)width * height;
+        DevBuf<uint16_t> d_o, d_c;
+        d_o.ensure(px * k_stride);
+        d_c.ensure(px);
+        ctx->scratch_maps.ensure(px * k_count);
+        ctx->scratch_grads.ensure(px * k_count);
+        ctx->staging.ensure(4 * px);
+        CK(cudaMemcpyAsync(d_o.p, order, px * k_stride * 2, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d_c.p, count, px * 2, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->scratch_maps.p, partials, px * k_count * sizeof(float4), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(ctx->staging.p, grad_color, 3 * px * 4, cudaMemcpyHostToDevice, ctx->stream));
+        if (grad_trans_total)
+            CK(cudaMemcpyAsync(ctx->staging.p + 3 * px, grad_trans_total, px * 4, cudaMemcpyHostToDevice,
+                               ctx->stream));
+        launch_merge_bwd_ordered((int)px, k_count, k_stride, d_o.p, d_c.p, ctx->scratch_maps.p, ctx->staging.p,
+                                 grad_trans_total ? ctx->staging.p + 3 * px : nullptr, bg, ctx->scratch_grads.p,
+                                 ctx->stream);
+        CK(cudaMemcpyAsync(out_grads, ctx->scratch_grads.p, px * k_count * sizeof(float4), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int dgs_render_partial_backward(dgs_ctx* ctx, int32_t k, const dgs_camera* cam, const float* grad_ct,
                                 dgs_splats* grads) {
     return dgs_guard([&] {

@@ -85,6 +85,11 @@ void launch_loss(int W, int H, int row0, int row1, int in_base, int in_rows, con
 void launch_reduce_sums(const double* block_sums, int n_blocks, double* out3, cudaStream_t s);
 
 // K7: merge adjoint (engine.hpp:195-234) for rows [row0, row1); grad_rgb window (g_base, g_rows).
+void launch_merge_ordered(int px, int kstride, const uint16_t* order, const uint16_t* count, const float4* partials,
+                          const float bg[3], float* out_rgb, float* out_t, cudaStream_t s);
+void launch_merge_bwd_ordered(int px, int kcount, int kstride, const uint16_t* order, const uint16_t* count,
+                              const float4* partials, const float* grad_color, const float* grad_tt,
+                              const float bg[3], float4* out, cudaStream_t s);
 void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int row0, int row1,
                       const float4* const* partials, int prow0, const float* grad_rgb, int g_base, int g_rows,
                       const float bg[3], float4* const* grad_out, int grow0, cudaStream_t s);

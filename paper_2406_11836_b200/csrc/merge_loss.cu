@@ -97,6 +97,67 @@ __global__ void k_merge_bwd(ViewParams vp, const Table* __restrict__ tb, int own
     }
 }
 
+/// merge with caller-supplied PixelOrders (engine.hpp:152-182 verbatim
+/// contract): order [px][kstride], count [px]; partials [K][px] float4;
+/// output HWC rgb + T.
+__global__ void k_merge_ordered(int px, int kstride, const uint16_t* __restrict__ order,
+                                const uint16_t* __restrict__ count, const float4* __restrict__ partials, float bg0,
+                                float bg1, float bg2, float* __restrict__ out_rgb, float* __restrict__ out_t) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= px) return;
+    const int n = count[p];
+    float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, tr = 1.0f;
+    for (int i = 0; i < n; ++i) {
+        const float4 q = partials[(size_t)order[(size_t)p * kstride + i] * px + p];
+        c0 = fadd(c0, fmul(tr, q.x));
+        c1 = fadd(c1, fmul(tr, q.y));
+        c2 = fadd(c2, fmul(tr, q.z));
+        tr = fmul(tr, q.w);
+    }
+    out_rgb[3 * (size_t)p] = fadd(c0, fmul(tr, bg0));
+    out_rgb[3 * (size_t)p + 1] = fadd(c1, fmul(tr, bg1));
+    out_rgb[3 * (size_t)p + 2] = fadd(c2, fmul(tr, bg2));
+    out_t[p] = tr;
+}
+
+/// merge_backward with caller-supplied orders and grad_trans_total
+/// (engine.hpp:195-234); grad_color HWC, grad_tt [px] or null (= 0).
+__global__ void k_merge_bwd_ordered(int px, int kcount, int kstride, const uint16_t* __restrict__ order,
+                                    const uint16_t* __restrict__ count, const float4* __restrict__ partials,
+                                    const float* __restrict__ grad_color, const float* __restrict__ grad_tt,
+                                    float bg0, float bg1, float bg2, float4* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= px) return;
+    const int n = count[p];
+    const float gc0 = grad_color[3 * (size_t)p], gc1 = grad_color[3 * (size_t)p + 1],
+                gc2 = grad_color[3 * (size_t)p + 2];
+    const float gt_eff = fadd(grad_tt ? grad_tt[p] : 0.0f, dot3(gc0, gc1, gc2, bg0, bg1, bg2));
+    uint16_t ord[kMaxSubsets];
+    float prefix[kMaxSubsets + 1];
+    float4 pk[kMaxSubsets];
+    prefix[0] = 1.0f;
+    uint32_t present = 0;
+    for (int i = 0; i < n; ++i) {
+        ord[i] = order[(size_t)p * kstride + i];
+        present |= 1u << ord[i];
+        pk[i] = partials[(size_t)ord[i] * px + p];
+        prefix[i + 1] = fmul(prefix[i], pk[i].w);
+    }
+    for (int k = 0; k < kcount; ++k)
+        if (!(present & (1u << k))) out[(size_t)k * px + p] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, tail = 1.0f;
+    for (int i = n - 1; i >= 0; --i) {
+        const float pf = prefix[i];
+        const float dT = fmul(pf, fadd(dot3(gc0, gc1, gc2, s0, s1, s2), fmul(gt_eff, tail)));
+        out[(size_t)ord[i] * px + p] = make_float4(fmul(pf, gc0), fmul(pf, gc1), fmul(pf, gc2), dT);
+        const float4 q = pk[i];
+        s0 = fadd(q.x, fmul(q.w, s0));
+        s1 = fadd(q.y, fmul(q.w, s1));
+        s2 = fadd(q.z, fmul(q.w, s2));
+        tail = fmul(tail, q.w);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Fused L1 + D-SSIM (loss.hpp:94-177), one channel plane per blockIdx.z.
 // ---------------------------------------------------------------------------
@@ -317,6 +378,21 @@ void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int 
     dim3 grid((vp.width + 127) / 128, row1 - row0);
     k_merge_bwd<<<grid, 128, 0, s>>>(vp, tb_dev, owner, row0, row1, partials, prow0, grad_rgb, g_base, g_rows, bg[0],
                                      bg[1], bg[2], grad_out, grow0);
+}
+
+void launch_merge_ordered(int px, int kstride, const uint16_t* order, const uint16_t* count, const float4* partials,
+                          const float bg[3], float* out_rgb, float* out_t, cudaStream_t s) {
+    if (px <= 0) return;
+    k_merge_ordered<<<(unsigned)((px + 255) / 256), 256, 0, s>>>(px, kstride, order, count, partials, bg[0], bg[1],
+                                                                  bg[2], out_rgb, out_t);
+}
+
+void launch_merge_bwd_ordered(int px, int kcount, int kstride, const uint16_t* order, const uint16_t* count,
+                              const float4* partials, const float* grad_color, const float* grad_tt,
+                              const float bg[3], float4* out, cudaStream_t s) {
+    if (px <= 0) return;
+    k_merge_bwd_ordered<<<(unsigned)((px + 255) / 256), 256, 0, s>>>(px, kcount, kstride, order, count, partials,
+                                                                      grad_color, grad_tt, bg[0], bg[1], bg[2], out);
 }
 
 void launch_loss(int W, int H, int row0, int row1, int in_base, int in_rows, const float* x, const float* y,
