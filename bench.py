@@ -40,7 +40,7 @@ REF_DUMP = ROOT / "oracle" / "_ref" / "ref_dump"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--count", type=int, default=10_000_000)
@@ -71,27 +71,51 @@ def workload_config(a, world):
 # clocks sampler (B200_PROFILING.md clocks line)
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clock + throttle reasons sampled every 20 ms during the timed region
+    (NVML; nvidia-smi as the fallback)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(device))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return float(sm), float(mx), int(rs)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        bits = sum(v for v, x in zip((0x8, 0x20, 0x40, 0x4), f[2:6]) if x == "Active")
+        return float(f[0]), float(f[1]), bits
 
     def start(self):
         def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    self.samples.append(self._sample())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.02)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -100,24 +124,23 @@ class Clocks:
         if self._t:
             self._t.join(timeout=10)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
+        reasons = sorted({n for s in self.samples for n, bit in self.REASONS.items() if s[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref: the unmodified reference headers)
 # ---------------------------------------------------------------------------
-def run_reference_steps(a, steps: int, budget_s: float, target_path: str | None):
+def run_reference_steps(a, steps: int, budget_s: float, target_path: str | None, kd: int = 0):
     if not REF_DUMP.exists():
         return None, "oracle/_ref/ref_dump not built (needs /root/reference at build time)"
     threads = os.cpu_count() or 1
     argv = [str(REF_DUMP), "scene=synth", f"count={a.count}", f"w={a.width}", f"h={a.height}", "n_views=64",
-            "seed=11", "kd=0", "perturb=5", f"view={a.view}", f"time_direct={steps}", f"budget_s={budget_s}",
+            "seed=11", f"kd={kd}", "perturb=5", f"view={a.view}", f"time_direct={steps}", f"budget_s={budget_s}",
             f"target={target_path or 'zeros'}", "out=/tmp/dgs_ref_bench"]
     t0 = time.time()
     p = subprocess.run(argv, capture_output=True, text=True, env={**os.environ, "DGS_THREADS": str(threads)})
@@ -145,7 +168,7 @@ def reference_arm(a, world, rank):
         return
     px = a.width * a.height
     # each step is a full-frame reference step; stop once the budget is spent (>= 1 step)
-    res, err = run_reference_steps(a, a.warmup + a.steps, a.cpu_budget_s, None)
+    res, err = run_reference_steps(a, a.warmup + a.steps, a.cpu_budget_s, None, kd=int(math.log2(max(1, world))))
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
         return
@@ -157,7 +180,7 @@ def reference_arm(a, world, rank):
         "impl": "reference", "metric": METRIC, "value": mpx, "unit": "Mpixel/s", "n_gpus": 0, "steps": len(timed),
         "steps_requested": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3, "steps_per_s": 1.0 / t,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(a, 1),
+        "config": workload_config(a, world),
         "cpu_baseline": {"value": mpx, "unit": "Mpixel/s", "cores": res["effective_threads"], "kind": "reference",
                          "sample": f"{len(timed)} full-frame C3 step(s) of the unmodified reference (oracle/_ref/ref_dump "
                                    f"time_direct: Manager::train_step call sequence, no IPC copies), DGS_THREADS="
@@ -177,48 +200,80 @@ def b200_arm(a, world, rank, local_rank):
     from paper_2406_11836_b200 import engine
 
     torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    nccl_id = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if world > 1:
-        raise SystemExit("multi-rank model-parallel run is wired through dgs_ctx NCCL; see DESIGN.md")
+        if world & (world - 1):
+            raise SystemExit("--gpus must be a power of two (one KD subset per rank, K = 2^depth)")
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_ranks(x: float) -> list:
+        if world == 1:
+            return [x]
+        t = torch.zeros(world, dtype=torch.float64, device=dev)
+        t[rank] = x
+        dist.all_reduce(t)
+        return [float(v) for v in t.tolist()]
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize()
 
     t_setup = time.time()
     gt = engine.synth_splats(a.count, seed=11, sh_degree=3)
     cam = engine.ring_camera(a.width, a.height, a.view, n_views=64)
     init = engine.perturb(gt, 5)
-    # targets: GT rendered in oracle mode by this path (io.hpp:540-541)
+    # targets: GT rendered in oracle mode by this path (io.hpp:540-541); every
+    # rank renders the same full target on its own GPU (bitwise identical)
     tmgr = engine.Manager(gt, engine.train_config(kd_depth=0), engine.render_options(oracle=True), device=local_rank)
     target, _ = tmgr.render(cam)
     tmgr.close()
     del gt
     cfg = engine.train_config(kd_depth=int(math.log2(world)), iterations=30000, deterministic=0)
     ro = engine.render_options(grad_skip_eps=0.0)
-    mgr = engine.Manager(init, cfg, ro, device=local_rank)
+    mgr = engine.Manager(init, cfg, ro, device=local_rank, rank=rank, world=world, nccl_id=nccl_id)
     ctx = mgr.ctx
+    n_local = sum(int(engine.lib().dgs_subset_size(ctx.handle, k)) for k in range(mgr.table.subset_count)
+                  if engine.subset_owner(k, mgr.table.subset_count, world) == rank)
     tdev = ctx.upload_targets(target[None])
     setup_s = time.time() - t_setup
 
-    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local_rank))
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
     for _ in range(a.warmup):
         mgr.train_step([cam], None, targets_device_ptr=tdev)
-    torch.cuda.synchronize()
+    barrier()
 
     # ---- device-resident timed region ---------------------------------------
     ctx.set_profiling(True)
     clocks = Clocks(local_rank)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    barrier()
     e0.record(stream)
     results = []
     for _ in range(a.steps):
         results.append(mgr.train_step([cam], None, targets_device_ptr=tdev))
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms_local = e0.elapsed_time(e1)
     clk = clocks.stop()
+    ms = max_over_ranks(ms_local)
     stages = ctx.stage_times()
     ctx.set_profiling(False)
+    rank_ms = gather_ranks(ms_local)
+    rank_blend_ms = gather_ranks((stages["blend_fwd"][0] + stages["blend_bwd"][0]) / max(1, a.steps))
+    rank_members = gather_ranks(float(n_local))
 
     # ---- counters (separate short run: the stats variants of the blends are slower) ----
     ctx.set_collect_stats(True)
@@ -230,7 +285,7 @@ def b200_arm(a, world, rank, local_rank):
     pinned.numpy()[:] = target.reshape(-1)
     host_target = pinned.numpy().reshape(1, a.height, a.width, 3)
     mgr.train_step([cam], host_target)
-    torch.cuda.synchronize()
+    barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     w0 = time.perf_counter()
@@ -240,8 +295,8 @@ def b200_arm(a, world, rank, local_rank):
         e2e_losses.append(r["loss"])
     f1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    e2e_wall = (time.perf_counter() - w0) * 1e3
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    e2e_wall = max_over_ranks((time.perf_counter() - w0) * 1e3)
 
     px = a.width * a.height
     step_ms = ms / a.steps
@@ -254,7 +309,7 @@ def b200_arm(a, world, rank, local_rank):
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     per_stage = {k: v[0] / max(1, a.steps) for k, v in stages.items()}
     dom = max(per_stage, key=per_stage.get)
-    n_all = init.n
+    n_all = n_local
     rows = 59
     alg_bytes = {
         # K10 streaming Adam: read p, m, v + the 17-float gradient record, write p, m, v (every member)
@@ -299,6 +354,11 @@ def b200_arm(a, world, rank, local_rank):
         "warmup": a.warmup, "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(a, world),
+        "ranks": {"ms_per_step": [v / a.steps for v in rank_ms], "blend_ms_per_step": rank_blend_ms,
+                  "members": [int(v) for v in rank_members],
+                  "blend_imbalance_max_over_mean": max(rank_blend_ms) / (sum(rank_blend_ms) / world)
+                  if sum(rank_blend_ms) > 0 else None,
+                  "nccl_bytes_per_step": results[-1].get("nccl_bytes")},
         "e2e": {"value": e2e_value, "unit": "Mpixel/s", "h2d_bytes_per_step": px * 3 * 4,
                 "d2h_bytes_per_step": 3 * 8 + 16 * 4, "ms_per_step_events": e2e_ms / a.steps,
                 "ms_per_step_wall": e2e_wall / a.steps},
@@ -322,6 +382,9 @@ def b200_arm(a, world, rank, local_rank):
     if rank == 0:
         print(json.dumps(line))
     mgr.close()
+    if world > 1:
+        barrier()
+        dist.destroy_process_group()
 
 
 def main():

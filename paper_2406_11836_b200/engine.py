@@ -170,6 +170,14 @@ def slice_plan(height: int, slices: int, s: int) -> tuple[int, int, int, int]:
     return tuple(int(x) for x in out)
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) through the C-ABI; rank 0 creates it, the
+    caller broadcasts it (torch.distributed) before building the Managers."""
+    buf = C.create_string_buffer(128)
+    check(lib().dgs_nccl_unique_id(buf))
+    return buf.raw
+
+
 def subset_owner(k: int, k_count: int, world: int) -> int:
     return int(lib().dgs_subset_owner(k, k_count, world))
 
@@ -397,10 +405,20 @@ class Manager:
     host (bit-exact), every subset resident on this rank's GPU."""
 
     def __init__(self, splats: Splats, config: capi.TrainConfigC | None = None,
-                 options: capi.RenderOptionsC | None = None, device: int = 0):
+                 options: capi.RenderOptionsC | None = None, device: int = 0, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None):
+        """world > 1: one Manager per rank (one process per GPU).  Every rank
+        builds the same KD table on the host (bit-exact, deterministic) and
+        loads only the subsets it owns (`subset_owner`, contiguous blocks);
+        `train_step` then exchanges partial rows and their gradients over the
+        context's NCCL communicator (`nccl_id` from `nccl_unique_id()` on rank
+        0, broadcast by the caller)."""
         self.config = config if config is not None else train_config()
         self.options = options if options is not None else render_options()
-        self.ctx = Context(device)
+        if world > 1 and nccl_id is None:
+            raise ValueError("Manager: world > 1 needs the NCCL unique id of rank 0")
+        self.rank, self.world = rank, world
+        self.ctx = Context(device, rank, world, nccl_id)
         self.sh_coeffs = splats.sh_coeffs
         self.ids = np.sort(splats.id.copy())
         self._distribute(splats, epoch=0)
@@ -411,7 +429,12 @@ class Manager:
         self.members = assign_subsets(self.table, splats, float(self.options.truncation_radius))
         self.ctx.set_table(self.table)
         self.ctx.set_options(self.options, self.config)
+        K = self.table.subset_count
+        if K < self.world:
+            raise ValueError(f"Manager: {K} KD subsets cannot cover {self.world} ranks (kd_depth too small)")
         for k, idx in enumerate(self.members):
+            if subset_owner(k, K, self.world) != self.rank:
+                continue
             self.ctx.load_subset(k, splats.take(idx), m.take(idx) if m is not None else None,
                                  v.take(idx) if v is not None else None, adam_step=adam_step, epoch=epoch)
         self.epoch = epoch
@@ -424,6 +447,8 @@ class Manager:
 
     def snapshot(self):
         """manager.hpp:390-418: the replica held by the subspace containing the centre wins."""
+        if self.world > 1:
+            raise NotImplementedError("snapshot/repartition across ranks is SURVEY §8(f) row 1 (not built)")
         parts = [self.ctx.store_subset(k, self.sh_coeffs) for k in range(self.table.subset_count)]
         chosen: dict[int, tuple[int, int]] = {}
         for k, (p, _, _, _) in enumerate(parts):

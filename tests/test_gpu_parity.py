@@ -64,7 +64,18 @@ def test_projection_and_tile_bins_bit_exact(golden):
             a = np.sort(ent[off[t]:off[t + 1]])
             b = np.sort(rent[roff[t]:roff[t + 1]])
             np.testing.assert_array_equal(a, b, err_msg=f"tile {t}")
+        check_order_bounds(ctx, k, recs, off, ent)
     ctx.close()
+
+
+def check_order_bounds(ctx, k, recs, off, ent):
+    """The blend kernels' ordering contract (binning.cu): every tile list is
+    ordered by range ||mu - o|| (non-decreasing), which makes
+    sqrt(r_n^2 - D_max^2) a lower bound on t for every later entry."""
+    rng = recs[:, 15]
+    for t in range(len(off) - 1):
+        e = ent[off[t]:off[t + 1]]
+        assert (np.diff(rng[e]) >= 0).all(), f"tile {t}: list not in range order"
 
 
 def test_partial_render_and_contributor_order(golden):
