@@ -257,19 +257,40 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                         if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
                 }
             } else {
-                const int leader = __ffs(gm) - 1;
-#pragma unroll
-                for (int f = 0; f < 9; ++f) {
-                    float x = v[f];
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
-                    v[f] = x;
+                // Transposed butterfly: every exchange halves the values a lane
+                // still carries (4 + 2 + 1 + 1 + 1 shuffles for fields 0-7
+                // instead of 8 x 5), leaving the full sum of field
+                // (lane >> 2) & 7 in every lane; lanes 0, 4, ..., 28 then issue
+                // the eight reductions with one RED instruction.  Field 8
+                // (d_alpha) takes a plain 5-step butterfly.
+                const uint32_t mem_w = __shfl_sync(kFull, mem, __ffs(gm) - 1);
+                float a0 = v[0], a1 = v[1], a2 = v[2], a3 = v[3];
+                {
+                    const bool hi = lane & 16;
+                    const float s0 = hi ? a0 : v[4], s1 = hi ? a1 : v[5], s2 = hi ? a2 : v[6], s3 = hi ? a3 : v[7];
+                    a0 = (hi ? v[4] : a0) + __shfl_xor_sync(kFull, s0, 16);
+                    a1 = (hi ? v[5] : a1) + __shfl_xor_sync(kFull, s1, 16);
+                    a2 = (hi ? v[6] : a2) + __shfl_xor_sync(kFull, s2, 16);
+                    a3 = (hi ? v[7] : a3) + __shfl_xor_sync(kFull, s3, 16);
                 }
-                if (lane == leader) {
-#pragma unroll
-                    for (int f = 0; f < 9; ++f)
-                        if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+                {
+                    const bool hi = lane & 8;
+                    const float s0 = hi ? a0 : a2, s1 = hi ? a1 : a3;
+                    a0 = (hi ? a2 : a0) + __shfl_xor_sync(kFull, s0, 8);
+                    a1 = (hi ? a3 : a1) + __shfl_xor_sync(kFull, s1, 8);
                 }
+                {
+                    const bool hi = lane & 4;
+                    const float s0 = hi ? a0 : a1;
+                    a0 = (hi ? a1 : a0) + __shfl_xor_sync(kFull, s0, 4);
+                }
+                a0 += __shfl_xor_sync(kFull, a0, 2);
+                a0 += __shfl_xor_sync(kFull, a0, 1);
+                float a8 = v[8];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) a8 += __shfl_xor_sync(kFull, a8, off);
+                if ((lane & 3) == 0 && a0 != 0.0f) atomicAdd(g2d + ((lane >> 2) & 7) * ld2 + mem_w, a0);
+                if (lane == 0 && a8 != 0.0f) atomicAdd(g2d + 8 * ld2 + mem_w, a8);
             }
         }
     };
