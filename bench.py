@@ -347,7 +347,7 @@ def b200_arm(a, world, rank, local_rank):
 
     last = dict(results[-1])
     for key in ("evals_fwd", "contribs_fwd", "evals_bwd", "contribs_bwd", "overflow_pixels", "subrounds_bwd",
-                "small_subrounds_bwd", "tiles_work_fwd"):
+                "small_subrounds_bwd", "tiles_work_fwd", "replay_tiles_bwd"):
         last[key] = results_stats[-1][key]
     line = {
         "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": a.steps,
@@ -375,6 +375,7 @@ def b200_arm(a, world, rank, local_rank):
                        "evals_bwd": last["evals_bwd"], "contribs_bwd": last["contribs_bwd"],
                        "overflow_pixels": last["overflow_pixels"], "subrounds_bwd": last["subrounds_bwd"],
                        "small_subrounds_bwd": last["small_subrounds_bwd"], "tiles_work_fwd": last["tiles_work_fwd"],
+                       "replay_tiles_bwd": last["replay_tiles_bwd"],
                        "comm_bytes_reference_accounting":
                            last["comm_bytes"]},
         "setup_s": setup_s,

@@ -112,6 +112,7 @@ typedef struct dgs_step_result {
     uint64_t evals_fwd, contribs_fwd, evals_bwd, contribs_bwd, overflow_pixels;
     uint64_t kernel_launches; /* kernels this call launched */
     uint64_t subrounds_bwd, small_subrounds_bwd, tiles_work_fwd; /* blend work counters (stats mode) */
+    uint64_t replay_tiles_bwd; /* tiles the backward replayed (records incomplete; stats mode) */
 } dgs_step_result;
 
 const char* dgs_last_error(void);
@@ -231,6 +232,10 @@ int32_t dgs_subset_owner(int32_t k, int32_t k_count, int32_t world);
 /* Single-rank test mode: run the multi-rank manager path (halo windows,
  * exchange buffers, per-slice loss sums) over `slices` virtual slices with
  * device copies in place of NCCL.  Default 1 (whole image, zero-copy). */
+/* Backward blend strategy: 1 (default) = the forward records each pixel's
+ * composite sequence and the backward walks it; 0 = the backward replays the
+ * ordered traversal (ring) itself.  Same contributions, same order. */
+int dgs_set_backward_records(dgs_ctx* ctx, int32_t enabled);
 int dgs_set_virtual_slices(dgs_ctx* ctx, int32_t slices);
 /* Partial map (C_k, T_k) and its gradient (dL/dC_k, dL/dT_k) of local
  * subset k for view slot v of the last dgs_train_step (debug / parity):

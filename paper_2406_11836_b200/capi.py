@@ -76,7 +76,8 @@ class StepResult(C.Structure):
                 ("pairs", C.c_uint64), ("evals_fwd", C.c_uint64), ("contribs_fwd", C.c_uint64),
                 ("evals_bwd", C.c_uint64), ("contribs_bwd", C.c_uint64), ("overflow_pixels", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("subrounds_bwd", C.c_uint64),
-                ("small_subrounds_bwd", C.c_uint64), ("tiles_work_fwd", C.c_uint64)]
+                ("small_subrounds_bwd", C.c_uint64), ("tiles_work_fwd", C.c_uint64),
+                ("replay_tiles_bwd", C.c_uint64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -125,6 +126,7 @@ _SIGS = {
     "dgs_set_profiling": (C.c_int, [_P, C.c_int32]),
     "dgs_set_collect_stats": (C.c_int, [_P, C.c_int32]),
     "dgs_stage_times": (C.c_int, [_P, _P, _P]),
+    "dgs_set_backward_records": (C.c_int, [_P, C.c_int32]),
     "dgs_set_virtual_slices": (C.c_int, [_P, C.c_int32]),
     "dgs_slice_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P]),
     "dgs_subset_owner": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32]),

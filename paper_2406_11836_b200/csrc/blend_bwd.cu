@@ -127,6 +127,53 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     v[4] = h * (w1 * w1);
 }
 
+/// One emission sub-round's accumulation: all `go` lanes hold adjoints of the
+/// same member `mem`.  One or two lanes: direct atomics.  Otherwise a
+/// transposed butterfly (every exchange halves the values a lane still
+/// carries: 4 + 2 + 1 + 1 + 1 shuffles for fields 0-7 instead of 8 x 5)
+/// leaves the full sum of field (lane >> 2) & 7 in every lane; lanes 0, 4,
+/// ..., 28 issue the eight reductions with one RED instruction.  Field 8
+/// (d_alpha) takes a plain 5-step butterfly.
+__device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint32_t mem, const float v[9],
+                                            float* __restrict__ g2d, size_t ld2) {
+    if (__popc(gm) <= 2) {
+        if (go) {
+#pragma unroll
+            for (int f = 0; f < 9; ++f)
+                if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+        }
+        return;
+    }
+    const uint32_t mem_w = __shfl_sync(kFull, mem, __ffs(gm) - 1);
+    float a0 = v[0], a1 = v[1], a2 = v[2], a3 = v[3];
+    {
+        const bool hi = lane & 16;
+        const float s0 = hi ? a0 : v[4], s1 = hi ? a1 : v[5], s2 = hi ? a2 : v[6], s3 = hi ? a3 : v[7];
+        a0 = (hi ? v[4] : a0) + __shfl_xor_sync(kFull, s0, 16);
+        a1 = (hi ? v[5] : a1) + __shfl_xor_sync(kFull, s1, 16);
+        a2 = (hi ? v[6] : a2) + __shfl_xor_sync(kFull, s2, 16);
+        a3 = (hi ? v[7] : a3) + __shfl_xor_sync(kFull, s3, 16);
+    }
+    {
+        const bool hi = lane & 8;
+        const float s0 = hi ? a0 : a2, s1 = hi ? a1 : a3;
+        a0 = (hi ? a2 : a0) + __shfl_xor_sync(kFull, s0, 8);
+        a1 = (hi ? a3 : a1) + __shfl_xor_sync(kFull, s1, 8);
+    }
+    {
+        const bool hi = lane & 4;
+        const float s0 = hi ? a0 : a1;
+        a0 = (hi ? a1 : a0) + __shfl_xor_sync(kFull, s0, 4);
+    }
+    a0 += __shfl_xor_sync(kFull, a0, 2);
+    a0 += __shfl_xor_sync(kFull, a0, 1);
+    float a8 = v[8];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a8 += __shfl_xor_sync(kFull, a8, off);
+    if ((lane & 3) == 0 && a0 != 0.0f) atomicAdd(g2d + ((lane >> 2) & 7) * ld2 + mem_w, a0);
+    if (lane == 0 && a8 != 0.0f) atomicAdd(g2d + 8 * ld2 + mem_w, a8);
+}
+
 template <bool STATS>
 __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, RenderOpts ro, Subspace gate,
                                                              const SplatRec* __restrict__ recs,
@@ -138,8 +185,10 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                                                              const double* __restrict__ fwd_cd,
                                                              const float4* __restrict__ grad_ct,
                                                              const uint8_t* __restrict__ ovf_flag,
+                                                             const uint8_t* __restrict__ tile_replay,
                                                              float* __restrict__ g2d, size_t ld2,
                                                              BlendStats* __restrict__ stats) {
+    if (tile_replay != nullptr && tile_replay[blockIdx.x] == 0) return;  // handled by k_blend_bwd_rec
     extern __shared__ float4 smem4[];
     float4* sA = smem4;
     float4* sB = sA + kBlendThreads;
@@ -250,48 +299,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                 ++n_rounds;
                 if (__popc(gm) <= 2) ++n_small;
             }
-            if (__popc(gm) <= 2) {  // one or two lanes: direct atomics
-                if (go) {
-#pragma unroll
-                    for (int f = 0; f < 9; ++f)
-                        if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
-                }
-            } else {
-                // Transposed butterfly: every exchange halves the values a lane
-                // still carries (4 + 2 + 1 + 1 + 1 shuffles for fields 0-7
-                // instead of 8 x 5), leaving the full sum of field
-                // (lane >> 2) & 7 in every lane; lanes 0, 4, ..., 28 then issue
-                // the eight reductions with one RED instruction.  Field 8
-                // (d_alpha) takes a plain 5-step butterfly.
-                const uint32_t mem_w = __shfl_sync(kFull, mem, __ffs(gm) - 1);
-                float a0 = v[0], a1 = v[1], a2 = v[2], a3 = v[3];
-                {
-                    const bool hi = lane & 16;
-                    const float s0 = hi ? a0 : v[4], s1 = hi ? a1 : v[5], s2 = hi ? a2 : v[6], s3 = hi ? a3 : v[7];
-                    a0 = (hi ? v[4] : a0) + __shfl_xor_sync(kFull, s0, 16);
-                    a1 = (hi ? v[5] : a1) + __shfl_xor_sync(kFull, s1, 16);
-                    a2 = (hi ? v[6] : a2) + __shfl_xor_sync(kFull, s2, 16);
-                    a3 = (hi ? v[7] : a3) + __shfl_xor_sync(kFull, s3, 16);
-                }
-                {
-                    const bool hi = lane & 8;
-                    const float s0 = hi ? a0 : a2, s1 = hi ? a1 : a3;
-                    a0 = (hi ? a2 : a0) + __shfl_xor_sync(kFull, s0, 8);
-                    a1 = (hi ? a3 : a1) + __shfl_xor_sync(kFull, s1, 8);
-                }
-                {
-                    const bool hi = lane & 4;
-                    const float s0 = hi ? a0 : a1;
-                    a0 = (hi ? a1 : a0) + __shfl_xor_sync(kFull, s0, 4);
-                }
-                a0 += __shfl_xor_sync(kFull, a0, 2);
-                a0 += __shfl_xor_sync(kFull, a0, 1);
-                float a8 = v[8];
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) a8 += __shfl_xor_sync(kFull, a8, off);
-                if ((lane & 3) == 0 && a0 != 0.0f) atomicAdd(g2d + ((lane >> 2) & 7) * ld2 + mem_w, a0);
-                if (lane == 0 && a8 != 0.0f) atomicAdd(g2d + 8 * ld2 + mem_w, a8);
-            }
+            reduce_emit(gm, go, lane, mem, v, g2d, ld2);
         }
     };
 
@@ -381,6 +389,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
     }
     emit_ready(kInf);
 
+    if (STATS && stats != nullptr && tid == 0) atomicAdd(&stats->tiles_work, 1ull);  // replayed tiles
     if (STATS && stats != nullptr) {
         unsigned long long e = n_eval, c = (unsigned long long)nemit;
         for (int off = 16; off > 0; off >>= 1) {
@@ -389,6 +398,116 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
         }
         if (lane == 0) {
             atomicAdd(&stats->evals, e);
+            atomicAdd(&stats->contribs, c);
+            atomicAdd(&stats->subrounds, n_rounds);
+            atomicAdd(&stats->small_rounds, n_small);
+        }
+    }
+}
+
+// Record walk (default path): every pixel replays exactly the contributions
+// the forward composited, in composite order, from the forward's records
+// (CompRecords: tile-list positions), so no candidate is re-evaluated and no
+// reorder ring is needed.  Sub-rounds group the lanes whose next contribution
+// is the same list position (the minimum over the warp), as in the replay
+// kernel, and the adjoint of each sub-round is reduced once.  The next
+// contribution's record is fetched right after an emission, so its L2 latency
+// overlaps the reduction and the other lanes' sub-rounds.
+template <bool STATS>
+__global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams vp, RenderOpts ro,
+                                                                 const SplatRec* __restrict__ recs,
+                                                                 const uint32_t* __restrict__ pair_val,
+                                                                 const uint2* __restrict__ ranges,
+                                                                 const float4* __restrict__ fwd_ct,
+                                                                 const double* __restrict__ fwd_cd,
+                                                                 const float4* __restrict__ grad_ct,
+                                                                 const uint8_t* __restrict__ ovf_flag,
+                                                                 CompRecords crec, float* __restrict__ g2d,
+                                                                 size_t ld2, BlendStats* __restrict__ stats) {
+    const int tile = blockIdx.x;
+    if (crec.tile_replay[tile]) return;  // handled by the replay kernel
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
+    const int px = tx * kTileSize + (tid & 15), py = ty * kTileSize + (tid >> 4);
+    const bool inside = px < vp.width && py < vp.height;
+    const size_t pix = (size_t)py * vp.width + px;
+    PixState ps;
+    ps.T = 1.0f;
+    ps.a0 = ps.a1 = ps.a2 = 0.0;
+    ps.pxf = fadd((float)px, 0.5f);
+    ps.pyf = fadd((float)py, 0.5f);
+    int n = 0;
+    if (inside) {
+        const float4 g = grad_ct[pix];
+        const float4 f = fwd_ct[pix];
+        ps.gc0 = g.x;
+        ps.gc1 = g.y;
+        ps.gc2 = g.z;
+        ps.gT = g.w;
+        ps.Cf0 = fwd_cd[3 * pix];
+        ps.Cf1 = fwd_cd[3 * pix + 1];
+        ps.Cf2 = fwd_cd[3 * pix + 2];
+        ps.Tf = f.w;
+        const float e = ro.grad_skip_eps;
+        const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
+        if (!((gc_zero && g.w == 0.0f) || ovf_flag[pix])) n = crec.cnt[pix];
+    }
+    const uint32_t base = ranges[tile].x;
+    const ushort4* rp = reinterpret_cast<const ushort4*>(crec.pos) + (size_t)tile * (kRecCap / 4) * kBlendThreads + tid;
+    ushort4 q4 = make_ushort4(0, 0, 0, 0);
+    int k = 0;
+    uint32_t key = 0xffffffffu, m = 0;
+    float4 A, B, D;
+    auto fetch = [&]() {
+        if (k < n) {
+            if ((k & 3) == 0) q4 = rp[(k >> 2) * kBlendThreads];
+            const int sel = k & 3;
+            const uint32_t r = sel == 0 ? q4.x : (sel == 1 ? q4.y : (sel == 2 ? q4.z : q4.w));
+            key = r;
+            m = pair_val[base + r];
+            const float4* r4 = reinterpret_cast<const float4*>(recs + m);
+            A = __ldg(r4 + 0);
+            B = __ldg(r4 + 1);
+            D = __ldg(r4 + 3);
+        } else {
+            key = 0xffffffffu;
+        }
+    };
+    fetch();
+    unsigned long long n_rounds = 0, n_small = 0;
+    for (;;) {
+        const bool ready = key != 0xffffffffu;
+        if (!__any_sync(kFull, ready)) break;
+        const uint32_t pmin = __reduce_min_sync(kFull, key);
+        const bool go = ready && key == pmin;
+        float v[9];
+#pragma unroll
+        for (int f = 0; f < 9; ++f) v[f] = 0.0f;
+        uint32_t mem = 0;
+        if (go) {
+            // sigma and g exactly as the forward computed them (eval_candidate)
+            const float dx = fsub(ps.pxf, A.x), dy = fsub(ps.pyf, A.y);
+            const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
+                                  fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
+            const float g = __expf(fmul(-0.5f, m2));
+            const float ag = fmul(A.z, g);
+            const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
+            contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
+            mem = m;
+            ++k;
+            fetch();
+        }
+        const unsigned gm = __ballot_sync(kFull, go);
+        if (STATS) {
+            ++n_rounds;
+            if (__popc(gm) <= 2) ++n_small;
+        }
+        reduce_emit(gm, go, lane, mem, v, g2d, ld2);
+    }
+    if (STATS && stats != nullptr) {
+        unsigned long long c = (unsigned long long)k;
+        for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
+        if (lane == 0) {
             atomicAdd(&stats->contribs, c);
             atomicAdd(&stats->subrounds, n_rounds);
             atomicAdd(&stats->small_rounds, n_small);
@@ -488,7 +607,7 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
 
 void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
-                      float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s) {
+                      const CompRecords& rec, float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
     static bool configured = false;
@@ -497,14 +616,23 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
         cudaFuncSetAttribute(k_blend_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
         configured = true;
     }
+    if (rec.pos != nullptr) {
+        if (stats)
+            k_blend_bwd_rec<true><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
+                                                                  fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats);
+        else
+            k_blend_bwd_rec<false><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
+                                                                   fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats);
+    }
+    // replay: flagged tiles only (every tile without records)
     if (stats)
         k_blend_bwd<true><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
                                                                  vb.ext_y, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
-                                                                 ovf_flag, g2d, ld2, stats);
+                                                                 ovf_flag, rec.tile_replay, g2d, ld2, stats);
     else
         k_blend_bwd<false><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
                                                                   vb.ext_y, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
-                                                                  ovf_flag, g2d, ld2, stats);
+                                                                  ovf_flag, rec.tile_replay, g2d, ld2, stats);
 }
 
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                                                              uint32_t* __restrict__ dbg_ids,
                                                              uint32_t* __restrict__ dbg_cnt, int dbg_cap,
                                                              BlendStats* __restrict__ stats,
-                                                             double* __restrict__ out_cd) {
+                                                             double* __restrict__ out_cd, CompRecords crec) {
     extern __shared__ float4 smem4[];
     float4* sA = smem4;
     float4* sB = sA + kBlendThreads;
@@ -103,9 +103,11 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     Ring* bt = reinterpret_cast<Ring*>(sD + kBlendThreads);
     uint32_t(*bid)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bt + KBUF);
     Ring* bs = reinterpret_cast<Ring*>(bid + KBUF);
-    uint32_t(*bmem)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bs + KBUF);
-    uint16_t* wlist = reinterpret_cast<uint16_t*>(bmem + KBUF) + (threadIdx.x >> 5) * kBlendThreads;
-    uint8_t* smask = reinterpret_cast<uint8_t*>(reinterpret_cast<uint16_t*>(bmem + KBUF) +
+    // list position of each ring entry (colour from the staged batch or, for
+    // entries accepted in an earlier batch, through pair_val; also recorded)
+    uint32_t(*bpos)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bs + KBUF);
+    uint16_t* wlist = reinterpret_cast<uint16_t*>(bpos + KBUF) + (threadIdx.x >> 5) * kBlendThreads;
+    uint8_t* smask = reinterpret_cast<uint8_t*>(reinterpret_cast<uint16_t*>(bpos + KBUF) +
                                                 (kBlendThreads / 32) * kBlendThreads);
 
     const int tid = threadIdx.x;
@@ -126,6 +128,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     int head = 0, cnt = 0, nemit = 0;
     float head_t = kInf;
     unsigned long long n_eval = 0;
+    const uint2 rg = ranges[tile];
+    uint32_t cur_base = rg.x, cur_nb = 0;  // batch currently staged in shared memory
+    const bool record = crec.pos != nullptr && rg.y - rg.x <= 65535u;
+    uint16_t* rec16 = record ? crec.pos + (size_t)tile * kRecCap * kBlendThreads + 4 * tid : nullptr;
 
     auto emit_head = [&]() {
         if (ro.stop > 0.0f && T < ro.stop) {  // raster.hpp:183
@@ -136,7 +142,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         }
         const int sl = head & (KBUF - 1);
         const float sg = bs[sl][tid];
-        const float4 col = __ldg(reinterpret_cast<const float4*>(recs + bmem[sl][tid]) + 3);
+        const uint32_t lp = bpos[sl][tid];
+        const float4 col = (lp - cur_base < cur_nb) ? sD[lp - cur_base]
+                                                    : __ldg(reinterpret_cast<const float4*>(recs + pair_val[lp]) + 3);
+        if (record && nemit < kRecCap) rec16[(nemit >> 2) * (4 * kBlendThreads) + (nemit & 3)] = (uint16_t)(lp - rg.x);
         const float w = fmul(sg, T);
         C0 = fadd(C0, fmul(col.x, w));
         C1 = fadd(C1, fmul(col.y, w));
@@ -149,15 +158,16 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         }
         T = fmul(T, fsub(1.0f, sg));
         if (DBG && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][tid];
-        if (DBG || STATS) ++nemit;
+        ++nemit;
         ++head;
         --cnt;
         head_t = cnt ? bt[head & (KBUF - 1)][tid] : kInf;
     };
 
-    const uint2 rg = ranges[tile];
     for (uint32_t base = rg.x; base < rg.y; base += kBlendThreads) {
         if (__syncthreads_count(!done) == 0) break;
+        cur_base = base;
+        cur_nb = min((uint32_t)kBlendThreads, rg.y - base);
         const uint32_t p = base + tid;
         if (p < rg.y) {
             float4 A, B, C, D;
@@ -222,7 +232,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                     bt[ps][tid] = tp;
                     bid[ps][tid] = ip;
                     bs[ps][tid] = bs[pl][tid];
-                    bmem[ps][tid] = bmem[pl][tid];
+                    bpos[ps][tid] = bpos[pl][tid];
                     --pos;
                 } else {
                     break;
@@ -232,13 +242,20 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             bt[ps][tid] = t;
             bid[ps][tid] = id;
             bs[ps][tid] = sigma;
-            bmem[ps][tid] = pair_val[base + j];
+            bpos[ps][tid] = base + (uint32_t)j;
             ++cnt;
             if (pos == head) head_t = t;
         }
     }
     while (cnt > 0 && !done) emit_head();
 
+    if (crec.pos != nullptr) {
+        // tiles whose records are incomplete are replayed by the backward
+        const bool short_rec = inside && !ovf && nemit > kRecCap;
+        const int rep = __syncthreads_or(short_rec || !record);
+        if (inside) crec.cnt[pix] = (uint16_t)min(nemit, kRecCap);
+        if (tid == 0) crec.tile_replay[tile] = (uint8_t)(rep != 0);
+    }
     if (inside) {
         if (ovf) {
             ovf_flag[pix] = 1;
@@ -363,7 +380,7 @@ __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
 void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       float4* out_ct, uint8_t* ovf_flag, uint32_t* ovf_list, uint32_t* ovf_count,
                       uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, double* out_cd,
-                      cudaStream_t s) {
+                      const CompRecords& rec, cudaStream_t s) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
     const size_t smem = kFwdSmem;
@@ -377,7 +394,7 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
 #define DGS_FWD(D, S)                                                                                              \
     k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext_y, vb.dmax_bits, \
                                                          onorm, out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids,       \
-                                                         dbg_cnt, dbg_cap, stats, out_cd)
+                                                         dbg_cnt, dbg_cap, stats, out_cd, rec)
     if (dbg_ids != nullptr && dbg_cnt != nullptr) DGS_FWD(true, true);
     else if (stats != nullptr) DGS_FWD(false, true);
     else DGS_FWD(false, false);

@@ -97,6 +97,16 @@ struct ViewSlot {
     DevBuf<uint8_t> temp, ovf_flag;
     DevBuf<float4> ct, grad_ct;
     DevBuf<double> cd;  // double colour sums for the backward suffix
+    DevBuf<uint16_t> rec_pos;  // composite records (kernels.h CompRecords)
+    DevBuf<uint16_t> rec_cnt;
+    DevBuf<uint8_t> rec_replay;
+    CompRecords crec() const {
+        CompRecords r;
+        r.pos = rec_pos.p;
+        r.cnt = rec_cnt.p;
+        r.tile_replay = rec_replay.p;
+        return r;
+    }
     int64_t pair_cap = 0;
     size_t temp_bytes = 0;
     ViewBins vb;
@@ -206,6 +216,7 @@ struct Ctx {
     DevBuf<float> targets_win;
     int virtual_slices = 1;        // single-rank sliced mode (tests the multi-rank manager path)
     bool collect_stats = false;    // blend evaluation/contribution counters (costs ~5% in the blends)
+    bool records = true;           // forward composite records -> record-walk backward (else ring replay)
     DevBuf<BlendStats> stats;
     DevBuf<int> bad;
     uint64_t launches = 0;
@@ -361,9 +372,16 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     CK(cudaMemcpyAsync(&err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
     CK(cudaStreamSynchronize(ctx.stream));
     if (err != INT_MAX) throw std::domain_error("zero quaternion");
+    if (ctx.records) {
+        vs.rec_pos.ensure((size_t)tiles * kRecCap * kBlendThreads);
+        vs.rec_cnt.ensure(px);
+        vs.rec_replay.ensure(tiles);
+    }
+    CompRecords crec;
+    if (ctx.records) crec = vs.crec();
     Stage st_fwd(ctx.timer, kStFwd, ctx.stream);
     launch_blend_fwd(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_flag.p, vs.ovf_list.p, vs.ovf_count.p,
-                     dbg_ids, dbg_cnt, dbg_cap, stats, vs.cd.p, ctx.stream);
+                     dbg_ids, dbg_cnt, dbg_cap, stats, vs.cd.p, crec, ctx.stream);
     st_fwd.end();
     ++ctx.launches;
     CK(cudaMemcpyAsync(&vs.n_ovf, vs.ovf_count.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
@@ -383,8 +401,10 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     S.g2d.ensure(9 * S.ld);
     CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
     Stage st(ctx.timer, kStBwd, ctx.stream);
-    launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, S.g2d.p,
-                     S.ld, stats, ctx.stream);
+    CompRecords crec;
+    if (ctx.records && vs.rec_pos.p) crec = vs.crec();
+    launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, crec,
+                     S.g2d.p, S.ld, stats, ctx.stream);
     ++ctx.launches;
     if (vs.n_ovf > 0) {
         launch_blend_bwd_fallback(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p,
@@ -1266,6 +1286,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             out->subrounds_bwd = st[1].subrounds;
             out->small_subrounds_bwd = st[1].small_rounds;
             out->tiles_work_fwd = st[0].tiles_work;
+            out->replay_tiles_bwd = st[1].tiles_work;
             out->kernel_launches = ctx->launches - launches0;
         }
     });
@@ -1287,6 +1308,10 @@ int dgs_dump_grad_maps(dgs_ctx* ctx, int32_t k, int32_t view, float* partial_ct,
 
 int dgs_set_collect_stats(dgs_ctx* ctx, int32_t enabled) {
     return dgs_guard([&] { ctx->collect_stats = enabled != 0; });
+}
+
+int dgs_set_backward_records(dgs_ctx* ctx, int32_t enabled) {
+    return dgs_guard([&] { ctx->records = enabled != 0; });
 }
 
 int dgs_set_virtual_slices(dgs_ctx* ctx, int32_t slices) {

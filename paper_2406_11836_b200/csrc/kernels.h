@@ -47,20 +47,36 @@ struct BlendStats {
     unsigned long long small_rounds; // backward: sub-rounds with <= 2 lanes
 };
 
+/// Per-pixel composite records: the forward blend writes, for every pixel, the
+/// tile-list positions (u16, relative to the tile's range start) of its first
+/// kRecCap contributions in composite order; the backward blend walks them
+/// directly instead of re-evaluating and re-ordering the tile list.  Tiles
+/// where a pixel exceeds the cap (or the list exceeds 65,535 entries) are
+/// flagged and replayed by the ordered-ring backward.
+constexpr int kRecCap = 256;
+struct CompRecords {
+    uint16_t* pos = nullptr;         // [tiles][kRecCap / 4][256][4]
+    uint16_t* cnt = nullptr;         // [px] recorded contributions
+    uint8_t* tile_replay = nullptr;  // [tiles] 1: replay this tile in the backward
+};
+
 // K4: forward alpha blend with the RetinaGS subspace gate, exact per-ray (t, id) order.
+// `rec` (pos == nullptr: no records) receives the composite records.
 void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       float4* out_ct, uint8_t* ovf_flag, uint32_t* ovf_list, uint32_t* ovf_count,
                       uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, double* out_cd,
-                      cudaStream_t s);
+                      const CompRecords& rec, cudaStream_t s);
 void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                                float4* out_ct, const uint32_t* ovf_list, uint32_t n_ovf, uint32_t* dbg_ids,
                                uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s);
 
 // K8: backward blend; accumulates 9 pixel-space adjoints per member into g2d (SoA [9][ld2]).
 // fwd_cd: the forward's double-precision colour sums (suffix = C - prefix without cancellation loss).
+// With records (rec.pos != nullptr): the record walk for unflagged tiles plus
+// the ordered-ring replay for flagged tiles; without: replay everywhere.
 void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
-                      float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s);
+                      const CompRecords& rec, float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s);
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
                                const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
                                const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s);

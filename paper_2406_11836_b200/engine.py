@@ -240,6 +240,9 @@ class Context:
     def set_collect_stats(self, on: bool):
         check(lib().dgs_set_collect_stats(self._h, int(on)))
 
+    def set_backward_records(self, on: bool):
+        check(lib().dgs_set_backward_records(self._h, int(on)))
+
     def set_profiling(self, on: bool):
         check(lib().dgs_set_profiling(self._h, int(on)))
 

@@ -144,9 +144,11 @@ def _grad_check(got, g, prefix, fields, tol=1e-3):
     return worst
 
 
-def test_partial_backward_gradients(golden):
+@pytest.mark.parametrize("records", [True, False], ids=["record-walk", "ring-replay"])
+def test_partial_backward_gradients(golden, records):
     g = golden
     ctx, table, s = make_ctx(g, members_of(g))
+    ctx.set_backward_records(records)
     cam = g.camera()
     for k in range(g.subsets()):
         grad_ct = np.concatenate([g[f"k{k}_dC"], g[f"k{k}_dT"][..., None]], axis=-1)

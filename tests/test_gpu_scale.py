@@ -84,3 +84,30 @@ def test_medium_scene_bins_order_and_render(scene):
         if m and not np.array_equal(ids[p, :m], ids_ref[p, :m]):
             raise AssertionError(f"pixel {p}: contributor order differs")
     ctx.close()
+
+
+def test_medium_scene_backward_record_walk_matches_replay(scene):
+    """The record-walk backward (default) and the ordered-ring replay
+    backward accumulate the same contributions in the same per-pixel order;
+    only the float-atomic summation order across pixels differs."""
+    s, cam = scene
+    table = engine.build_kdtree(s.mu, 0)
+    H, W = cam.height, cam.width
+    rng = np.random.default_rng(3)
+    grad_ct = (rng.standard_normal((H, W, 4)) * 1e-3).astype(np.float32)
+    out = {}
+    for records in (True, False):
+        ctx = engine.Context(0)
+        ctx.set_table(table)
+        ctx.set_options(engine.render_options(grad_skip_eps=0.0), engine.train_config())
+        ctx.load_subset(0, s)
+        ctx.set_backward_records(records)
+        ctx.render_partial(0, cam)
+        ctx.render_partial_backward(0, cam, grad_ct, s.sh_coeffs)
+        out[records] = ctx.dump_pixel_grads(0)
+        ctx.close()
+    a, b = out[True], out[False]
+    assert np.abs(a).max() > 0
+    floor = 1e-4 * np.abs(b).max(axis=0, keepdims=True)
+    err = np.abs(a - b) / np.maximum(np.abs(b), floor)
+    assert err.max() <= 1e-3, float(err.max())
