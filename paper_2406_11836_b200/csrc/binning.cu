@@ -18,9 +18,16 @@ namespace dgs_b200 {
 
 namespace {
 
-__global__ void k_iota(uint32_t* v, int n) {
+/// 24-bit sort key: range bits relative to the view's minimum visible range,
+/// clamped (members past the window, and culled members, share the top key;
+/// the blends bound them by the window edge), plus the identity values.
+__global__ void k_key24(const uint32_t* __restrict__ rkey, const uint32_t* __restrict__ dmax_bits,
+                        uint32_t* __restrict__ key, uint32_t* __restrict__ vals, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = (uint32_t)i;
+    if (i >= n) return;
+    const uint32_t b = rkey[i], lo = dmax_bits[1];
+    key[i] = (b == 0xffffffffu || b < lo) ? 0xffffffu : min(b - lo, 0xffffffu);
+    vals[i] = (uint32_t)i;
 }
 
 __global__ void k_gather_counts(const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ counts,
@@ -35,7 +42,7 @@ __global__ void k_gather_counts(const uint32_t* __restrict__ sorted_idx, const u
 /// so every store instruction writes 32 consecutive words.
 __global__ void k_emit_pairs(const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ offsets,
                              const uint32_t* __restrict__ counts, const uint32_t* __restrict__ rect, int tiles_x,
-                             int n, uint32_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_val) {
+                             int n, uint16_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_val) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint32_t i = 0, c = 0, off = 0, x0 = 0, w = 1, y0 = 0;
@@ -77,13 +84,13 @@ __global__ void k_emit_pairs(const uint32_t* __restrict__ sorted_idx, const uint
         if (q < total) {
             const uint32_t r = q - ex;
             const uint32_t ty = my0 + r / mw, tx = mx0 + r % mw;
-            pair_tile[base + q] = ty * (uint32_t)tiles_x + tx;
+            pair_tile[base + q] = (uint16_t)(ty * (uint32_t)tiles_x + tx);
             pair_val[base + q] = mi;
         }
     }
 }
 
-__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__ a, uint32_t n, uint32_t key) {
+__device__ __forceinline__ uint32_t lower_bound_u16(const uint16_t* __restrict__ a, uint32_t n, uint32_t key) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -94,10 +101,10 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__
 }
 
 /// Per-tile [start, end) by binary search over the sorted tile keys (one thread per tile).
-__global__ void k_tile_ranges(const uint32_t* __restrict__ tile, uint32_t P, int tiles, uint2* __restrict__ ranges) {
+__global__ void k_tile_ranges(const uint16_t* __restrict__ tile, uint32_t P, int tiles, uint2* __restrict__ ranges) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= tiles) return;
-    ranges[t] = make_uint2(lower_bound_u32(tile, P, (uint32_t)t), lower_bound_u32(tile, P, (uint32_t)t + 1));
+    ranges[t] = make_uint2(lower_bound_u16(tile, P, (uint32_t)t), lower_bound_u16(tile, P, (uint32_t)t + 1));
 }
 
 struct CountOf {
@@ -117,8 +124,9 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
     size_t a = 0, b = 0, c = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (uint32_t*)nullptr, n);
-    cub::DoubleBuffer<uint32_t> dk, dv;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, dk, dv, (int)pair_cap, 0, 32);
+    cub::DoubleBuffer<uint16_t> dk;
+    cub::DoubleBuffer<uint32_t> dv;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, dk, dv, (int)pair_cap, 0, 16);
     cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it((const uint32_t*)nullptr, CountOf{nullptr});
     cub::DeviceScan::InclusiveSum(nullptr, c, it, (uint32_t*)nullptr, n);
     size_t m = a > b ? a : b;
@@ -126,17 +134,18 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
 }
 
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
-                    uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint32_t* pair_tile_alt,
+                    uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
                     uint32_t* pair_val_alt, uint32_t* scan_buf, cudaStream_t s) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     cudaMemsetAsync(vb.ranges, 0, sizeof(uint2) * tiles, s);
     vb.pairs = 0;
     if (n <= 0) return 0;
     const int blk = 256, grid = (n + blk - 1) / blk;
-    k_iota<<<grid, blk, 0, s>>>(sort_vals, n);
+    // 1) members by range: 24-bit keys relative to the minimum range (3 radix
+    //    passes; culled members and any beyond the window share the top key)
+    k_key24<<<grid, blk, 0, s>>>(vb.rkey, vb.dmax_bits, scan_buf, sort_vals, n);
     size_t tb = temp_bytes;
-    // 1) members by range (culled members carry 0xffffffff and sort last)
-    cub::DeviceRadixSort::SortPairs(temp, tb, vb.rkey, sort_keys_alt, sort_vals, sort_vals_alt, n, 0, 32, s);
+    cub::DeviceRadixSort::SortPairs(temp, tb, scan_buf, sort_keys_alt, sort_vals, sort_vals_alt, n, 0, 24, s);
     // 2) tile counts in range order -> inclusive scan -> pair end offsets
     //    (the gather is fused into the scan through a transform iterator)
     cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> cnt_it(sort_vals_alt, CountOf{vb.counts});
@@ -153,11 +162,12 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     k_emit_pairs<<<grid, blk, 0, s>>>(sort_vals_alt, scan_buf, vb.counts, vb.rect, vp.tiles_x, n, vb.pair_tile,
                                       vb.pair_val);  // scan_buf holds inclusive ends: start = end - count
     // 4) stable LSD radix sort by tile id only
-    cub::DoubleBuffer<uint32_t> dk(vb.pair_tile, pair_tile_alt), dv(vb.pair_val, pair_val_alt);
+    cub::DoubleBuffer<uint16_t> dk(vb.pair_tile, pair_tile_alt);
+    cub::DoubleBuffer<uint32_t> dv(vb.pair_val, pair_val_alt);
     tb = temp_bytes;
     cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, (int)P, 0, bits_for((uint32_t)tiles), s);
     if (dk.Current() != vb.pair_tile) {
-        cudaMemcpyAsync(vb.pair_tile, dk.Current(), 4 * (size_t)P, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(vb.pair_tile, dk.Current(), 2 * (size_t)P, cudaMemcpyDeviceToDevice, s);
         cudaMemcpyAsync(vb.pair_val, dv.Current(), 4 * (size_t)P, cudaMemcpyDeviceToDevice, s);
     }
     // 5) per-tile [start, end)

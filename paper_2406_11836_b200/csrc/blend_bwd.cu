@@ -214,7 +214,10 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
     pixel_ray_dir(vp, px, py, pr.d);
     pr.pxf = fadd((float)px, 0.5f);
     pr.pyf = fadd((float)py, 0.5f);
-    const float dmax = __uint_as_float(*dmax_bits);
+    const float dmax = __uint_as_float(dmax_bits[0]);
+    // members whose range is beyond the 24-bit sort window are unordered among
+    // themselves (binning.cu): their bound is the window edge
+    const float r_edge = __uint_as_float(min(dmax_bits[1] + 0xffffffu, 0x7f7fffffu));
 
     PixState ps;
     ps.T = 1.0f;
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
             float4 A, B, C, D;
             const uint32_t m = pair_val[p];
             load_rec(recs, m, A, B, C, D);
-            D.w = order_bound(D.w, dmax, onorm);
+            D.w = order_bound(fminf(D.w, r_edge), dmax, onorm);
             sA[tid] = A;
             sB[tid] = B;
             sC[tid] = C;

@@ -89,7 +89,8 @@ struct DevBuf {
 
 struct ViewSlot {
     DevBuf<SplatRec> recs;
-    DevBuf<uint32_t> rect, counts, rkey, dmax, pair_tile, pair_val, pair_tile_alt, pair_val_alt;
+    DevBuf<uint32_t> rect, counts, rkey, dmax, pair_val, pair_val_alt;
+    DevBuf<uint16_t> pair_tile, pair_tile_alt;
     DevBuf<float> ext_y;
     DevBuf<uint32_t> sort_keys_alt, sort_vals, sort_vals_alt, scan, ovf_list, ovf_count;
     DevBuf<int> err;
@@ -317,12 +318,13 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     const size_t px = (size_t)vp.width * vp.height;
     vs.vp = vp;
     ViewBins& vb = vs.vb;
+    if (tiles > 65535) throw std::invalid_argument("render: more than 65535 16x16 tiles (16-bit tile keys)");
     vb.recs = vs.recs.ensure(n);
     vb.rect = vs.rect.ensure(2 * n);
     vb.counts = vs.counts.ensure(n);
     vb.rkey = vs.rkey.ensure(n);
     vb.ext_y = vs.ext_y.ensure(n);
-    vb.dmax_bits = vs.dmax.ensure(1);
+    vb.dmax_bits = vs.dmax.ensure(2);
     vb.err_index = vs.err.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);
     vs.sort_keys_alt.ensure(n);
@@ -345,7 +347,8 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         vs.temp_bytes = vs.temp.n;
     };
     alloc_pairs();
-    CK(cudaMemsetAsync(vb.dmax_bits, 0, 4, ctx.stream));
+    const uint32_t dmax0[2] = {0u, 0x7f7fffffu};  // (max D, min range)
+    CK(cudaMemcpyAsync(vb.dmax_bits, dmax0, sizeof(dmax0), cudaMemcpyHostToDevice, ctx.stream));
     const int int_max = INT_MAX;
     CK(cudaMemcpyAsync(vb.err_index, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));
     CK(cudaMemsetAsync(vs.ovf_count.p, 0, 4, ctx.stream));

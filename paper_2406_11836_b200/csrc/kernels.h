@@ -17,9 +17,9 @@ struct ViewBins {
     uint32_t* counts = nullptr;      // [n] tile count per member (0 = culled)
     uint32_t* rkey = nullptr;        // [n] range bits (0xffffffff = culled)
     float* ext_y = nullptr;          // [n] conservative row half-extent of the m^2 <= 9 region (warp culling)
-    uint32_t* dmax_bits = nullptr;   // [1] max world_radius over visible members
+    uint32_t* dmax_bits = nullptr;   // [2] max world_radius over visible members, min range (float bits)
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
-    uint32_t* pair_tile = nullptr;   // [cap] tile key of each (splat, tile) pair
+    uint16_t* pair_tile = nullptr;   // [cap] tile key of each (splat, tile) pair
     uint32_t* pair_val = nullptr;    // [cap] member index
     uint2* ranges = nullptr;         // [tiles] (start, end) into the sorted pair list
     int64_t pairs = 0;
@@ -35,7 +35,7 @@ size_t binning_temp_bytes(int n, int64_t pair_cap);
 // tile, fills vb.ranges.  Returns the pair count (host sync).  `cap` is the
 // pair buffer capacity; returns -needed if it is too small.
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
-                    uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint32_t* pair_tile_alt,
+                    uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
                     uint32_t* pair_val_alt, uint32_t* scan_buf, cudaStream_t s);
 
 struct BlendStats {

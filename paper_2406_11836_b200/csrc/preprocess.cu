@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
         for (int r = 0; r < ROWS; ++r) bulk_g2s(tile + r * kPreTB, P + (size_t)r * ld + i0, bytes, &bar);
     }
     mbar_wait(&bar, 0);
-    float dmax_local = 0.0f;
+    float dmax_local = 0.0f, rmin_local = __int_as_float(0x7f7fffff);
     if (i < n) {
         auto row = [&](int r) { return tile[r * kPreTB + tid]; };
         const float mu0 = row(kRowMu), mu1 = row(kRowMu + 1), mu2 = row(kRowMu + 2);
@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
                 vb.recs[i] = rec;
                 vb.rkey[i] = f2u(rec.range);
                 dmax_local = wr;
+                rmin_local = rec.range;
             }
         }
         if (!visible) {
@@ -180,15 +181,26 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
             vb.rkey[i] = 0xffffffffu;
         }
     }
-    // block max of D over visible members -> one atomic per block
-    __shared__ float s_max[kPreTB / 32];
-    float m = dmax_local;
-    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
+    // block max of D and min of the range over visible members -> one atomic each per block
+    __shared__ float s_max[kPreTB / 32], s_min[kPreTB / 32];
+    float m = dmax_local, lo = rmin_local;
+    for (int off = 16; off > 0; off >>= 1) {
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_max[threadIdx.x >> 5] = m;
+        s_min[threadIdx.x >> 5] = lo;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, s_max[w]);
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            m = fmaxf(m, s_max[w]);
+            lo = fminf(lo, s_min[w]);
+        }
+        // non-negative floats order like their bit patterns
         if (m > 0.0f) atomicMax(vb.dmax_bits, __float_as_uint(m));
+        atomicMin(vb.dmax_bits + 1, __float_as_uint(lo));
     }
 }
 
