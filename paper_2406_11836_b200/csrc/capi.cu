@@ -99,6 +99,7 @@ struct ViewSlot {
     DevBuf<float4> ct, grad_ct;
     DevBuf<double> cd;  // double colour sums for the backward suffix
     DevBuf<uint16_t> rec_pos;  // composite records (kernels.h CompRecords)
+    DevBuf<float> shjac;       // [10][ld] SH colour Jacobian + clamp mask (ViewBins::shjac)
     DevBuf<uint16_t> rec_cnt;
     DevBuf<uint8_t> rec_replay;
     CompRecords crec() const {
@@ -319,6 +320,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vs.vp = vp;
     ViewBins& vb = vs.vb;
     if (tiles > 65535) throw std::invalid_argument("render: more than 65535 16x16 tiles (16-bit tile keys)");
+    vb.shjac = vs.shjac.ensure((size_t)10 * S.ld);
     vb.recs = vs.recs.ensure(n);
     vb.rect = vs.rect.ensure(2 * n);
     vb.counts = vs.counts.ensure(n);
@@ -1222,7 +1224,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                         CK(cudaEventRecord(a, ctx->stream));
                     }
                     launch_project_bwd_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro,
-                                            vs.vb.counts, S_.g2d.p, S_.ld, batch > 1 ? S_.G.p : nullptr, ap,
+                                            vs.vb.counts, vs.vb.shjac, S_.g2d.p, S_.ld, batch > 1 ? S_.G.p : nullptr, ap,
                                             ctx->bad.p, S_.rec.p, m1, m2, ctx->stream);
                     if (ctx->timer.on) {
                         b = ctx->timer.get();

@@ -217,6 +217,45 @@ DGS_HD void sh_basis(const float d[3], int deg, float b[16]) {
     b[15] = fmul(fmul((float)-0.5900435899266435, x), fsub(xx, fmul(3.0f, yy)));
 }
 
+constexpr float kShC1f = 0.4886025119029199f;
+
+/// splat.hpp:180-204 sh::basis_jacobian, row i -> (dx, dy, dz).
+DGS_HD void sh_basis_jac(const float d[3], int deg, int i, float j[3]) {
+    j[0] = j[1] = j[2] = 0.0f;
+    if (deg < 1 || i == 0) return;
+    const float x = d[0], y = d[1], z = d[2];
+    const float c2_0 = 1.0925484305920792f, c2_1 = -1.0925484305920792f, c2_2 = 0.31539156525252005f,
+                c2_3 = -1.0925484305920792f, c2_4 = 0.5462742152960396f;
+    const float c3_0 = -0.5900435899266435f, c3_1 = 2.890611442640554f, c3_2 = -0.4570457994644657f,
+                c3_3 = 0.3731763325901154f, c3_4 = -0.4570457994644657f, c3_5 = 1.445305721320277f,
+                c3_6 = -0.5900435899266435f;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    switch (i) {
+        case 1: j[1] = -kShC1f; break;
+        case 2: j[2] = kShC1f; break;
+        case 3: j[0] = -kShC1f; break;
+        case 4: j[0] = c2_0 * y; j[1] = c2_0 * x; break;
+        case 5: j[1] = c2_1 * z; j[2] = c2_1 * y; break;
+        case 6: j[0] = (float)(-2 * 0.31539156525252005) * x; j[1] = (float)(-2 * 0.31539156525252005) * y;
+                j[2] = (float)(4 * 0.31539156525252005) * z; (void)c2_2; break;
+        case 7: j[0] = c2_3 * z; j[2] = c2_3 * x; break;
+        case 8: j[0] = (float)(2 * 0.5462742152960396) * x; j[1] = (float)(-2 * 0.5462742152960396) * y;
+                (void)c2_4; break;
+        case 9: j[0] = (float)(6 * -0.5900435899266435) * x * y; j[1] = c3_0 * (3.0f * xx - 3.0f * yy); break;
+        case 10: j[0] = c3_1 * y * z; j[1] = c3_1 * x * z; j[2] = c3_1 * x * y; break;
+        case 11: j[0] = (float)(-2 * -0.4570457994644657) * x * y; j[1] = c3_2 * (4.0f * zz - xx - 3.0f * yy);
+                 j[2] = (float)(8 * -0.4570457994644657) * y * z; break;
+        case 12: j[0] = (float)(-6 * 0.3731763325901154) * x * z; j[1] = (float)(-6 * 0.3731763325901154) * y * z;
+                 j[2] = c3_3 * (6.0f * zz - 3.0f * xx - 3.0f * yy); break;
+        case 13: j[0] = c3_4 * (4.0f * zz - 3.0f * xx - yy); j[1] = (float)(-2 * -0.4570457994644657) * x * y;
+                 j[2] = (float)(8 * -0.4570457994644657) * x * z; break;
+        case 14: j[0] = (float)(2 * 1.445305721320277) * x * z; j[1] = (float)(-2 * 1.445305721320277) * y * z;
+                 j[2] = c3_5 * (xx - yy); break;
+        case 15: j[0] = c3_6 * (3.0f * xx - 3.0f * yy); j[1] = (float)(-6 * -0.5900435899266435) * x * y; break;
+        default: break;
+    }
+}
+
 }  // namespace dgs_b200
 
 // ---------------------------------------------------------------------------

@@ -19,6 +19,8 @@ struct ViewBins {
     float* ext_y = nullptr;          // [n] conservative row half-extent of the m^2 <= 9 region (warp culling)
     uint32_t* dmax_bits = nullptr;   // [2] max world_radius over visible members, min range (float bits)
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
+    float* shjac = nullptr;          // [10][ld] (optional): d colour_ch / d dir_a (row 3 ch + a) and the
+                                     //     pre-clamp sign mask (row 9, bits) for the gradient record (K9)
     uint16_t* pair_tile = nullptr;   // [cap] tile key of each (splat, tile) pair
     uint32_t* pair_val = nullptr;    // [cap] member index
     uint2* ranges = nullptr;         // [tiles] (start, end) into the sorted pair list
@@ -124,8 +126,10 @@ void launch_project_bwd(int n, const float* P, size_t ld, int sh_coeffs, const V
                         const RenderOpts& ro, const uint32_t* counts, const float* g2d, size_t ld2, float* G,
                         int* bad_index, cudaStream_t s);
 // g_rec: scratch of 17 rows x ld floats (the per-member gradient record).
+// shjac: the preprocess's SH colour Jacobian rows ([10][ld], ViewBins::shjac) or nullptr (read the SH rows).
 void launch_project_bwd_adam(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, const ViewParams& vp,
-                             const RenderOpts& ro, const uint32_t* counts, const float* g2d, size_t ld2,
+                             const RenderOpts& ro, const uint32_t* counts, const float* shjac, const float* g2d,
+                             size_t ld2,
                              const float* G_extra, const AdamParams& ap, int* bad_index, float* g_rec,
                              cudaEvent_t mid_end, cudaEvent_t mid_begin, cudaStream_t s);
 constexpr int kGradRecordRows = 17;

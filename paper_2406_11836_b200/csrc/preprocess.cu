@@ -154,8 +154,32 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
                 sh_basis(dir, deg, b);
                 const int nb = (deg + 1) * (deg + 1);
                 float col[3] = {0.5f, 0.5f, 0.5f};
-                for (int k = 0; k < nb; ++k)
-                    for (int ch = 0; ch < 3; ++ch) col[ch] = fadd(col[ch], fmul(b[k], row(kRowSh + 3 * k + ch)));
+#pragma unroll
+                for (int k = 0; k < SHC; ++k)
+                    if (k < nb)
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) col[ch] = fadd(col[ch], fmul(b[k], row(kRowSh + 3 * k + ch)));
+                if (vb.shjac != nullptr) {
+                    // d colour / d dir for the gradient record (tolerance-level, splat.hpp:223-239)
+                    float J[9] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                    for (int k = 1; k < SHC; ++k) {
+                        if (k >= nb) break;
+                        float jb[3];
+                        sh_basis_jac(dir, deg, k, jb);
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const float c = row(kRowSh + 3 * k + ch);
+                            J[ch * 3 + 0] += jb[0] * c;
+                            J[ch * 3 + 1] += jb[1] * c;
+                            J[ch * 3 + 2] += jb[2] * c;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) vb.shjac[(size_t)q * ld + i] = J[q];
+                    const uint32_t mask = (col[0] < 0.0f ? 1u : 0u) | (col[1] < 0.0f ? 2u : 0u) | (col[2] < 0.0f ? 4u : 0u);
+                    vb.shjac[9 * ld + i] = __uint_as_float(mask);
+                }
                 rec.cr = col[0] < 0.0f ? 0.0f : col[0];  // cwiseMax(0) = std::max(c, 0)
                 rec.cg = col[1] < 0.0f ? 0.0f : col[1];
                 rec.cb = col[2] < 0.0f ? 0.0f : col[2];
