@@ -135,7 +135,7 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
 
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
                     uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
-                    uint32_t* pair_val_alt, uint32_t* scan_buf, cudaStream_t s) {
+                    uint32_t* pair_val_alt, uint32_t* scan_buf, uint32_t* pairs_host, cudaStream_t s) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     cudaMemsetAsync(vb.ranges, 0, sizeof(uint2) * tiles, s);
     vb.pairs = 0;
@@ -151,10 +151,11 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> cnt_it(sort_vals_alt, CountOf{vb.counts});
     tb = temp_bytes;
     cub::DeviceScan::InclusiveSum(temp, tb, cnt_it, scan_buf, n, s);
-    uint32_t last_end = 0;
-    cudaMemcpyAsync(&last_end, scan_buf + (n - 1), 4, cudaMemcpyDeviceToHost, s);
+    // the one host round trip of the step's forward: the pair count sizes the
+    // tile sort (pinned readback; the caller's pending readbacks ride along)
+    cudaMemcpyAsync(pairs_host, scan_buf + (n - 1), 4, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    const int64_t P = (int64_t)last_end;
+    const int64_t P = (int64_t)*pairs_host;
     if (P > cap) return -P;
     vb.pairs = P;
     if (P == 0) return 0;

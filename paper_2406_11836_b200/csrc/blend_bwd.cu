@@ -526,9 +526,10 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
                                      const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
                                      const float4* __restrict__ fwd_ct, const double* __restrict__ fwd_cd,
                                      const float4* __restrict__ grad_ct, const uint32_t* __restrict__ ovf_list,
-                                     uint32_t n_ovf, float* __restrict__ g2d, size_t ld2) {
-    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= n_ovf) return;
+                                     const uint32_t* __restrict__ n_ovf_dev, float* __restrict__ g2d, size_t ld2) {
+    // grid-stride over the device-side overflow count (no host round trip)
+    const uint32_t n_ovf = *n_ovf_dev;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_ovf; w += gridDim.x * blockDim.x) {
     const uint32_t pix = ovf_list[w];
     const int px = pix % vp.width, py = pix / vp.width;
     const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
@@ -551,7 +552,7 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
     ps.Cf2 = fwd_cd[3 * (size_t)pix + 2];
     ps.Tf = ff.w;
     const float e = ro.grad_skip_eps;
-    if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) return;
+    if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) continue;
     const uint2 rg = ranges[tile];
     float wt = -kInf;
     uint32_t wid = 0;
@@ -604,6 +605,7 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
             have_w = true;
         }
     }
+    }
 }
 
 }  // namespace
@@ -640,10 +642,10 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
 
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
                                const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
-                               const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s) {
-    if (n_ovf == 0) return;
-    k_blend_bwd_fallback<<<(n_ovf + 63) / 64, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
-                                                          fwd_cd, grad_ct, ovf_list, n_ovf, g2d, ld2);
+                               const uint32_t* ovf_list, const uint32_t* n_ovf_dev, float* g2d, size_t ld2,
+                               cudaStream_t s) {
+    k_blend_bwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, fwd_ct, fwd_cd, grad_ct,
+                                               ovf_list, n_ovf_dev, g2d, ld2);
 }
 
 }  // namespace dgs_b200

@@ -297,10 +297,11 @@ constexpr int FB = 16;
 __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate, const SplatRec* __restrict__ recs,
                                      const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
                                      float4* __restrict__ out_ct, const uint32_t* __restrict__ ovf_list,
-                                     uint32_t n_ovf, uint32_t* __restrict__ dbg_ids, uint32_t* __restrict__ dbg_cnt,
+                                     const uint32_t* __restrict__ n_ovf_dev, uint32_t* __restrict__ dbg_ids, uint32_t* __restrict__ dbg_cnt,
                                      int dbg_cap, double* __restrict__ out_cd) {
-    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= n_ovf) return;
+    // grid-stride over the device-side overflow count (no host round trip)
+    const uint32_t n_ovf = *n_ovf_dev;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_ovf; w += gridDim.x * blockDim.x) {
     const uint32_t pix = ovf_list[w];
     const int px = pix % vp.width, py = pix / vp.width;
     const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
@@ -376,6 +377,7 @@ __global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
         out_cd[3 * (size_t)pix + 2] = D2;
     }
     if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
+    }
 }
 
 }  // namespace
@@ -405,11 +407,11 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
 }
 
 void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
-                               float4* out_ct, const uint32_t* ovf_list, uint32_t n_ovf, uint32_t* dbg_ids,
+                               float4* out_ct, const uint32_t* ovf_list, const uint32_t* n_ovf_dev, uint32_t* dbg_ids,
                                uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s) {
-    if (n_ovf == 0) return;
-    k_blend_fwd_fallback<<<(n_ovf + 63) / 64, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, out_ct,
-                                                          ovf_list, n_ovf, dbg_ids, dbg_cnt, dbg_cap, out_cd);
+    // fixed grid, device-side count: launched unconditionally (exits at once when nothing overflowed)
+    k_blend_fwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, out_ct, ovf_list,
+                                               n_ovf_dev, dbg_ids, dbg_cnt, dbg_cap, out_cd);
 }
 
 }  // namespace dgs_b200

@@ -113,7 +113,6 @@ struct ViewSlot {
     size_t temp_bytes = 0;
     ViewBins vb;
     ViewParams vp{};
-    uint32_t n_ovf = 0;
 };
 
 struct SubsetState {
@@ -197,8 +196,15 @@ struct Stage {
 };
 enum { kStPre = 0, kStBin, kStFwd, kStMerge, kStLoss, kStMergeBwd, kStBwd, kStProjBwd, kStAdam, kStExchange };
 
+/// Pinned host scalars read back once per forward (one stream sync).
+struct HostScalars {
+    int err;
+    uint32_t pairs;
+};
+
 struct Ctx {
     int device = 0, rank = 0, world = 1;
+    HostScalars* hs = nullptr;  // cudaHostAlloc'd
     StageTimer timer;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
@@ -359,24 +365,25 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         launch_preprocess((int)n, S.P.p, S.ld, S.sh_coeffs, S.ids32.p, vp, ctx.ro, vb, ctx.stream);
     }
     ++ctx.launches;
+    // zero-quaternion flag: rides along with the binning's pair-count readback
+    CK(cudaMemcpyAsync(&ctx.hs->err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
     Stage st_bin(ctx.timer, kStBin, ctx.stream);
     int64_t P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p,
                             vs.sort_vals.p, vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p,
-                            ctx.stream);
+                            &ctx.hs->pairs, ctx.stream);
     ctx.launches += 3;
     if (P < 0) {
         vs.pair_cap = (-P) + (-P) / 4 + 1024;
         alloc_pairs();
         P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
-                        vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, ctx.stream);
+                        vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, &ctx.hs->pairs,
+                        ctx.stream);
         ctx.launches += 3;
         if (P < 0) throw std::runtime_error("binning: pair buffer sizing failed");
     }
     st_bin.end();
-    int err = INT_MAX;
-    CK(cudaMemcpyAsync(&err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
-    CK(cudaStreamSynchronize(ctx.stream));
-    if (err != INT_MAX) throw std::domain_error("zero quaternion");
+    if (n <= 0) CK(cudaStreamSynchronize(ctx.stream));  // run_binning synced otherwise
+    if (ctx.hs->err != INT_MAX) throw std::domain_error("zero quaternion");
     if (ctx.records) {
         vs.rec_pos.ensure((size_t)tiles * kRecCap * kBlendThreads);
         vs.rec_cnt.ensure(px);
@@ -389,12 +396,10 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
                      dbg_ids, dbg_cnt, dbg_cap, stats, vs.cd.p, crec, ctx.stream);
     st_fwd.end();
     ++ctx.launches;
-    CK(cudaMemcpyAsync(&vs.n_ovf, vs.ovf_count.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
-    CK(cudaStreamSynchronize(ctx.stream));
-    if (vs.n_ovf > 0) {
+    {
         Stage st(ctx.timer, kStFwd, ctx.stream);
-        launch_blend_fwd_fallback(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_list.p, vs.n_ovf, dbg_ids,
-                                  dbg_cnt, dbg_cap, vs.cd.p, ctx.stream);
+        launch_blend_fwd_fallback(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_list.p, vs.ovf_count.p,
+                                  dbg_ids, dbg_cnt, dbg_cap, vs.cd.p, ctx.stream);
         ++ctx.launches;
     }
 }
@@ -411,11 +416,9 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, crec,
                      S.g2d.p, S.ld, stats, ctx.stream);
     ++ctx.launches;
-    if (vs.n_ovf > 0) {
-        launch_blend_bwd_fallback(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p,
-                                  vs.ovf_list.p, vs.n_ovf, S.g2d.p, S.ld, ctx.stream);
-        ++ctx.launches;
-    }
+    launch_blend_bwd_fallback(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p,
+                              vs.ovf_list.p, vs.ovf_count.p, S.g2d.p, S.ld, ctx.stream);
+    ++ctx.launches;
 }
 
 AdamParams adam_params(const Ctx& ctx, const SubsetState& S, uint64_t step_after) {
@@ -596,6 +599,7 @@ int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl
         c->rank = rank;
         c->world = world;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hs), sizeof(HostScalars), cudaHostAllocDefault));
         if (world > 1) {
             if (nccl_id == nullptr) throw std::invalid_argument("dgs_ctx_create: world > 1 needs an nccl id");
             ncclUniqueId id;
@@ -618,6 +622,7 @@ int dgs_ctx_destroy(dgs_ctx* ctx) {
         if (ctx->comm) nccl().CommDestroy(ctx->comm);
         ctx->subsets.clear();
         cudaStreamDestroy(ctx->stream);
+        if (ctx->hs) cudaFreeHost(ctx->hs);
         delete ctx;
     });
 }

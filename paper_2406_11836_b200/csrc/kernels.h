@@ -38,7 +38,7 @@ size_t binning_temp_bytes(int n, int64_t pair_cap);
 // pair buffer capacity; returns -needed if it is too small.
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
                     uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
-                    uint32_t* pair_val_alt, uint32_t* scan_buf, cudaStream_t s);
+                    uint32_t* pair_val_alt, uint32_t* scan_buf, uint32_t* pairs_host, cudaStream_t s);
 
 struct BlendStats {
     unsigned long long evals;      // (pixel, candidate) 2D evaluations
@@ -69,7 +69,7 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
                       uint32_t* dbg_ids, uint32_t* dbg_cnt, int dbg_cap, BlendStats* stats, double* out_cd,
                       const CompRecords& rec, cudaStream_t s);
 void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
-                               float4* out_ct, const uint32_t* ovf_list, uint32_t n_ovf, uint32_t* dbg_ids,
+                               float4* out_ct, const uint32_t* ovf_list, const uint32_t* n_ovf_dev, uint32_t* dbg_ids,
                                uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s);
 
 // K8: backward blend; accumulates 9 pixel-space adjoints per member into g2d (SoA [9][ld2]).
@@ -81,7 +81,8 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
                       const CompRecords& rec, float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s);
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
                                const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
-                               const uint32_t* ovf_list, uint32_t n_ovf, float* g2d, size_t ld2, cudaStream_t s);
+                               const uint32_t* ovf_list, const uint32_t* n_ovf_dev, float* g2d, size_t ld2,
+                               cudaStream_t s);
 
 // Row windows: an array "with base b and rows r" holds image rows [b, b + r)
 // (planar arrays: plane = r * W).  partials[k] / grad_out[k] hold float4
