@@ -167,6 +167,181 @@ constexpr int kIn = kOT + 4 * kR;   // 52: input tile with 10-pixel halo
 constexpr int kMid = kOT + 2 * kR;  // 42: first-stage maps with 5-pixel halo
 constexpr size_t kLossSmem = (2 * kIn * kIn + 5 * kIn * kMid + 5 * kMid * kMid) * sizeof(float);
 
+// Register-blocked stages: every thread produces a run of consecutive outputs
+// along the blur direction, loading the run's 11 + R - 1 inputs from shared
+// memory once.  Each output is still accumulated tap by tap (k = 0..10) with
+// unfused _rn multiply-adds, i.e. the reference's gauss_blur op sequence, so
+// the gradient is bit-identical.  Tiles whose 10-pixel halo lies inside the
+// image (BORDER = false, ~90% at 1080p) skip every per-tap padding test.
+constexpr int kR1 = 6;   // stage 1 run (42 = 7 x 6)
+constexpr int kR2 = 7;   // stage 2 run (42 = 6 x 7)
+constexpr int kR3 = 8;   // stage 3 run (32 = 4 x 8)
+constexpr int kR4 = 4;   // stage 4 run (32 = 8 x 4)
+
+template <bool BORDER>
+__device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int in_base, int in_rows,
+                                          const float* __restrict__ xp, const float* __restrict__ yp, float lam,
+                                          float c1, float c2, float nf, float inv_batch, const float* kern,
+                                          float* __restrict__ gp, float* X, float* Y, float* Hb, float* Vb, int ox,
+                                          int oy, double& s_l1, double& s_ssim, double& s_mse) {
+    const int tid = threadIdx.x;
+    // stage 0: inputs with zero padding outside the image / provided window
+    for (int i = tid; i < kIn * kIn; i += 256) {
+        const int r = i / kIn, c = i % kIn;
+        const int gy = oy - 2 * kR + r, gx = ox - 2 * kR + c;
+        const bool in = !BORDER || (gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= in_base && gy < in_base + in_rows);
+        X[i] = in ? xp[(size_t)(gy - in_base) * W + gx] : 0.0f;
+        Y[i] = in ? yp[(size_t)(gy - in_base) * W + gx] : 0.0f;
+    }
+    __syncthreads();
+    // stage 1: horizontal blur of x, y, x*x, y*y, x*y (rows -10..+41, cols -5..+36)
+    for (int it = tid; it < kIn * (kMid / kR1); it += 256) {
+        const int r = it / (kMid / kR1), c0 = (it % (kMid / kR1)) * kR1;
+        float xv[kR1 + 10], yv[kR1 + 10];
+#pragma unroll
+        for (int i = 0; i < kR1 + 10; ++i) {
+            xv[i] = X[r * kIn + c0 + i];
+            yv[i] = Y[r * kIn + c0 + i];
+        }
+        const int gxb = ox - 2 * kR + c0;  // image column of input i = gxb + i
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            float in[kR1 + 10];
+#pragma unroll
+            for (int i = 0; i < kR1 + 10; ++i)
+                in[i] = q == 0 ? xv[i] : q == 1 ? yv[i] : q == 2 ? fmul(xv[i], xv[i]) : q == 3 ? fmul(yv[i], yv[i])
+                                                                                           : fmul(xv[i], yv[i]);
+#pragma unroll
+            for (int j = 0; j < kR1; ++j) {
+                float a = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) {
+                    if (BORDER && (gxb + j + k < 0 || gxb + j + k >= W)) continue;  // loss.hpp:44 padding
+                    a = fadd(a, fmul(kern[k], in[j + k]));
+                }
+                Hb[q * kIn * kMid + r * kMid + c0 + j] = a;
+            }
+        }
+    }
+    __syncthreads();
+    // stage 2: vertical blur -> mu_x, mu_y, E[xx], E[yy], E[xy] at tile +-5;
+    // then the per-pixel SSIM partials A, B, B mu_x, C, C mu_y (zero outside the image).
+    for (int it = tid; it < kMid * (kMid / kR2); it += 256) {
+        const int c = it % kMid, r0 = (it / kMid) * kR2;
+        const int gx = ox - kR + c;
+        const int gyb = oy - 2 * kR + r0;  // image row of input i = gyb + i
+        float m[5][kR2];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            float col[kR2 + 10];
+#pragma unroll
+            for (int i = 0; i < kR2 + 10; ++i) col[i] = Hb[q * kIn * kMid + (r0 + i) * kMid + c];
+#pragma unroll
+            for (int j = 0; j < kR2; ++j) {
+                float a = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) {
+                    if (BORDER && (gyb + j + k < 0 || gyb + j + k >= H)) continue;
+                    a = fadd(a, fmul(kern[k], col[j + k]));
+                }
+                m[q][j] = a;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kR2; ++j) {
+            const int r = r0 + j, gy = oy - kR + r;
+            const bool in = !BORDER || (gy >= 0 && gy < H && gx >= 0 && gx < W);
+            float A = 0.0f, B = 0.0f, Cc = 0.0f, Bm = 0.0f, Cm = 0.0f;
+            if (in) {
+                const float mx = m[0][j], my = m[1][j];
+                const float sxx = fsub(m[2][j], fmul(mx, mx));
+                const float syy = fsub(m[3][j], fmul(my, my));
+                const float sxy = fsub(m[4][j], fmul(mx, my));
+                const float n1 = fadd(fmul(fmul(2.0f, mx), my), c1), n2 = fadd(fmul(2.0f, sxy), c2);
+                const float d1 = fadd(fadd(fmul(mx, mx), fmul(my, my)), c1), d2 = fadd(fadd(sxx, syy), c2);
+                const float dd = fmul(d1, d2);
+                const float sv = fdiv(fmul(n1, n2), dd);
+                A = fsub(fdiv(fmul(fmul(2.0f, my), n2), dd), fdiv(fmul(fmul(2.0f, mx), sv), d1));
+                B = fdiv(-sv, d2);
+                Cc = fdiv(fmul(2.0f, n1), dd);
+                Bm = fmul(B, mx);
+                Cm = fmul(Cc, my);
+                const bool own = r >= kR && r < kR + kOT && c >= kR && c < kR + kOT && gy < row1;
+                if (own) s_ssim += (double)sv;
+            }
+            const int i = r * kMid + c;
+            Vb[0 * kMid * kMid + i] = A;
+            Vb[1 * kMid * kMid + i] = B;
+            Vb[2 * kMid * kMid + i] = Bm;
+            Vb[3 * kMid * kMid + i] = Cc;
+            Vb[4 * kMid * kMid + i] = Cm;
+        }
+    }
+    __syncthreads();
+    // stage 3: horizontal blur of the five maps (rows -5..+36, cols 0..31)
+    float* H2 = Hb;  // [5][kMid][kOT]
+    for (int it = tid; it < 5 * (kOT / kR3) * kMid; it += 256) {
+        const int r = it % kMid, qc = it / kMid;
+        const int q = qc / (kOT / kR3), c0 = (qc % (kOT / kR3)) * kR3;
+        const int gxb = ox - kR + c0;
+        float row[kR3 + 10];
+#pragma unroll
+        for (int i = 0; i < kR3 + 10; ++i) row[i] = Vb[q * kMid * kMid + r * kMid + c0 + i];
+#pragma unroll
+        for (int j = 0; j < kR3; ++j) {
+            float a = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                if (BORDER && (gxb + j + k < 0 || gxb + j + k >= W)) continue;
+                a = fadd(a, fmul(kern[k], row[j + k]));
+            }
+            H2[q * kMid * kOT + r * kOT + c0 + j] = a;
+        }
+    }
+    __syncthreads();
+    // stage 4: vertical blur -> gradient (loss.hpp:138-140, 160-175)
+    for (int it = tid; it < kOT * (kOT / kR4); it += 256) {
+        const int c = it % kOT, r0 = (it / kOT) * kR4;
+        const int gx = ox + c;
+        const int gyb = oy + r0 - kR;
+        float cv[5][kR4];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            float col[kR4 + 10];
+#pragma unroll
+            for (int i = 0; i < kR4 + 10; ++i) col[i] = H2[q * kMid * kOT + (r0 + i) * kOT + c];
+#pragma unroll
+            for (int j = 0; j < kR4; ++j) {
+                float a = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) {
+                    if (BORDER && (gyb + j + k < 0 || gyb + j + k >= H)) continue;
+                    a = fadd(a, fmul(kern[k], col[j + k]));
+                }
+                cv[q][j] = a;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kR4; ++j) {
+            const int r = r0 + j, gy = oy + r;
+            if (gy >= row1 || gy >= H || gx >= W) continue;
+            const float xv = X[(r + 2 * kR) * kIn + c + 2 * kR], yv = Y[(r + 2 * kR) * kIn + c + 2 * kR];
+            // dS/dx = (conv(A) + 2x conv(B) - 2 conv(B mu_x) + y conv(C) - conv(C mu_y)) / n
+            const float sg = fdiv(fsub(fadd(fsub(fadd(cv[0][j], fmul(fmul(2.0f, xv), cv[1][j])), fmul(2.0f, cv[2][j])),
+                                            fmul(yv, cv[3][j])),
+                                       cv[4][j]),
+                                  nf);
+            const float d = fsub(xv, yv);
+            const float sgn = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
+            const float gl1 = fdiv(fmul(fsub(1.0f, lam), sgn), nf);
+            const float g = fsub(gl1, fmul(lam, sg));
+            gp[(size_t)(gy - in_base) * W + gx] = fmul(g, inv_batch);
+            s_l1 += (double)fabsf(d);
+            s_mse += (double)fmul(d, d);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, int in_base, int in_rows,
                                               const float* __restrict__ xs, const float* __restrict__ ys, float lam,
                                               float c1, float c2, float nf, float inv_batch,
@@ -186,140 +361,17 @@ __global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, 
     const int ox = blockIdx.x * kOT, oy = row0 + blockIdx.y * kOT;
     const int ch = blockIdx.z;
     const size_t plane = (size_t)W * in_rows;
-    const float* xp = xs + ch * plane;
-    const float* yp = ys + ch * plane;
-    // stage 0: inputs with zero padding outside the image (rows outside the
-    // provided window only feed outputs beyond [row0, row1), which are dropped)
-    for (int i = tid; i < kIn * kIn; i += 256) {
-        const int r = i / kIn, c = i % kIn;
-        const int gy = oy - 2 * kR + r, gx = ox - 2 * kR + c;
-        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= in_base && gy < in_base + in_rows;
-        X[i] = in ? xp[(size_t)(gy - in_base) * W + gx] : 0.0f;
-        Y[i] = in ? yp[(size_t)(gy - in_base) * W + gx] : 0.0f;
-    }
-    __syncthreads();
-    // stage 1: horizontal blur of x, y, x*x, y*y, x*y  (rows -10..+41, cols -5..+36)
-    for (int i = tid; i < kIn * kMid; i += 256) {
-        const int r = i / kMid, c = i % kMid;
-        float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f, a4 = 0.0f;
-        const float* xr = X + r * kIn + c;
-        const float* yr = Y + r * kIn + c;
-        const int gx0 = ox - kR + c - kR;
-#pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const int gx = gx0 + k;
-            if (gx < 0 || gx >= W) continue;  // zero padding = skipped term (loss.hpp:44)
-            const float xv = xr[k], yv = yr[k], w = kern[k];
-            a0 = fadd(a0, fmul(w, xv));
-            a1 = fadd(a1, fmul(w, yv));
-            a2 = fadd(a2, fmul(w, fmul(xv, xv)));
-            a3 = fadd(a3, fmul(w, fmul(yv, yv)));
-            a4 = fadd(a4, fmul(w, fmul(xv, yv)));
-        }
-        Hb[0 * kIn * kMid + i] = a0;
-        Hb[1 * kIn * kMid + i] = a1;
-        Hb[2 * kIn * kMid + i] = a2;
-        Hb[3 * kIn * kMid + i] = a3;
-        Hb[4 * kIn * kMid + i] = a4;
-    }
-    __syncthreads();
-    // stage 2: vertical blur -> mu_x, mu_y, E[xx], E[yy], E[xy] at tile +-5;
-    // then the per-pixel SSIM partials A, B, C, B*mu_x, C*mu_y (zero outside the image).
-    double s_ssim = 0.0;
-    for (int i = tid; i < kMid * kMid; i += 256) {
-        const int r = i / kMid, c = i % kMid;
-        const int gy = oy - kR + r, gx = ox - kR + c;
-        float m[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            float a = 0.0f;
-            const float* col = Hb + q * kIn * kMid + r * kMid + c;
-#pragma unroll
-            for (int k = 0; k < 11; ++k) {
-                const int yy = gy - kR + k;
-                if (yy < 0 || yy >= H) continue;
-                a = fadd(a, fmul(kern[k], col[k * kMid]));
-            }
-            m[q] = a;
-        }
-        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-        float A = 0.0f, B = 0.0f, C = 0.0f, Bm = 0.0f, Cm = 0.0f;
-        if (in) {
-            const float mx = m[0], my = m[1];
-            const float sxx = fsub(m[2], fmul(mx, mx));
-            const float syy = fsub(m[3], fmul(my, my));
-            const float sxy = fsub(m[4], fmul(mx, my));
-            const float n1 = fadd(fmul(fmul(2.0f, mx), my), c1), n2 = fadd(fmul(2.0f, sxy), c2);
-            const float d1 = fadd(fadd(fmul(mx, mx), fmul(my, my)), c1), d2 = fadd(fadd(sxx, syy), c2);
-            const float dd = fmul(d1, d2);
-            const float s = fdiv(fmul(n1, n2), dd);
-            A = fsub(fdiv(fmul(fmul(2.0f, my), n2), dd), fdiv(fmul(fmul(2.0f, mx), s), d1));
-            B = fdiv(-s, d2);
-            C = fdiv(fmul(2.0f, n1), dd);
-            Bm = fmul(B, mx);
-            Cm = fmul(C, my);
-            const bool own = r >= kR && r < kR + kOT && c >= kR && c < kR + kOT && gy < row1;
-            if (own) s_ssim += (double)s;
-        }
-        Vb[0 * kMid * kMid + i] = A;
-        Vb[1 * kMid * kMid + i] = B;
-        Vb[2 * kMid * kMid + i] = Bm;
-        Vb[3 * kMid * kMid + i] = C;
-        Vb[4 * kMid * kMid + i] = Cm;
-    }
-    __syncthreads();
-    // stage 3: horizontal blur of the five maps (rows -5..+36, cols 0..31)
-    float* H2 = Hb;  // [5][kMid][kOT]
-    for (int i = tid; i < kMid * kOT; i += 256) {
-        const int r = i / kOT, c = i % kOT;
-        const int gx0 = ox + c - kR;
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            float a = 0.0f;
-            const float* row = Vb + q * kMid * kMid + r * kMid + c;
-#pragma unroll
-            for (int k = 0; k < 11; ++k) {
-                const int gx = gx0 + k;
-                if (gx < 0 || gx >= W) continue;
-                a = fadd(a, fmul(kern[k], row[k]));
-            }
-            H2[q * kMid * kOT + i] = a;
-        }
-    }
-    __syncthreads();
-    // stage 4: vertical blur -> gradient (loss.hpp:138-140, 160-175)
-    double s_l1 = 0.0, s_mse = 0.0;
-    for (int i = tid; i < kOT * kOT; i += 256) {
-        const int r = i / kOT, c = i % kOT;
-        const int gy = oy + r, gx = ox + c;
-        if (gy >= row1 || gy >= H || gx >= W) continue;
-        float cv[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            float a = 0.0f;
-            const float* col = H2 + q * kMid * kOT + r * kOT + c;
-#pragma unroll
-            for (int k = 0; k < 11; ++k) {
-                const int yy = gy - kR + k;
-                if (yy < 0 || yy >= H) continue;
-                a = fadd(a, fmul(kern[k], col[k * kOT]));
-            }
-            cv[q] = a;
-        }
-        const float xv = X[(r + 2 * kR) * kIn + c + 2 * kR], yv = Y[(r + 2 * kR) * kIn + c + 2 * kR];
-        // dS/dx = (conv(A) + 2x conv(B) - 2 conv(B mu_x) + y conv(C) - conv(C mu_y)) / n
-        const float sg = fdiv(fsub(fadd(fsub(fadd(cv[0], fmul(fmul(2.0f, xv), cv[1])), fmul(2.0f, cv[2])),
-                                        fmul(yv, cv[3])),
-                                   cv[4]),
-                              nf);
-        const float d = fsub(xv, yv);
-        const float sgn = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
-        const float gl1 = fdiv(fmul(fsub(1.0f, lam), sgn), nf);
-        const float g = fsub(gl1, fmul(lam, sg));
-        grad[ch * plane + (size_t)(gy - in_base) * W + gx] = fmul(g, inv_batch);
-        s_l1 += (double)fabsf(d);
-        s_mse += (double)fmul(d, d);
-    }
+    // interior: the 10-pixel halo is inside the image and inside the provided window
+    const bool interior = ox - 2 * kR >= 0 && ox + kOT + 2 * kR <= W && oy - 2 * kR >= 0 &&
+                          oy + kOT + 2 * kR <= H && oy - 2 * kR >= in_base && oy + kOT + 2 * kR <= in_base + in_rows;
+    double s_l1 = 0.0, s_ssim = 0.0, s_mse = 0.0;
+    __syncthreads();  // kern
+    if (interior)
+        loss_tile<false>(W, H, row0, row1, in_base, in_rows, xs + ch * plane, ys + ch * plane, lam, c1, c2, nf,
+                         inv_batch, kern, grad + ch * plane, X, Y, Hb, Vb, ox, oy, s_l1, s_ssim, s_mse);
+    else
+        loss_tile<true>(W, H, row0, row1, in_base, in_rows, xs + ch * plane, ys + ch * plane, lam, c1, c2, nf,
+                        inv_batch, kern, grad + ch * plane, X, Y, Hb, Vb, ox, oy, s_l1, s_ssim, s_mse);
     // block sums (deterministic)
     double v[3] = {s_l1, s_ssim, s_mse};
     for (int q = 0; q < 3; ++q) {
