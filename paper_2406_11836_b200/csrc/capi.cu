@@ -216,6 +216,9 @@ struct Ctx {
     RenderOpts ro{};
     std::map<int, std::unique_ptr<SubsetState>> subsets;
     DevBuf<float> merged, grad_rgb, targets, staging, kern;
+    DevBuf<float> tgt_stage;                  // host targets prefetched on copy_stream (HWC windows, all views)
+    cudaStream_t copy_stream = nullptr;       // H2D of host targets, overlapped with the forward
+    cudaEvent_t copy_done = nullptr;
     DevBuf<double> block_sums, sums;
     DevBuf<const float4*> partial_ptrs;
     DevBuf<float4*> grad_ptrs;
@@ -600,6 +603,8 @@ int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl
         c->world = world;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hs), sizeof(HostScalars), cudaHostAllocDefault));
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming));
         if (world > 1) {
             if (nccl_id == nullptr) throw std::invalid_argument("dgs_ctx_create: world > 1 needs an nccl id");
             ncclUniqueId id;
@@ -623,6 +628,8 @@ int dgs_ctx_destroy(dgs_ctx* ctx) {
         ctx->subsets.clear();
         cudaStreamDestroy(ctx->stream);
         if (ctx->hs) cudaFreeHost(ctx->hs);
+        if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+        if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
         delete ctx;
     });
 }
@@ -1102,9 +1109,35 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         ctx->sums.ensure((size_t)3 * batch * S);
         for (int v = 0; v < batch; ++v) {
             vps[v] = view_params(cams[v]);
-            const ViewParams& vp = vps[v];
-            if (v > 0 && (vp.width != vps[0].width || vp.height != vps[0].height))
+            if (v > 0 && (vps[v].width != vps[0].width || vps[v].height != vps[0].height))
                 throw std::invalid_argument("train_step: all views of a batch must share a resolution");
+        }
+        // Host targets: the H2D copy of every view's target window runs on the
+        // copy stream while the forward renders (the main stream waits for it
+        // only at the first loss); pinned host memory makes it asynchronous.
+        const int my_slice = W > 1 ? rank : -1;
+        size_t tgt_win = 0;
+        if (!targets_on_device) {
+            const int Wd0 = vps[0].width, H0 = vps[0].height;
+            int h0 = 0, h1 = H0;
+            if (my_slice >= 0) {
+                const SliceRows R = slice_rows(H0, S, my_slice);
+                h0 = R.h0;
+                h1 = R.h1;
+            }
+            tgt_win = (size_t)(h1 - h0) * Wd0 * 3;
+            ctx->tgt_stage.ensure(tgt_win * batch);
+            CK(cudaEventRecord(ctx->copy_done, ctx->stream));  // staging reuse: previous step's readers are done
+            CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_done, 0));
+            for (int v = 0; v < batch; ++v)
+                CK(cudaMemcpyAsync(ctx->tgt_stage.p + (size_t)v * tgt_win,
+                                   targets + (size_t)v * 3 * Wd0 * H0 + (size_t)h0 * Wd0 * 3, tgt_win * 4,
+                                   cudaMemcpyHostToDevice, ctx->copy_stream));
+            CK(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+        }
+        bool waited_copy = false;
+        for (int v = 0; v < batch; ++v) {
+            const ViewParams& vp = vps[v];
             const int Wd = vp.width, H = vp.height;
             const size_t px = (size_t)Wd * H;
             // ---- render_batch (manager.hpp:262-304): per-subset partials ----
@@ -1168,11 +1201,16 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                                            (size_t)hr * Wd * 4, cudaMemcpyDeviceToDevice, ctx->stream));
                     tgt = ctx->targets_win.p;
                 } else {
-                    ctx->staging.ensure((size_t)3 * hr * Wd);
-                    CK(cudaMemcpyAsync(ctx->staging.p, targets + (size_t)v * 3 * px + (size_t)R.h0 * Wd * 3,
-                                       (size_t)hr * Wd * 12, cudaMemcpyHostToDevice, ctx->stream));
+                    if (!waited_copy) {
+                        CK(cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
+                        waited_copy = true;
+                    }
+                    // window rows [h0, h1) inside the prefetched window (which starts at
+                    // row 0 for a single rank, at this rank's halo start otherwise)
+                    const int base_row = my_slice >= 0 ? slice_rows(H, S, my_slice).h0 : 0;
+                    const float* src = ctx->tgt_stage.p + (size_t)v * tgt_win + (size_t)(R.h0 - base_row) * Wd * 3;
                     k_hwc_to_planar<<<(unsigned)(((size_t)hr * Wd + 255) / 256), 256, 0, ctx->stream>>>(
-                        ctx->staging.p, ctx->targets_win.p, (size_t)hr * Wd);
+                        src, ctx->targets_win.p, (size_t)hr * Wd);
                     ++ctx->launches;
                     tgt = ctx->targets_win.p;
                 }
