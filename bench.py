@@ -346,9 +346,39 @@ def b200_arm(a, world, rank, local_rank):
             cpu = {"value": None, "unit": "Mpixel/s", "cores": 0, "kind": "reference", "sample": err}
 
     last = dict(results[-1])
+    last_stats = results_stats[-1]
     for key in ("evals_fwd", "contribs_fwd", "evals_bwd", "contribs_bwd", "overflow_pixels", "subrounds_bwd",
-                "small_subrounds_bwd", "tiles_work_fwd", "replay_tiles_bwd"):
+                "small_subrounds_bwd", "tiles_work_fwd", "replay_tiles_bwd", "visible"):
         last[key] = results_stats[-1][key]
+    # ---- per-kernel roofline (algorithmic bytes / FLOPs per launch) ----
+    nv, npairs = last["visible"], last["pairs"]
+    ef, nc = last_stats["evals_fwd"], last_stats["contribs_fwd"]
+    fp32_peak = 148 * 128 * 2 * (clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # TFLOP/s, FMA = 2
+    algo = {
+        # params in; record 64 + rect 8 + count 4 + key 4 + ext_y 4 + SH Jacobian 40 out per visible member
+        "preprocess": ("hbm", n_all * rows * 4 + nv * 124 + (n_all - nv) * 8),
+        # 24-bit key + 3 radix passes over members, count scan, pair emission, 2 radix passes over pairs
+        "binning": ("hbm", 88 * n_all + 30 * npairs),
+        "blend_fwd": ("fp32", 50 * ef + 15 * nc),
+        "blend_bwd": ("fp32", 110 * nc),
+        "loss": ("fp32", 678 * 3 * px),
+        # 11 param rows + 10 Jacobian rows + 9 adjoint rows in per visible member, 17-float record out
+        "project_bwd": ("hbm", nv * 120 + n_all * 68),
+        "adam": ("hbm", alg_bytes["adam"]),
+    }
+    kernels = {}
+    for k, (bound, amount) in algo.items():
+        t = per_stage.get(k, 0.0)
+        if t <= 0:
+            continue
+        if bound == "hbm":
+            ach = amount / (t / 1e3) / 1e9
+            kernels[k] = {"bound": "hbm", "ms": round(t, 4), "algorithmic_bytes": int(amount),
+                          "achieved_gbs": round(ach, 1), "frac": round(ach / hbm_peak, 3)}
+        else:
+            ach = amount / (t / 1e3) / 1e12
+            kernels[k] = {"bound": "fp32-issue", "ms": round(t, 4), "algorithmic_flop": int(amount),
+                          "achieved_tflops": round(ach, 2), "frac_of_fp32_peak": round(ach / fp32_peak, 3)}
     line = {
         "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True,
@@ -366,6 +396,8 @@ def b200_arm(a, world, rank, local_rank):
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes[roof_kernel], "launch_ms": t_kernel_ms},
         "stages_ms_per_step": {k: round(v, 4) for k, v in per_stage.items()},
+        "kernels": kernels,
+        "fp32_peak_tflops_nominal": round(fp32_peak, 1),
         "dominant_stage": dom,
         "cpu_baseline": cpu,
         "clocks": clk,

@@ -113,6 +113,7 @@ typedef struct dgs_step_result {
     uint64_t kernel_launches; /* kernels this call launched */
     uint64_t subrounds_bwd, small_subrounds_bwd, tiles_work_fwd; /* blend work counters (stats mode) */
     uint64_t replay_tiles_bwd; /* tiles the backward replayed (records incomplete; stats mode) */
+    uint64_t visible;          /* projected (visible) members over all local subsets and views */
 } dgs_step_result;
 
 const char* dgs_last_error(void);

@@ -77,7 +77,7 @@ class StepResult(C.Structure):
                 ("evals_bwd", C.c_uint64), ("contribs_bwd", C.c_uint64), ("overflow_pixels", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("subrounds_bwd", C.c_uint64),
                 ("small_subrounds_bwd", C.c_uint64), ("tiles_work_fwd", C.c_uint64),
-                ("replay_tiles_bwd", C.c_uint64)]
+                ("replay_tiles_bwd", C.c_uint64), ("visible", C.c_uint64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

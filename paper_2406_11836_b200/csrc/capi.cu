@@ -200,6 +200,7 @@ enum { kStPre = 0, kStBin, kStFwd, kStMerge, kStLoss, kStMergeBwd, kStBwd, kStPr
 struct HostScalars {
     int err;
     uint32_t pairs;
+    uint32_t visible;
 };
 
 struct Ctx {
@@ -335,7 +336,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vb.counts = vs.counts.ensure(n);
     vb.rkey = vs.rkey.ensure(n);
     vb.ext_y = vs.ext_y.ensure(n);
-    vb.dmax_bits = vs.dmax.ensure(2);
+    vb.dmax_bits = vs.dmax.ensure(3);
     vb.err_index = vs.err.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);
     vs.sort_keys_alt.ensure(n);
@@ -358,7 +359,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         vs.temp_bytes = vs.temp.n;
     };
     alloc_pairs();
-    const uint32_t dmax0[2] = {0u, 0x7f7fffffu};  // (max D, min range)
+    const uint32_t dmax0[3] = {0u, 0x7f7fffffu, 0u};  // (max D, min range, visible count)
     CK(cudaMemcpyAsync(vb.dmax_bits, dmax0, sizeof(dmax0), cudaMemcpyHostToDevice, ctx.stream));
     const int int_max = INT_MAX;
     CK(cudaMemcpyAsync(vb.err_index, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));
@@ -370,6 +371,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     ++ctx.launches;
     // zero-quaternion flag: rides along with the binning's pair-count readback
     CK(cudaMemcpyAsync(&ctx.hs->err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaMemcpyAsync(&ctx.hs->visible, vb.dmax_bits + 2, 4, cudaMemcpyDeviceToHost, ctx.stream));
     Stage st_bin(ctx.timer, kStBin, ctx.stream);
     int64_t P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p,
                             vs.sort_vals.p, vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p,
@@ -387,6 +389,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     st_bin.end();
     if (n <= 0) CK(cudaStreamSynchronize(ctx.stream));  // run_binning synced otherwise
     if (ctx.hs->err != INT_MAX) throw std::domain_error("zero quaternion");
+    vb.visible = n > 0 ? ctx.hs->visible : 0;
     if (ctx.records) {
         vs.rec_pos.ensure((size_t)tiles * kRecCap * kBlendThreads);
         vs.rec_cnt.ensure(px);
@@ -1099,7 +1102,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         uint64_t nccl_bytes = 0;
         CK(cudaMemsetAsync(ctx->stats.p, 0, 2 * sizeof(BlendStats), ctx->stream));
         std::vector<ViewParams> vps(batch);
-        uint64_t pairs = 0;
+        uint64_t pairs = 0, visible = 0;
         const float lam = (float)ctx->cfg.lambda_ssim;
         const float inv_batch = 1.0f / (float)batch;  // manager.hpp:329
         const int S = W > 1 ? W : std::max(1, ctx->virtual_slices);
@@ -1145,6 +1148,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                 SubsetState& S_ = subset(*ctx, k);
                 forward_subset(*ctx, S_, v, vp, 0, nullptr, nullptr, ctx->collect_stats ? ctx->stats.p : nullptr);
                 pairs += (uint64_t)S_.slot(v).vb.pairs;
+                visible += (uint64_t)S_.slot(v).vb.visible;
                 S_.slot(v).grad_ct.ensure(px);
             }
             const int owner = table_locate(ctx->table, vp.o);
@@ -1335,6 +1339,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             out->small_subrounds_bwd = st[1].small_rounds;
             out->tiles_work_fwd = st[0].tiles_work;
             out->replay_tiles_bwd = st[1].tiles_work;
+            out->visible = visible;
             out->kernel_launches = ctx->launches - launches0;
         }
     });

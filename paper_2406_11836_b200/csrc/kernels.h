@@ -17,7 +17,8 @@ struct ViewBins {
     uint32_t* counts = nullptr;      // [n] tile count per member (0 = culled)
     uint32_t* rkey = nullptr;        // [n] range bits (0xffffffff = culled)
     float* ext_y = nullptr;          // [n] conservative row half-extent of the m^2 <= 9 region (warp culling)
-    uint32_t* dmax_bits = nullptr;   // [2] max world_radius over visible members, min range (float bits)
+    uint32_t* dmax_bits = nullptr;   // [3] max world_radius over visible members, min range (float bits),
+                                     //     visible member count
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
     float* shjac = nullptr;          // [10][ld] (optional): d colour_ch / d dir_a (row 3 ch + a) and the
                                      //     pre-clamp sign mask (row 9, bits) for the gradient record (K9)
@@ -25,6 +26,7 @@ struct ViewBins {
     uint32_t* pair_val = nullptr;    // [cap] member index
     uint2* ranges = nullptr;         // [tiles] (start, end) into the sorted pair list
     int64_t pairs = 0;
+    int64_t visible = 0;
 };
 
 // K1: projection + SH colour + tile rectangles (splat.hpp:288-321, raster.hpp:113-125).

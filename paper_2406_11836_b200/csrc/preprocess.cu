@@ -216,8 +216,9 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
         s_max[threadIdx.x >> 5] = m;
         s_min[threadIdx.x >> 5] = lo;
     }
-    __syncthreads();
+    const int nvis = __syncthreads_count(dmax_local > 0.0f);
     if (threadIdx.x == 0) {
+        if (nvis) atomicAdd(vb.dmax_bits + 2, (uint32_t)nvis);
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
             m = fmaxf(m, s_max[w]);
             lo = fminf(lo, s_min[w]);
