@@ -107,6 +107,33 @@ __global__ void k_tile_ranges(const uint16_t* __restrict__ tile, uint32_t P, int
     ranges[t] = make_uint2(lower_bound_u16(tile, P, (uint32_t)t), lower_bound_u16(tile, P, (uint32_t)t + 1));
 }
 
+/// Onesweep policy for the 24-bit member sort, measured on B200
+/// (scripts/sortbench.cu: 10M u32 keys + u32 values, 3 passes): 256 threads x
+/// 23 items 0.250 ms vs 0.313 ms for the library default dispatch.  The other
+/// policies of the chain are the library's sm_100 ones (unused by onesweep).
+struct MemberSortHub {
+    using Base = cub::detail::radix::policy_hub<uint32_t, uint32_t, int>::Policy1000;
+    struct Policy : cub::ChainedPolicy<1000, Policy, Policy> {
+        static constexpr bool ONESWEEP = true;
+        static constexpr int ONESWEEP_RADIX_BITS = 8;
+        using HistogramPolicy = Base::HistogramPolicy;
+        using ExclusiveSumPolicy = Base::ExclusiveSumPolicy;
+        using OnesweepPolicy =
+            cub::AgentRadixSortOnesweepPolicy<256, 23, uint32_t, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
+                                              cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+        using ScanPolicy = Base::ScanPolicy;
+        using DownsweepPolicy = Base::DownsweepPolicy;
+        using AltDownsweepPolicy = Base::AltDownsweepPolicy;
+        using UpsweepPolicy = Base::UpsweepPolicy;
+        using AltUpsweepPolicy = Base::AltUpsweepPolicy;
+        using SingleTilePolicy = Base::SingleTilePolicy;
+        using SegmentedPolicy = Base::SegmentedPolicy;
+        using AltSegmentedPolicy = Base::AltSegmentedPolicy;
+    };
+    using MaxPolicy = Policy;
+};
+using MemberSort = cub::DispatchRadixSort<false, uint32_t, uint32_t, int, MemberSortHub>;
+
 struct CountOf {
     const uint32_t* counts;
     __host__ __device__ uint32_t operator()(uint32_t i) const { return counts[i]; }
@@ -122,8 +149,10 @@ int bits_for(uint32_t v) {
 
 size_t binning_temp_bytes(int n, int64_t pair_cap) {
     size_t a = 0, b = 0, c = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, n);
+    {
+        cub::DoubleBuffer<uint32_t> k, v;
+        MemberSort::Dispatch(nullptr, a, k, v, n, 0, 24, true, 0);
+    }
     cub::DoubleBuffer<uint16_t> dk;
     cub::DoubleBuffer<uint32_t> dv;
     cub::DeviceRadixSort::SortPairs(nullptr, b, dk, dv, (int)pair_cap, 0, 16);
@@ -145,7 +174,12 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     //    passes; culled members and any beyond the window share the top key)
     k_key24<<<grid, blk, 0, s>>>(vb.rkey, vb.dmax_bits, scan_buf, sort_vals, n);
     size_t tb = temp_bytes;
-    cub::DeviceRadixSort::SortPairs(temp, tb, scan_buf, sort_keys_alt, sort_vals, sort_vals_alt, n, 0, 24, s);
+    {
+        cub::DoubleBuffer<uint32_t> k(scan_buf, sort_keys_alt), v(sort_vals, sort_vals_alt);
+        MemberSort::Dispatch(temp, tb, k, v, n, 0, 24, true, s);
+        if (v.Current() != sort_vals_alt)  // 3 passes land in the alternate buffers; keep the contract anyway
+            cudaMemcpyAsync(sort_vals_alt, v.Current(), 4 * (size_t)n, cudaMemcpyDeviceToDevice, s);
+    }
     // 2) tile counts in range order -> inclusive scan -> pair end offsets
     //    (the gather is fused into the scan through a transform iterator)
     cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> cnt_it(sort_vals_alt, CountOf{vb.counts});

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
                                                              const uint2* __restrict__ ranges,
-                                                             const float* __restrict__ ext_y,
+                                                             const float2* __restrict__ ext,
                                                              const uint32_t* __restrict__ dmax_bits, float onorm,
                                                              const float4* __restrict__ fwd_ct,
                                                              const double* __restrict__ fwd_cd,
@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
     const int tid = threadIdx.x, lane = tid & 31;
     const int tile = blockIdx.x;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
-    const int px = tx * kTileSize + (tid & 15), py = ty * kTileSize + (tid >> 4);
+    int px, py;
+    tile_pixel(tid, tx, ty, px, py);
     const bool inside = px < vp.width && py < vp.height;
     const size_t pix = (size_t)py * vp.width + px;
     PixelRay pr;
@@ -319,17 +320,8 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
             sB[tid] = B;
             sC[tid] = C;
             sD[tid] = D;
-            // which warps (pixel row pairs of this tile) can see m^2 <= 9: a warp is
-            // skipped only if |dy| > ext_y on both of its rows (same float dy as eval)
-            const float ey = __ldg(ext_y + m);
-            uint32_t wm = 0;
-#pragma unroll
-            for (int w = 0; w < kBlendThreads / 32; ++w) {
-                const float y0 = fadd((float)(ty * kTileSize + 2 * w), 0.5f);
-                const float y1 = fadd((float)(ty * kTileSize + 2 * w + 1), 0.5f);
-                const float d0 = fabsf(fsub(y0, A.y)), d1 = fabsf(fsub(y1, A.y));
-                if (!(fminf(d0, d1) > ey)) wm |= 1u << w;
-            }
+            // which warps (8x4 pixel blocks of this tile) can see m^2 <= 9
+            const uint32_t wm = warp_block_mask(__ldg(ext + m), A.x, A.y, tx, ty);
             smask[tid] = (uint8_t)wm;
         }
         __syncthreads();
@@ -431,7 +423,8 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
     if (crec.tile_replay[tile]) return;  // handled by the replay kernel
     const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
-    const int px = tx * kTileSize + (tid & 15), py = ty * kTileSize + (tid >> 4);
+    int px, py;
+    tile_pixel(tid, tx, ty, px, py);
     const bool inside = px < vp.width && py < vp.height;
     const size_t pix = (size_t)py * vp.width + px;
     PixState ps;
@@ -632,11 +625,11 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
     // replay: flagged tiles only (every tile without records)
     if (stats)
         k_blend_bwd<true><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
-                                                                 vb.ext_y, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
+                                                                 vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
                                                                  ovf_flag, rec.tile_replay, g2d, ld2, stats);
     else
         k_blend_bwd<false><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
-                                                                  vb.ext_y, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
+                                                                  vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
                                                                   ovf_flag, rec.tile_replay, g2d, ld2, stats);
 }
 

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
                                                              const uint2* __restrict__ ranges,
-                                                             const float* __restrict__ ext_y,
+                                                             const float2* __restrict__ ext,
                                                              const uint32_t* __restrict__ dmax_bits, float onorm,
                                                              float4* __restrict__ out_ct, uint8_t* __restrict__ ovf_flag,
                                                              uint32_t* __restrict__ ovf_list,
@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     const int tid = threadIdx.x;
     const int tile = blockIdx.x;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
-    const int px = tx * kTileSize + (tid & 15), py = ty * kTileSize + (tid >> 4);
+    int px, py;
+    tile_pixel(tid, tx, ty, px, py);
     const bool inside = px < vp.width && py < vp.height;
     const size_t pix = (size_t)py * vp.width + px;
     PixelRay pr;
@@ -181,17 +182,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             sB[tid] = B;
             sC[tid] = C;
             sD[tid] = D;
-            // which warps (pixel row pairs of this tile) can see m^2 <= 9: a warp is
-            // skipped only if |dy| > ext_y on both of its rows (same float dy as eval)
-            const float ey = __ldg(ext_y + m);
-            uint32_t wm = 0;
-#pragma unroll
-            for (int w = 0; w < kBlendThreads / 32; ++w) {
-                const float y0 = fadd((float)(ty * kTileSize + 2 * w), 0.5f);
-                const float y1 = fadd((float)(ty * kTileSize + 2 * w + 1), 0.5f);
-                const float d0 = fabsf(fsub(y0, A.y)), d1 = fabsf(fsub(y1, A.y));
-                if (!(fminf(d0, d1) > ey)) wm |= 1u << w;
-            }
+            // which warps (8x4 pixel blocks of this tile) can see m^2 <= 9
+            const uint32_t wm = warp_block_mask(__ldg(ext + m), A.x, A.y, tx, ty);
             smask[tid] = (uint8_t)wm;
         }
         __syncthreads();
@@ -397,7 +389,7 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
         configured = true;
     }
 #define DGS_FWD(D, S)                                                                                              \
-    k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext_y, vb.dmax_bits, \
+    k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, vb.dmax_bits, \
                                                          onorm, out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids,       \
                                                          dbg_cnt, dbg_cap, stats, out_cd, rec)
     if (dbg_ids != nullptr && dbg_cnt != nullptr) DGS_FWD(true, true);

@@ -91,7 +91,7 @@ struct ViewSlot {
     DevBuf<SplatRec> recs;
     DevBuf<uint32_t> rect, counts, rkey, dmax, pair_val, pair_val_alt;
     DevBuf<uint16_t> pair_tile, pair_tile_alt;
-    DevBuf<float> ext_y;
+    DevBuf<float2> ext;
     DevBuf<uint32_t> sort_keys_alt, sort_vals, sort_vals_alt, scan, ovf_list, ovf_count;
     DevBuf<int> err;
     DevBuf<uint2> ranges;
@@ -335,7 +335,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vb.rect = vs.rect.ensure(2 * n);
     vb.counts = vs.counts.ensure(n);
     vb.rkey = vs.rkey.ensure(n);
-    vb.ext_y = vs.ext_y.ensure(n);
+    vb.ext = vs.ext.ensure(n);
     vb.dmax_bits = vs.dmax.ensure(3);
     vb.err_index = vs.err.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);

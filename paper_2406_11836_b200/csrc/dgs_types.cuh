@@ -122,6 +122,43 @@ DGS_HD int subspace_order(const Table& tb, int owner, const float o[3], const fl
     return cnt;
 }
 
+#if defined(__CUDACC__)
+/// Pixel <-> thread mapping inside a 16x16 tile (all blend kernels and the
+/// composite records): warp w covers the 8x4 pixel block (w & 1, w >> 1),
+/// lane l the pixel (l & 7, l >> 3) inside it.
+__device__ __forceinline__ void tile_pixel(int tid, int tx, int ty, int& px, int& py) {
+    const int w = tid >> 5, l = tid & 31;
+    px = tx * kTileSize + (w & 1) * 8 + (l & 7);
+    py = ty * kTileSize + (w >> 1) * 4 + (l >> 3);
+}
+
+/// 8-bit mask of the warps of tile (tx, ty) whose 8x4 block may contain a
+/// pixel with m^2 <= trunc^2 for a splat at (mx, my) with half-extents ext
+/// (K1's conservative bound on the float dx, dy of eval_2d).  A block is
+/// skipped only if the float dx (dy) of its nearest pixel column (row) already
+/// exceeds the extent: fsub is monotone, so every other column (row) does too.
+__device__ __forceinline__ uint32_t warp_block_mask(float2 ext, float mx, float my, int tx, int ty) {
+    uint32_t cm = 0, rm = 0;
+#pragma unroll
+    for (int bx = 0; bx < 2; ++bx) {
+        const float lo = fadd((float)(tx * kTileSize + bx * 8), 0.5f);
+        const float hi = fadd((float)(tx * kTileSize + bx * 8 + 7), 0.5f);
+        if (!(fsub(lo, mx) > ext.x || fsub(mx, hi) > ext.x)) cm |= 1u << bx;
+    }
+#pragma unroll
+    for (int by = 0; by < 4; ++by) {
+        const float lo = fadd((float)(ty * kTileSize + by * 4), 0.5f);
+        const float hi = fadd((float)(ty * kTileSize + by * 4 + 3), 0.5f);
+        if (!(fsub(lo, my) > ext.y || fsub(my, hi) > ext.y)) rm |= 1u << by;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int by = 0; by < 4; ++by)
+        if ((rm >> by) & 1u) m |= cm << (2 * by);
+    return m;
+}
+#endif
+
 /// partition.hpp:66-71 locate (first subspace containing x).
 DGS_HD int table_locate(const Table& tb, const float x[3]) {
     for (int k = 0; k < tb.k_count; ++k)

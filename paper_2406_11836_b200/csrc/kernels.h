@@ -16,7 +16,7 @@ struct ViewBins {
     uint32_t* rect = nullptr;        // [2n]: x0 | x1 << 16, y0 | y1 << 16
     uint32_t* counts = nullptr;      // [n] tile count per member (0 = culled)
     uint32_t* rkey = nullptr;        // [n] range bits (0xffffffff = culled)
-    float* ext_y = nullptr;          // [n] conservative row half-extent of the m^2 <= 9 region (warp culling)
+    float2* ext = nullptr;           // [n] conservative (x, y) half-extents of the m^2 <= 9 region (warp culling)
     uint32_t* dmax_bits = nullptr;   // [3] max world_radius over visible members, min range (float bits),
                                      //     visible member count
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)

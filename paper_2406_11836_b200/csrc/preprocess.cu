@@ -122,13 +122,15 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
                     const double a = rec.i00, b = rec.i01, c = rec.i10, d = rec.i11, g = 1e-6;
                     const double ap = a * (1.0 - g), dp = d * (1.0 - g);
                     const double h = 0.5 * (fabs(b + c) + g * (fabs(b) + fabs(c)));
-                    float ey = __int_as_float(0x7f800000);
+                    // (and symmetrically |dx| <= trunc * sqrt(d' / (a'd' - h^2)))
+                    float ex = __int_as_float(0x7f800000), ey = ex;
                     if (a > 0.0 && d > 0.0 && ap * dp > h * h * (1.0 + 1e-9)) {
                         const double t2 = (double)fmul(ro.trunc, ro.trunc);
-                        const double e = sqrt(t2 * ap / (ap * dp - h * h));
-                        ey = (float)(e * (1.0 + 1e-6) + 1e-5);
+                        const double den = ap * dp - h * h;
+                        ey = (float)(sqrt(t2 * ap / den) * (1.0 + 1e-6) + 1e-5);
+                        ex = (float)(sqrt(t2 * dp / den) * (1.0 + 1e-6) + 1e-5);
                     }
-                    vb.ext_y[i] = ey;
+                    vb.ext[i] = make_float2(ex, ey);
                 }
                 // tile rectangle (raster.hpp:117-121): C++ truncating int division, then clamp
                 const int x0 = clampi(x86_float_to_int(floorf(fsub(mx, rx))) / kTileSize, 0, vp.tiles_x - 1);

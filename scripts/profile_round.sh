@@ -1,13 +1,14 @@
 #!/bin/bash
-# One GPU call: bench line, kernel launch list, ncu --set full of the hot
-# kernels of one training step (after the target render).  Outputs -> $OUT.
+# One GPU call: bench line, kernel launch list of one training step, ncu --set full of the hot kernels.
+# Outputs -> $OUT (default gpurun_out/prof).  Summarise with scripts/summarize_profile.py.
 set -x
-OUT=${OUT:-gpurun_out/r1}
+OUT=${OUT:-gpurun_out/prof}
 mkdir -p $OUT
-timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; tail -c 4000 $OUT/bench.json
+timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; tail -c 3000 $OUT/bench.json
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+# every matching launch of the target render, the warm-up step and the timed step (summary keeps the last of each)
 timeout 1800 ncu --set full --import-source on --clock-control none \
-    -k "regex:k_(preprocess|blend_fwd|blend_bwd|grad_record|adam_stream4|loss|emit_pairs)|Onesweep" -s 8 -c 12 \
-    -o $OUT/full python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $OUT/ncu.log 2>&1
+    -k "regex:k_(preprocess|blend_fwd|blend_bwd_rec|grad_record|adam_stream4|loss|emit_pairs|merge)|Onesweep" \
+    -c 80 -o $OUT/full python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $OUT/ncu.log 2>&1
 ls -la $OUT
