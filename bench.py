@@ -367,6 +367,7 @@ def b200_arm(a, world, rank, local_rank):
         "adam": ("hbm", alg_bytes["adam"]),
     }
     kernels = {}
+    tj = json.loads(tf.read_text()) if tf.exists() else {}
     for k, (bound, amount) in algo.items():
         t = per_stage.get(k, 0.0)
         if t <= 0:
@@ -374,7 +375,8 @@ def b200_arm(a, world, rank, local_rank):
         if bound == "hbm":
             ach = amount / (t / 1e3) / 1e9
             kernels[k] = {"bound": "hbm", "ms": round(t, 4), "algorithmic_bytes": int(amount),
-                          "achieved_gbs": round(ach, 1), "frac": round(ach / hbm_peak, 3)}
+                          "achieved_gbs": round(ach, 1), "frac": round(ach / hbm_peak, 3),
+                          "traffic_ncu": tj.get(k)}
         else:
             ach = amount / (t / 1e3) / 1e12
             kernels[k] = {"bound": "fp32-issue", "ms": round(t, 4), "algorithmic_flop": int(amount),

@@ -73,7 +73,7 @@ stall = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_") an
 last = {}
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
-    short = name.split("(")[0].replace("void ", "").replace("unnamed>::", "").replace("dgs_b200::", "")
+    short = name.split("(")[0].replace("void ", "").replace("unnamed>::", "").replace("dgs_b200::", "").lstrip("<")
     if "Onesweep" in short:
         short = f"cub::Onesweep(grid {r[hdr.index('Grid Size')]})"
     last[short] = r
