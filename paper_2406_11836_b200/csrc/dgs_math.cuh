@@ -280,10 +280,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
+        "r"(phase), "r"(0x100000u)  // suspend-time hint (ns): sleep until the phase completes, do not spin
         : "memory");
 }
 /// global -> shared bulk copy completing on an mbarrier (UBLKCP).
