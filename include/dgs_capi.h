@@ -175,6 +175,18 @@ int dgs_dump_bins(dgs_ctx* ctx, int32_t k, int64_t* tile_off, int32_t* entries, 
 /* Projected records of the last render (n x 16 floats: SplatRec layout, culled rows zero) and tile counts. */
 int dgs_dump_records(dgs_ctx* ctx, int32_t k, float* recs, uint32_t* counts);
 
+/* Manager::repartition (manager.hpp:421-430 -> snapshot + distribute, :389-482)
+ * entirely on the device (world == 1, every subset resident): snapshot (one
+ * replica per id: the holder whose subspace contains the centre, else the
+ * lowest k), build_kdtree(depth) over the merged centres (bit-exact medians),
+ * assign_subsets(d_multiplier) and migration of parameters and Adam moments
+ * into 2^depth new subsets (epoch `epoch`, same Adam step).  expected_splats
+ * >= 0: the snapshot must hold exactly that many ids ("snapshot lost
+ * splats").  planes_out (optional): 2^depth * depth planes, as
+ * dgs_build_kdtree. */
+int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t expected_splats, uint64_t epoch,
+                    dgs_plane* planes_out);
+
 /* ---- Manager side (engine.hpp:108-234, loss.hpp:153-177) ------------------------ */
 int dgs_pixel_orders(dgs_ctx* ctx, const dgs_camera* cam, uint16_t* order, uint16_t* count);
 /* merge: partials[k] = H*W*4 (rgb, T) for every k of the table. out_rgb HWC, out_t HW. */

@@ -104,6 +104,7 @@ _SIGS = {
     "dgs_set_options": (C.c_int, [_P, C.POINTER(RenderOptionsC), C.POINTER(TrainConfigC)]),
     "dgs_subset_load": (C.c_int, [_P, C.c_int32, C.POINTER(SplatsC), C.POINTER(SplatsC), C.POINTER(SplatsC),
                                   C.c_uint64, C.c_uint64]),
+    "dgs_repartition": (C.c_int, [_P, C.c_int32, C.c_double, C.c_int64, C.c_uint64, C.POINTER(Plane)]),
     "dgs_subset_store": (C.c_int, [_P, C.c_int32, C.POINTER(SplatsC), C.POINTER(SplatsC), C.POINTER(SplatsC),
                                    C.POINTER(C.c_uint64)]),
     "dgs_subset_size": (C.c_int64, [_P, C.c_int32]),

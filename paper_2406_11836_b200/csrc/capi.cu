@@ -749,6 +749,270 @@ int dgs_subset_load(dgs_ctx* ctx, int32_t k, const dgs_splats* params, const dgs
     });
 }
 
+int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t expected_splats, uint64_t epoch,
+                    dgs_plane* planes_out) {
+    return dgs_guard([&] {
+        require_table(*ctx);
+        if (ctx->world != 1) throw std::invalid_argument("repartition: the device path is single-rank (world == 1)");
+        if (depth < 0 || depth > 5) throw std::invalid_argument("repartition: kd depth must be 0..5 (<= 32 subsets)");
+        const int K0 = ctx->table.k_count;
+        for (int k = 0; k < K0; ++k) subset(*ctx, k);  // every subset resident
+        CK(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const SubsetState& S0 = subset(*ctx, 0);
+        const int shc = S0.sh_coeffs, rows = S0.rows;
+        const uint64_t adam_step = S0.adam_step;
+        // ---- snapshot (manager.hpp:389-418): one replica per id ----
+        std::vector<uint32_t> offs(K0 + 1, 0);
+        for (int k = 0; k < K0; ++k) {
+            const SubsetState& S = subset(*ctx, k);
+            if (S.sh_coeffs != shc) throw std::invalid_argument("repartition: subsets disagree on the SH degree");
+            offs[k + 1] = offs[k] + (uint32_t)S.n;
+        }
+        const int R = (int)offs[K0];
+        if (R <= 0) throw std::invalid_argument("build_kdtree: empty point set");
+        DevBuf<uint64_t> keys, keys_alt;
+        DevBuf<uint32_t> vals, vals_alt, winners;
+        DevBuf<uint8_t> flags, temp;
+        DevBuf<int> count;
+        keys.ensure(R);
+        keys_alt.ensure(R);
+        vals.ensure(R);
+        vals_alt.ensure(R);
+        winners.ensure(R);
+        flags.ensure(R);
+        count.ensure(1);
+        const size_t tb = repart_temp_bytes(R);
+        temp.ensure(tb);
+        for (int k = 0; k < K0; ++k) {
+            const SubsetState& S = subset(*ctx, k);
+            repart_snapshot_keys((int)S.n, S.P.p, S.ld, S.ids32.p, ctx->table_dev.p, k, offs[k], keys.p, vals.p, s);
+        }
+        uint64_t* kp = keys.p;
+        uint64_t* kap = keys_alt.p;
+        uint32_t* vp = vals.p;
+        uint32_t* vap = vals_alt.p;
+        repart_sort_pairs(kp, kap, vp, vap, R, 40, temp.p, tb, s);
+        repart_first_of_run(R, kp, flags.p, s);
+        repart_select(R, vp, flags.p, winners.p, count.p, temp.p, tb, s);
+        int N = 0;
+        CK(cudaMemcpyAsync(&N, count.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (expected_splats >= 0 && (int64_t)N != expected_splats) throw std::runtime_error("snapshot lost splats");
+        // merged SoA state, id order
+        const size_t ldm = (size_t)(N + 31) / 32 * 32;
+        DevBuf<float> mP, mM, mV;
+        DevBuf<uint32_t> mIds;
+        mP.ensure(rows * ldm);
+        mM.ensure(rows * ldm);
+        mV.ensure(rows * ldm);
+        mIds.ensure(N);
+        {
+            std::vector<const float*> hp(K0), hm(K0), hv(K0);
+            std::vector<const uint32_t*> hi(K0);
+            std::vector<size_t> hl(K0);
+            for (int k = 0; k < K0; ++k) {
+                const SubsetState& S = subset(*ctx, k);
+                hp[k] = S.P.p;
+                hm[k] = S.M.p;
+                hv[k] = S.V.p;
+                hi[k] = S.ids32.p;
+                hl[k] = S.ld;
+            }
+            DevBuf<const float*> dp, dm, dv;
+            DevBuf<const uint32_t*> di;
+            DevBuf<size_t> dl;
+            DevBuf<uint32_t> doffs;
+            dp.ensure(K0);
+            dm.ensure(K0);
+            dv.ensure(K0);
+            di.ensure(K0);
+            dl.ensure(K0);
+            doffs.ensure(K0 + 1);
+            CK(cudaMemcpyAsync(dp.p, hp.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dm.p, hm.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dv.p, hv.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(di.p, hi.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dl.p, hl.data(), K0 * sizeof(size_t), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(doffs.p, offs.data(), (K0 + 1) * 4, cudaMemcpyHostToDevice, s));
+            repart_gather_replicas(N, rows, winners.p, doffs.p, K0, dp.p, dm.p, dv.p, di.p, dl.p, mP.p, mM.p, mV.p,
+                                   mIds.p, ldm, s);
+            CK(cudaStreamSynchronize(s));  // host arrays above go out of scope
+        }
+        // ---- build_kdtree (partition.hpp:93-184) on the merged centres ----
+        struct HostRegion {
+            std::vector<dgs_plane> planes;
+            float amin[3], amax[3];
+        };
+        std::vector<HostRegion> regions(1);
+        for (int a = 0; a < 3; ++a) {
+            regions[0].amin[a] = -INFINITY;
+            regions[0].amax[a] = INFINITY;
+        }
+        DevBuf<uint8_t> node;
+        node.ensure(N);
+        CK(cudaMemsetAsync(node.p, 0, N, s));
+        DevBuf<uint32_t> lo, hi, cnt;
+        DevBuf<int> d_axis;
+        DevBuf<float> d_plane;
+        const int maxn = 1 << depth;
+        lo.ensure(3 * maxn);
+        hi.ensure(3 * maxn);
+        cnt.ensure(maxn);
+        d_axis.ensure(maxn);
+        d_plane.ensure(maxn);
+        auto from_order = [](uint32_t o) {
+            const uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+            float f;
+            std::memcpy(&f, &b, 4);
+            return f;
+        };
+        for (int d = 0; d < depth; ++d) {
+            const int nn = 1 << d;
+            std::vector<uint32_t> h_lo(3 * nn, 0xffffffffu), h_hi(3 * nn, 0u), h_cnt(nn, 0u);
+            CK(cudaMemcpyAsync(lo.p, h_lo.data(), 12 * nn, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(hi.p, h_hi.data(), 12 * nn, cudaMemcpyHostToDevice, s));
+            CK(cudaMemsetAsync(cnt.p, 0, 4 * nn, s));
+            repart_node_extent(N, mP.p, ldm, node.p, nn, lo.p, hi.p, cnt.p, s);
+            CK(cudaMemcpyAsync(h_lo.data(), lo.p, 12 * nn, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(h_hi.data(), hi.p, 12 * nn, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(h_cnt.data(), cnt.p, 4 * nn, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (d == 0) {  // build_kdtree's degenerate-set check (partition.hpp:164-171)
+                float m = from_order(h_hi[0]) - from_order(h_lo[0]);
+                for (int a = 1; a < 3; ++a) m = std::max(m, from_order(h_hi[a]) - from_order(h_lo[a]));
+                if (m <= 0.0f) throw std::invalid_argument("degenerate point set");
+            }
+            std::vector<int> axis(nn, 0);
+            for (int q = 0; q < nn; ++q) {
+                if (!h_cnt[q]) continue;
+                float ext[3];
+                for (int a = 0; a < 3; ++a) ext[a] = from_order(h_hi[3 * q + a]) - from_order(h_lo[3 * q + a]);
+                float m = ext[0];  // maxCoeff(&axis): first maximum
+                for (int a = 1; a < 3; ++a)
+                    if (ext[a] > m) {
+                        m = ext[a];
+                        axis[q] = a;
+                    }
+            }
+            CK(cudaMemcpyAsync(d_axis.p, axis.data(), 4 * nn, cudaMemcpyHostToDevice, s));
+            // exact medians: sort (node, coordinate) keys, read the two middle values of every node
+            repart_node_keys(N, mP.p, ldm, node.p, d_axis.p, keys.p, s);
+            uint64_t* k1 = keys.p;
+            uint64_t* k2 = keys_alt.p;
+            repart_sort_keys(k1, k2, N, 32 + d + 1, temp.p, tb, s);
+            std::vector<float> plane(nn, 0.0f);
+            std::vector<uint64_t> mid(2);
+            uint32_t start = 0;
+            for (int q = 0; q < nn; ++q) {
+                const uint32_t c = h_cnt[q];
+                HostRegion& reg = regions[q];
+                if (c > 0) {
+                    const uint32_t i1 = start + c / 2;
+                    const uint32_t i0 = c % 2 == 0 ? i1 - 1 : i1;
+                    CK(cudaMemcpyAsync(&mid[0], k1 + i0, 8, cudaMemcpyDeviceToHost, s));
+                    CK(cudaMemcpyAsync(&mid[1], k1 + i1, 8, cudaMemcpyDeviceToHost, s));
+                    CK(cudaStreamSynchronize(s));
+                    const float lower = from_order((uint32_t)mid[0]), upper = from_order((uint32_t)mid[1]);
+                    plane[q] = c % 2 == 0 ? (lower + upper) / 2.0f : upper;
+                } else {
+                    const int a = axis[q];
+                    const float l = reg.amin[a], h = reg.amax[a];
+                    plane[q] = (std::isfinite(l) && std::isfinite(h)) ? (l + h) / 2.0f
+                               : std::isfinite(l)                    ? l + 1.0f
+                               : std::isfinite(h)                    ? h - 1.0f
+                                                                     : 0.0f;
+                }
+                start += c;
+            }
+            CK(cudaMemcpyAsync(d_plane.p, plane.data(), 4 * nn, cudaMemcpyHostToDevice, s));
+            repart_node_split(N, mP.p, ldm, node.p, d_axis.p, d_plane.p, s);
+            std::vector<HostRegion> next(2 * nn);
+            for (int q = 0; q < nn; ++q) {
+                const int a = axis[q];
+                HostRegion left = regions[q], right = regions[q];
+                dgs_plane lp{};
+                lp.n[a] = 1.0f;
+                lp.d = -plane[q];
+                lp.closed = 0;
+                left.planes.push_back(lp);
+                left.amax[a] = std::min(left.amax[a], plane[q]);
+                dgs_plane rp{};
+                rp.n[a] = -1.0f;
+                rp.d = plane[q];
+                rp.closed = 1;
+                right.planes.push_back(rp);
+                right.amin[a] = std::max(right.amin[a], plane[q]);
+                next[2 * q] = std::move(left);
+                next[2 * q + 1] = std::move(right);
+            }
+            regions = std::move(next);
+            CK(cudaStreamSynchronize(s));  // host vectors used by async copies
+        }
+        const int K = 1 << depth;
+        std::vector<dgs_plane> planes((size_t)K * depth);
+        for (int k = 0; k < K; ++k)
+            for (int j = 0; j < depth; ++j) planes[(size_t)k * depth + j] = regions[k].planes[j];
+        if (planes_out) std::memcpy(planes_out, planes.data(), planes.size() * sizeof(dgs_plane));
+        // new table
+        {
+            Table t{};
+            t.k_count = K;
+            for (int k = 0; k < K; ++k) {
+                t.sub[k].n = depth;
+                for (int j = 0; j < depth; ++j) {
+                    const dgs_plane& p = planes[(size_t)k * depth + j];
+                    t.sub[k].nx[j] = p.n[0];
+                    t.sub[k].ny[j] = p.n[1];
+                    t.sub[k].nz[j] = p.n[2];
+                    t.sub[k].d[j] = p.d;
+                    t.sub[k].closed[j] = p.closed;
+                }
+            }
+            ctx->table = t;
+            CK(cudaMemcpyAsync(ctx->table_dev.p, &ctx->table, sizeof(Table), cudaMemcpyHostToDevice, s));
+        }
+        // ---- assign_subsets (partition.hpp:234-251) + migration (manager.hpp:440-482) ----
+        DevBuf<uint32_t> mask, idx;
+        mask.ensure(N);
+        idx.ensure(N);
+        repart_assign(N, mP.p, ldm, ctx->table_dev.p, (float)d_multiplier, mask.p, s);
+        std::map<int, std::unique_ptr<SubsetState>> fresh;
+        for (int k = 0; k < K; ++k) {
+            repart_flag_bit(N, mask.p, k, flags.p, s);
+            repart_select_iota(N, flags.p, idx.p, count.p, temp.p, tb, s);
+            int nk = 0;
+            CK(cudaMemcpyAsync(&nk, count.p, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::unique_ptr<SubsetState> S(new SubsetState());
+            S->k = k;
+            S->n = nk;
+            S->sh_coeffs = shc;
+            S->rows = rows;
+            S->ld = (size_t)((nk + 31) / 32 * 32);
+            S->adam_step = adam_step;
+            S->epoch = epoch;
+            S->P.ensure(rows * S->ld);
+            S->M.ensure(rows * S->ld);
+            S->V.ensure(rows * S->ld);
+            S->ids32.ensure(nk);
+            if (S->ld > (size_t)nk) {  // keep the padded tail defined (private scratch of the Adam stream)
+                CK(cudaMemsetAsync(S->P.p, 0, rows * S->ld * sizeof(float), s));
+                CK(cudaMemsetAsync(S->M.p, 0, rows * S->ld * sizeof(float), s));
+                CK(cudaMemsetAsync(S->V.p, 0, rows * S->ld * sizeof(float), s));
+            }
+            repart_gather_members(nk, rows, idx.p, mP.p, mM.p, mV.p, mIds.p, ldm, S->P.p, S->M.p, S->V.p,
+                                  S->ids32.p, S->ld, s);
+            std::vector<uint32_t> ids32(nk);
+            if (nk) CK(cudaMemcpyAsync(ids32.data(), S->ids32.p, 4 * (size_t)nk, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            S->ids64.assign(ids32.begin(), ids32.end());
+            fresh[k] = std::move(S);
+        }
+        ctx->subsets = std::move(fresh);
+    });
+}
+
 int dgs_subset_store(dgs_ctx* ctx, int32_t k, dgs_splats* params, dgs_splats* m, dgs_splats* v,
                      uint64_t* adam_step) {
     return dgs_guard([&] {

@@ -115,6 +115,34 @@ void launch_merge_bwd(const ViewParams& vp, const Table* tb_dev, int owner, int 
                       const float4* const* partials, int prow0, const float* grad_rgb, int g_base, int g_rows,
                       const float bg[3], float4* const* grad_out, int grow0, cudaStream_t s);
 
+// Device-side repartition (repartition.cu; orchestration in capi.cu dgs_repartition).
+void repart_snapshot_keys(int n, const float* P, size_t ld, const uint32_t* ids32, const Table* tb, int k,
+                          uint32_t base, uint64_t* keys, uint32_t* vals, cudaStream_t s);
+size_t repart_temp_bytes(int64_t n);
+void repart_sort_pairs(uint64_t*& keys, uint64_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt, int n, int bits,
+                       void* temp, size_t tb, cudaStream_t s);
+void repart_sort_keys(uint64_t*& keys, uint64_t*& keys_alt, int n, int bits, void* temp, size_t tb, cudaStream_t s);
+void repart_first_of_run(int n, const uint64_t* keys, uint8_t* flags, cudaStream_t s);
+void repart_select(int n, const uint32_t* in, const uint8_t* flags, uint32_t* out, int* count, void* temp, size_t tb,
+                   cudaStream_t s);
+void repart_select_iota(int n, const uint8_t* flags, uint32_t* out, int* count, void* temp, size_t tb,
+                        cudaStream_t s);
+void repart_gather_replicas(int n, int rows, const uint32_t* winners, const uint32_t* offsets, int K,
+                            const float* const* srcP, const float* const* srcM, const float* const* srcV,
+                            const uint32_t* const* srcId, const size_t* lds, float* P, float* M, float* V,
+                            uint32_t* ids, size_t ld, cudaStream_t s);
+void repart_node_extent(int n, const float* P, size_t ld, const uint8_t* node, int nnodes, uint32_t* lo,
+                        uint32_t* hi, uint32_t* cnt, cudaStream_t s);
+void repart_node_keys(int n, const float* P, size_t ld, const uint8_t* node, const int* axis, uint64_t* keys,
+                      cudaStream_t s);
+void repart_node_split(int n, const float* P, size_t ld, uint8_t* node, const int* axis, const float* plane,
+                       cudaStream_t s);
+void repart_assign(int n, const float* P, size_t ld, const Table* tb, float mult, uint32_t* mask, cudaStream_t s);
+void repart_flag_bit(int n, const uint32_t* mask, int k, uint8_t* flags, cudaStream_t s);
+void repart_gather_members(int n, int rows, const uint32_t* idx, const float* P, const float* M, const float* V,
+                           const uint32_t* ids, size_t ld_src, float* dP, float* dM, float* dV, uint32_t* dids,
+                           size_t ld_dst, cudaStream_t s);
+
 struct AdamParams {
     float lr[kMaxParamRows];  // per row
     float b1, b2, eps, bc1, bc2;

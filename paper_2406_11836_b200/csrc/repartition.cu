@@ -1,0 +1,269 @@
+// Device-side repartition (Manager::repartition / snapshot / distribute,
+// manager.hpp:389-482; build_kdtree / assign_subsets, partition.hpp:93-251):
+// the kernels; the orchestration (a few host round trips of O(2^L) scalars)
+// lives in capi.cu (dgs_repartition).
+//
+//   snapshot   every replica (subset k, member i) gets the key
+//              id << 8 | (locate(mu) == k ? 0 : 1) << 5 | k; a radix sort and a
+//              first-of-run selection keep, per splat id, the replica held by
+//              the subspace containing its centre, else the lowest k
+//              (manager.hpp:400-414).
+//   KD build   level by level over the merged centres: per-node extents
+//              (order-preserving integer atomics), the widest axis (first
+//              maximum), a radix sort of (node, axis coordinate) keys for the
+//              exact lower/upper medians, and the < plane / >= plane split
+//              (partition.hpp:100-153).  Identical float values to the
+//              reference's std::sort + std::nth_element: sorting is exact.
+//   assign     one thread per splat: membership bits of every subspace
+//              (plane values <= 3 max(exp(log_scale)), glibc-expf port).
+//   migrate    per new subset: flagged compaction, gather of the p, m, v rows.
+#include <cub/cub.cuh>
+
+#include "kernels.h"
+
+namespace dgs_b200 {
+
+namespace {
+
+__device__ __forceinline__ uint32_t float_order(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__global__ void k_snapshot_keys(int n, const float* __restrict__ P, size_t ld, const uint32_t* __restrict__ ids32,
+                                const Table* __restrict__ tb, int k, uint32_t base, uint64_t* __restrict__ keys,
+                                uint32_t* __restrict__ vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float x[3] = {P[i], P[ld + i], P[2 * ld + i]};
+    const int owner = table_locate(*tb, x);
+    const uint64_t prio = owner == k ? 0u : 1u;
+    keys[base + i] = ((uint64_t)ids32[i] << 8) | (prio << 5) | (uint64_t)k;
+    vals[base + i] = base + (uint32_t)i;
+}
+
+__global__ void k_first_of_run(int n, const uint64_t* __restrict__ keys, uint8_t* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    flags[i] = (i == 0 || (keys[i] >> 8) != (keys[i - 1] >> 8)) ? 1 : 0;
+}
+
+/// merged[r][j] = src_k[r][i] for replica (k, i) = winners[j]; K sources given
+/// as device arrays of row-0 pointers, leading dimensions and replica offsets.
+__global__ void k_gather_replicas(int n, int rows, const uint32_t* __restrict__ winners,
+                                  const uint32_t* __restrict__ offsets, int K, const float* const* __restrict__ srcP,
+                                  const float* const* __restrict__ srcM, const float* const* __restrict__ srcV,
+                                  const uint32_t* const* __restrict__ srcId, const size_t* __restrict__ lds,
+                                  float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
+                                  uint32_t* __restrict__ ids, size_t ld) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint32_t r = winners[j];
+    int k = 0;
+    while (k + 1 < K && offsets[k + 1] <= r) ++k;
+    const size_t i = r - offsets[k], sl = lds[k];
+    for (int q = 0; q < rows; ++q) {
+        P[(size_t)q * ld + j] = srcP[k][(size_t)q * sl + i];
+        M[(size_t)q * ld + j] = srcM[k][(size_t)q * sl + i];
+        V[(size_t)q * ld + j] = srcV[k][(size_t)q * sl + i];
+    }
+    ids[j] = srcId[k][i];
+}
+
+/// Per-node extents and counts (nodes < 256): block-local accumulation, one
+/// atomic per (block, node, quantity).
+__global__ void k_node_extent(int n, const float* __restrict__ P, size_t ld, const uint8_t* __restrict__ node,
+                              int nnodes, uint32_t* __restrict__ lo, uint32_t* __restrict__ hi,
+                              uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t slo[3 * 256], shi[3 * 256], scnt[256];
+    for (int q = threadIdx.x; q < nnodes; q += blockDim.x) {
+        scnt[q] = 0;
+        for (int a = 0; a < 3; ++a) {
+            slo[3 * q + a] = 0xffffffffu;
+            shi[3 * q + a] = 0u;
+        }
+    }
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int q = node[i];
+        atomicAdd(&scnt[q], 1u);
+        for (int a = 0; a < 3; ++a) {
+            const uint32_t o = float_order(P[(size_t)a * ld + i]);
+            atomicMin(&slo[3 * q + a], o);
+            atomicMax(&shi[3 * q + a], o);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nnodes; q += blockDim.x) {
+        if (scnt[q] == 0) continue;
+        atomicAdd(&cnt[q], scnt[q]);
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&lo[3 * q + a], slo[3 * q + a]);
+            atomicMax(&hi[3 * q + a], shi[3 * q + a]);
+        }
+    }
+}
+
+__global__ void k_node_keys(int n, const float* __restrict__ P, size_t ld, const uint8_t* __restrict__ node,
+                            const int* __restrict__ axis, uint64_t* __restrict__ keys) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int q = node[i];
+    keys[i] = ((uint64_t)q << 32) | float_order(P[(size_t)axis[q] * ld + i]);
+}
+
+/// partition.hpp:130-131: < plane goes left (child 2q), >= plane right (2q + 1).
+__global__ void k_node_split(int n, const float* __restrict__ P, size_t ld, uint8_t* __restrict__ node,
+                             const int* __restrict__ axis, const float* __restrict__ plane) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int q = node[i];
+    node[i] = (uint8_t)(2 * q + (P[(size_t)axis[q] * ld + i] < plane[q] ? 0 : 1));
+}
+
+/// assign_subsets (partition.hpp:234-251): bit k set iff every plane value of
+/// subspace k at mu is <= d_mult * max(exp(log_scale)).
+__global__ void k_assign(int n, const float* __restrict__ P, size_t ld, const Table* __restrict__ tb, float mult,
+                         uint32_t* __restrict__ mask) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float mu0 = P[i], mu1 = P[ld + i], mu2 = P[2 * ld + i];
+    const float s0 = glibc_expf(P[(size_t)kRowLogScale * ld + i]), s1 = glibc_expf(P[(size_t)(kRowLogScale + 1) * ld + i]),
+                s2 = glibc_expf(P[(size_t)(kRowLogScale + 2) * ld + i]);
+    float smax = s0;  // Vec3::maxCoeff
+    if (s1 > smax) smax = s1;
+    if (s2 > smax) smax = s2;
+    const float di = fmul(mult, smax);
+    uint32_t m = 0;
+    for (int k = 0; k < tb->k_count; ++k) {
+        const Subspace& s = tb->sub[k];
+        bool member = true;
+        for (int p = 0; p < s.n; ++p) {
+            const float v = fadd(dot3(s.nx[p], s.ny[p], s.nz[p], mu0, mu1, mu2), s.d[p]);
+            if (v > di) {
+                member = false;
+                break;
+            }
+        }
+        if (member) m |= 1u << k;
+    }
+    mask[i] = m;
+}
+
+__global__ void k_flag_bit(int n, const uint32_t* __restrict__ mask, int k, uint8_t* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = (mask[i] >> k) & 1u;
+}
+
+__global__ void k_gather_members(int n, int rows, const uint32_t* __restrict__ idx, const float* __restrict__ P,
+                                 const float* __restrict__ M, const float* __restrict__ V,
+                                 const uint32_t* __restrict__ ids, size_t ld_src, float* __restrict__ dP,
+                                 float* __restrict__ dM, float* __restrict__ dV, uint32_t* __restrict__ dids,
+                                 size_t ld_dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const size_t i = idx[j];
+    for (int q = 0; q < rows; ++q) {
+        dP[(size_t)q * ld_dst + j] = P[(size_t)q * ld_src + i];
+        dM[(size_t)q * ld_dst + j] = M[(size_t)q * ld_src + i];
+        dV[(size_t)q * ld_dst + j] = V[(size_t)q * ld_src + i];
+    }
+    dids[j] = ids[i];
+}
+
+inline unsigned blocks(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void repart_snapshot_keys(int n, const float* P, size_t ld, const uint32_t* ids32, const Table* tb, int k,
+                          uint32_t base, uint64_t* keys, uint32_t* vals, cudaStream_t s) {
+    if (n > 0) k_snapshot_keys<<<blocks(n), 256, 0, s>>>(n, P, ld, ids32, tb, k, base, keys, vals);
+}
+
+size_t repart_temp_bytes(int64_t n) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DoubleBuffer<uint64_t> dk;
+    cub::DoubleBuffer<uint32_t> dv;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)n, 0, 64);
+    cub::DeviceRadixSort::SortKeys(nullptr, b, dk, (int)n, 0, 64);
+    cub::DeviceSelect::Flagged(nullptr, c, (const uint32_t*)nullptr, (const uint8_t*)nullptr, (uint32_t*)nullptr,
+                               (int*)nullptr, (int)n);
+    size_t d = 0;
+    cub::DeviceSelect::Flagged(nullptr, d, cub::CountingInputIterator<uint32_t>(0u), (const uint8_t*)nullptr,
+                               (uint32_t*)nullptr, (int*)nullptr, (int)n);
+    return std::max(std::max(a, b), std::max(c, d)) + 256;
+}
+
+void repart_sort_pairs(uint64_t*& keys, uint64_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt, int n, int bits,
+                       void* temp, size_t tb, cudaStream_t s) {
+    cub::DoubleBuffer<uint64_t> dk(keys, keys_alt);
+    cub::DoubleBuffer<uint32_t> dv(vals, vals_alt);
+    cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, n, 0, bits, s);
+    if (dk.Current() != keys) {
+        std::swap(keys, keys_alt);
+        std::swap(vals, vals_alt);
+    }
+}
+
+void repart_sort_keys(uint64_t*& keys, uint64_t*& keys_alt, int n, int bits, void* temp, size_t tb, cudaStream_t s) {
+    cub::DoubleBuffer<uint64_t> dk(keys, keys_alt);
+    cub::DeviceRadixSort::SortKeys(temp, tb, dk, n, 0, bits, s);
+    if (dk.Current() != keys) std::swap(keys, keys_alt);
+}
+
+void repart_first_of_run(int n, const uint64_t* keys, uint8_t* flags, cudaStream_t s) {
+    if (n > 0) k_first_of_run<<<blocks(n), 256, 0, s>>>(n, keys, flags);
+}
+
+void repart_select(int n, const uint32_t* in, const uint8_t* flags, uint32_t* out, int* count, void* temp, size_t tb,
+                   cudaStream_t s) {
+    cub::DeviceSelect::Flagged(temp, tb, in, flags, out, count, n, s);
+}
+
+void repart_select_iota(int n, const uint8_t* flags, uint32_t* out, int* count, void* temp, size_t tb,
+                        cudaStream_t s) {
+    cub::CountingInputIterator<uint32_t> it(0u);
+    cub::DeviceSelect::Flagged(temp, tb, it, flags, out, count, n, s);
+}
+
+void repart_gather_replicas(int n, int rows, const uint32_t* winners, const uint32_t* offsets, int K,
+                            const float* const* srcP, const float* const* srcM, const float* const* srcV,
+                            const uint32_t* const* srcId, const size_t* lds, float* P, float* M, float* V,
+                            uint32_t* ids, size_t ld, cudaStream_t s) {
+    if (n > 0)
+        k_gather_replicas<<<blocks(n), 256, 0, s>>>(n, rows, winners, offsets, K, srcP, srcM, srcV, srcId, lds, P, M,
+                                                    V, ids, ld);
+}
+
+void repart_node_extent(int n, const float* P, size_t ld, const uint8_t* node, int nnodes, uint32_t* lo,
+                        uint32_t* hi, uint32_t* cnt, cudaStream_t s) {
+    if (n > 0) k_node_extent<<<std::min<unsigned>(blocks(n), 148 * 4), 256, 0, s>>>(n, P, ld, node, nnodes, lo, hi,
+                                                                                     cnt);
+}
+
+void repart_node_keys(int n, const float* P, size_t ld, const uint8_t* node, const int* axis, uint64_t* keys,
+                      cudaStream_t s) {
+    if (n > 0) k_node_keys<<<blocks(n), 256, 0, s>>>(n, P, ld, node, axis, keys);
+}
+
+void repart_node_split(int n, const float* P, size_t ld, uint8_t* node, const int* axis, const float* plane,
+                       cudaStream_t s) {
+    if (n > 0) k_node_split<<<blocks(n), 256, 0, s>>>(n, P, ld, node, axis, plane);
+}
+
+void repart_assign(int n, const float* P, size_t ld, const Table* tb, float mult, uint32_t* mask, cudaStream_t s) {
+    if (n > 0) k_assign<<<blocks(n), 256, 0, s>>>(n, P, ld, tb, mult, mask);
+}
+
+void repart_flag_bit(int n, const uint32_t* mask, int k, uint8_t* flags, cudaStream_t s) {
+    if (n > 0) k_flag_bit<<<blocks(n), 256, 0, s>>>(n, mask, k, flags);
+}
+
+void repart_gather_members(int n, int rows, const uint32_t* idx, const float* P, const float* M, const float* V,
+                           const uint32_t* ids, size_t ld_src, float* dP, float* dM, float* dV, uint32_t* dids,
+                           size_t ld_dst, cudaStream_t s) {
+    if (n > 0)
+        k_gather_members<<<blocks(n), 256, 0, s>>>(n, rows, idx, P, M, V, ids, ld_src, dP, dM, dV, dids, ld_dst);
+}
+
+}  // namespace dgs_b200

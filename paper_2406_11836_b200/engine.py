@@ -474,7 +474,32 @@ class Manager:
             return out
         return gather(0), gather(1), gather(2), parts[0][3]
 
-    def repartition(self):
+    def repartition(self, device: bool = True):
+        """Manager::repartition (manager.hpp:421-430).  device=True (default):
+        snapshot, KD build, assignment and migration on the GPU
+        (dgs_repartition, single rank); device=False: the host path through
+        snapshot() and a reload (the reference's message-level data flow)."""
+        if not device:
+            return self.repartition_host()
+        if self.world > 1:
+            raise NotImplementedError("device repartition across ranks (NCCL migration) is SURVEY §8(f) row 1, "
+                                      "multi-rank part")
+        depth = int(self.config.kd_depth)
+        K = 1 << depth
+        arr = (Plane * max(K * depth, 1))()
+        check(lib().dgs_repartition(self.ctx.handle, depth, float(self.options.truncation_radius), len(self.ids),
+                                    self.epoch + 1, arr))
+        planes = np.zeros((K, depth, 5), np.float32)
+        for k in range(K):
+            for j in range(depth):
+                q = arr[k * depth + j]
+                planes[k, j] = (q.n[0], q.n[1], q.n[2], q.d, q.closed)
+        self.table = PartitionTable(planes, depth)
+        self.ctx.table = self.table
+        self.members = None  # membership lives on the device
+        self.epoch += 1
+
+    def repartition_host(self):
         p, m, v, step = self.snapshot()
         if not np.array_equal(np.sort(p.id), self.ids):
             raise RuntimeError("repartition checksum mismatch")
