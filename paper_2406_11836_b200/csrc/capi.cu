@@ -229,6 +229,11 @@ struct Ctx {
     int virtual_slices = 1;        // single-rank sliced mode (tests the multi-rank manager path)
     bool collect_stats = false;    // blend evaluation/contribution counters (costs ~5% in the blends)
     bool records = true;           // forward composite records -> record-walk backward (else ring replay)
+    // shared replicas for config.grad_sync (rebuilt after every load / repartition)
+    bool shared_dirty = true;
+    DevBuf<uint64_t> sh_keys;
+    DevBuf<uint32_t> sh_reps, sh_starts;
+    int sh_slots = 0, sh_nrep = 0;
     DevBuf<BlendStats> stats;
     DevBuf<int> bad;
     uint64_t launches = 0;
@@ -570,6 +575,55 @@ uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int W
     return sent;
 }
 
+/// Shared-replica index over the resident subsets (grad sync): replicas sorted
+/// by (id, k); sh_starts = first sorted position of every id held >= 2 times.
+void build_shared(Ctx& ctx) {
+    if (!ctx.shared_dirty) return;
+    cudaStream_t s = ctx.stream;
+    std::vector<uint32_t> offs(1, 0);
+    std::vector<int> ks;
+    for (auto& kv : ctx.subsets) {
+        ks.push_back(kv.first);
+        offs.push_back(offs.back() + (uint32_t)kv.second->n);
+    }
+    const int R = (int)offs.back();
+    ctx.sh_slots = 0;
+    ctx.sh_nrep = R;
+    if (R > 0) {
+        DevBuf<uint64_t> kalt;
+        DevBuf<uint32_t> valt;
+        DevBuf<uint8_t> flags, temp;
+        DevBuf<int> count;
+        ctx.sh_keys.ensure(R);
+        kalt.ensure(R);
+        ctx.sh_reps.ensure(R);
+        valt.ensure(R);
+        flags.ensure(R);
+        count.ensure(1);
+        ctx.sh_starts.ensure(R);
+        const size_t tb = repart_temp_bytes(R);
+        temp.ensure(tb);
+        for (size_t q = 0; q < ks.size(); ++q) {
+            const SubsetState& S = *ctx.subsets[ks[q]];
+            shared_replica_keys((int)S.n, S.ids32.p, ks[q], offs[q], ctx.sh_keys.p, ctx.sh_reps.p, s);
+        }
+        uint64_t* kp = ctx.sh_keys.p;
+        uint64_t* kap = kalt.p;
+        uint32_t* vp = ctx.sh_reps.p;
+        uint32_t* vap = valt.p;
+        repart_sort_pairs(kp, kap, vp, vap, R, 40, temp.p, tb, s);
+        if (kp != ctx.sh_keys.p) {  // keep the sorted data in the persistent buffers
+            CK(cudaMemcpyAsync(ctx.sh_keys.p, kp, 8 * (size_t)R, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(ctx.sh_reps.p, vp, 4 * (size_t)R, cudaMemcpyDeviceToDevice, s));
+        }
+        shared_run_starts(R, ctx.sh_keys.p, flags.p, s);
+        repart_select_iota(R, flags.p, ctx.sh_starts.p, count.p, temp.p, tb, s);
+        CK(cudaMemcpyAsync(&ctx.sh_slots, count.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    ctx.shared_dirty = false;
+}
+
 void require_table(const Ctx& ctx) {
     if (!ctx.table_set) throw std::invalid_argument("partition table not set (dgs_set_table)");
 }
@@ -746,6 +800,7 @@ int dgs_subset_load(dgs_ctx* ctx, int32_t k, const dgs_splats* params, const dgs
         if (v) upload_fields(*ctx, *S, *v, S->V.p);
         else CK(cudaMemset(S->V.p, 0, S->rows * S->ld * sizeof(float)));
         ctx->subsets[k] = std::move(S);
+        ctx->shared_dirty = true;
     });
 }
 
@@ -1010,6 +1065,7 @@ int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t ex
             fresh[k] = std::move(S);
         }
         ctx->subsets = std::move(fresh);
+        ctx->shared_dirty = true;
     });
 }
 
@@ -1509,7 +1565,57 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         }
         // ---- MsgBackwardTask x B, then apply_step (worker.hpp:86-127, 162-167) ----
         reset_bad(*ctx);
-        for (int k : local) {
+        const bool sync = ctx->cfg.grad_sync != 0 && K > 1;
+        if (sync) {
+            // config.grad_sync (worker.hpp:103-144, manager.hpp:351-379): full gradients of
+            // every member, shared replicas summed in worker order, then the dense Adam step
+            if (W > 1) throw std::invalid_argument("train_step: grad_sync across ranks is not built (single rank only)");
+            build_shared(*ctx);
+            std::vector<float*> gp;
+            std::vector<size_t> gl;
+            for (int k : local) {
+                SubsetState& S_ = subset(*ctx, k);
+                S_.G.ensure(S_.rows * S_.ld);
+                CK(cudaMemsetAsync(S_.G.p, 0, S_.rows * S_.ld * sizeof(float), ctx->stream));
+                for (int v = 0; v < batch; ++v) {
+                    ViewSlot& vs = S_.slot(v);
+                    backward_blend(*ctx, S_, v, ctx->collect_stats ? ctx->stats.p + 1 : nullptr);
+                    Stage st(ctx->timer, kStProjBwd, ctx->stream);
+                    launch_project_bwd((int)S_.n, S_.P.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S_.g2d.p,
+                                       S_.ld, S_.G.p, ctx->bad.p, ctx->stream);
+                    ++ctx->launches;
+                }
+            }
+            // G pointers indexed by subset id k (reps encode k)
+            int kmax = 0;
+            for (int k : local) kmax = std::max(kmax, k);
+            gp.assign(kmax + 1, nullptr);
+            gl.assign(kmax + 1, 0);
+            for (int k : local) {
+                gp[k] = subset(*ctx, k).G.p;
+                gl[k] = subset(*ctx, k).ld;
+            }
+            DevBuf<float*> dG;
+            DevBuf<size_t> dL;
+            dG.ensure(kmax + 1);
+            dL.ensure(kmax + 1);
+            CK(cudaMemcpyAsync(dG.p, gp.data(), (kmax + 1) * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(dL.p, gl.data(), (kmax + 1) * sizeof(size_t), cudaMemcpyHostToDevice, ctx->stream));
+            const int rows = subset(*ctx, local[0]).rows;
+            grad_sync(ctx->sh_slots, rows, ctx->sh_starts.p, ctx->sh_nrep, ctx->sh_keys.p, ctx->sh_reps.p, dG.p, dL.p,
+                      ctx->stream);
+            ++ctx->launches;
+            for (int k : local) {
+                SubsetState& S_ = subset(*ctx, k);
+                const AdamParams ap = adam_params(*ctx, S_, S_.adam_step + 1);
+                Stage st(ctx->timer, kStAdam, ctx->stream);
+                launch_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.rows, S_.G.p, ap, ctx->stream);
+                ++ctx->launches;
+                ++S_.adam_step;
+            }
+            CK(cudaStreamSynchronize(ctx->stream));  // dG / dL scoped to this block
+        }
+        for (int k : (sync ? std::vector<int>{} : local)) {
             SubsetState& S_ = subset(*ctx, k);
             const AdamParams ap = adam_params(*ctx, S_, S_.adam_step + 1);
             if (batch > 1) {

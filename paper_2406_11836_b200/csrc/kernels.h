@@ -143,6 +143,13 @@ void repart_gather_members(int n, int rows, const uint32_t* idx, const float* P,
                            const uint32_t* ids, size_t ld_src, float* dP, float* dM, float* dV, uint32_t* dids,
                            size_t ld_dst, cudaStream_t s);
 
+// Gradient sync of shared replicas (config.grad_sync; manager.hpp:351-379, worker.hpp:103-144).
+void shared_replica_keys(int n, const uint32_t* ids32, int k, uint32_t base, uint64_t* keys, uint32_t* vals,
+                         cudaStream_t s);
+void shared_run_starts(int n, const uint64_t* keys, uint8_t* flags, cudaStream_t s);
+void grad_sync(int nslots, int rows, const uint32_t* starts, int nrep, const uint64_t* keys, const uint32_t* reps,
+               float* const* G, const size_t* lds, cudaStream_t s);
+
 struct AdamParams {
     float lr[kMaxParamRows];  // per row
     float b1, b2, eps, bc1, bc2;

@@ -171,6 +171,49 @@ __global__ void k_gather_members(int n, int rows, const uint32_t* __restrict__ i
     dids[j] = ids[i];
 }
 
+/// Shared-replica index (grad sync): key id << 8 | k, value k << 27 | i.
+__global__ void k_replica_keys(int n, const uint32_t* __restrict__ ids32, int k, uint32_t base,
+                               uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[base + i] = ((uint64_t)ids32[i] << 8) | (uint64_t)k;
+    vals[base + i] = ((uint32_t)k << 27) | (uint32_t)i;
+}
+
+/// flags[j] = 1 iff sorted position j starts a run of >= 2 replicas of one id.
+__global__ void k_shared_run_starts(int n, const uint64_t* __restrict__ keys, uint8_t* __restrict__ flags) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint64_t id = keys[j] >> 8;
+    const bool start = j == 0 || (keys[j - 1] >> 8) != id;
+    flags[j] = (start && j + 1 < n && (keys[j + 1] >> 8) == id) ? 1 : 0;
+}
+
+/// manager.hpp:359-378: per shared id and gradient row, the sum over its
+/// replicas in worker order (first replica's value, then += the next ones),
+/// written back to every replica's gradient row.
+__global__ void k_grad_sync(int nslots, int rows, const uint32_t* __restrict__ starts, int nrep,
+                            const uint64_t* __restrict__ keys, const uint32_t* __restrict__ reps,
+                            float* const* __restrict__ G, const size_t* __restrict__ lds) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nslots * rows) return;
+    const int s = t / rows, r = t % rows;
+    const uint32_t b = starts[s];
+    const uint64_t id = keys[b] >> 8;
+    uint32_t e = b + 1;
+    while (e < (uint32_t)nrep && (keys[e] >> 8) == id) ++e;
+    float acc = 0.0f;
+    for (uint32_t j = b; j < e; ++j) {
+        const uint32_t k = reps[j] >> 27, i = reps[j] & 0x7ffffffu;
+        const float g = G[k][(size_t)r * lds[k] + i];
+        acc = j == b ? g : fadd(acc, g);
+    }
+    for (uint32_t j = b; j < e; ++j) {
+        const uint32_t k = reps[j] >> 27, i = reps[j] & 0x7ffffffu;
+        G[k][(size_t)r * lds[k] + i] = acc;
+    }
+}
+
 inline unsigned blocks(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -264,6 +307,21 @@ void repart_gather_members(int n, int rows, const uint32_t* idx, const float* P,
                            size_t ld_dst, cudaStream_t s) {
     if (n > 0)
         k_gather_members<<<blocks(n), 256, 0, s>>>(n, rows, idx, P, M, V, ids, ld_src, dP, dM, dV, dids, ld_dst);
+}
+
+void shared_replica_keys(int n, const uint32_t* ids32, int k, uint32_t base, uint64_t* keys, uint32_t* vals,
+                         cudaStream_t s) {
+    if (n > 0) k_replica_keys<<<blocks(n), 256, 0, s>>>(n, ids32, k, base, keys, vals);
+}
+
+void shared_run_starts(int n, const uint64_t* keys, uint8_t* flags, cudaStream_t s) {
+    if (n > 0) k_shared_run_starts<<<blocks(n), 256, 0, s>>>(n, keys, flags);
+}
+
+void grad_sync(int nslots, int rows, const uint32_t* starts, int nrep, const uint64_t* keys, const uint32_t* reps,
+               float* const* G, const size_t* lds, cudaStream_t s) {
+    if (nslots > 0) k_grad_sync<<<blocks((int64_t)nslots * rows), 256, 0, s>>>(nslots, rows, starts, nrep, keys, reps, G,
+                                                                              lds);
 }
 
 }  // namespace dgs_b200
