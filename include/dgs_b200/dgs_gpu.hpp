@@ -377,13 +377,8 @@ inline LossResult<float> loss(const Image<float>& render, const Image<float>& ta
 }
 
 /// partition.hpp:160-184 (host; bit-exact)
-inline PartitionTable<float> build_kdtree(std::span<const Vec3<float>> centers, int depth) {
-    std::vector<float> c(3 * centers.size());
-    for (size_t i = 0; i < centers.size(); ++i)
-        for (int a = 0; a < 3; ++a) c[3 * i + a] = centers[i][a];
+inline PartitionTable<float> table_from_planes(const std::vector<dgs_plane>& planes, int depth) {
     const int K = 1 << std::max(depth, 0);
-    std::vector<dgs_plane> planes(std::max(1, K * depth));
-    check(dgs_build_kdtree(c.data(), static_cast<int64_t>(centers.size()), depth, planes.data()));
     PartitionTable<float> t;
     t.depth = depth;
     t.kind = PartitionKind::kKdTree;
@@ -402,6 +397,16 @@ inline PartitionTable<float> build_kdtree(std::span<const Vec3<float>> centers, 
     }
     t.membership.resize(K);
     return t;
+}
+
+inline PartitionTable<float> build_kdtree(std::span<const Vec3<float>> centers, int depth) {
+    std::vector<float> c(3 * centers.size());
+    for (size_t i = 0; i < centers.size(); ++i)
+        for (int a = 0; a < 3; ++a) c[3 * i + a] = centers[i][a];
+    const int K = 1 << std::max(depth, 0);
+    std::vector<dgs_plane> planes(std::max(1, K * depth));
+    check(dgs_build_kdtree(c.data(), static_cast<int64_t>(centers.size()), depth, planes.data()));
+    return table_from_planes(planes, depth);
 }
 
 /// partition.hpp:234-251 (host; bit-exact)
@@ -533,8 +538,26 @@ class Manager {
         return merged;
     }
 
-    /// manager.hpp:422-430
+    /// manager.hpp:422-430, on the device (dgs_repartition): snapshot, KD build,
+    /// assignment and migration never leave the GPU.  The table's membership
+    /// lists come back in id order (the reference's are in snapshot order).
     void repartition() {
+        const int depth = config_.kd_depth, K = 1 << std::max(depth, 0);
+        std::vector<dgs_plane> planes(std::max(1, K * depth));
+        check(dgs_repartition(dev_.get(), depth, options_.truncation_radius, static_cast<int64_t>(ids_.size()),
+                              epoch_ + 1, planes.data()));
+        epoch_ += 1;
+        table_ = table_from_planes(planes, depth);
+        for (int k = 0; k < K; ++k) {
+            const int64_t n = dgs_subset_size(dev_.get(), k);
+            std::vector<uint64_t> ids(static_cast<size_t>(std::max<int64_t>(n, 0)));
+            if (n > 0) check(dgs_subset_ids(dev_.get(), k, ids.data()));
+            table_.membership[k].assign(ids.begin(), ids.end());
+        }
+    }
+
+    /// The host data flow of manager.hpp:422-430 (snapshot through the host, rebuild, reload).
+    void repartition_host() {
         auto packs = snapshot();
         std::vector<SplatId> ids;
         for (const auto& p : packs) ids.push_back(p.splat.id);

@@ -186,6 +186,16 @@ int dgs_dump_records(dgs_ctx* ctx, int32_t k, float* recs, uint32_t* counts);
  * dgs_build_kdtree. */
 int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t expected_splats, uint64_t epoch,
                     dgs_plane* planes_out);
+/* init_from_pointcloud (trainer.hpp:24-91): `target` splats sampled from the
+ * cloud with the reference's libstdc++ streams (std::sample without
+ * replacement, or uniform picks + Gaussian jitter when oversampling), isotropic
+ * log-scale from the mean distance to the 3 nearest sampled neighbours (exact
+ * k-NN on the GPU, ctx's device), identity rotation, opacity logit(0.1), DC
+ * colour from the point colour.  colors may be NULL (n_colors = 0). */
+int dgs_init_from_pointcloud(dgs_ctx* ctx, const float* points, int64_t n_points, const float* colors,
+                             int64_t n_colors, int64_t target, uint64_t seed, int32_t sh_degree, dgs_splats* out);
+/* Splat ids of subset k (dgs_subset_size(ctx, k) entries, member order). */
+int dgs_subset_ids(dgs_ctx* ctx, int32_t k, uint64_t* ids);
 
 /* ---- Manager side (engine.hpp:108-234, loss.hpp:153-177) ------------------------ */
 int dgs_pixel_orders(dgs_ctx* ctx, const dgs_camera* cam, uint16_t* order, uint16_t* count);

@@ -26,6 +26,7 @@
 #include "dgs/optim.hpp"
 #include "dgs/partition.hpp"
 #include "dgs/raster.hpp"
+#include "dgs/trainer.hpp"
 
 #include <chrono>
 #include <cstdio>
@@ -422,6 +423,20 @@ int main(int argc, char** argv) {
     try {
         g_out = arg("out", ".");
         std::filesystem::create_directories(g_out);
+
+        // ---- init_from_pointcloud (trainer.hpp:24-91) on a given cloud ----
+        if (has("init_pc")) {
+            const auto pts = load_npy<Real>(arg("pc_points", ""));
+            std::vector<Real> cols;
+            if (has("pc_colors")) cols = load_npy<Real>(arg("pc_colors", ""));
+            std::vector<Vec3<Real>> P(pts.size() / 3), Cc(cols.size() / 3);
+            for (std::size_t i = 0; i < P.size(); ++i) P[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+            for (std::size_t i = 0; i < Cc.size(); ++i) Cc[i] = {cols[3 * i], cols[3 * i + 1], cols[3 * i + 2]};
+            const auto out = init_from_pointcloud<Real>(P, Cc, std::size_t(iarg("target", 1000)),
+                                                        std::uint64_t(iarg("seed", 1)), int(iarg("sh_degree", 3)));
+            save_splats("init_", out);
+            return 0;
+        }
 
         // ---- scene -------------------------------------------------------
         const double t_setup0 = now_s();

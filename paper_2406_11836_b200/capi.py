@@ -105,6 +105,9 @@ _SIGS = {
     "dgs_subset_load": (C.c_int, [_P, C.c_int32, C.POINTER(SplatsC), C.POINTER(SplatsC), C.POINTER(SplatsC),
                                   C.c_uint64, C.c_uint64]),
     "dgs_repartition": (C.c_int, [_P, C.c_int32, C.c_double, C.c_int64, C.c_uint64, C.POINTER(Plane)]),
+    "dgs_subset_ids": (C.c_int, [_P, C.c_int32, _P]),
+    "dgs_init_from_pointcloud": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_uint64, C.c_int32,
+                                         C.POINTER(SplatsC)]),
     "dgs_subset_store": (C.c_int, [_P, C.c_int32, C.POINTER(SplatsC), C.POINTER(SplatsC), C.POINTER(SplatsC),
                                    C.POINTER(C.c_uint64)]),
     "dgs_subset_size": (C.c_int64, [_P, C.c_int32]),

@@ -11,8 +11,10 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <iterator>
 #include <map>
 #include <memory>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -1077,6 +1079,96 @@ int dgs_subset_store(dgs_ctx* ctx, int32_t k, dgs_splats* params, dgs_splats* m,
         download_fields(*ctx, S, S.M.p, m);
         download_fields(*ctx, S, S.V.p, v);
         if (adam_step) *adam_step = S.adam_step;
+    });
+}
+
+int dgs_init_from_pointcloud(dgs_ctx* ctx, const float* points, int64_t n_points, const float* colors,
+                             int64_t n_colors, int64_t target, uint64_t seed, int32_t sh_degree, dgs_splats* out) {
+    return dgs_guard([&] {
+        // trainer.hpp:24-91, host RNG in libstdc++ (bit-identical picks/jitter), neighbour term on the GPU
+        if (n_points <= 0) throw std::invalid_argument("init_from_pointcloud: empty cloud");
+        if (n_colors != 0 && n_colors != n_points) throw std::invalid_argument("init_from_pointcloud: color count mismatch");
+        if (sh_degree < 0 || sh_degree > 3) throw std::invalid_argument("init_from_pointcloud: sh_degree must be 0..3");
+        const int n_coeff = (sh_degree + 1) * (sh_degree + 1);
+        if (out->n < target || out->sh_coeffs != n_coeff) throw std::invalid_argument("init_from_pointcloud: output too small");
+        std::mt19937_64 rng(seed);
+        std::vector<size_t> picks;
+        picks.reserve((size_t)target);
+        float jitter = 0.0f;
+        if ((size_t)target <= (size_t)n_points) {
+            std::vector<size_t> all((size_t)n_points);
+            for (size_t i = 0; i < all.size(); ++i) all[i] = i;
+            std::sample(all.begin(), all.end(), std::back_inserter(picks), (size_t)target, rng);
+        } else {
+            float lo[3], hi[3];
+            for (int a = 0; a < 3; ++a) lo[a] = hi[a] = points[a];
+            for (int64_t i = 0; i < n_points; ++i)
+                for (int a = 0; a < 3; ++a) {
+                    lo[a] = std::min(lo[a], points[3 * i + a]);
+                    hi[a] = std::max(hi[a], points[3 * i + a]);
+                }
+            const float d0 = hi[0] - lo[0], d1 = hi[1] - lo[1], d2 = hi[2] - lo[2];
+            jitter = 1e-3f * std::sqrt(dot3(d0, d1, d2, d0, d1, d2));  // T(1e-3) * (hi - lo).norm()
+            std::uniform_int_distribution<size_t> pick(0, (size_t)n_points - 1);
+            for (int64_t i = 0; i < target; ++i) picks.push_back(pick(rng));
+        }
+        std::normal_distribution<double> gauss;
+        const size_t n = picks.size();
+        std::vector<float> centers(3 * n);
+        float lo[3], hi[3];
+        for (size_t i = 0; i < n; ++i) {
+            for (int a = 0; a < 3; ++a) centers[3 * i + a] = points[3 * picks[i] + a];
+            if (jitter > 0.0f) {
+                const float j0 = (float)gauss(rng) * jitter, j1 = (float)gauss(rng) * jitter,
+                            j2 = (float)gauss(rng) * jitter;
+                centers[3 * i] += j0;
+                centers[3 * i + 1] += j1;
+                centers[3 * i + 2] += j2;
+            }
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = i ? std::min(lo[a], centers[3 * i + a]) : centers[3 * i + a];
+                hi[a] = i ? std::max(hi[a], centers[3 * i + a]) : centers[3 * i + a];
+            }
+        }
+        std::vector<float> nn_mean(n, 1.0f);
+        const int k_nn = (int)std::min<size_t>(3, n - 1);
+        if (k_nn > 0) {
+            CK(cudaSetDevice(ctx->device));
+            DevBuf<float> dp, dm;
+            dp.ensure(3 * n);
+            dm.ensure(n);
+            CK(cudaMemcpyAsync(dp.p, centers.data(), 12 * n, cudaMemcpyHostToDevice, ctx->stream));
+            knn_mean_distance((int)n, k_nn, dp.p, dm.p, lo, hi, ctx->stream);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(nn_mean.data(), dm.p, 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        const float op = std::log(0.1f / (1.0f - 0.1f));  // logit(T(0.1)), math.hpp:27-29
+        const float c0 = (float)0.28209479177387814;     // T(sh::kC0)
+        for (size_t i = 0; i < n; ++i) {
+            if (out->id) out->id[i] = (uint64_t)i;
+            const float ls = std::log(std::max(nn_mean[i], 1e-7f));
+            for (int a = 0; a < 3; ++a) {
+                out->mu[3 * i + a] = centers[3 * i + a];
+                out->log_scale[3 * i + a] = ls;
+            }
+            out->rotation[4 * i] = 1.0f;
+            out->rotation[4 * i + 1] = out->rotation[4 * i + 2] = out->rotation[4 * i + 3] = 0.0f;
+            out->opacity_logit[i] = op;
+            for (int c = 0; c < n_coeff; ++c)
+                for (int a = 0; a < 3; ++a) out->sh[(i * n_coeff + c) * 3 + a] = 0.0f;
+            for (int a = 0; a < 3; ++a) {
+                const float col = n_colors ? colors[3 * picks[i] + a] : 0.5f;
+                out->sh[(i * n_coeff) * 3 + a] = (col - 0.5f) / c0;
+            }
+        }
+    });
+}
+
+int dgs_subset_ids(dgs_ctx* ctx, int32_t k, uint64_t* ids) {
+    return dgs_guard([&] {
+        const SubsetState& S = subset(*ctx, k);
+        std::memcpy(ids, S.ids64.data(), S.ids64.size() * sizeof(uint64_t));
     });
 }
 

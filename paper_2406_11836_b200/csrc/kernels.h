@@ -150,6 +150,11 @@ void shared_run_starts(int n, const uint64_t* keys, uint8_t* flags, cudaStream_t
 void grad_sync(int nslots, int rows, const uint32_t* starts, int nrep, const uint64_t* keys, const uint32_t* reps,
                float* const* G, const size_t* lds, cudaStream_t s);
 
+// init_from_pointcloud's neighbour term (knn.cu): out[i] = mean of the sqrt of the
+// k_nn (<= 3) smallest squared distances from point i to the others (exact).
+void knn_mean_distance(int n, int k_nn, const float* d_pts, float* d_out, const float lo[3], const float hi[3],
+                       cudaStream_t s);
+
 struct AdamParams {
     float lr[kMaxParamRows];  // per row
     float b1, b2, eps, bc1, bc2;

@@ -120,6 +120,20 @@ def ring_camera(width: int, height: int, i: int, n_views: int = 64, fov_deg: flo
     return cam
 
 
+def init_from_pointcloud(ctx: "Context", points: np.ndarray, colors: np.ndarray | None, target_count: int,
+                         seed: int, sh_degree: int = 3) -> Splats:
+    """trainer.hpp:24-91 init_from_pointcloud; the 3-nearest-neighbour term runs
+    on ctx's GPU (exact k-NN on a uniform grid instead of O(N^2))."""
+    points = np.ascontiguousarray(points, np.float32).reshape(-1, 3)
+    cols = None if colors is None else np.ascontiguousarray(colors, np.float32).reshape(-1, 3)
+    out = Splats.empty(int(target_count), (sh_degree + 1) ** 2)
+    oc = out.c()
+    check(lib().dgs_init_from_pointcloud(ctx.handle, ptr(points), points.shape[0], ptr(cols),
+                                         0 if cols is None else cols.shape[0], int(target_count), int(seed),
+                                         int(sh_degree), C.byref(oc)))
+    return out
+
+
 def perturb(splats: Splats, seed: int) -> Splats:
     s = splats.copy()
     cs = s.c()

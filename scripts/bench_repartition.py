@@ -23,3 +23,16 @@ for dev in (True, False):
                                                             for k in range(8)]
     mgr.close()
 print(json.dumps(out))
+
+# init_from_pointcloud at the same scale (trainer.hpp:24-91): the reference's
+# neighbour term is O(N^2) on the CPU (days at 10M); here an exact grid k-NN.
+import numpy as np  # noqa: E402
+
+rng = np.random.default_rng(1)
+pts = (rng.random((n, 3)) * 2 - 1).astype(np.float32)
+ctx = engine.Context(0)
+engine.init_from_pointcloud(ctx, pts[:1000], None, 1000, seed=1, sh_degree=3)  # warm-up
+t = time.perf_counter()
+engine.init_from_pointcloud(ctx, pts, None, n, seed=1, sh_degree=3)
+print(json.dumps({"init_from_pointcloud_points": n, "seconds": time.perf_counter() - t}))
+ctx.close()

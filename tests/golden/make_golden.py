@@ -30,6 +30,13 @@ SETS = {
     "g4_synth_kd3_bg": dict(scene="synth", count=2000, w=48, h=48, n_views=6, seed=23, kd=3, mode="default",
                             view=2, perturb=4, bg_r=0.2, bg_g=0.5, bg_b=0.9),
 }
+# init_from_pointcloud (trainer.hpp:24-91) on a numpy-generated cloud (committed with the fixture)
+INIT_SETS = {
+    # target <= points: std::sample without replacement, no jitter
+    "g5_init_pc_sample": dict(points=6000, target=4000, seed=17, sh_degree=3, cloud_seed=5),
+    # target > points: uniform picks with replacement + 1e-3 * bbox-diagonal jitter
+    "g6_init_pc_oversample": dict(points=1500, target=5000, seed=29, sh_degree=1, cloud_seed=6),
+}
 DUMPS = ["save_scene", "dump_table", "dump_orders", "dump_project", "dump_partials", "contributors", "dump_render",
          "dump_step", "dump_g2d"]
 
@@ -46,6 +53,25 @@ def run(name, args, out):
                                                    "generator": "oracle/_ref/ref_dump"}, indent=1))
 
 
+def run_init(name, args, out):
+    tmp = out / "_npy"
+    tmp.mkdir()
+    rng = np.random.default_rng(args["cloud_seed"])
+    pts = (rng.random((args["points"], 3)) * 2 - 1).astype(np.float32)
+    pts[: args["points"] // 3] *= 0.2  # a dense cluster: uneven neighbour distances
+    cols = rng.random((args["points"], 3)).astype(np.float32)
+    np.save(tmp / "pc_points.npy", pts)
+    np.save(tmp / "pc_colors.npy", cols)
+    argv = [str(REF), "init_pc=1", f"pc_points={tmp / 'pc_points.npy'}", f"pc_colors={tmp / 'pc_colors.npy'}",
+            f"target={args['target']}", f"seed={args['seed']}", f"sh_degree={args['sh_degree']}", f"out={tmp}"]
+    subprocess.run(argv, check=True)
+    arrays = {f.stem: np.load(f) for f in sorted(tmp.glob("*.npy"))}
+    np.savez_compressed(out / "golden.npz", **arrays)
+    shutil.rmtree(tmp)
+    (out / "manifest.json").write_text(json.dumps({"name": name, "args": args, "dumps": ["init_pc"],
+                                                   "generator": "oracle/_ref/ref_dump init_pc"}, indent=1))
+
+
 def main():
     if not REF.exists():
         sys.exit("build oracle/_ref first: make -C oracle ref")
@@ -57,6 +83,14 @@ def main():
         shutil.rmtree(out, ignore_errors=True)
         out.mkdir(parents=True)
         run(name, args, out)
+        print(name, sum(f.stat().st_size for f in out.iterdir()) // 1024, "KiB")
+    for name, args in INIT_SETS.items():
+        if only and name not in only:
+            continue
+        out = HERE / name
+        shutil.rmtree(out, ignore_errors=True)
+        out.mkdir(parents=True)
+        run_init(name, args, out)
         print(name, sum(f.stat().st_size for f in out.iterdir()) // 1024, "KiB")
 
 
