@@ -194,6 +194,12 @@ int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t ex
  * colour from the point colour.  colors may be NULL (n_colors = 0). */
 int dgs_init_from_pointcloud(dgs_ctx* ctx, const float* points, int64_t n_points, const float* colors,
                              int64_t n_colors, int64_t target, uint64_t seed, int32_t sh_degree, dgs_splats* out);
+/* save_splats_ply (io.hpp:257-297): 3DGS property convention, float32,
+ * binary_little_endian (binary != 0) or ascii; byte-identical to the reference. */
+int dgs_save_splats_ply(const dgs_splats* splats, const char* path, int32_t binary);
+/* load_ply's splat mode (io.hpp:85-255) for float32 checkpoints: out == NULL
+ * returns only the count and the SH coefficient count; ids are 0..n-1. */
+int dgs_load_splats_ply(const char* path, dgs_splats* out, int64_t* n, int32_t* sh_coeffs);
 /* Splat ids of subset k (dgs_subset_size(ctx, k) entries, member order). */
 int dgs_subset_ids(dgs_ctx* ctx, int32_t k, uint64_t* ids);
 

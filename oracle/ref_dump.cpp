@@ -481,6 +481,7 @@ int main(int argc, char** argv) {
         const std::vector<Splat<Real>> gt_splats = splats;  // targets render the unperturbed scene
         if (has("perturb")) perturb(splats, std::uint64_t(iarg("perturb", 1)));
 
+        if (has("save_ply")) save_splats_ply(std::span<const Splat<Real>>(splats), arg("save_ply", "scene.ply"), true);
         if (has("save_scene")) {
             save_splats("scene_", splats);
             std::vector<Real> cr;

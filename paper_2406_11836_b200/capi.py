@@ -108,6 +108,8 @@ _SIGS = {
     "dgs_subset_ids": (C.c_int, [_P, C.c_int32, _P]),
     "dgs_init_from_pointcloud": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_uint64, C.c_int32,
                                          C.POINTER(SplatsC)]),
+    "dgs_save_splats_ply": (C.c_int, [C.POINTER(SplatsC), C.c_char_p, C.c_int32]),
+    "dgs_load_splats_ply": (C.c_int, [C.c_char_p, C.POINTER(SplatsC), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "dgs_subset_store": (C.c_int, [_P, C.c_int32, C.POINTER(SplatsC), C.POINTER(SplatsC), C.POINTER(SplatsC),
                                    C.POINTER(C.c_uint64)]),
     "dgs_subset_size": (C.c_int64, [_P, C.c_int32]),

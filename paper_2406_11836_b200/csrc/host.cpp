@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -331,6 +333,130 @@ int dgs_perturb_splats(dgs_splats* s, uint64_t seed) {
             for (int a = 0; a < 3; ++a) gs[a] = (float)g(rng);
             float* sh = s->sh + (size_t)i * s->sh_coeffs * 3;
             for (int a = 0; a < 3; ++a) sh[a] = sh[a] + gs[a] * 0.1f;
+        }
+    });
+}
+
+/* save_splats_ply (io.hpp:257-297): the 3DGS property convention, float32. */
+int dgs_save_splats_ply(const dgs_splats* s, const char* path, int32_t binary) {
+    return dgs_guard([&] {
+        std::ofstream f(path, std::ios::binary);
+        if (!f) throw std::runtime_error(std::string("save_splats_ply: cannot open ") + path);
+        const int n_coeff = s->n ? s->sh_coeffs : 1;
+        const int rest = 3 * (n_coeff - 1);
+        f << "ply\nformat " << (binary ? "binary_little_endian" : "ascii") << " 1.0\n";
+        f << "element vertex " << s->n << "\n";
+        for (const char* p : {"x", "y", "z", "nx", "ny", "nz"}) f << "property float " << p << "\n";
+        for (int a = 0; a < 3; ++a) f << "property float f_dc_" << a << "\n";
+        for (int a = 0; a < rest; ++a) f << "property float f_rest_" << a << "\n";
+        f << "property float opacity\n";
+        for (int a = 0; a < 3; ++a) f << "property float scale_" << a << "\n";
+        for (int a = 0; a < 4; ++a) f << "property float rot_" << a << "\n";
+        f << "end_header\n";
+        std::vector<float> row;
+        for (int64_t i = 0; i < s->n; ++i) {
+            row.clear();
+            for (int a = 0; a < 3; ++a) row.push_back(s->mu[3 * i + a]);
+            for (int a = 0; a < 3; ++a) row.push_back(0.0f);  // normals unused
+            for (int a = 0; a < 3; ++a) row.push_back(s->sh[(i * n_coeff) * 3 + a]);
+            for (int a = 0; a < 3; ++a)  // f_rest channel-major
+                for (int c = 1; c < n_coeff; ++c) row.push_back(s->sh[(i * n_coeff + c) * 3 + a]);
+            row.push_back(s->opacity_logit[i]);
+            for (int a = 0; a < 3; ++a) row.push_back(s->log_scale[3 * i + a]);
+            for (int a = 0; a < 4; ++a) row.push_back(s->rotation[4 * i + a]);
+            if (binary) {
+                f.write(reinterpret_cast<const char*>(row.data()), std::streamsize(row.size() * sizeof(float)));
+            } else {
+                for (size_t q = 0; q < row.size(); ++q) f << (q ? " " : "") << row[q];
+                f << "\n";
+            }
+        }
+        if (!f) throw std::runtime_error(std::string("save_splats_ply: write failed for ") + path);
+    });
+}
+
+/* Splat checkpoints written by dgs_save_splats_ply / the reference's
+ * save_splats_ply (binary_little_endian float32 or ascii, any property order
+ * of the 3DGS convention; load_ply's splat mode, io.hpp:85-255).  out == NULL:
+ * only *n and *sh_coeffs are returned.  Ids are 0..n-1 (io.hpp:236-238). */
+int dgs_load_splats_ply(const char* path, dgs_splats* out, int64_t* n_out, int32_t* sh_coeffs_out) {
+    return dgs_guard([&] {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw std::runtime_error(std::string("load_ply: cannot open ") + path);
+        std::string line;
+        std::getline(in, line);
+        if (line != "ply") throw std::runtime_error("ply: missing magic");
+        bool binary = false, in_vertex = false;
+        int64_t count = -1;
+        std::vector<std::string> props;
+        while (std::getline(in, line)) {
+            std::istringstream ls(line);
+            std::string w;
+            ls >> w;
+            if (w == "format") {
+                std::string fmt;
+                ls >> fmt;
+                if (fmt == "binary_little_endian") binary = true;
+                else if (fmt != "ascii") throw std::runtime_error("ply: unsupported format " + fmt);
+            } else if (w == "element") {
+                std::string name;
+                ls >> name >> count;
+                in_vertex = name == "vertex";
+                if (!in_vertex) throw std::runtime_error("ply: only a vertex element is supported here");
+            } else if (w == "property" && in_vertex) {
+                std::string type, name;
+                ls >> type >> name;
+                if (type != "float" && type != "float32") throw std::runtime_error("ply: float32 properties only");
+                props.push_back(name);
+            } else if (w == "end_header") {
+                break;
+            }
+        }
+        if (count < 0) throw std::runtime_error("ply: no vertex element");
+        auto index_of = [&](const std::string& nme) {
+            for (size_t q = 0; q < props.size(); ++q)
+                if (props[q] == nme) return int(q);
+            return -1;
+        };
+        size_t rest = 0;
+        while (index_of("f_rest_" + std::to_string(rest)) >= 0) ++rest;
+        int degree = -1;
+        for (int d = 0; d <= 3; ++d)
+            if (rest == size_t(3 * ((d + 1) * (d + 1) - 1))) degree = d;
+        if (degree < 0) throw std::runtime_error("ply: f_rest count does not match any SH degree <= 3");
+        const int n_coeff = (degree + 1) * (degree + 1);
+        if (n_out) *n_out = count;
+        if (sh_coeffs_out) *sh_coeffs_out = n_coeff;
+        if (!out) return;
+        if (out->n < count || out->sh_coeffs != n_coeff) throw std::invalid_argument("load_ply: output too small");
+        const int ix = index_of("x"), iy = index_of("y"), iz = index_of("z"), iop = index_of("opacity");
+        int isc[3], irt[4], idc[3];
+        for (int a = 0; a < 3; ++a) isc[a] = index_of("scale_" + std::to_string(a));
+        for (int a = 0; a < 4; ++a) irt[a] = index_of("rot_" + std::to_string(a));
+        for (int a = 0; a < 3; ++a) idc[a] = index_of("f_dc_" + std::to_string(a));
+        if (ix < 0 || iy < 0 || iz < 0) throw std::runtime_error("ply: vertex element lacks x/y/z");
+        if (iop < 0 || isc[2] < 0 || irt[3] < 0 || idc[2] < 0)
+            throw std::runtime_error("ply: incomplete splat property set");
+        std::vector<float> row(props.size());
+        for (int64_t i = 0; i < count; ++i) {
+            if (binary) {
+                in.read(reinterpret_cast<char*>(row.data()), std::streamsize(row.size() * sizeof(float)));
+            } else {
+                for (auto& v : row) in >> v;
+            }
+            if (!in) throw std::runtime_error("ply: truncated vertex data");
+            if (out->id) out->id[i] = (uint64_t)i;
+            out->mu[3 * i] = row[ix];
+            out->mu[3 * i + 1] = row[iy];
+            out->mu[3 * i + 2] = row[iz];
+            for (int a = 0; a < 3; ++a) out->log_scale[3 * i + a] = row[isc[a]];
+            for (int a = 0; a < 4; ++a) out->rotation[4 * i + a] = row[irt[a]];
+            out->opacity_logit[i] = row[iop];
+            for (int a = 0; a < 3; ++a) out->sh[(i * n_coeff) * 3 + a] = row[idc[a]];
+            for (int c = 1; c < n_coeff; ++c)
+                for (int a = 0; a < 3; ++a)
+                    out->sh[(i * n_coeff + c) * 3 + a] =
+                        row[index_of("f_rest_" + std::to_string(size_t(a) * (n_coeff - 1) + (c - 1)))];
         }
     });
 }

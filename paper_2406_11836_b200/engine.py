@@ -120,6 +120,22 @@ def ring_camera(width: int, height: int, i: int, n_views: int = 64, fov_deg: flo
     return cam
 
 
+def save_splats_ply(splats: Splats, path: str, binary: bool = True) -> None:
+    """io.hpp:257-297 (3DGS property convention, float32)."""
+    sc = splats.c()
+    check(lib().dgs_save_splats_ply(C.byref(sc), str(path).encode(), int(binary)))
+
+
+def load_splats_ply(path: str) -> Splats:
+    """load_ply's splat mode (io.hpp:85-255); ids 0..n-1."""
+    n, shc = C.c_int64(), C.c_int32()
+    check(lib().dgs_load_splats_ply(str(path).encode(), None, C.byref(n), C.byref(shc)))
+    out = Splats.empty(int(n.value), int(shc.value))
+    oc = out.c()
+    check(lib().dgs_load_splats_ply(str(path).encode(), C.byref(oc), None, None))
+    return out
+
+
 def init_from_pointcloud(ctx: "Context", points: np.ndarray, colors: np.ndarray | None, target_count: int,
                          seed: int, sh_degree: int = 3) -> Splats:
     """trainer.hpp:24-91 init_from_pointcloud; the 3-nearest-neighbour term runs
@@ -487,6 +503,12 @@ class Manager:
                     getattr(out, f)[j] = getattr(src, f)[i]
             return out
         return gather(0), gather(1), gather(2), parts[0][3]
+
+    def checkpoint(self, path: str) -> None:
+        """snapshot(checkpoint_path) (manager.hpp:390-396): the merged splats as a
+        3DGS PLY (Adam moments are not part of the file format)."""
+        p, _, _, _ = self.snapshot()
+        save_splats_ply(p, path)
 
     def repartition(self, device: bool = True):
         """Manager::repartition (manager.hpp:421-430).  device=True (default):

@@ -37,6 +37,7 @@ INIT_SETS = {
     # target > points: uniform picks with replacement + 1e-3 * bbox-diagonal jitter
     "g6_init_pc_oversample": dict(points=1500, target=5000, seed=29, sh_degree=1, cloud_seed=6),
 }
+PLY_SETS = {"g3_random_kd0_oracle"}
 DUMPS = ["save_scene", "dump_table", "dump_orders", "dump_project", "dump_partials", "contributors", "dump_render",
          "dump_step", "dump_g2d"]
 
@@ -45,6 +46,8 @@ def run(name, args, out):
     tmp = out / "_npy"
     tmp.mkdir()
     argv = [str(REF)] + [f"{k}={v}" for k, v in args.items()] + DUMPS + [f"out={tmp}"]
+    if name in PLY_SETS:  # the reference's save_splats_ply of the (perturbed) scene, io.hpp:257-297
+        argv.append(f"save_ply={out / 'scene_perturbed.ply'}")
     subprocess.run(argv, check=True)
     arrays = {f.stem: np.load(f) for f in sorted(tmp.glob("*.npy"))}
     np.savez_compressed(out / "golden.npz", **arrays)
