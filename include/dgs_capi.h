@@ -149,6 +149,21 @@ int dgs_perturb_splats(dgs_splats* s, uint64_t seed);
  * made by dgs_nccl_unique_id on rank 0 and shared by the caller. */
 int dgs_nccl_unique_id(void* out128);
 int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl_id, dgs_ctx** out);
+/* Test transport for the multi-rank step: the exchanges and the loss
+ * all-reduce go through host callbacks instead of NCCL (NCCL refuses two
+ * ranks on one device; tests run two processes on one GPU over
+ * torch.distributed gloo).  send() must not block; flush() completes every
+ * send and receive posted since the last flush.  Callbacks return 0 on
+ * success. */
+typedef struct dgs_host_transport {
+    void* user;
+    int (*send)(void* user, const void* buf, uint64_t bytes, int32_t peer);
+    int (*recv)(void* user, void* buf, uint64_t bytes, int32_t peer);
+    int (*flush)(void* user);
+    int (*allreduce_sum_f64)(void* user, double* buf, uint64_t n);
+} dgs_host_transport;
+int dgs_ctx_create_host_transport(int32_t device, int32_t rank, int32_t world, const dgs_host_transport* transport,
+                                  dgs_ctx** out);
 int dgs_ctx_destroy(dgs_ctx* ctx);
 /* The full partition table (every rank knows every subspace). */
 int dgs_set_table(dgs_ctx* ctx, const dgs_plane* planes, int32_t k_count, int32_t planes_per_subset);

@@ -71,6 +71,18 @@ class SplatsC(C.Structure):
                 ("sh", C.POINTER(C.c_float))]
 
 
+XFER_SEND = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32)
+XFER_RECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32)
+XFER_FLUSH = C.CFUNCTYPE(C.c_int, C.c_void_p)
+XFER_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_uint64)
+
+
+class HostTransportC(C.Structure):
+    """dgs_host_transport: test transport of the multi-rank step."""
+    _fields_ = [("user", C.c_void_p), ("send", XFER_SEND), ("recv", XFER_RECV), ("flush", XFER_FLUSH),
+                ("allreduce_sum_f64", XFER_ALLREDUCE)]
+
+
 class StepResult(C.Structure):
     _fields_ = [("loss", C.c_double), ("psnr", C.c_double), ("comm_bytes", C.c_uint64), ("nccl_bytes", C.c_uint64),
                 ("pairs", C.c_uint64), ("evals_fwd", C.c_uint64), ("contribs_fwd", C.c_uint64),
@@ -99,6 +111,8 @@ _SIGS = {
     "dgs_perturb_splats": (C.c_int, [C.POINTER(SplatsC), C.c_uint64]),
     "dgs_nccl_unique_id": (C.c_int, [_P]),
     "dgs_ctx_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
+    "dgs_ctx_create_host_transport": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(HostTransportC),
+                                              C.POINTER(_P)]),
     "dgs_ctx_destroy": (C.c_int, [_P]),
     "dgs_set_table": (C.c_int, [_P, C.POINTER(Plane), C.c_int32, C.c_int32]),
     "dgs_set_options": (C.c_int, [_P, C.POINTER(RenderOptionsC), C.POINTER(TrainConfigC)]),

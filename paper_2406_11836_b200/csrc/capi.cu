@@ -207,6 +207,8 @@ struct HostScalars {
 
 struct Ctx {
     int device = 0, rank = 0, world = 1;
+    bool host_xfer = false;        // exchange through host callbacks instead of NCCL (tests)
+    dgs_host_transport xfer_cb{};
     HostScalars* hs = nullptr;  // cudaHostAlloc'd
     StageTimer timer;
     cudaStream_t stream = nullptr;
@@ -509,6 +511,52 @@ SliceRows slice_rows(int H, int S, int s) {
 /// Rank that owns KD subset k (contiguous blocks of subsets per rank).
 int subset_owner(int k, int K, int W) { return (int)((int64_t)k * W / K); }
 
+/// One grouped point-to-point exchange of a multi-rank context: NCCL
+/// (production; one ncclGroup) or the host callbacks of a test transport
+/// (device rows staged through host memory; the callbacks must post sends
+/// without blocking, flush() completes every posted send and receive).
+class Xfer {
+  public:
+    explicit Xfer(Ctx& ctx) : ctx_(ctx) {
+        if (ctx_.host_xfer) CK(cudaStreamSynchronize(ctx_.stream));
+        else NK(nccl().GroupStart());
+    }
+    void send(const float* dev, size_t floats, int peer) {
+        if (!ctx_.host_xfer) {
+            NK(nccl().Send(dev, floats, ncclFloat, peer, ctx_.comm, ctx_.stream));
+            return;
+        }
+        stage_.emplace_back(floats);
+        CK(cudaMemcpy(stage_.back().data(), dev, floats * 4, cudaMemcpyDeviceToHost));
+        if (ctx_.xfer_cb.send(ctx_.xfer_cb.user, stage_.back().data(), floats * 4, peer))
+            throw std::runtime_error("host transport: send failed");
+    }
+    void recv(float* dev, size_t floats, int peer) {
+        if (!ctx_.host_xfer) {
+            NK(nccl().Recv(dev, floats, ncclFloat, peer, ctx_.comm, ctx_.stream));
+            return;
+        }
+        stage_.emplace_back(floats);
+        if (ctx_.xfer_cb.recv(ctx_.xfer_cb.user, stage_.back().data(), floats * 4, peer))
+            throw std::runtime_error("host transport: recv failed");
+        pending_.push_back({dev, stage_.size() - 1});
+    }
+    void finish() {
+        if (!ctx_.host_xfer) {
+            NK(nccl().GroupEnd());
+            return;
+        }
+        if (ctx_.xfer_cb.flush(ctx_.xfer_cb.user)) throw std::runtime_error("host transport: flush failed");
+        for (const auto& p : pending_)
+            CK(cudaMemcpy(p.first, stage_[p.second].data(), stage_[p.second].size() * 4, cudaMemcpyHostToDevice));
+    }
+
+  private:
+    Ctx& ctx_;
+    std::vector<std::vector<float>> stage_;
+    std::vector<std::pair<float*, size_t>> pending_;
+};
+
 /// Forward exchange for slice `sl`: rows [h0, h1) of every subset's partial
 /// map land in ctx.xrecv[k].  Multi-rank: one NCCL group of send/recv (the
 /// all-to-all of manager.hpp:280-293's gather, sliced); single rank
@@ -520,23 +568,23 @@ uint64_t exchange_forward(Ctx& ctx, int v, const std::vector<int>& local, int Wd
     const size_t hr = (size_t)(me.h1 - me.h0);
     uint64_t sent = 0;
     if (W > 1) {
-        NK(nccl().GroupStart());
+        Xfer x(ctx);
         for (int k : local) {
             const float4* src = subset(ctx, k).slot(v).ct.p;
             for (int j = 0; j < W; ++j) {
                 if (j == rank) continue;
                 const SliceRows R = slice_rows(H, S, j);
                 const size_t cnt = (size_t)(R.h1 - R.h0) * Wd * 4;
-                NK(nccl().Send(src + (size_t)R.h0 * Wd, cnt, ncclFloat, j, ctx.comm, ctx.stream));
+                x.send(reinterpret_cast<const float*>(src + (size_t)R.h0 * Wd), cnt, j);
                 sent += cnt * 4;
             }
         }
         for (int k = 0; k < K; ++k) {
             const int o = subset_owner(k, K, W);
             if (o == rank) continue;
-            NK(nccl().Recv(ctx.xrecv.p + (size_t)k * hr * Wd, hr * Wd * 4, ncclFloat, o, ctx.comm, ctx.stream));
+            x.recv(reinterpret_cast<float*>(ctx.xrecv.p + (size_t)k * hr * Wd), hr * Wd * 4, o);
         }
-        NK(nccl().GroupEnd());
+        x.finish();
     }
     for (int k : local)  // own subsets: local copy
         CK(cudaMemcpyAsync(ctx.xrecv.p + (size_t)k * hr * Wd, subset(ctx, k).slot(v).ct.p + (size_t)me.h0 * Wd,
@@ -553,11 +601,11 @@ uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int W
     const size_t orows = (size_t)(me.r1 - me.r0);
     uint64_t sent = 0;
     if (W > 1) {
-        NK(nccl().GroupStart());
+        Xfer x(ctx);
         for (int k = 0; k < K; ++k) {
             const int o = subset_owner(k, K, W);
             if (o == rank) continue;
-            NK(nccl().Send(ctx.xgrad.p + (size_t)k * orows * Wd, orows * Wd * 4, ncclFloat, o, ctx.comm, ctx.stream));
+            x.send(reinterpret_cast<const float*>(ctx.xgrad.p + (size_t)k * orows * Wd), orows * Wd * 4, o);
             sent += orows * Wd * 16;
         }
         for (int k : local) {
@@ -565,11 +613,10 @@ uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int W
             for (int j = 0; j < W; ++j) {
                 if (j == rank) continue;
                 const SliceRows R = slice_rows(H, S, j);
-                NK(nccl().Recv(dst + (size_t)R.r0 * Wd, (size_t)(R.r1 - R.r0) * Wd * 4, ncclFloat, j, ctx.comm,
-                               ctx.stream));
+                x.recv(reinterpret_cast<float*>(dst + (size_t)R.r0 * Wd), (size_t)(R.r1 - R.r0) * Wd * 4, j);
             }
         }
-        NK(nccl().GroupEnd());
+        x.finish();
     }
     for (int k : local)
         CK(cudaMemcpyAsync(subset(ctx, k).slot(v).grad_ct.p + (size_t)me.r0 * Wd, ctx.xgrad.p + (size_t)k * orows * Wd,
@@ -675,6 +722,20 @@ int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl
         c->ro = to_render_opts(c->ro_in);
         c->stats.ensure(2);  // [0] forward blend, [1] backward blend
         *out = c.release();
+    });
+}
+
+int dgs_ctx_create_host_transport(int32_t device, int32_t rank, int32_t world, const dgs_host_transport* t,
+                                  dgs_ctx** out) {
+    return dgs_guard([&] {
+        if (!t || !t->send || !t->recv || !t->flush || !t->allreduce_sum_f64)
+            throw std::invalid_argument("dgs_ctx_create_host_transport: incomplete callbacks");
+        if (dgs_ctx_create(device, 0, 1, nullptr, out) != 0) throw std::runtime_error(g_last_error);
+        (*out)->rank = rank;
+        (*out)->world = world;
+        (*out)->host_xfer = true;
+        (*out)->xfer_cb = *t;
+        if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("dgs_ctx_create: bad rank/world");
     });
 }
 
@@ -1756,7 +1817,12 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             for (int v = 0; v < batch; ++v)
                 for (int q = 0; q < 3; ++q) mine[(size_t)3 * (v * S + rank) + q] = sums[(size_t)3 * (v * S + rank) + q];
             CK(cudaMemcpyAsync(ctx->sums.p, mine.data(), mine.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-            {
+            if (ctx->host_xfer) {
+                if (ctx->xfer_cb.allreduce_sum_f64(ctx->xfer_cb.user, mine.data(), mine.size()))
+                    throw std::runtime_error("host transport: allreduce failed");
+                CK(cudaMemcpyAsync(ctx->sums.p, mine.data(), mine.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+                CK(cudaStreamSynchronize(ctx->stream));
+            } else {
                 Stage st(ctx->timer, kStExchange, ctx->stream);
                 NK(nccl().AllReduce(ctx->sums.p, ctx->sums.p, mine.size(), ncclDouble, ncclSum, ctx->comm, ctx->stream));
             }

@@ -240,10 +240,24 @@ def assign_subsets(table: PartitionTable, splats: Splats, d_multiplier: float = 
 class Context:
     """One dgs_ctx (one GPU / rank).  Owns subset state in HBM."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 transport=None):
+        """transport: an object with send/recv/flush/allreduce methods (e.g.
+        tests/host_transport.py) replacing NCCL for the multi-rank exchange."""
         self._h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        check(lib().dgs_ctx_create(device, rank, world, idbuf, C.byref(self._h)))
+        self._transport = None
+        if transport is not None:
+            t = capi.HostTransportC()
+            t.user = None
+            t.send = capi.XFER_SEND(transport.send)
+            t.recv = capi.XFER_RECV(transport.recv)
+            t.flush = capi.XFER_FLUSH(transport.flush)
+            t.allreduce_sum_f64 = capi.XFER_ALLREDUCE(transport.allreduce)
+            self._transport = (transport, t)  # keep the callbacks alive
+            check(lib().dgs_ctx_create_host_transport(device, rank, world, C.byref(t), C.byref(self._h)))
+        else:
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            check(lib().dgs_ctx_create(device, rank, world, idbuf, C.byref(self._h)))
         self.table: PartitionTable | None = None
 
     def close(self):
@@ -439,7 +453,7 @@ class Manager:
 
     def __init__(self, splats: Splats, config: capi.TrainConfigC | None = None,
                  options: capi.RenderOptionsC | None = None, device: int = 0, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, transport=None):
         """world > 1: one Manager per rank (one process per GPU).  Every rank
         builds the same KD table on the host (bit-exact, deterministic) and
         loads only the subsets it owns (`subset_owner`, contiguous blocks);
@@ -448,10 +462,10 @@ class Manager:
         0, broadcast by the caller)."""
         self.config = config if config is not None else train_config()
         self.options = options if options is not None else render_options()
-        if world > 1 and nccl_id is None:
+        if world > 1 and nccl_id is None and transport is None:
             raise ValueError("Manager: world > 1 needs the NCCL unique id of rank 0")
         self.rank, self.world = rank, world
-        self.ctx = Context(device, rank, world, nccl_id)
+        self.ctx = Context(device, rank, world, nccl_id, transport)
         self.sh_coeffs = splats.sh_coeffs
         self.ids = np.sort(splats.id.copy())
         self._distribute(splats, epoch=0)

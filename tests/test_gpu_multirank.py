@@ -1,0 +1,76 @@
+"""GPU: the real multi-rank step (world = 2 or 4 dgs contexts in as many
+processes on one B200, contiguous blocks of the 8 KD subsets per rank; row slices with the
+10-row SSIM halo; forward all-to-all of partial rows, backward return of
+(dL/dC_k, dL/dT_k), all-reduced loss sums).  The transport is the C-ABI's test
+transport over gloo (NCCL refuses two ranks on one device), so everything of
+the N > 1 path runs except the NCCL calls themselves.  It must reproduce the
+single-rank virtual-slice run bit for bit: the loss and every subset's
+gradient map."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+NAME = "g4_synth_kd3_bg"
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from conftest import Golden
+        from host_transport import GlooTransport
+        from paper_2406_11836_b200 import engine
+        g = Golden(NAME)
+        s = g.splats()
+        cfg = engine.train_config(kd_depth=g.args["kd"])
+        mgr = engine.Manager(s, cfg, engine.render_options(oracle=g.oracle_mode), device=0, rank=rank, world=world,
+                             transport=GlooTransport())
+        cam = g.camera()
+        res = mgr.train_step([cam], g["step_target"][None], g.bg)
+        K = mgr.table.subset_count
+        maps = {}
+        for k in range(K):
+            if engine.subset_owner(k, K, world) == rank:
+                ct, gr = mgr.ctx.dump_grad_maps(k, 0, cam)
+                maps[f"ct{k}"], maps[f"gr{k}"] = ct, gr
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), loss=np.array([res["loss"]]),
+                 nccl_bytes=np.array([res["nccl_bytes"]]), **maps)
+        mgr.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_step_matches_single_rank_virtual_slices(tmp_path, world):
+    from conftest import Golden
+    from paper_2406_11836_b200 import engine
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    g = Golden(NAME)
+    s = g.splats()
+    cam = g.camera()
+    mgr = engine.Manager(s, engine.train_config(kd_depth=g.args["kd"]), engine.render_options(oracle=g.oracle_mode))
+    mgr.ctx.set_virtual_slices(world)
+    ref = mgr.train_step([cam], g["step_target"][None], g.bg)
+    K = mgr.table.subset_count
+    got = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    for r in range(world):
+        assert got[r]["loss"][0] == ref["loss"], (r, got[r]["loss"][0], ref["loss"])
+        assert got[r]["nccl_bytes"][0] > 0
+    for k in range(K):
+        r = engine.subset_owner(k, K, world)
+        ct, gr = mgr.ctx.dump_grad_maps(k, 0, cam)
+        np.testing.assert_array_equal(got[r][f"ct{k}"], ct, err_msg=f"partial map of subset {k}")
+        np.testing.assert_array_equal(got[r][f"gr{k}"], gr, err_msg=f"gradient map of subset {k}")
+    mgr.close()
