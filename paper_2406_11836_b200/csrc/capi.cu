@@ -104,6 +104,7 @@ struct ViewSlot {
     DevBuf<float> shjac;       // [10][ld] SH colour Jacobian + clamp mask (ViewBins::shjac)
     DevBuf<uint16_t> rec_cnt;
     DevBuf<uint8_t> rec_replay;
+    bool rec_valid = false;  // the last forward of this slot wrote records
     CompRecords crec() const {
         CompRecords r;
         r.pos = rec_pos.p;
@@ -399,13 +400,25 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     if (n <= 0) CK(cudaStreamSynchronize(ctx.stream));  // run_binning synced otherwise
     if (ctx.hs->err != INT_MAX) throw std::domain_error("zero quaternion");
     vb.visible = n > 0 ? ctx.hs->visible : 0;
-    if (ctx.records) {
+    // Composite records need tiles x 256 x kRecCap x 2 bytes per (subset, view)
+    // slot (1.07 GB at 1080p, 4.2 GB at 4K).  A slot whose records would take
+    // more than a quarter of the free HBM falls back to the ring-replay
+    // backward (same results, slower) instead of failing the allocation.
+    bool use_rec = ctx.records;
+    if (use_rec && !vs.rec_pos.p) {
+        const size_t need = (size_t)tiles * kRecCap * kBlendThreads * sizeof(uint16_t) + px * 2 + tiles;
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        use_rec = need <= free_b / 4;
+    }
+    if (use_rec) {
         vs.rec_pos.ensure((size_t)tiles * kRecCap * kBlendThreads);
         vs.rec_cnt.ensure(px);
         vs.rec_replay.ensure(tiles);
     }
+    vs.rec_valid = use_rec;
     CompRecords crec;
-    if (ctx.records) crec = vs.crec();
+    if (use_rec) crec = vs.crec();
     Stage st_fwd(ctx.timer, kStFwd, ctx.stream);
     launch_blend_fwd(vp, ctx.ro, ctx.table.sub[S.k], vb, vs.ct.p, vs.ovf_flag.p, vs.ovf_list.p, vs.ovf_count.p,
                      dbg_ids, dbg_cnt, dbg_cap, stats, vs.cd.p, crec, ctx.stream);
@@ -427,7 +440,7 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
     Stage st(ctx.timer, kStBwd, ctx.stream);
     CompRecords crec;
-    if (ctx.records && vs.rec_pos.p) crec = vs.crec();
+    if (ctx.records && vs.rec_valid) crec = vs.crec();
     launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, crec,
                      S.g2d.p, S.ld, stats, ctx.stream);
     ++ctx.launches;
