@@ -30,6 +30,19 @@ __global__ void k_key24(const uint32_t* __restrict__ rkey, const uint32_t* __res
     vals[i] = (uint32_t)i;
 }
 
+/// Members in range order: their tile rectangle and tile count (the count is
+/// derived from the rectangle; culled members carry an empty one).  One random
+/// 8-byte gather per member; the scan and the emission then stream.
+__global__ void k_gather_sorted_rects(const uint32_t* __restrict__ sorted_idx, const uint2* __restrict__ rect,
+                                      uint2* __restrict__ rect_sorted, uint32_t* __restrict__ cnt_sorted, int n) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint2 r = rect[sorted_idx[j]];
+    const uint32_t x0 = r.x & 0xffffu, x1 = r.x >> 16, y0 = r.y & 0xffffu, y1 = r.y >> 16;
+    rect_sorted[j] = r;
+    cnt_sorted[j] = (x1 >= x0 && y1 >= y0) ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
+}
+
 __global__ void k_gather_counts(const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ counts,
                                 uint32_t* __restrict__ out, int n) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -41,20 +54,20 @@ __global__ void k_gather_counts(const uint32_t* __restrict__ sorted_idx, const u
 /// of that run, finding its member by a search over the warp's prefix sums,
 /// so every store instruction writes 32 consecutive words.
 __global__ void k_emit_pairs(const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ offsets,
-                             const uint32_t* __restrict__ counts, const uint32_t* __restrict__ rect, int tiles_x,
-                             int n, uint16_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_val) {
+                             const uint32_t* __restrict__ cnt_sorted, const uint2* __restrict__ rect_sorted,
+                             int tiles_x, int n, uint16_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_val) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint32_t i = 0, c = 0, off = 0, x0 = 0, w = 1, y0 = 0;
     if (j < n) {
         i = sorted_idx[j];
-        c = counts[i];
+        c = cnt_sorted[j];
         off = offsets[j];
         if (c) {
-            const uint32_t rx = rect[2 * (size_t)i], ry = rect[2 * (size_t)i + 1];
-            x0 = rx & 0xffff;
-            w = (rx >> 16) - x0 + 1;
-            y0 = ry & 0xffff;
+            const uint2 r = rect_sorted[j];
+            x0 = r.x & 0xffff;
+            w = (r.x >> 16) - x0 + 1;
+            y0 = r.y & 0xffff;
         }
     }
     // inclusive prefix of counts within the warp
@@ -158,13 +171,17 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
     cub::DeviceRadixSort::SortPairs(nullptr, b, dk, dv, (int)pair_cap, 0, 16);
     cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it((const uint32_t*)nullptr, CountOf{nullptr});
     cub::DeviceScan::InclusiveSum(nullptr, c, it, (uint32_t*)nullptr, n);
+    size_t c2 = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, c2, (const uint32_t*)nullptr, (uint32_t*)nullptr, n);
+    c = c > c2 ? c : c2;
     size_t m = a > b ? a : b;
     return (m > c ? m : c) + 256;
 }
 
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
                     uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
-                    uint32_t* pair_val_alt, uint32_t* scan_buf, uint32_t* pairs_host, cudaStream_t s) {
+                    uint32_t* pair_val_alt, uint32_t* scan_buf, uint2* rect_sorted, uint32_t* pairs_host,
+                    cudaStream_t s) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     cudaMemsetAsync(vb.ranges, 0, sizeof(uint2) * tiles, s);
     vb.pairs = 0;
@@ -182,9 +199,11 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     }
     // 2) tile counts in range order -> inclusive scan -> pair end offsets
     //    (the gather is fused into the scan through a transform iterator)
-    cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> cnt_it(sort_vals_alt, CountOf{vb.counts});
+    uint32_t* cnt_sorted = sort_keys_alt;  // the sorted keys are not needed after the sort
+    k_gather_sorted_rects<<<grid, blk, 0, s>>>(sort_vals_alt, reinterpret_cast<const uint2*>(vb.rect), rect_sorted,
+                                               cnt_sorted, n);
     tb = temp_bytes;
-    cub::DeviceScan::InclusiveSum(temp, tb, cnt_it, scan_buf, n, s);
+    cub::DeviceScan::InclusiveSum(temp, tb, cnt_sorted, scan_buf, n, s);
     // the one host round trip of the step's forward: the pair count sizes the
     // tile sort (pinned readback; the caller's pending readbacks ride along)
     cudaMemcpyAsync(pairs_host, scan_buf + (n - 1), 4, cudaMemcpyDeviceToHost, s);
@@ -194,7 +213,7 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     vb.pairs = P;
     if (P == 0) return 0;
     // 3) emit (tile, member) pairs, range-ordered within every tile
-    k_emit_pairs<<<grid, blk, 0, s>>>(sort_vals_alt, scan_buf, vb.counts, vb.rect, vp.tiles_x, n, vb.pair_tile,
+    k_emit_pairs<<<grid, blk, 0, s>>>(sort_vals_alt, scan_buf, cnt_sorted, rect_sorted, vp.tiles_x, n, vb.pair_tile,
                                       vb.pair_val);  // scan_buf holds inclusive ends: start = end - count
     // 4) stable LSD radix sort by tile id only
     cub::DoubleBuffer<uint16_t> dk(vb.pair_tile, pair_tile_alt);

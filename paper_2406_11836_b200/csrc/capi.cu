@@ -94,6 +94,7 @@ struct ViewSlot {
     DevBuf<uint32_t> rect, counts, rkey, dmax, pair_val, pair_val_alt;
     DevBuf<uint16_t> pair_tile, pair_tile_alt;
     DevBuf<float2> ext;
+    DevBuf<uint2> rect_sorted;
     DevBuf<uint32_t> sort_keys_alt, sort_vals, sort_vals_alt, scan, ovf_list, ovf_count;
     DevBuf<int> err;
     DevBuf<uint2> ranges;
@@ -385,14 +386,14 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     Stage st_bin(ctx.timer, kStBin, ctx.stream);
     int64_t P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p,
                             vs.sort_vals.p, vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p,
-                            &ctx.hs->pairs, ctx.stream);
+                            vs.rect_sorted.ensure(n), &ctx.hs->pairs, ctx.stream);
     ctx.launches += 3;
     if (P < 0) {
         vs.pair_cap = (-P) + (-P) / 4 + 1024;
         alloc_pairs();
         P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
-                        vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, &ctx.hs->pairs,
-                        ctx.stream);
+                        vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, vs.rect_sorted.p,
+                        &ctx.hs->pairs, ctx.stream);
         ctx.launches += 3;
         if (P < 0) throw std::runtime_error("binning: pair buffer sizing failed");
     }

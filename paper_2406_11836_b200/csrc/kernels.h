@@ -40,7 +40,8 @@ size_t binning_temp_bytes(int n, int64_t pair_cap);
 // pair buffer capacity; returns -needed if it is too small.
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
                     uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
-                    uint32_t* pair_val_alt, uint32_t* scan_buf, uint32_t* pairs_host, cudaStream_t s);
+                    uint32_t* pair_val_alt, uint32_t* scan_buf, uint2* rect_sorted, uint32_t* pairs_host,
+                    cudaStream_t s);
 
 struct BlendStats {
     unsigned long long evals;      // (pixel, candidate) 2D evaluations

@@ -204,6 +204,9 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
         }
         if (!visible) {
             vb.counts[i] = 0;
+            // empty tile rectangle (x0 > x1): the binning derives counts from rect alone
+            vb.rect[2 * (size_t)i] = 0x0000ffffu;
+            vb.rect[2 * (size_t)i + 1] = 0x0000ffffu;
             vb.rkey[i] = 0xffffffffu;
         }
     }
