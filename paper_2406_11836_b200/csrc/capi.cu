@@ -638,6 +638,192 @@ uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int W
     return sent;
 }
 
+/// build_kdtree (partition.hpp:93-184) on device-resident centres (rows 0-2
+/// of C, leading dimension ldc): per level, node extents, the widest axis,
+/// exact medians from radix-sorted (node, coordinate) keys and the split.
+/// Deterministic: every rank that runs it on the same centres gets the same
+/// planes (KD leaves in DFS order, `depth` planes each).
+std::vector<dgs_plane> kd_build_device(Ctx& ctx, const float* C, size_t ldc, int N, int depth) {
+    cudaStream_t s = ctx.stream;
+    DevBuf<uint64_t> keys, keys_alt;
+    DevBuf<uint8_t> temp;
+    keys.ensure(N);
+    keys_alt.ensure(N);
+    const size_t tb = repart_temp_bytes(N);
+    temp.ensure(tb);
+    struct HostRegion {
+        std::vector<dgs_plane> planes;
+        float amin[3], amax[3];
+    };
+    std::vector<HostRegion> regions(1);
+    for (int a = 0; a < 3; ++a) {
+        regions[0].amin[a] = -INFINITY;
+        regions[0].amax[a] = INFINITY;
+    }
+    DevBuf<uint8_t> node;
+    node.ensure(N);
+    CK(cudaMemsetAsync(node.p, 0, N, s));
+    DevBuf<uint32_t> lo, hi, cnt;
+    DevBuf<int> d_axis;
+    DevBuf<float> d_plane;
+    const int maxn = 1 << depth;
+    lo.ensure(3 * maxn);
+    hi.ensure(3 * maxn);
+    cnt.ensure(maxn);
+    d_axis.ensure(maxn);
+    d_plane.ensure(maxn);
+    auto from_order = [](uint32_t o) {
+        const uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+        float f;
+        std::memcpy(&f, &b, 4);
+        return f;
+    };
+    for (int d = 0; d < depth; ++d) {
+        const int nn = 1 << d;
+        std::vector<uint32_t> h_lo(3 * nn, 0xffffffffu), h_hi(3 * nn, 0u), h_cnt(nn, 0u);
+        CK(cudaMemcpyAsync(lo.p, h_lo.data(), 12 * nn, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(hi.p, h_hi.data(), 12 * nn, cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(cnt.p, 0, 4 * nn, s));
+        repart_node_extent(N, C, ldc, node.p, nn, lo.p, hi.p, cnt.p, s);
+        CK(cudaMemcpyAsync(h_lo.data(), lo.p, 12 * nn, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_hi.data(), hi.p, 12 * nn, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_cnt.data(), cnt.p, 4 * nn, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (d == 0) {  // build_kdtree's degenerate-set check (partition.hpp:164-171)
+            float m = from_order(h_hi[0]) - from_order(h_lo[0]);
+            for (int a = 1; a < 3; ++a) m = std::max(m, from_order(h_hi[a]) - from_order(h_lo[a]));
+            if (m <= 0.0f) throw std::invalid_argument("degenerate point set");
+        }
+        std::vector<int> axis(nn, 0);
+        for (int q = 0; q < nn; ++q) {
+            if (!h_cnt[q]) continue;
+            float ext[3];
+            for (int a = 0; a < 3; ++a) ext[a] = from_order(h_hi[3 * q + a]) - from_order(h_lo[3 * q + a]);
+            float m = ext[0];  // maxCoeff(&axis): first maximum
+            for (int a = 1; a < 3; ++a)
+                if (ext[a] > m) {
+                    m = ext[a];
+                    axis[q] = a;
+                }
+        }
+        CK(cudaMemcpyAsync(d_axis.p, axis.data(), 4 * nn, cudaMemcpyHostToDevice, s));
+        // exact medians: sort (node, coordinate) keys, read the two middle values of every node
+        repart_node_keys(N, C, ldc, node.p, d_axis.p, keys.p, s);
+        uint64_t* k1 = keys.p;
+        uint64_t* k2 = keys_alt.p;
+        repart_sort_keys(k1, k2, N, 32 + d + 1, temp.p, tb, s);
+        std::vector<float> plane(nn, 0.0f);
+        std::vector<uint64_t> mid(2);
+        uint32_t start = 0;
+        for (int q = 0; q < nn; ++q) {
+            const uint32_t c = h_cnt[q];
+            HostRegion& reg = regions[q];
+            if (c > 0) {
+                const uint32_t i1 = start + c / 2;
+                const uint32_t i0 = c % 2 == 0 ? i1 - 1 : i1;
+                CK(cudaMemcpyAsync(&mid[0], k1 + i0, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(&mid[1], k1 + i1, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                const float lower = from_order((uint32_t)mid[0]), upper = from_order((uint32_t)mid[1]);
+                plane[q] = c % 2 == 0 ? (lower + upper) / 2.0f : upper;
+            } else {
+                const int a = axis[q];
+                const float l = reg.amin[a], h = reg.amax[a];
+                plane[q] = (std::isfinite(l) && std::isfinite(h)) ? (l + h) / 2.0f
+                           : std::isfinite(l)                    ? l + 1.0f
+                           : std::isfinite(h)                    ? h - 1.0f
+                                                                 : 0.0f;
+            }
+            start += c;
+        }
+        CK(cudaMemcpyAsync(d_plane.p, plane.data(), 4 * nn, cudaMemcpyHostToDevice, s));
+        repart_node_split(N, C, ldc, node.p, d_axis.p, d_plane.p, s);
+        std::vector<HostRegion> next(2 * nn);
+        for (int q = 0; q < nn; ++q) {
+            const int a = axis[q];
+            HostRegion left = regions[q], right = regions[q];
+            dgs_plane lp{};
+            lp.n[a] = 1.0f;
+            lp.d = -plane[q];
+            lp.closed = 0;
+            left.planes.push_back(lp);
+            left.amax[a] = std::min(left.amax[a], plane[q]);
+            dgs_plane rp{};
+            rp.n[a] = -1.0f;
+            rp.d = plane[q];
+            rp.closed = 1;
+            right.planes.push_back(rp);
+            right.amin[a] = std::max(right.amin[a], plane[q]);
+            next[2 * q] = std::move(left);
+            next[2 * q + 1] = std::move(right);
+        }
+        regions = std::move(next);
+        CK(cudaStreamSynchronize(s));  // host vectors used by async copies
+    }
+    const int K = 1 << depth;
+    std::vector<dgs_plane> planes((size_t)K * depth);
+    for (int k = 0; k < K; ++k)
+        for (int j = 0; j < depth; ++j) planes[(size_t)k * depth + j] = regions[k].planes[j];
+    return planes;
+}
+
+/// The new partition table (device copy included).
+void set_table_from_planes(Ctx& ctx, const std::vector<dgs_plane>& planes, int depth) {
+    const int K = 1 << depth;
+    Table t{};
+    t.k_count = K;
+    for (int k = 0; k < K; ++k) {
+        t.sub[k].n = depth;
+        for (int j = 0; j < depth; ++j) {
+            const dgs_plane& p = planes[(size_t)k * depth + j];
+            t.sub[k].nx[j] = p.n[0];
+            t.sub[k].ny[j] = p.n[1];
+            t.sub[k].nz[j] = p.n[2];
+            t.sub[k].d[j] = p.d;
+            t.sub[k].closed[j] = p.closed;
+        }
+    }
+    ctx.table = t;
+    ctx.table_dev.ensure(1);
+    CK(cudaMemcpyAsync(ctx.table_dev.p, &ctx.table, sizeof(Table), cudaMemcpyHostToDevice, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+}
+
+/// One u64 per peer: send[d] to rank d, returns what every rank sent to this one.
+std::vector<uint64_t> xfer_counts(Ctx& ctx, const std::vector<uint64_t>& send) {
+    const int W = ctx.world, me = ctx.rank;
+    DevBuf<uint64_t> ds, dr;
+    ds.ensure(W);
+    dr.ensure(W);
+    CK(cudaMemcpy(ds.p, send.data(), 8 * W, cudaMemcpyHostToDevice));
+    {
+        Xfer x(ctx);
+        for (int d = 0; d < W; ++d)
+            if (d != me) x.send(reinterpret_cast<const float*>(ds.p + d), 2, d);
+        for (int r = 0; r < W; ++r)
+            if (r != me) x.recv(reinterpret_cast<float*>(dr.p + r), 2, r);
+        x.finish();
+    }
+    CK(cudaStreamSynchronize(ctx.stream));
+    std::vector<uint64_t> out(W);
+    CK(cudaMemcpy(out.data(), dr.p, 8 * W, cudaMemcpyDeviceToHost));
+    out[me] = send[me];
+    return out;
+}
+
+/// Variable-size all-to-all of float buffers (own slot excluded: the caller copies it).
+void xfer_alltoallv(Ctx& ctx, const std::vector<const float*>& sp, const std::vector<size_t>& sn,
+                    const std::vector<float*>& rp, const std::vector<size_t>& rn) {
+    const int W = ctx.world, me = ctx.rank;
+    Xfer x(ctx);
+    for (int d = 0; d < W; ++d)
+        if (d != me && sn[d]) x.send(sp[d], sn[d], d);
+    for (int r = 0; r < W; ++r)
+        if (r != me && rn[r]) x.recv(rp[r], rn[r], r);
+    x.finish();
+    CK(cudaStreamSynchronize(ctx.stream));
+}
+
 /// Shared-replica index over the resident subsets (grad sync): replicas sorted
 /// by (id, k); sh_starts = first sorted position of every id held >= 2 times.
 void build_shared(Ctx& ctx) {
@@ -885,24 +1071,38 @@ int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t ex
                     dgs_plane* planes_out) {
     return dgs_guard([&] {
         require_table(*ctx);
-        if (ctx->world != 1) throw std::invalid_argument("repartition: the device path is single-rank (world == 1)");
         if (depth < 0 || depth > 5) throw std::invalid_argument("repartition: kd depth must be 0..5 (<= 32 subsets)");
-        const int K0 = ctx->table.k_count;
-        for (int k = 0; k < K0; ++k) subset(*ctx, k);  // every subset resident
+        const int W = ctx->world, me = ctx->rank;
+        if ((1 << depth) < W) throw std::invalid_argument("repartition: fewer KD subsets than ranks");
         CK(cudaSetDevice(ctx->device));
         cudaStream_t s = ctx->stream;
-        const SubsetState& S0 = subset(*ctx, 0);
+        // local subsets in ascending k (the replica numbering of this rank)
+        std::vector<int> ks;
+        for (auto& kv : ctx->subsets) ks.push_back(kv.first);
+        if (W == 1)
+            for (int k = 0; k < ctx->table.k_count; ++k) subset(*ctx, k);  // every subset resident
+        if (ks.empty()) throw std::invalid_argument("repartition: no subset resident on this rank");
+        const SubsetState& S0 = *ctx->subsets.begin()->second;
         const int shc = S0.sh_coeffs, rows = S0.rows;
         const uint64_t adam_step = S0.adam_step;
-        // ---- snapshot (manager.hpp:389-418): one replica per id ----
-        std::vector<uint32_t> offs(K0 + 1, 0);
-        for (int k = 0; k < K0; ++k) {
+        std::vector<uint32_t> offs(1, 0);
+        for (int k : ks) {
             const SubsetState& S = subset(*ctx, k);
             if (S.sh_coeffs != shc) throw std::invalid_argument("repartition: subsets disagree on the SH degree");
-            offs[k + 1] = offs[k] + (uint32_t)S.n;
+            offs.push_back(offs.back() + (uint32_t)S.n);
         }
-        const int R = (int)offs[K0];
-        if (R <= 0) throw std::invalid_argument("build_kdtree: empty point set");
+        const int Rme = (int)offs.back();
+        // ---- snapshot (manager.hpp:389-418): one replica per id, across ranks ----
+        std::vector<uint64_t> rcount(W, 0);
+        rcount[me] = (uint64_t)Rme;
+        if (W > 1) rcount = xfer_counts(*ctx, std::vector<uint64_t>(W, (uint64_t)Rme));
+        uint64_t Rtot = 0, base = 0;
+        for (int r = 0; r < W; ++r) {
+            if (r < me) base += rcount[r];
+            Rtot += rcount[r];
+        }
+        if (Rtot == 0 || Rtot > 0x7fffffffull) throw std::invalid_argument("build_kdtree: empty point set");
+        const int R = (int)Rtot;
         DevBuf<uint64_t> keys, keys_alt;
         DevBuf<uint32_t> vals, vals_alt, winners;
         DevBuf<uint8_t> flags, temp;
@@ -914,11 +1114,36 @@ int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t ex
         winners.ensure(R);
         flags.ensure(R);
         count.ensure(1);
-        const size_t tb = repart_temp_bytes(R);
+        size_t tb = repart_temp_bytes(R);
         temp.ensure(tb);
-        for (int k = 0; k < K0; ++k) {
-            const SubsetState& S = subset(*ctx, k);
-            repart_snapshot_keys((int)S.n, S.P.p, S.ld, S.ids32.p, ctx->table_dev.p, k, offs[k], keys.p, vals.p, s);
+        for (size_t q = 0; q < ks.size(); ++q) {
+            const SubsetState& S = subset(*ctx, ks[q]);
+            repart_snapshot_keys((int)S.n, S.P.p, S.ld, S.ids32.p, ctx->table_dev.p, ks[q], (uint32_t)(base + offs[q]),
+                                 keys.p, vals.p, s);
+        }
+        if (W > 1) {  // all-gather the replica keys (u64) and their global indices
+            std::vector<const float*> sp(W);
+            std::vector<size_t> sn(W), rn(W);
+            std::vector<float*> rp(W);
+            for (int r = 0; r < W; ++r) {
+                uint64_t off = 0;
+                for (int q = 0; q < r; ++q) off += rcount[q];
+                sp[r] = reinterpret_cast<const float*>(keys.p + base);
+                sn[r] = 2 * (size_t)Rme;
+                rp[r] = reinterpret_cast<float*>(keys.p + off);
+                rn[r] = 2 * (size_t)rcount[r];
+            }
+            CK(cudaStreamSynchronize(s));
+            xfer_alltoallv(*ctx, sp, sn, rp, rn);
+            for (int r = 0; r < W; ++r) {
+                uint64_t off = 0;
+                for (int q = 0; q < r; ++q) off += rcount[q];
+                sp[r] = reinterpret_cast<const float*>(vals.p + base);
+                sn[r] = (size_t)Rme;
+                rp[r] = reinterpret_cast<float*>(vals.p + off);
+                rn[r] = (size_t)rcount[r];
+            }
+            xfer_alltoallv(*ctx, sp, sn, rp, rn);
         }
         uint64_t* kp = keys.p;
         uint64_t* kap = keys_alt.p;
@@ -927,192 +1152,185 @@ int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t ex
         repart_sort_pairs(kp, kap, vp, vap, R, 40, temp.p, tb, s);
         repart_first_of_run(R, kp, flags.p, s);
         repart_select(R, vp, flags.p, winners.p, count.p, temp.p, tb, s);
-        int N = 0;
-        CK(cudaMemcpyAsync(&N, count.p, 4, cudaMemcpyDeviceToHost, s));
+        int Ntot = 0;
+        CK(cudaMemcpyAsync(&Ntot, count.p, 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        if (expected_splats >= 0 && (int64_t)N != expected_splats) throw std::runtime_error("snapshot lost splats");
-        // merged SoA state, id order
-        const size_t ldm = (size_t)(N + 31) / 32 * 32;
+        if (expected_splats >= 0 && (int64_t)Ntot != expected_splats) throw std::runtime_error("snapshot lost splats");
+        // this rank's winners (global replica index in [base, base + Rme)) -> local replica index
+        int N = Ntot;
+        uint32_t* mine = winners.p;
+        DevBuf<uint32_t> mine_buf;
+        if (W > 1) {
+            mine_buf.ensure(std::max(Ntot, 1));
+            repart_flag_range(Ntot, winners.p, (uint32_t)base, (uint32_t)(base + Rme), flags.p, s);
+            repart_select(Ntot, winners.p, flags.p, mine_buf.p, count.p, temp.p, tb, s);
+            CK(cudaMemcpyAsync(&N, count.p, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            repart_sub_const(N, mine_buf.p, (uint32_t)base, s);
+            mine = mine_buf.p;
+        }
+        // my winners' state, SoA
+        const size_t ldm = (size_t)(std::max(N, 1) + 31) / 32 * 32;
         DevBuf<float> mP, mM, mV;
         DevBuf<uint32_t> mIds;
         mP.ensure(rows * ldm);
         mM.ensure(rows * ldm);
         mV.ensure(rows * ldm);
-        mIds.ensure(N);
+        mIds.ensure(ldm);
         {
-            std::vector<const float*> hp(K0), hm(K0), hv(K0);
-            std::vector<const uint32_t*> hi(K0);
-            std::vector<size_t> hl(K0);
-            for (int k = 0; k < K0; ++k) {
-                const SubsetState& S = subset(*ctx, k);
-                hp[k] = S.P.p;
-                hm[k] = S.M.p;
-                hv[k] = S.V.p;
-                hi[k] = S.ids32.p;
-                hl[k] = S.ld;
+            const int KL = (int)ks.size();
+            std::vector<const float*> hp(KL), hm(KL), hv(KL);
+            std::vector<const uint32_t*> hi(KL);
+            std::vector<size_t> hl(KL);
+            for (int q = 0; q < KL; ++q) {
+                const SubsetState& S = subset(*ctx, ks[q]);
+                hp[q] = S.P.p;
+                hm[q] = S.M.p;
+                hv[q] = S.V.p;
+                hi[q] = S.ids32.p;
+                hl[q] = S.ld;
             }
             DevBuf<const float*> dp, dm, dv;
             DevBuf<const uint32_t*> di;
             DevBuf<size_t> dl;
             DevBuf<uint32_t> doffs;
-            dp.ensure(K0);
-            dm.ensure(K0);
-            dv.ensure(K0);
-            di.ensure(K0);
-            dl.ensure(K0);
-            doffs.ensure(K0 + 1);
-            CK(cudaMemcpyAsync(dp.p, hp.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(dm.p, hm.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(dv.p, hv.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(di.p, hi.data(), K0 * sizeof(void*), cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(dl.p, hl.data(), K0 * sizeof(size_t), cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(doffs.p, offs.data(), (K0 + 1) * 4, cudaMemcpyHostToDevice, s));
-            repart_gather_replicas(N, rows, winners.p, doffs.p, K0, dp.p, dm.p, dv.p, di.p, dl.p, mP.p, mM.p, mV.p,
-                                   mIds.p, ldm, s);
-            CK(cudaStreamSynchronize(s));  // host arrays above go out of scope
-        }
-        // ---- build_kdtree (partition.hpp:93-184) on the merged centres ----
-        struct HostRegion {
-            std::vector<dgs_plane> planes;
-            float amin[3], amax[3];
-        };
-        std::vector<HostRegion> regions(1);
-        for (int a = 0; a < 3; ++a) {
-            regions[0].amin[a] = -INFINITY;
-            regions[0].amax[a] = INFINITY;
-        }
-        DevBuf<uint8_t> node;
-        node.ensure(N);
-        CK(cudaMemsetAsync(node.p, 0, N, s));
-        DevBuf<uint32_t> lo, hi, cnt;
-        DevBuf<int> d_axis;
-        DevBuf<float> d_plane;
-        const int maxn = 1 << depth;
-        lo.ensure(3 * maxn);
-        hi.ensure(3 * maxn);
-        cnt.ensure(maxn);
-        d_axis.ensure(maxn);
-        d_plane.ensure(maxn);
-        auto from_order = [](uint32_t o) {
-            const uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
-            float f;
-            std::memcpy(&f, &b, 4);
-            return f;
-        };
-        for (int d = 0; d < depth; ++d) {
-            const int nn = 1 << d;
-            std::vector<uint32_t> h_lo(3 * nn, 0xffffffffu), h_hi(3 * nn, 0u), h_cnt(nn, 0u);
-            CK(cudaMemcpyAsync(lo.p, h_lo.data(), 12 * nn, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(hi.p, h_hi.data(), 12 * nn, cudaMemcpyHostToDevice, s));
-            CK(cudaMemsetAsync(cnt.p, 0, 4 * nn, s));
-            repart_node_extent(N, mP.p, ldm, node.p, nn, lo.p, hi.p, cnt.p, s);
-            CK(cudaMemcpyAsync(h_lo.data(), lo.p, 12 * nn, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(h_hi.data(), hi.p, 12 * nn, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(h_cnt.data(), cnt.p, 4 * nn, cudaMemcpyDeviceToHost, s));
+            dp.ensure(KL);
+            dm.ensure(KL);
+            dv.ensure(KL);
+            di.ensure(KL);
+            dl.ensure(KL);
+            doffs.ensure(KL + 1);
+            CK(cudaMemcpyAsync(dp.p, hp.data(), KL * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dm.p, hm.data(), KL * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dv.p, hv.data(), KL * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(di.p, hi.data(), KL * sizeof(void*), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dl.p, hl.data(), KL * sizeof(size_t), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(doffs.p, offs.data(), (KL + 1) * 4, cudaMemcpyHostToDevice, s));
+            repart_gather_replicas(N, rows, mine, doffs.p, KL, dp.p, dm.p, dv.p, di.p, dl.p, mP.p, mM.p, mV.p, mIds.p,
+                                   ldm, s);
             CK(cudaStreamSynchronize(s));
-            if (d == 0) {  // build_kdtree's degenerate-set check (partition.hpp:164-171)
-                float m = from_order(h_hi[0]) - from_order(h_lo[0]);
-                for (int a = 1; a < 3; ++a) m = std::max(m, from_order(h_hi[a]) - from_order(h_lo[a]));
-                if (m <= 0.0f) throw std::invalid_argument("degenerate point set");
-            }
-            std::vector<int> axis(nn, 0);
-            for (int q = 0; q < nn; ++q) {
-                if (!h_cnt[q]) continue;
-                float ext[3];
-                for (int a = 0; a < 3; ++a) ext[a] = from_order(h_hi[3 * q + a]) - from_order(h_lo[3 * q + a]);
-                float m = ext[0];  // maxCoeff(&axis): first maximum
-                for (int a = 1; a < 3; ++a)
-                    if (ext[a] > m) {
-                        m = ext[a];
-                        axis[q] = a;
-                    }
-            }
-            CK(cudaMemcpyAsync(d_axis.p, axis.data(), 4 * nn, cudaMemcpyHostToDevice, s));
-            // exact medians: sort (node, coordinate) keys, read the two middle values of every node
-            repart_node_keys(N, mP.p, ldm, node.p, d_axis.p, keys.p, s);
-            uint64_t* k1 = keys.p;
-            uint64_t* k2 = keys_alt.p;
-            repart_sort_keys(k1, k2, N, 32 + d + 1, temp.p, tb, s);
-            std::vector<float> plane(nn, 0.0f);
-            std::vector<uint64_t> mid(2);
-            uint32_t start = 0;
-            for (int q = 0; q < nn; ++q) {
-                const uint32_t c = h_cnt[q];
-                HostRegion& reg = regions[q];
-                if (c > 0) {
-                    const uint32_t i1 = start + c / 2;
-                    const uint32_t i0 = c % 2 == 0 ? i1 - 1 : i1;
-                    CK(cudaMemcpyAsync(&mid[0], k1 + i0, 8, cudaMemcpyDeviceToHost, s));
-                    CK(cudaMemcpyAsync(&mid[1], k1 + i1, 8, cudaMemcpyDeviceToHost, s));
-                    CK(cudaStreamSynchronize(s));
-                    const float lower = from_order((uint32_t)mid[0]), upper = from_order((uint32_t)mid[1]);
-                    plane[q] = c % 2 == 0 ? (lower + upper) / 2.0f : upper;
-                } else {
-                    const int a = axis[q];
-                    const float l = reg.amin[a], h = reg.amax[a];
-                    plane[q] = (std::isfinite(l) && std::isfinite(h)) ? (l + h) / 2.0f
-                               : std::isfinite(l)                    ? l + 1.0f
-                               : std::isfinite(h)                    ? h - 1.0f
-                                                                     : 0.0f;
-                }
-                start += c;
-            }
-            CK(cudaMemcpyAsync(d_plane.p, plane.data(), 4 * nn, cudaMemcpyHostToDevice, s));
-            repart_node_split(N, mP.p, ldm, node.p, d_axis.p, d_plane.p, s);
-            std::vector<HostRegion> next(2 * nn);
-            for (int q = 0; q < nn; ++q) {
-                const int a = axis[q];
-                HostRegion left = regions[q], right = regions[q];
-                dgs_plane lp{};
-                lp.n[a] = 1.0f;
-                lp.d = -plane[q];
-                lp.closed = 0;
-                left.planes.push_back(lp);
-                left.amax[a] = std::min(left.amax[a], plane[q]);
-                dgs_plane rp{};
-                rp.n[a] = -1.0f;
-                rp.d = plane[q];
-                rp.closed = 1;
-                right.planes.push_back(rp);
-                right.amin[a] = std::max(right.amin[a], plane[q]);
-                next[2 * q] = std::move(left);
-                next[2 * q + 1] = std::move(right);
-            }
-            regions = std::move(next);
-            CK(cudaStreamSynchronize(s));  // host vectors used by async copies
         }
-        const int K = 1 << depth;
-        std::vector<dgs_plane> planes((size_t)K * depth);
-        for (int k = 0; k < K; ++k)
-            for (int j = 0; j < depth; ++j) planes[(size_t)k * depth + j] = regions[k].planes[j];
+        // ---- build_kdtree (partition.hpp:93-184) over every winner's centre ----
+        std::vector<dgs_plane> planes;
+        if (W == 1) {
+            planes = kd_build_device(*ctx, mP.p, ldm, N, depth);
+        } else {
+            std::vector<uint64_t> ncount = xfer_counts(*ctx, std::vector<uint64_t>(W, (uint64_t)N));
+            const size_t ldc = (size_t)(Ntot + 31) / 32 * 32;
+            DevBuf<float> cAll, cMine, cRecv;
+            cAll.ensure(3 * ldc);
+            cMine.ensure(3 * (size_t)std::max(N, 1));
+            size_t maxr = 1;
+            for (int r = 0; r < W; ++r) maxr = std::max<size_t>(maxr, ncount[r]);
+            cRecv.ensure(3 * maxr * W);
+            for (int a = 0; a < 3; ++a)
+                CK(cudaMemcpyAsync(cMine.p + (size_t)a * N, mP.p + (size_t)a * ldm, 4 * (size_t)N,
+                                   cudaMemcpyDeviceToDevice, s));
+            CK(cudaStreamSynchronize(s));
+            std::vector<const float*> sp(W, cMine.p);
+            std::vector<size_t> sn(W, 3 * (size_t)N), rn(W);
+            std::vector<float*> rp(W);
+            for (int r = 0; r < W; ++r) {
+                rp[r] = cRecv.p + 3 * maxr * r;
+                rn[r] = 3 * (size_t)ncount[r];
+            }
+            xfer_alltoallv(*ctx, sp, sn, rp, rn);
+            CK(cudaMemcpyAsync(rp[me], cMine.p, 12 * (size_t)N, cudaMemcpyDeviceToDevice, s));
+            uint64_t off = 0;
+            for (int r = 0; r < W; ++r) {
+                for (int a = 0; a < 3; ++a)
+                    CK(cudaMemcpyAsync(cAll.p + (size_t)a * ldc + off, rp[r] + (size_t)a * ncount[r],
+                                       4 * (size_t)ncount[r], cudaMemcpyDeviceToDevice, s));
+                off += ncount[r];
+            }
+            CK(cudaStreamSynchronize(s));
+            planes = kd_build_device(*ctx, cAll.p, ldc, Ntot, depth);
+        }
         if (planes_out) std::memcpy(planes_out, planes.data(), planes.size() * sizeof(dgs_plane));
-        // new table
-        {
-            Table t{};
-            t.k_count = K;
-            for (int k = 0; k < K; ++k) {
-                t.sub[k].n = depth;
-                for (int j = 0; j < depth; ++j) {
-                    const dgs_plane& p = planes[(size_t)k * depth + j];
-                    t.sub[k].nx[j] = p.n[0];
-                    t.sub[k].ny[j] = p.n[1];
-                    t.sub[k].nz[j] = p.n[2];
-                    t.sub[k].d[j] = p.d;
-                    t.sub[k].closed[j] = p.closed;
-                }
-            }
-            ctx->table = t;
-            CK(cudaMemcpyAsync(ctx->table_dev.p, &ctx->table, sizeof(Table), cudaMemcpyHostToDevice, s));
-        }
-        // ---- assign_subsets (partition.hpp:234-251) + migration (manager.hpp:440-482) ----
-        DevBuf<uint32_t> mask, idx;
-        mask.ensure(N);
-        idx.ensure(N);
+        set_table_from_planes(*ctx, planes, depth);
+        const int K = 1 << depth;
+        // ---- assign_subsets (partition.hpp:234-251) ----
+        DevBuf<uint32_t> mask;
+        mask.ensure(std::max(N, 1));
         repart_assign(N, mP.p, ldm, ctx->table_dev.p, (float)d_multiplier, mask.p, s);
+        // ---- migration (manager.hpp:440-482): winners to the ranks owning their new subsets ----
+        const float* srcP = mP.p;
+        const float* srcM = mM.p;
+        const float* srcV = mV.p;
+        const uint32_t* srcIds = mIds.p;
+        const uint32_t* srcMask = mask.p;
+        size_t lds = ldm;
+        int Nsrc = N;
+        DevBuf<float> rP, rM, rV;
+        DevBuf<uint32_t> rIds, rMask;
+        if (W > 1) {
+            const int stride = 3 * rows + 2;
+            std::vector<DevBuf<float>> packs(W);
+            std::vector<uint64_t> scount(W, 0);
+            DevBuf<uint32_t> idx;
+            idx.ensure(std::max(N, 1));
+            for (int d = 0; d < W; ++d) {
+                uint32_t owned = 0;
+                for (int k = 0; k < K; ++k)
+                    if (subset_owner(k, K, W) == d) owned |= 1u << k;
+                repart_flag_owned(N, mask.p, owned, flags.p, s);
+                repart_select_iota(N, flags.p, idx.p, count.p, temp.p, tb, s);
+                int nd = 0;
+                CK(cudaMemcpyAsync(&nd, count.p, 4, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                scount[d] = (uint64_t)nd;
+                packs[d].ensure((size_t)std::max(nd, 1) * stride);
+                repart_pack(nd, rows, idx.p, mP.p, mM.p, mV.p, mIds.p, mask.p, ldm, packs[d].p, s);
+            }
+            CK(cudaStreamSynchronize(s));
+            std::vector<uint64_t> rcnt = xfer_counts(*ctx, scount);
+            std::vector<DevBuf<float>> inbox(W);
+            std::vector<const float*> sp(W);
+            std::vector<size_t> sn(W), rn(W);
+            std::vector<float*> rp(W);
+            uint64_t total_in = 0;
+            for (int r = 0; r < W; ++r) {
+                sp[r] = packs[r].p;
+                sn[r] = (size_t)scount[r] * stride;
+                inbox[r].ensure((size_t)std::max<uint64_t>(rcnt[r], 1) * stride);
+                rp[r] = inbox[r].p;
+                rn[r] = (size_t)rcnt[r] * stride;
+                total_in += rcnt[r];
+            }
+            xfer_alltoallv(*ctx, sp, sn, rp, rn);
+            if (scount[me])
+                CK(cudaMemcpyAsync(inbox[me].p, packs[me].p, 4 * (size_t)scount[me] * stride,
+                                   cudaMemcpyDeviceToDevice, s));
+            Nsrc = (int)total_in;
+            lds = (size_t)(std::max(Nsrc, 1) + 31) / 32 * 32;
+            rP.ensure(rows * lds);
+            rM.ensure(rows * lds);
+            rV.ensure(rows * lds);
+            rIds.ensure(lds);
+            rMask.ensure(lds);
+            uint64_t off = 0;
+            for (int r = 0; r < W; ++r) {  // source-rank order
+                repart_unpack((int)rcnt[r], rows, inbox[r].p, rP.p + off, rM.p + off, rV.p + off, rIds.p + off,
+                              rMask.p + off, lds, s);
+                off += rcnt[r];
+            }
+            CK(cudaStreamSynchronize(s));
+            srcP = rP.p;
+            srcM = rM.p;
+            srcV = rV.p;
+            srcIds = rIds.p;
+            srcMask = rMask.p;
+            if ((size_t)Nsrc > flags.n) flags.ensure(Nsrc);
+            tb = repart_temp_bytes(std::max<int64_t>(Nsrc, R));
+            temp.ensure(tb);
+        }
+        DevBuf<uint32_t> idx2;
+        idx2.ensure(std::max(Nsrc, 1));
         std::map<int, std::unique_ptr<SubsetState>> fresh;
         for (int k = 0; k < K; ++k) {
-            repart_flag_bit(N, mask.p, k, flags.p, s);
-            repart_select_iota(N, flags.p, idx.p, count.p, temp.p, tb, s);
+            if (subset_owner(k, K, W) != me) continue;
+            repart_flag_bit(Nsrc, srcMask, k, flags.p, s);
+            repart_select_iota(Nsrc, flags.p, idx2.p, count.p, temp.p, tb, s);
             int nk = 0;
             CK(cudaMemcpyAsync(&nk, count.p, 4, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -1133,7 +1351,7 @@ int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t ex
                 CK(cudaMemsetAsync(S->M.p, 0, rows * S->ld * sizeof(float), s));
                 CK(cudaMemsetAsync(S->V.p, 0, rows * S->ld * sizeof(float), s));
             }
-            repart_gather_members(nk, rows, idx.p, mP.p, mM.p, mV.p, mIds.p, ldm, S->P.p, S->M.p, S->V.p,
+            repart_gather_members(nk, rows, idx2.p, srcP, srcM, srcV, srcIds, lds, S->P.p, S->M.p, S->V.p,
                                   S->ids32.p, S->ld, s);
             std::vector<uint32_t> ids32(nk);
             if (nk) CK(cudaMemcpyAsync(ids32.data(), S->ids32.p, 4 * (size_t)nk, cudaMemcpyDeviceToHost, s));

@@ -144,6 +144,15 @@ void repart_gather_members(int n, int rows, const uint32_t* idx, const float* P,
                            const uint32_t* ids, size_t ld_src, float* dP, float* dM, float* dV, uint32_t* dids,
                            size_t ld_dst, cudaStream_t s);
 
+// Multi-rank repartition helpers (repartition.cu).
+void repart_flag_owned(int n, const uint32_t* mask, uint32_t owned, uint8_t* flags, cudaStream_t s);
+void repart_flag_range(int n, const uint32_t* v, uint32_t lo, uint32_t hi, uint8_t* flags, cudaStream_t s);
+void repart_sub_const(int n, uint32_t* v, uint32_t c, cudaStream_t s);
+void repart_pack(int n, int rows, const uint32_t* idx, const float* P, const float* M, const float* V,
+                 const uint32_t* ids, const uint32_t* mask, size_t ld, float* out, cudaStream_t s);
+void repart_unpack(int n, int rows, const float* in, float* P, float* M, float* V, uint32_t* ids, uint32_t* mask,
+                   size_t ld, cudaStream_t s);
+
 // Gradient sync of shared replicas (config.grad_sync; manager.hpp:351-379, worker.hpp:103-144).
 void shared_replica_keys(int n, const uint32_t* ids32, int k, uint32_t base, uint64_t* keys, uint32_t* vals,
                          cudaStream_t s);

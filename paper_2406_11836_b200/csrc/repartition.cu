@@ -324,4 +324,76 @@ void grad_sync(int nslots, int rows, const uint32_t* starts, int nrep, const uin
                                                                               lds);
 }
 
+namespace {
+
+__global__ void k_flag_owned(int n, const uint32_t* __restrict__ mask, uint32_t owned, uint8_t* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = (mask[i] & owned) != 0u;
+}
+
+__global__ void k_flag_range(int n, const uint32_t* __restrict__ v, uint32_t lo, uint32_t hi,
+                             uint8_t* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = v[i] >= lo && v[i] < hi;
+}
+
+__global__ void k_sub_const(int n, uint32_t* __restrict__ v, uint32_t c) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] -= c;
+}
+
+/// AoS record per migrating splat: rows of p, then m, then v, the id and the
+/// membership mask (as float bits).
+__global__ void k_pack(int n, int rows, const uint32_t* __restrict__ idx, const float* __restrict__ P,
+                       const float* __restrict__ M, const float* __restrict__ V, const uint32_t* __restrict__ ids,
+                       const uint32_t* __restrict__ mask, size_t ld, float* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const size_t i = idx[j];
+    const int stride = 3 * rows + 2;
+    float* o = out + (size_t)j * stride;
+    for (int q = 0; q < rows; ++q) {
+        o[q] = P[(size_t)q * ld + i];
+        o[rows + q] = M[(size_t)q * ld + i];
+        o[2 * rows + q] = V[(size_t)q * ld + i];
+    }
+    o[3 * rows] = __uint_as_float(ids[i]);
+    o[3 * rows + 1] = __uint_as_float(mask[i]);
+}
+
+__global__ void k_unpack(int n, int rows, const float* __restrict__ in, float* __restrict__ P, float* __restrict__ M,
+                         float* __restrict__ V, uint32_t* __restrict__ ids, uint32_t* __restrict__ mask, size_t ld) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int stride = 3 * rows + 2;
+    const float* r = in + (size_t)j * stride;
+    for (int q = 0; q < rows; ++q) {
+        P[(size_t)q * ld + j] = r[q];
+        M[(size_t)q * ld + j] = r[rows + q];
+        V[(size_t)q * ld + j] = r[2 * rows + q];
+    }
+    ids[j] = __float_as_uint(r[3 * rows]);
+    mask[j] = __float_as_uint(r[3 * rows + 1]);
+}
+
+}  // namespace
+
+void repart_flag_owned(int n, const uint32_t* mask, uint32_t owned, uint8_t* flags, cudaStream_t s) {
+    if (n > 0) k_flag_owned<<<blocks(n), 256, 0, s>>>(n, mask, owned, flags);
+}
+void repart_flag_range(int n, const uint32_t* v, uint32_t lo, uint32_t hi, uint8_t* flags, cudaStream_t s) {
+    if (n > 0) k_flag_range<<<blocks(n), 256, 0, s>>>(n, v, lo, hi, flags);
+}
+void repart_sub_const(int n, uint32_t* v, uint32_t c, cudaStream_t s) {
+    if (n > 0) k_sub_const<<<blocks(n), 256, 0, s>>>(n, v, c);
+}
+void repart_pack(int n, int rows, const uint32_t* idx, const float* P, const float* M, const float* V,
+                 const uint32_t* ids, const uint32_t* mask, size_t ld, float* out, cudaStream_t s) {
+    if (n > 0) k_pack<<<blocks(n), 256, 0, s>>>(n, rows, idx, P, M, V, ids, mask, ld, out);
+}
+void repart_unpack(int n, int rows, const float* in, float* P, float* M, float* V, uint32_t* ids, uint32_t* mask,
+                   size_t ld, cudaStream_t s) {
+    if (n > 0) k_unpack<<<blocks(n), 256, 0, s>>>(n, rows, in, P, M, V, ids, mask, ld);
+}
+
 }  // namespace dgs_b200

@@ -527,13 +527,11 @@ class Manager:
     def repartition(self, device: bool = True):
         """Manager::repartition (manager.hpp:421-430).  device=True (default):
         snapshot, KD build, assignment and migration on the GPU
-        (dgs_repartition, single rank); device=False: the host path through
-        snapshot() and a reload (the reference's message-level data flow)."""
+        (dgs_repartition; across ranks the replica keys and centres are
+        all-gathered and the migrating state moves all-to-all); device=False:
+        the host path through snapshot() and a reload (single rank)."""
         if not device:
             return self.repartition_host()
-        if self.world > 1:
-            raise NotImplementedError("device repartition across ranks (NCCL migration) is SURVEY §8(f) row 1, "
-                                      "multi-rank part")
         depth = int(self.config.kd_depth)
         K = 1 << depth
         arr = (Plane * max(K * depth, 1))()

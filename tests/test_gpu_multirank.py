@@ -74,3 +74,83 @@ def test_multi_rank_step_matches_single_rank_virtual_slices(tmp_path, world):
         np.testing.assert_array_equal(got[r][f"ct{k}"], ct, err_msg=f"partial map of subset {k}")
         np.testing.assert_array_equal(got[r][f"gr{k}"], gr, err_msg=f"gradient map of subset {k}")
     mgr.close()
+
+
+def _diverge_replicas(mgr, K, world, rank):
+    """Deterministic per-subset edits so replicas of shared splats differ (the
+    snapshot must pick by the reference's rule) and the Adam moments are
+    non-trivial."""
+    from paper_2406_11836_b200 import engine
+    for k in range(K):
+        if engine.subset_owner(k, K, world) != rank:
+            continue
+        p, m, v, step = mgr.ctx.store_subset(k, mgr.sh_coeffs)
+        p.mu += np.float32(2e-3 * (k + 1))
+        rng = np.random.default_rng(100 + k)
+        for x in (m, v):
+            for f in ("mu", "log_scale", "rotation", "opacity_logit", "sh"):
+                a = getattr(x, f)
+                a[...] = rng.random(a.shape, dtype=np.float32) if x is v else rng.standard_normal(a.shape).astype(np.float32)
+        mgr.ctx.load_subset(k, p, m, v, adam_step=7, epoch=0)
+
+
+def _rep_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from conftest import Golden
+        from host_transport import GlooTransport
+        from paper_2406_11836_b200 import engine
+        g = Golden(NAME)
+        s = g.splats()
+        mgr = engine.Manager(s, engine.train_config(kd_depth=g.args["kd"]), engine.render_options(), device=0,
+                             rank=rank, world=world, transport=GlooTransport())
+        K = mgr.table.subset_count
+        _diverge_replicas(mgr, K, world, rank)
+        mgr.config.kd_depth = 2
+        mgr.repartition(device=True)
+        out = {"planes": mgr.table.planes}
+        for k in range(mgr.table.subset_count):
+            if engine.subset_owner(k, mgr.table.subset_count, world) == rank:
+                p, m, v, step = mgr.ctx.store_subset(k, s.sh_coeffs)
+                out[f"id{k}"] = p.id
+                out[f"step{k}"] = np.array([step])
+                for tag, x in (("p", p), ("m", m), ("v", v)):
+                    out[f"{tag}{k}"] = np.concatenate([x.mu, x.log_scale, x.rotation, x.opacity_logit[:, None],
+                                                       x.sh.reshape(x.n, -1)], axis=1)
+        np.savez(os.path.join(out_dir, f"rep{rank}.npz"), **out)
+        mgr.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_device_repartition_matches_single_rank(tmp_path, world):
+    """dgs_repartition across ranks (replica keys and centres all-gathered,
+    state migrated all-to-all) equals the single-rank device repartition:
+    planes, every new subset's member set and every migrated p/m/v value."""
+    from conftest import Golden
+    from paper_2406_11836_b200 import engine
+    mp.spawn(_rep_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    g = Golden(NAME)
+    s = g.splats()
+    mgr = engine.Manager(s, engine.train_config(kd_depth=g.args["kd"]), engine.render_options())
+    _diverge_replicas(mgr, mgr.table.subset_count, 1, 0)
+    mgr.config.kd_depth = 2
+    mgr.repartition(device=True)
+    got = [np.load(tmp_path / f"rep{r}.npz") for r in range(world)]
+    for r in range(world):
+        np.testing.assert_array_equal(got[r]["planes"], mgr.table.planes)
+    K = mgr.table.subset_count
+    for k in range(K):
+        r = engine.subset_owner(k, K, world)
+        p, m, v, step = mgr.ctx.store_subset(k, s.sh_coeffs)
+        assert got[r][f"step{k}"][0] == step
+        order_ref = np.argsort(p.id)
+        order_got = np.argsort(got[r][f"id{k}"])
+        np.testing.assert_array_equal(got[r][f"id{k}"][order_got], p.id[order_ref], err_msg=f"subset {k} members")
+        for tag, x in (("p", p), ("m", m), ("v", v)):
+            ref = np.concatenate([x.mu, x.log_scale, x.rotation, x.opacity_logit[:, None], x.sh.reshape(x.n, -1)],
+                                 axis=1)
+            np.testing.assert_array_equal(got[r][f"{tag}{k}"][order_got], ref[order_ref], err_msg=f"subset {k} {tag}")
+    mgr.close()
