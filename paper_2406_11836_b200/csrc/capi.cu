@@ -240,6 +240,14 @@ struct Ctx {
     DevBuf<uint64_t> sh_keys;
     DevBuf<uint32_t> sh_reps, sh_starts;
     int sh_slots = 0, sh_nrep = 0;
+    // cross-rank variant (world > 1): the globally sorted shared replicas
+    DevBuf<uint64_t> xs_keys;                 // [S] id << 8 | k
+    DevBuf<uint32_t> xs_g, xs_src, xs_pos;    // [S] global replica index, row in the gathered rows; my entries
+    DevBuf<uint8_t> xs_mine;                  // [S] held by this rank
+    DevBuf<uint32_t> xs_offs;                 // local replica offsets (ascending k)
+    std::vector<uint64_t> xs_count;           // shared entries held per rank
+    uint32_t xs_base = 0;
+    int xs_S = 0, xs_nmine = 0;
     DevBuf<BlendStats> stats;
     DevBuf<int> bad;
     uint64_t launches = 0;
@@ -822,6 +830,151 @@ void xfer_alltoallv(Ctx& ctx, const std::vector<const float*>& sp, const std::ve
         if (r != me && rn[r]) x.recv(rp[r], rn[r], r);
     x.finish();
     CK(cudaStreamSynchronize(ctx.stream));
+}
+
+/// Cross-rank shared-replica index (grad sync, world > 1): every rank
+/// all-gathers the (id, k) keys of all replicas, sorts them and keeps the runs
+/// of >= 2 replicas; for each such replica it records the holder rank and its
+/// row in the per-step gathered gradient rows.
+void build_shared_multi(Ctx& ctx) {
+    if (!ctx.shared_dirty) return;
+    cudaStream_t s = ctx.stream;
+    const int W = ctx.world, me = ctx.rank;
+    std::vector<int> ks;
+    std::vector<uint32_t> offs(1, 0);
+    for (auto& kv : ctx.subsets) {
+        ks.push_back(kv.first);
+        offs.push_back(offs.back() + (uint32_t)kv.second->n);
+    }
+    const uint32_t Rme = offs.back();
+    std::vector<uint64_t> rcount = xfer_counts(ctx, std::vector<uint64_t>(W, Rme));
+    uint64_t base = 0, R = 0;
+    for (int r = 0; r < W; ++r) {
+        if (r < me) base += rcount[r];
+        R += rcount[r];
+    }
+    ctx.xs_base = (uint32_t)base;
+    ctx.xs_offs.ensure(ks.size() + 1);
+    CK(cudaMemcpy(ctx.xs_offs.p, offs.data(), 4 * offs.size(), cudaMemcpyHostToDevice));
+    DevBuf<uint64_t> keys, kalt;
+    DevBuf<uint32_t> vals, valt;
+    DevBuf<uint8_t> flags, temp;
+    DevBuf<int> count;
+    keys.ensure(std::max<uint64_t>(R, 1));
+    kalt.ensure(std::max<uint64_t>(R, 1));
+    vals.ensure(std::max<uint64_t>(R, 1));
+    valt.ensure(std::max<uint64_t>(R, 1));
+    flags.ensure(std::max<uint64_t>(R, 1));
+    count.ensure(1);
+    const size_t tb = repart_temp_bytes((int64_t)std::max<uint64_t>(R, 1));
+    temp.ensure(tb);
+    for (size_t q = 0; q < ks.size(); ++q) {
+        const SubsetState& S = *ctx.subsets[ks[q]];
+        shared_replica_keys((int)S.n, S.ids32.p, ks[q], (uint32_t)(base + offs[q]), keys.p, vals.p, s);
+        // shared_replica_keys stores k << 27 | i as the value; here the value is the global index
+    }
+    {
+        // global indices as values
+        std::vector<uint32_t> gi(Rme);
+        for (uint32_t j = 0; j < Rme; ++j) gi[j] = (uint32_t)base + j;
+        CK(cudaMemcpyAsync(vals.p + base, gi.data(), 4 * (size_t)Rme, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    std::vector<const float*> sp(W);
+    std::vector<size_t> sn(W), rn(W);
+    std::vector<float*> rp(W);
+    uint64_t off = 0;
+    for (int r = 0; r < W; ++r) {
+        sp[r] = reinterpret_cast<const float*>(keys.p + base);
+        sn[r] = 2 * (size_t)Rme;
+        rp[r] = reinterpret_cast<float*>(keys.p + off);
+        rn[r] = 2 * (size_t)rcount[r];
+        off += rcount[r];
+    }
+    xfer_alltoallv(ctx, sp, sn, rp, rn);
+    off = 0;
+    for (int r = 0; r < W; ++r) {
+        sp[r] = reinterpret_cast<const float*>(vals.p + base);
+        sn[r] = (size_t)Rme;
+        rp[r] = reinterpret_cast<float*>(vals.p + off);
+        rn[r] = (size_t)rcount[r];
+        off += rcount[r];
+    }
+    xfer_alltoallv(ctx, sp, sn, rp, rn);
+    uint64_t* kp = keys.p;
+    uint64_t* kap = kalt.p;
+    uint32_t* vp = vals.p;
+    uint32_t* vap = valt.p;
+    repart_sort_pairs(kp, kap, vp, vap, (int)R, 40, temp.p, tb, s);
+    shared_mark((int)R, kp, flags.p, s);
+    ctx.xs_keys.ensure(std::max<uint64_t>(R, 1));
+    ctx.xs_g.ensure(std::max<uint64_t>(R, 1));
+    repart_select_u64((int)R, kp, flags.p, ctx.xs_keys.p, count.p, temp.p, tb, s);
+    repart_select((int)R, vp, flags.p, ctx.xs_g.p, count.p, temp.p, tb, s);
+    int S = 0;
+    CK(cudaMemcpyAsync(&S, count.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx.xs_S = S;
+    // holder rank, row in the gathered rows, my entries (host bookkeeping, O(S))
+    std::vector<uint32_t> g(S), src(S), pos;
+    std::vector<uint8_t> mine(S);
+    if (S) CK(cudaMemcpy(g.data(), ctx.xs_g.p, 4 * (size_t)S, cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> rb(W + 1, 0);
+    for (int r = 0; r < W; ++r) rb[r + 1] = rb[r] + rcount[r];
+    ctx.xs_count.assign(W, 0);
+    std::vector<uint32_t> owner(S);
+    for (int j = 0; j < S; ++j) {
+        int r = 0;
+        while (r + 1 < W && rb[r + 1] <= g[j]) ++r;
+        owner[j] = r;
+        ++ctx.xs_count[r];
+    }
+    std::vector<uint64_t> cb(W + 1, 0), seen(W, 0);
+    for (int r = 0; r < W; ++r) cb[r + 1] = cb[r] + ctx.xs_count[r];
+    for (int j = 0; j < S; ++j) {
+        const int r = owner[j];
+        src[j] = (uint32_t)(cb[r] + seen[r]++);
+        mine[j] = r == me;
+        if (r == me) pos.push_back((uint32_t)j);
+    }
+    ctx.xs_nmine = (int)pos.size();
+    ctx.xs_src.ensure(std::max(S, 1));
+    ctx.xs_mine.ensure(std::max(S, 1));
+    ctx.xs_pos.ensure(std::max<size_t>(pos.size(), 1));
+    if (S) {
+        CK(cudaMemcpy(ctx.xs_src.p, src.data(), 4 * (size_t)S, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx.xs_mine.p, mine.data(), (size_t)S, cudaMemcpyHostToDevice));
+    }
+    if (!pos.empty()) CK(cudaMemcpy(ctx.xs_pos.p, pos.data(), 4 * pos.size(), cudaMemcpyHostToDevice));
+    ctx.shared_dirty = false;
+}
+
+/// One step's cross-rank sync: pack my shared replicas' gradient rows, all-gather,
+/// sum per id in worker order and write back (G pointers in ascending local k).
+void grad_sync_multi(Ctx& ctx, int rows, float* const* dG, const size_t* dL, int KL) {
+    cudaStream_t s = ctx.stream;
+    const int W = ctx.world, me = ctx.rank;
+    const int S = ctx.xs_S;
+    DevBuf<float> sendb, recvb;
+    sendb.ensure((size_t)std::max(ctx.xs_nmine, 1) * rows);
+    recvb.ensure((size_t)std::max(S, 1) * rows);
+    shared_pack(ctx.xs_nmine, rows, ctx.xs_pos.p, ctx.xs_g.p, ctx.xs_base, ctx.xs_offs.p, KL, dG, dL, sendb.p, s);
+    std::vector<const float*> sp(W, sendb.p);
+    std::vector<size_t> sn(W, (size_t)ctx.xs_nmine * rows), rn(W);
+    std::vector<float*> rp(W);
+    uint64_t off = 0;
+    for (int r = 0; r < W; ++r) {
+        rp[r] = recvb.p + off * rows;
+        rn[r] = (size_t)ctx.xs_count[r] * rows;
+        off += ctx.xs_count[r];
+    }
+    CK(cudaStreamSynchronize(s));
+    xfer_alltoallv(ctx, sp, sn, rp, rn);
+    if (ctx.xs_nmine)
+        CK(cudaMemcpyAsync(rp[me], sendb.p, 4 * (size_t)ctx.xs_nmine * rows, cudaMemcpyDeviceToDevice, s));
+    shared_sync(S, rows, ctx.xs_keys.p, ctx.xs_src.p, recvb.p, ctx.xs_mine.p, ctx.xs_g.p, ctx.xs_base, ctx.xs_offs.p,
+                KL, dG, dL, s);
+    CK(cudaStreamSynchronize(s));
 }
 
 /// Shared-replica index over the resident subsets (grad sync): replicas sorted
@@ -1954,8 +2107,8 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         if (sync) {
             // config.grad_sync (worker.hpp:103-144, manager.hpp:351-379): full gradients of
             // every member, shared replicas summed in worker order, then the dense Adam step
-            if (W > 1) throw std::invalid_argument("train_step: grad_sync across ranks is not built (single rank only)");
-            build_shared(*ctx);
+            if (W > 1) build_shared_multi(*ctx);
+            else build_shared(*ctx);
             std::vector<float*> gp;
             std::vector<size_t> gl;
             for (int k : local) {
@@ -1987,8 +2140,25 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             CK(cudaMemcpyAsync(dG.p, gp.data(), (kmax + 1) * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
             CK(cudaMemcpyAsync(dL.p, gl.data(), (kmax + 1) * sizeof(size_t), cudaMemcpyHostToDevice, ctx->stream));
             const int rows = subset(*ctx, local[0]).rows;
-            grad_sync(ctx->sh_slots, rows, ctx->sh_starts.p, ctx->sh_nrep, ctx->sh_keys.p, ctx->sh_reps.p, dG.p, dL.p,
-                      ctx->stream);
+            if (W > 1) {
+                // G pointers in ascending local k (the order of the cross-rank replica numbering)
+                std::vector<float*> gl2;
+                std::vector<size_t> ll2;
+                for (int k : local) {
+                    gl2.push_back(subset(*ctx, k).G.p);
+                    ll2.push_back(subset(*ctx, k).ld);
+                }
+                DevBuf<float*> dG2;
+                DevBuf<size_t> dL2;
+                dG2.ensure(gl2.size());
+                dL2.ensure(ll2.size());
+                CK(cudaMemcpy(dG2.p, gl2.data(), gl2.size() * sizeof(float*), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(dL2.p, ll2.data(), ll2.size() * sizeof(size_t), cudaMemcpyHostToDevice));
+                grad_sync_multi(*ctx, rows, dG2.p, dL2.p, (int)local.size());
+            } else {
+                grad_sync(ctx->sh_slots, rows, ctx->sh_starts.p, ctx->sh_nrep, ctx->sh_keys.p, ctx->sh_reps.p, dG.p,
+                          dL.p, ctx->stream);
+            }
             ++ctx->launches;
             for (int k : local) {
                 SubsetState& S_ = subset(*ctx, k);

@@ -128,6 +128,8 @@ void repart_select(int n, const uint32_t* in, const uint8_t* flags, uint32_t* ou
                    cudaStream_t s);
 void repart_select_iota(int n, const uint8_t* flags, uint32_t* out, int* count, void* temp, size_t tb,
                         cudaStream_t s);
+void repart_select_u64(int n, const uint64_t* in, const uint8_t* flags, uint64_t* out, int* count, void* temp,
+                       size_t tb, cudaStream_t s);
 void repart_gather_replicas(int n, int rows, const uint32_t* winners, const uint32_t* offsets, int K,
                             const float* const* srcP, const float* const* srcM, const float* const* srcV,
                             const uint32_t* const* srcId, const size_t* lds, float* P, float* M, float* V,
@@ -164,6 +166,14 @@ void grad_sync(int nslots, int rows, const uint32_t* starts, int nrep, const uin
 // k_nn (<= 3) smallest squared distances from point i to the others (exact).
 void knn_mean_distance(int n, int k_nn, const float* d_pts, float* d_out, const float lo[3], const float hi[3],
                        cudaStream_t s);
+
+// Cross-rank shared-replica gradient sync (repartition.cu).
+void shared_mark(int n, const uint64_t* keys, uint8_t* flags, cudaStream_t s);
+void shared_pack(int n, int rows, const uint32_t* pos, const uint32_t* sg, uint32_t base, const uint32_t* offs, int KL,
+                 float* const* G, const size_t* lds, float* out, cudaStream_t s);
+void shared_sync(int S, int rows, const uint64_t* skeys, const uint32_t* src, const float* recv, const uint8_t* mine,
+                 const uint32_t* sg, uint32_t base, const uint32_t* offs, int KL, float* const* G, const size_t* lds,
+                 cudaStream_t s);
 
 struct AdamParams {
     float lr[kMaxParamRows];  // per row

@@ -234,7 +234,10 @@ size_t repart_temp_bytes(int64_t n) {
     size_t d = 0;
     cub::DeviceSelect::Flagged(nullptr, d, cub::CountingInputIterator<uint32_t>(0u), (const uint8_t*)nullptr,
                                (uint32_t*)nullptr, (int*)nullptr, (int)n);
-    return std::max(std::max(a, b), std::max(c, d)) + 256;
+    size_t e = 0;
+    cub::DeviceSelect::Flagged(nullptr, e, (const uint64_t*)nullptr, (const uint8_t*)nullptr, (uint64_t*)nullptr,
+                               (int*)nullptr, (int)n);
+    return std::max(std::max(a, b), std::max(c, std::max(d, e))) + 256;
 }
 
 void repart_sort_pairs(uint64_t*& keys, uint64_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt, int n, int bits,
@@ -260,6 +263,11 @@ void repart_first_of_run(int n, const uint64_t* keys, uint8_t* flags, cudaStream
 
 void repart_select(int n, const uint32_t* in, const uint8_t* flags, uint32_t* out, int* count, void* temp, size_t tb,
                    cudaStream_t s) {
+    cub::DeviceSelect::Flagged(temp, tb, in, flags, out, count, n, s);
+}
+
+void repart_select_u64(int n, const uint64_t* in, const uint8_t* flags, uint64_t* out, int* count, void* temp,
+                       size_t tb, cudaStream_t s) {
     cub::DeviceSelect::Flagged(temp, tb, in, flags, out, count, n, s);
 }
 
@@ -394,6 +402,79 @@ void repart_pack(int n, int rows, const uint32_t* idx, const float* P, const flo
 void repart_unpack(int n, int rows, const float* in, float* P, float* M, float* V, uint32_t* ids, uint32_t* mask,
                    size_t ld, cudaStream_t s) {
     if (n > 0) k_unpack<<<blocks(n), 256, 0, s>>>(n, rows, in, P, M, V, ids, mask, ld);
+}
+
+// ---- cross-rank shared-replica gradient sync (grad_sync with world > 1) ----
+namespace {
+
+/// flags[j] = 1 iff sorted replica j belongs to a run of >= 2 replicas of one id.
+__global__ void k_mark_shared(int n, const uint64_t* __restrict__ keys, uint8_t* __restrict__ flags) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint64_t id = keys[j] >> 8;
+    flags[j] = ((j > 0 && (keys[j - 1] >> 8) == id) || (j + 1 < n && (keys[j + 1] >> 8) == id)) ? 1 : 0;
+}
+
+/// Map a global replica index to (local subset slot q, member i) of this rank.
+__device__ __forceinline__ void local_ref(uint32_t g, uint32_t base, const uint32_t* __restrict__ offs, int KL,
+                                          int& q, uint32_t& i) {
+    const uint32_t r = g - base;
+    q = 0;
+    while (q + 1 < KL && offs[q + 1] <= r) ++q;
+    i = r - offs[q];
+}
+
+__global__ void k_pack_shared(int n, int rows, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ sg,
+                              uint32_t base, const uint32_t* __restrict__ offs, int KL, float* const* __restrict__ G,
+                              const size_t* __restrict__ lds, float* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * rows) return;
+    const int e = t / rows, r = t % rows;
+    int q;
+    uint32_t i;
+    local_ref(sg[pos[e]], base, offs, KL, q, i);
+    out[(size_t)e * rows + r] = G[q][(size_t)r * lds[q] + i];
+}
+
+/// sums over each id's replicas in worker (k) order, then written back to
+/// this rank's replicas (manager.hpp:363-371 reduction, worker.hpp:131-140 apply).
+__global__ void k_sync_shared(int S, int rows, const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ src,
+                              const float* __restrict__ recv, const uint8_t* __restrict__ mine,
+                              const uint32_t* __restrict__ sg, uint32_t base, const uint32_t* __restrict__ offs, int KL,
+                              float* const* __restrict__ G, const size_t* __restrict__ lds) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= S * rows) return;
+    const int j = t / rows, r = t % rows;
+    const uint64_t id = skeys[j] >> 8;
+    if (!mine[j]) return;
+    int b = j;
+    while (b > 0 && (skeys[b - 1] >> 8) == id) --b;
+    float acc = 0.0f;
+    for (int e = b; e < S && (skeys[e] >> 8) == id; ++e) {
+        const float g = recv[(size_t)src[e] * rows + r];
+        acc = e == b ? g : fadd(acc, g);
+    }
+    int q;
+    uint32_t i;
+    local_ref(sg[j], base, offs, KL, q, i);
+    G[q][(size_t)r * lds[q] + i] = acc;
+}
+
+}  // namespace
+
+void shared_mark(int n, const uint64_t* keys, uint8_t* flags, cudaStream_t s) {
+    if (n > 0) k_mark_shared<<<blocks(n), 256, 0, s>>>(n, keys, flags);
+}
+void shared_pack(int n, int rows, const uint32_t* pos, const uint32_t* sg, uint32_t base, const uint32_t* offs, int KL,
+                 float* const* G, const size_t* lds, float* out, cudaStream_t s) {
+    if (n > 0) k_pack_shared<<<blocks((int64_t)n * rows), 256, 0, s>>>(n, rows, pos, sg, base, offs, KL, G, lds, out);
+}
+void shared_sync(int S, int rows, const uint64_t* skeys, const uint32_t* src, const float* recv, const uint8_t* mine,
+                 const uint32_t* sg, uint32_t base, const uint32_t* offs, int KL, float* const* G, const size_t* lds,
+                 cudaStream_t s) {
+    if (S > 0)
+        k_sync_shared<<<blocks((int64_t)S * rows), 256, 0, s>>>(S, rows, skeys, src, recv, mine, sg, base, offs, KL,
+                                                                   G, lds);
 }
 
 }  // namespace dgs_b200

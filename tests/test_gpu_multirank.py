@@ -154,3 +154,84 @@ def test_multi_rank_device_repartition_matches_single_rank(tmp_path, world):
                                  axis=1)
             np.testing.assert_array_equal(got[r][f"{tag}{k}"][order_got], ref[order_ref], err_msg=f"subset {k} {tag}")
     mgr.close()
+
+
+def _sync_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from conftest import Golden
+        from host_transport import GlooTransport
+        from paper_2406_11836_b200 import engine
+        g = Golden(NAME)
+        s = g.splats()
+        cfg = engine.train_config(kd_depth=g.args["kd"], grad_sync=1)
+        mgr = engine.Manager(s, cfg, engine.render_options(oracle=g.oracle_mode), device=0, rank=rank, world=world,
+                             transport=GlooTransport())
+        mgr.train_step([g.camera()], g["step_target"][None], g.bg)
+        out = {}
+        K = mgr.table.subset_count
+        for k in range(K):
+            if engine.subset_owner(k, K, world) == rank:
+                p, m, v, step = mgr.ctx.store_subset(k, s.sh_coeffs)
+                out[f"id{k}"] = p.id
+                for tag, x in (("p", p), ("m", m), ("v", v)):
+                    out[f"{tag}{k}"] = np.concatenate([x.mu, x.log_scale, x.rotation, x.opacity_logit[:, None],
+                                                       x.sh.reshape(x.n, -1)], axis=1)
+        np.savez(os.path.join(out_dir, f"sync{rank}.npz"), **out)
+        mgr.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_grad_sync_keeps_replicas_identical(tmp_path, world):
+    """grad_sync across ranks: shared splats held on different ranks receive
+    the same summed gradient, so after the step every replica (p, m, v) is
+    bit-identical across ranks, and the summed-gradient Adam step follows the
+    reference's per-subset gradients (as in tests/test_gpu_gradsync.py)."""
+    from conftest import Golden, adam_lr_rows, post_adam_ok
+    from paper_2406_11836_b200 import engine
+    mp.spawn(_sync_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    g = Golden(NAME)
+    s = g.splats()
+    K = g.subsets()
+    got = [np.load(tmp_path / f"sync{r}.npz") for r in range(world)]
+    seen, cross = {}, 0
+    for k in range(K):
+        r = engine.subset_owner(k, K, world)
+        ids = got[r][f"id{k}"]
+        for i, sid in enumerate(ids):
+            vals = tuple(got[r][f"{t}{k}"][i] for t in "pmv")
+            if int(sid) in seen:
+                r0, v0 = seen[int(sid)]
+                cross += r0 != r
+                for a, b in zip(v0, vals):
+                    np.testing.assert_array_equal(a, b, err_msg=f"replicas of splat {sid} diverged")
+            else:
+                seen[int(sid)] = (r, vals)
+    assert cross > 0, "no splat shared across ranks: the test would be vacuous"
+    # post-Adam against the reference's per-subset gradients summed in worker order
+    off, idl = g["kd_member_off"], g["kd_member_ids"]
+    members = [idl[off[k]:off[k + 1]].astype(np.int64) for k in range(K)]
+    cfg = engine.train_config(kd_depth=g.args["kd"], grad_sync=1)
+    lrs = adam_lr_rows(cfg, s.sh_coeffs)
+    widths = {"mu": 3, "log_scale": 3, "rotation": 4, "opacity_logit": 1, "sh": 3 * s.sh_coeffs}
+    gsum = {}
+    for k in range(K):
+        parts = [g[f"k{k}_grad_d_{f}"].reshape(len(members[k]), -1).astype(np.float32)
+                 for f in ("mu", "log_scale", "rotation", "opacity_logit", "sh")]
+        rows = np.concatenate(parts, axis=1)
+        for j, idx in enumerate(members[k]):
+            sid = int(s.id[idx])
+            gsum[sid] = rows[j].copy() if sid not in gsum else (gsum[sid] + rows[j]).astype(np.float32)
+    lr_row = np.concatenate([np.full(3, lrs["mu"]), np.full(3, lrs["log_scale"]), np.full(4, lrs["rotation"]),
+                             [lrs["opacity_logit"]], np.repeat(np.asarray(lrs["sh"]).ravel(), 3)])
+    p0 = np.concatenate([s.mu, s.log_scale, s.rotation, s.opacity_logit[:, None], s.sh.reshape(s.n, -1)], axis=1)
+    row_of = {int(i): j for j, i in enumerate(s.id)}
+    sids = sorted(seen)
+    got_p = np.stack([seen[i][1][0] for i in sids]).astype(np.float64)
+    want_g = np.stack([gsum[i] for i in sids]).astype(np.float64)
+    want = p0[[row_of[i] for i in sids]].astype(np.float64) - lr_row * want_g / (np.abs(want_g) + cfg.adam_eps)
+    ok, e, noisy = post_adam_ok(got_p, want, want_g, np.broadcast_to(lr_row, want.shape))
+    assert ok.all(), int((~ok).sum())
