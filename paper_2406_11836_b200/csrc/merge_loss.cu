@@ -185,13 +185,34 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
                                           float* __restrict__ gp, float* X, float* Y, float* Hb, float* Vb, int ox,
                                           int oy, double& s_l1, double& s_ssim, double& s_mse) {
     const int tid = threadIdx.x;
-    // stage 0: inputs with zero padding outside the image / provided window
-    for (int i = tid; i < kIn * kIn; i += 256) {
-        const int r = i / kIn, c = i % kIn;
-        const int gy = oy - 2 * kR + r, gx = ox - 2 * kR + c;
-        const bool in = !BORDER || (gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= in_base && gy < in_base + in_rows);
-        X[i] = in ? xp[(size_t)(gy - in_base) * W + gx] : 0.0f;
-        Y[i] = in ? yp[(size_t)(gy - in_base) * W + gx] : 0.0f;
+    // stage 0: inputs with zero padding outside the image / provided window;
+    // all of a thread's loads are issued before any is stored (memory-level parallelism)
+    {
+        constexpr int NIT = (kIn * kIn + 255) / 256;
+        float xr[NIT], yr[NIT];
+#pragma unroll
+        for (int u = 0; u < NIT; ++u) {
+            const int i = tid + u * 256;
+            xr[u] = yr[u] = 0.0f;
+            if (i < kIn * kIn) {
+                const int r = i / kIn, c = i % kIn;
+                const int gy = oy - 2 * kR + r, gx = ox - 2 * kR + c;
+                const bool in =
+                    !BORDER || (gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= in_base && gy < in_base + in_rows);
+                if (in) {
+                    xr[u] = __ldg(xp + (size_t)(gy - in_base) * W + gx);
+                    yr[u] = __ldg(yp + (size_t)(gy - in_base) * W + gx);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < NIT; ++u) {
+            const int i = tid + u * 256;
+            if (i < kIn * kIn) {
+                X[i] = xr[u];
+                Y[i] = yr[u];
+            }
+        }
     }
     __syncthreads();
     // stage 1: horizontal blur of x, y, x*x, y*y, x*y (rows -10..+41, cols -5..+36)
