@@ -168,14 +168,17 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         head_t = cnt ? bt[head & (KBUF - 1)][tid] : kInf;
     };
 
+    // the member index of this thread's entry in the next batch is loaded one batch ahead
+    uint32_t m_next = rg.x + tid < rg.y ? pair_val[rg.x + tid] : 0u;
     for (uint32_t base = rg.x; base < rg.y; base += kBlendThreads) {
         if (__syncthreads_count(!done) == 0) break;
         cur_base = base;
         cur_nb = min((uint32_t)kBlendThreads, rg.y - base);
         const uint32_t p = base + tid;
+        const uint32_t m = m_next;
+        if (p + kBlendThreads < rg.y) m_next = pair_val[p + kBlendThreads];
         if (p < rg.y) {
             float4 A, B, C, D;
-            const uint32_t m = pair_val[p];
             load_rec(recs, m, A, B, C, D);
             D.w = order_bound(fminf(D.w, r_edge), dmax, onorm);
             sA[tid] = A;
