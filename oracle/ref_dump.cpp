@@ -608,6 +608,60 @@ int main(int argc, char** argv) {
             }
         }
 
+        // ---- batch step (Manager::train_step with B views, manager.hpp:313-386;
+        //      worker.hpp:86-127: GradBuffers summed per subset, one Adam step) ----
+        if (has("dump_batch")) {
+            std::vector<int> views;
+            {
+                std::stringstream vs(arg("batch_views", "0,1"));
+                std::string tok;
+                while (std::getline(vs, tok, ',')) views.push_back(std::stoi(tok));
+            }
+            const std::size_t B = views.size();
+            TrainConfig cfg;
+            cfg.iterations = std::uint64_t(iarg("iterations", 2000));
+            cfg.batch_size = int(B);
+            const Real inv_batch = Real(1) / Real(B);
+            std::vector<GradBuffers<Real>> acc;
+            for (int k = 0; k < table.subset_count(); ++k)
+                acc.emplace_back(std::span<const Splat<Real>>(members[k]));
+            double loss_acc = 0.0;
+            std::vector<Real> cams_rec, tgts;
+            for (std::size_t v = 0; v < B; ++v) {
+                const Camera<Real>& c = cams[views[v]];
+                const auto rec = camera_record(c);
+                cams_rec.insert(cams_rec.end(), rec.begin(), rec.end());
+                const Image<Real> target = render_view<Real>(gt_splats, c, bg, oracle_options()).color;
+                tgts.insert(tgts.end(), target.data.begin(), target.data.end());
+                std::vector<PartialImage<Real>> partials;
+                for (int k = 0; k < table.subset_count(); ++k)
+                    partials.push_back(partial_render<Real>(members[k], table.subspaces[k], c, opts));
+                const PixelOrders orders = compute_pixel_orders(table, c);
+                const RenderedImage<Real> img = merge<Real>(partials, orders, bg);
+                LossResult<Real> l = loss<Real>(img.color, target, cfg.lambda_ssim);
+                loss_acc += double(l.value) / double(B);
+                for (auto& g : l.grad.data) g *= inv_batch;
+                const Image<Real> gt0(c.width, c.height, 1, Real(0));
+                auto per = merge_backward<Real>(partials, orders, l.grad, gt0, bg);
+                for (int k = 0; k < table.subset_count(); ++k)
+                    acc[k].add(partial_render_backward<Real>(members[k], table.subspaces[k], c, per[k].d_color,
+                                                             per[k].d_transmittance, opts));
+            }
+            save_npy("batch_loss", std::vector<double>{loss_acc});
+            save_npy("batch_cameras", cams_rec, {B, 13});
+            save_npy("batch_targets", tgts, {B, std::size_t(cams[views[0]].height), std::size_t(cams[views[0]].width), 3});
+            for (int k = 0; k < table.subset_count(); ++k) {
+                const std::string t = "k" + std::to_string(k) + "_";
+                save_grads(t + "batch_grad_", acc[k]);
+                std::vector<Splat<Real>> upd = members[k];
+                std::vector<AdamMoments<Real>> mom;
+                for (const auto& sp : upd) mom.push_back(AdamMoments<Real>::like(sp));
+                const double lr_pos = position_lr(cfg, 0);
+                for (std::size_t i = 0; i < upd.size(); ++i) adam_apply(upd[i], acc[k], i, mom[i], cfg, lr_pos, 1);
+                save_splats(t + "batch_adam_", upd);
+            }
+        }
+
         // ---- timed direct-call train step (CPU baseline) --------------------
         // The sequence of Manager<float>::train_step (manager.hpp:313-386) and
         // the worker side (worker.hpp:62-167) for every subset on this host,

@@ -218,3 +218,28 @@ def test_full_train_step_matches_reference(golden):
             ok, e, noisy = post_adam_ok(getattr(p, f).reshape(want.shape), want, g[f"k{k}_grad_d_{f}"], lrs[f])
             assert ok.all(), (k, f, float(e[~noisy].max()) if (~noisy).any() else 0.0, int((~ok).sum()))
     mgr.close()
+
+
+def test_batch_train_step_matches_reference():
+    """Manager::train_step with a batch of 3 views (manager.hpp:313-386: loss
+    averaged, gradient scaled by 1/B; worker.hpp:86-127: GradBuffers summed over
+    the views, one Adam step) against the reference's own batch step."""
+    from capi_helpers import camera_from_record
+    g = Golden("g7_synth_kd2_batch3")
+    s = g.splats()
+    B = int(g["batch_cameras"].shape[0])
+    cfg = engine.train_config(kd_depth=g.args["kd"], batch_size=B)
+    mgr = engine.Manager(s, cfg, engine.render_options(oracle=g.oracle_mode))
+    cams = [camera_from_record(r) for r in g["batch_cameras"]]
+    res = mgr.train_step(cams, g["batch_targets"], g.bg)
+    want_loss = float(g["batch_loss"][0])
+    assert abs(res["loss"] - want_loss) <= 1e-4 * max(1.0, abs(want_loss)), (res["loss"], want_loss)
+    lrs = adam_lr_rows(cfg, s.sh_coeffs)
+    for k in range(g.subsets()):
+        p, _, _, step = mgr.ctx.store_subset(k, s.sh_coeffs)
+        assert step == 1
+        for f in PARAM_FIELDS:
+            want = g[f"k{k}_batch_adam_{f}"]
+            ok, e, noisy = post_adam_ok(getattr(p, f).reshape(want.shape), want, g[f"k{k}_batch_grad_d_{f}"], lrs[f])
+            assert ok.all(), (k, f, int((~ok).sum()))
+    mgr.close()
