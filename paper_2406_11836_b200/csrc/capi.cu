@@ -2173,39 +2173,32 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         for (int k : (sync ? std::vector<int>{} : local)) {
             SubsetState& S_ = subset(*ctx, k);
             const AdamParams ap = adam_params(*ctx, S_, S_.adam_step + 1);
-            if (batch > 1) {
-                S_.G.ensure(S_.rows * S_.ld);
-                CK(cudaMemsetAsync(S_.G.p, 0, S_.rows * S_.ld * sizeof(float), ctx->stream));
-            }
+            // K9 (gradient record, one per view) + K10 (streaming Adam after the last view)
+            S_.rec.ensure(kGradRecordRows(batch) * S_.ld);
             for (int v = 0; v < batch; ++v) {
                 ViewSlot& vs = S_.slot(v);
                 backward_blend(*ctx, S_, v, ctx->collect_stats ? ctx->stats.p + 1 : nullptr);
-                if (v + 1 < batch) {
-                    Stage st(ctx->timer, kStProjBwd, ctx->stream);
-                    launch_project_bwd((int)S_.n, S_.P.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S_.g2d.p,
-                                       S_.ld, S_.G.p, ctx->bad.p, ctx->stream);
-                    ++ctx->launches;
-                } else {
-                    // K9 (gradient record) + K10 (streaming Adam) with a split event between them
-                    S_.rec.ensure((size_t)kGradRecordRows * S_.ld);
-                    cudaEvent_t a = nullptr, m1 = nullptr, m2 = nullptr, b = nullptr;
-                    if (ctx->timer.on) {
-                        a = ctx->timer.get();
-                        m1 = ctx->timer.get();
-                        m2 = ctx->timer.get();
-                        CK(cudaEventRecord(a, ctx->stream));
-                    }
-                    launch_project_bwd_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro,
-                                            vs.vb.counts, vs.vb.shjac, S_.g2d.p, S_.ld, batch > 1 ? S_.G.p : nullptr, ap,
-                                            ctx->bad.p, S_.rec.p, m1, m2, ctx->stream);
-                    if (ctx->timer.on) {
+                const bool last = v + 1 == batch;
+                cudaEvent_t a = nullptr, m1 = nullptr, m2 = nullptr, b = nullptr;
+                if (ctx->timer.on) {
+                    a = ctx->timer.get();
+                    m1 = ctx->timer.get();
+                    m2 = last ? ctx->timer.get() : nullptr;
+                    CK(cudaEventRecord(a, ctx->stream));
+                }
+                launch_project_bwd_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro,
+                                        vs.vb.counts, vs.vb.shjac, S_.g2d.p, S_.ld, v, batch, ap, ctx->bad.p,
+                                        S_.rec.p, last ? m1 : nullptr, m2, ctx->stream);
+                if (ctx->timer.on) {
+                    if (!last) CK(cudaEventRecord(m1, ctx->stream));
+                    ctx->timer.pending.push_back({kStProjBwd, {a, m1}});
+                    if (last) {
                         b = ctx->timer.get();
                         CK(cudaEventRecord(b, ctx->stream));
-                        ctx->timer.pending.push_back({kStProjBwd, {a, m1}});
                         ctx->timer.pending.push_back({kStAdam, {m2, b}});
                     }
-                    ctx->launches += 2;
                 }
+                ctx->launches += last ? 2 : 1;
             }
             ++S_.adam_step;
         }

@@ -188,14 +188,15 @@ struct AdamParams {
 void launch_project_bwd(int n, const float* P, size_t ld, int sh_coeffs, const ViewParams& vp,
                         const RenderOpts& ro, const uint32_t* counts, const float* g2d, size_t ld2, float* G,
                         int* bad_index, cudaStream_t s);
-// g_rec: scratch of 17 rows x ld floats (the per-member gradient record).
+// g_rec: scratch of kGradRecordRows(nviews) rows x ld floats (the per-member gradient record:
+// 11 non-SH gradient rows summed over the views, then colour adjoint + direction per view).
 // shjac: the preprocess's SH colour Jacobian rows ([10][ld], ViewBins::shjac) or nullptr (read the SH rows).
+// Call once per view v = 0 .. nviews-1 in order; the last call also runs the Adam stream.
 void launch_project_bwd_adam(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, const ViewParams& vp,
                              const RenderOpts& ro, const uint32_t* counts, const float* shjac, const float* g2d,
-                             size_t ld2,
-                             const float* G_extra, const AdamParams& ap, int* bad_index, float* g_rec,
+                             size_t ld2, int view, int nviews, const AdamParams& ap, int* bad_index, float* g_rec,
                              cudaEvent_t mid_end, cudaEvent_t mid_begin, cudaStream_t s);
-constexpr int kGradRecordRows = 17;
+constexpr size_t kGradRecordRows(int nviews) { return 11 + 6 * (size_t)nviews; }
 void launch_adam(int n, float* P, float* M, float* V, size_t ld, int rows, const float* G, const AdamParams& ap,
                  cudaStream_t s);
 
