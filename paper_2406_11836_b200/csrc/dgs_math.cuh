@@ -63,7 +63,9 @@ DGS_HD float dot4(const float* a, const float* b) {
 // must be bit-exact.
 // ---------------------------------------------------------------------------
 #if defined(__CUDA_ARCH__)
-__device__ __constant__ static const uint64_t kExp2fTab[32] = {
+// global (L1-cached through __ldg), not __constant__: the lanes of a warp
+// index it divergently, which the constant cache serialises
+__device__ static const uint64_t kExp2fTab[32] = {
 #else
 static const uint64_t kExp2fTab[32] = {
 #endif
@@ -97,7 +99,11 @@ DGS_HD float glibc_expf(float x) {
     const uint64_t ki = d2u(kd);
     kd = kd - SHIFT;
     const double r = dfma(InvLn2N, xd, -kd);
+#if defined(__CUDA_ARCH__)
+    uint64_t t = __ldg(&kExp2fTab[ki % 32]);
+#else
     uint64_t t = kExp2fTab[ki % 32];
+#endif
     t += ki << (52 - 5);
     const double s = u2d(t);
     const double z = dfma(C0, r, C1);
