@@ -13,7 +13,8 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libdgs_b200.so"
+# DGS_LIB: an alternative build of the same library (compile-time variants in scripts/)
+LIB_PATH = Path(os.environ["DGS_LIB"]) if os.environ.get("DGS_LIB") else _HERE / "libdgs_b200.so"
 
 DGS_OK = 0
 _ERRORS = {1: ValueError, 2: RuntimeError, 3: ArithmeticError, 4: RuntimeError, 5: RuntimeError}

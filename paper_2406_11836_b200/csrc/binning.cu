@@ -18,15 +18,15 @@ namespace dgs_b200 {
 
 namespace {
 
-/// 24-bit sort key: range bits relative to the view's minimum visible range,
-/// clamped (members past the window, and culled members, share the top key;
-/// the blends bound them by the window edge), plus the identity values.
-__global__ void k_key24(const uint32_t* __restrict__ rkey, const uint32_t* __restrict__ dmax_bits,
+/// 16-bit sort key: the range bucket (dgs_types.cuh range_key_shift; culled
+/// members take the top key and emit nothing), plus the identity values.
+__global__ void k_key16(const uint32_t* __restrict__ rkey, const uint32_t* __restrict__ dmax_bits,
                         uint32_t* __restrict__ key, uint32_t* __restrict__ vals, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t b = rkey[i], lo = dmax_bits[1];
-    key[i] = (b == 0xffffffffu || b < lo) ? 0xffffffu : min(b - lo, 0xffffffu);
+    const int sh = range_key_shift(lo, dmax_bits[3]);
+    key[i] = (b == 0xffffffffu || b < lo) ? kRangeKeyMax : min((b - lo) >> sh, kRangeKeyMax);
     vals[i] = (uint32_t)i;
 }
 
@@ -120,9 +120,10 @@ __global__ void k_tile_ranges(const uint16_t* __restrict__ tile, uint32_t P, int
     ranges[t] = make_uint2(lower_bound_u16(tile, P, (uint32_t)t), lower_bound_u16(tile, P, (uint32_t)t + 1));
 }
 
-/// Onesweep policy for the 24-bit member sort, measured on B200
-/// (scripts/sortbench.cu: 10M u32 keys + u32 values, 3 passes): 256 threads x
-/// 23 items 0.250 ms vs 0.313 ms for the library default dispatch.  The other
+/// Onesweep policy for the member sort, measured on B200
+/// (scripts/sortbench.cu: 10M u32 keys + u32 values, 24-bit keys / 3 passes at
+/// the time): 256 threads x 23 items 0.250 ms vs 0.313 ms for the library
+/// default dispatch.  The keys are 16-bit range buckets now (2 passes).  The other
 /// policies of the chain are the library's sm_100 ones (unused by onesweep).
 struct MemberSortHub {
     using Base = cub::detail::radix::policy_hub<uint32_t, uint32_t, int>::Policy1000;
@@ -164,7 +165,7 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
     size_t a = 0, b = 0, c = 0;
     {
         cub::DoubleBuffer<uint32_t> k, v;
-        MemberSort::Dispatch(nullptr, a, k, v, n, 0, 24, true, 0);
+        MemberSort::Dispatch(nullptr, a, k, v, n, 0, kRangeKeyBits, true, 0);
     }
     cub::DoubleBuffer<uint16_t> dk;
     cub::DoubleBuffer<uint32_t> dv;
@@ -187,20 +188,18 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     vb.pairs = 0;
     if (n <= 0) return 0;
     const int blk = 256, grid = (n + blk - 1) / blk;
-    // 1) members by range: 24-bit keys relative to the minimum range (3 radix
-    //    passes; culled members and any beyond the window share the top key)
-    k_key24<<<grid, blk, 0, s>>>(vb.rkey, vb.dmax_bits, scan_buf, sort_vals, n);
+    // 1) members by range bucket: 16-bit keys (2 radix passes)
+    k_key16<<<grid, blk, 0, s>>>(vb.rkey, vb.dmax_bits, scan_buf, sort_vals, n);
     size_t tb = temp_bytes;
+    const uint32_t* sorted_idx;
     {
         cub::DoubleBuffer<uint32_t> k(scan_buf, sort_keys_alt), v(sort_vals, sort_vals_alt);
-        MemberSort::Dispatch(temp, tb, k, v, n, 0, 24, true, s);
-        if (v.Current() != sort_vals_alt)  // 3 passes land in the alternate buffers; keep the contract anyway
-            cudaMemcpyAsync(sort_vals_alt, v.Current(), 4 * (size_t)n, cudaMemcpyDeviceToDevice, s);
+        MemberSort::Dispatch(temp, tb, k, v, n, 0, kRangeKeyBits, true, s);
+        sorted_idx = v.Current();
     }
     // 2) tile counts in range order -> inclusive scan -> pair end offsets
-    //    (the gather is fused into the scan through a transform iterator)
     uint32_t* cnt_sorted = sort_keys_alt;  // the sorted keys are not needed after the sort
-    k_gather_sorted_rects<<<grid, blk, 0, s>>>(sort_vals_alt, reinterpret_cast<const uint2*>(vb.rect), rect_sorted,
+    k_gather_sorted_rects<<<grid, blk, 0, s>>>(sorted_idx, reinterpret_cast<const uint2*>(vb.rect), rect_sorted,
                                                cnt_sorted, n);
     tb = temp_bytes;
     cub::DeviceScan::InclusiveSum(temp, tb, cnt_sorted, scan_buf, n, s);
@@ -213,7 +212,7 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     vb.pairs = P;
     if (P == 0) return 0;
     // 3) emit (tile, member) pairs, range-ordered within every tile
-    k_emit_pairs<<<grid, blk, 0, s>>>(sort_vals_alt, scan_buf, cnt_sorted, rect_sorted, vp.tiles_x, n, vb.pair_tile,
+    k_emit_pairs<<<grid, blk, 0, s>>>(sorted_idx, scan_buf, cnt_sorted, rect_sorted, vp.tiles_x, n, vb.pair_tile,
                                       vb.pair_val);  // scan_buf holds inclusive ends: start = end - count
     // 4) stable LSD radix sort by tile id only
     cub::DoubleBuffer<uint16_t> dk(vb.pair_tile, pair_tile_alt);

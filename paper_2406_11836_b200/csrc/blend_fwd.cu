@@ -122,9 +122,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     pr.pxf = fadd((float)px, 0.5f);
     pr.pyf = fadd((float)py, 0.5f);
     const float dmax = __uint_as_float(dmax_bits[0]);
-    // members whose range is beyond the 24-bit sort window are unordered among
-    // themselves (binning.cu): their bound is the window edge
-    const float r_edge = __uint_as_float(min(dmax_bits[1] + 0xffffffu, 0x7f7fffffu));
+    // tile lists are ordered by 16-bit range bucket (binning.cu): an entry's
+    // bound is the lower edge of its bucket
+    const uint32_t r_lo_bits = dmax_bits[1];
+    const int r_shift = range_key_shift(r_lo_bits, dmax_bits[3]);
 
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     double D0 = 0.0, D1 = 0.0, D2 = 0.0;  // exact-ish sum of c*sigma*A for the backward suffix
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
         if (p < rg.y) {
             float4 A, B, C, D;
             load_rec(recs, m, A, B, C, D);
-            D.w = order_bound(fminf(D.w, r_edge), dmax, onorm);
+            D.w = order_bound(range_bucket_lo(D.w, r_lo_bits, r_shift), dmax, onorm);
             sA[tid] = A;
             sB[tid] = B;
             sC[tid] = C;

@@ -355,7 +355,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vb.counts = vs.counts.ensure(n);
     vb.rkey = vs.rkey.ensure(n);
     vb.ext = vs.ext.ensure(n);
-    vb.dmax_bits = vs.dmax.ensure(3);
+    vb.dmax_bits = vs.dmax.ensure(4);
     vb.err_index = vs.err.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);
     vs.sort_keys_alt.ensure(n);
@@ -378,7 +378,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         vs.temp_bytes = vs.temp.n;
     };
     alloc_pairs();
-    const uint32_t dmax0[3] = {0u, 0x7f7fffffu, 0u};  // (max D, min range, visible count)
+    const uint32_t dmax0[4] = {0u, 0x7f7fffffu, 0u, 0u};  // (max D, min range, visible count, max range)
     CK(cudaMemcpyAsync(vb.dmax_bits, dmax0, sizeof(dmax0), cudaMemcpyHostToDevice, ctx.stream));
     const int int_max = INT_MAX;
     CK(cudaMemcpyAsync(vb.err_index, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));

@@ -159,6 +159,26 @@ __device__ __forceinline__ uint32_t warp_block_mask(float2 ext, float mx, float 
 }
 #endif
 
+#if defined(__CUDACC__)
+/// Member sort keys (binning.cu): the range's float bits above the view's
+/// minimum visible range (lo), in 16-bit buckets of 2^shift ulps, shift sized
+/// by the maximum visible range (hi).  Tile lists are ordered by bucket; the
+/// blends bound every later entry by the lower edge of the current bucket.
+#ifndef DGS_RANGE_KEY_BITS
+#define DGS_RANGE_KEY_BITS 16
+#endif
+constexpr int kRangeKeyBits = DGS_RANGE_KEY_BITS;
+constexpr uint32_t kRangeKeyMax = (1u << kRangeKeyBits) - 1u;
+__device__ __forceinline__ int range_key_shift(uint32_t lo, uint32_t hi) {
+    const uint32_t span = hi > lo ? hi - lo : 0u;
+    return span > kRangeKeyMax ? (32 - __clz(span)) - kRangeKeyBits : 0;
+}
+__device__ __forceinline__ float range_bucket_lo(float r, uint32_t lo, int shift) {
+    const uint32_t b = __float_as_uint(r);
+    return b > lo ? __uint_as_float(lo + (((b - lo) >> shift) << shift)) : r;
+}
+#endif
+
 /// partition.hpp:66-71 locate (first subspace containing x).
 DGS_HD int table_locate(const Table& tb, const float x[3]) {
     for (int k = 0; k < tb.k_count; ++k)

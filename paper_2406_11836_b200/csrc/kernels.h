@@ -17,8 +17,8 @@ struct ViewBins {
     uint32_t* counts = nullptr;      // [n] tile count per member (0 = culled)
     uint32_t* rkey = nullptr;        // [n] range bits (0xffffffff = culled)
     float2* ext = nullptr;           // [n] conservative (x, y) half-extents of the m^2 <= 9 region (warp culling)
-    uint32_t* dmax_bits = nullptr;   // [3] max world_radius over visible members, min range (float bits),
-                                     //     visible member count
+    uint32_t* dmax_bits = nullptr;   // [4] max world_radius over visible members, min range (float bits),
+                                     //     visible member count, max range (float bits)
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
     float* shjac = nullptr;          // [10][ld] (optional): d colour_ch / d dir_a (row 3 ch + a) and the
                                      //     pre-clamp sign mask (row 9, bits) for the gradient record (K9)

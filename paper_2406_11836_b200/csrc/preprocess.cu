@@ -211,15 +211,18 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
         }
     }
     // block max of D and min of the range over visible members -> one atomic each per block
-    __shared__ float s_max[kPreTB / 32], s_min[kPreTB / 32];
-    float m = dmax_local, lo = rmin_local;
+    // (and the max range, which sizes the binning's 16-bit range buckets)
+    __shared__ float s_max[kPreTB / 32], s_min[kPreTB / 32], s_hi[kPreTB / 32];
+    float m = dmax_local, lo = rmin_local, hi = dmax_local > 0.0f ? rmin_local : 0.0f;
     for (int off = 16; off > 0; off >>= 1) {
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
     }
     if ((threadIdx.x & 31) == 0) {
         s_max[threadIdx.x >> 5] = m;
         s_min[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
     }
     const int nvis = __syncthreads_count(dmax_local > 0.0f);
     if (threadIdx.x == 0) {
@@ -227,10 +230,12 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
             m = fmaxf(m, s_max[w]);
             lo = fminf(lo, s_min[w]);
+            hi = fmaxf(hi, s_hi[w]);
         }
         // non-negative floats order like their bit patterns
         if (m > 0.0f) atomicMax(vb.dmax_bits, __float_as_uint(m));
         atomicMin(vb.dmax_bits + 1, __float_as_uint(lo));
+        if (hi > 0.0f) atomicMax(vb.dmax_bits + 3, __float_as_uint(hi));
     }
 }
 

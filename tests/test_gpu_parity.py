@@ -64,18 +64,32 @@ def test_projection_and_tile_bins_bit_exact(golden):
             a = np.sort(ent[off[t]:off[t + 1]])
             b = np.sort(rent[roff[t]:roff[t + 1]])
             np.testing.assert_array_equal(a, b, err_msg=f"tile {t}")
-        check_order_bounds(ctx, k, recs, off, ent)
+        check_order_bounds(ctx, k, recs, off, ent, counts)
     ctx.close()
 
 
-def check_order_bounds(ctx, k, recs, off, ent):
+def range_buckets(recs, counts):
+    """binning.cu k_key16 / dgs_types.cuh range_key_shift: the 16-bit range
+    bucket of every visible member."""
+    bits = recs[:, 15].copy().view(np.uint32).astype(np.int64)
+    vis = counts > 0
+    lo, hi = int(bits[vis].min()), int(bits[vis].max())
+    span = hi - lo
+    shift = max(0, span.bit_length() - 16) if span > 0xFFFF else 0
+    return np.where(vis, (bits - lo) >> shift, 0xFFFF)
+
+
+def check_order_bounds(ctx, k, recs, off, ent, counts=None):
     """The blend kernels' ordering contract (binning.cu): every tile list is
-    ordered by range ||mu - o|| (non-decreasing), which makes
-    sqrt(r_n^2 - D_max^2) a lower bound on t for every later entry."""
-    rng = recs[:, 15]
+    ordered by range bucket (non-decreasing), which makes
+    sqrt(r_lo^2 - D_max^2), r_lo the lower edge of an entry's bucket, a lower
+    bound on t for every later entry."""
+    if counts is None:
+        counts = np.ones(len(recs), np.uint32)
+    key = range_buckets(recs, counts)
     for t in range(len(off) - 1):
         e = ent[off[t]:off[t + 1]]
-        assert (np.diff(rng[e]) >= 0).all(), f"tile {t}: list not in range order"
+        assert (np.diff(key[e]) >= 0).all(), f"tile {t}: list not in range-bucket order"
 
 
 def test_partial_render_and_contributor_order(golden):

@@ -74,7 +74,7 @@ def test_medium_scene_bins_order_and_render(scene):
     for t in range(tiles):
         np.testing.assert_array_equal(np.sort(ent[off[t]:off[t + 1]]), np.sort(rent[roff[t]:roff[t + 1]]),
                                       err_msg=f"tile {t}")
-    check_order_bounds(ctx, 0, recs, off, ent)
+    check_order_bounds(ctx, 0, recs, off, ent, counts)
     assert np.abs(ct - ct_ref).max() <= 1e-4
     c1 = np.minimum(cnt, dbg_cap).astype(np.int64)
     c2 = np.minimum(cnt_ref, dbg_cap).astype(np.int64)
