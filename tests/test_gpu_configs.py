@@ -1,0 +1,104 @@
+"""GPU: BASELINE.json configs 1 and 2 as parity cases.
+
+* C1 — 100k synthetic splats, one 800x800 view, single subset: one full
+  training step (partial render, merge, L1 + D-SSIM, merge adjoint, backward,
+  Adam) against the C restatement of the reference (oracle/dgs_oracle.c,
+  pinned bit-exact to the reference's own goldens in tests/test_oracle_cpu.py)
+  run through the same call sequence (manager.hpp:313-386).
+* C2 — 1M splats, 1920x1080, 2-way KD split: the merged partial maps equal
+  the unsplit render (the reference's merge == monolithic check,
+  test_engine.cpp:171-203, 1e-4 in float) with oracle options.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_binding as ob
+from conftest import adam_lr_rows, post_adam_ok
+from paper_2406_11836_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("mu", "log_scale", "rotation", "opacity_logit", "sh")
+
+
+def test_c1_train_step_matches_oracle():
+    gt = engine.synth_splats(100_000, seed=11, sh_degree=3)
+    cam = engine.ring_camera(800, 800, 0, n_views=64)
+    tmgr = engine.Manager(gt, engine.train_config(kd_depth=0), engine.render_options(oracle=True))
+    target, _ = tmgr.render(cam)
+    tmgr.close()
+    target = np.ascontiguousarray(target, np.float32)
+    s = engine.perturb(gt, 5)
+    bg = np.zeros(3, np.float32)
+    H, W = cam.height, cam.width
+
+    # GPU: Manager::train_step (K = 1)
+    cfg = engine.train_config(kd_depth=0)
+    mgr = engine.Manager(s, cfg, engine.render_options(grad_skip_eps=0.0))
+    res = mgr.train_step([cam], target[None], bg)
+    p, _, _, step = mgr.ctx.store_subset(0, s.sh_coeffs)
+    mgr.close()
+    assert step == 1
+
+    # oracle: the same sequence on the CPU
+    o = ob.opts(False, grad_skip_eps=0.0)
+    ocam = ob.cam_of(cam.record())
+    sub = ob.Sub()
+    sub.n = 0
+    sc = ob.Scene(s)
+    ct = np.zeros((H, W, 4), np.float32)
+    assert ob.lib().orc_partial_render(C.byref(sc.c), C.byref(sub), C.byref(ocam), C.byref(o), ob.p(ct), 0, None,
+                                       None) == 0
+    order = np.zeros((H, W, 1), np.uint16)
+    count = np.zeros((H, W), np.uint16)
+    ob.lib().orc_pixel_orders((ob.Sub * 1)(sub), 1, C.byref(ocam), ob.p(order), ob.p(count))
+    rgb = np.zeros((H, W, 3), np.float32)
+    ob.lib().orc_merge(ob.p(ct), ob.p(order), ob.p(count), 1, W, H, ob.p(bg), ob.p(rgb), None)
+    grad = np.zeros_like(rgb)
+    means = np.zeros(3, np.float32)
+    loss = ob.lib().orc_loss(ob.p(rgb), ob.p(target), W, H, C.c_float(cfg.lambda_ssim), ob.p(grad), ob.p(means))
+    assert abs(res["loss"] - loss) <= 1e-4 * max(1.0, abs(loss)), (res["loss"], loss)
+    gct = np.zeros((1, H, W, 4), np.float32)
+    ob.lib().orc_merge_backward(ob.p(ct), ob.p(order), ob.p(count), 1, W, H, ob.p(grad), ob.p(bg), ob.p(gct))
+    gr, garr = ob.empty_grads(s.n, s.sh_coeffs)
+    assert ob.lib().orc_partial_backward(C.byref(sc.c), C.byref(sub), C.byref(ocam), C.byref(o), ob.p(gct[0]),
+                                         C.byref(gr)) == 0
+    want = s.copy()
+    rows = 11 + 3 * s.sh_coeffs
+    mm = np.zeros((s.n, rows), np.float32)
+    vv = np.zeros((s.n, rows), np.float32)
+    ob.lib().orc_adam(C.c_int64(s.n), s.sh_coeffs, ob.p(want.mu), ob.p(want.log_scale), ob.p(want.rotation),
+                      ob.p(want.opacity_logit), ob.p(want.sh), ob.p(mm), ob.p(vv), C.byref(gr),
+                      C.c_double(cfg.lr_position_start), C.c_double(cfg.lr_scale), C.c_double(cfg.lr_rotation),
+                      C.c_double(cfg.lr_opacity), C.c_double(cfg.lr_sh_dc), C.c_double(cfg.lr_sh_rest),
+                      C.c_double(cfg.adam_beta1), C.c_double(cfg.adam_beta2), C.c_double(cfg.adam_eps),
+                      C.c_uint64(1))
+
+    # members by id (the subset stores them in its own order)
+    row = {int(i): j for j, i in enumerate(s.id)}
+    sel = np.array([row[int(i)] for i in p.id], np.int64)
+    lrs = adam_lr_rows(cfg, s.sh_coeffs)
+    assert np.abs(garr["d_mu"]).max() > 0
+    for f in FIELDS:
+        got = getattr(p, f)
+        ok, e, noisy = post_adam_ok(got, getattr(want, f)[sel], garr["d_" + f][sel], lrs[f])
+        assert ok.all(), (f, float(e[~noisy].max()) if (~noisy).any() else 0.0, int((~ok).sum()))
+
+
+def test_c2_kd_split_merge_equals_unsplit_render():
+    s = engine.synth_splats(1_000_000, seed=11, sh_degree=3)
+    cam = engine.ring_camera(1920, 1080, 0, n_views=64)
+    ro = engine.render_options(oracle=True)
+    out = {}
+    for depth in (0, 1):
+        mgr = engine.Manager(s, engine.train_config(kd_depth=depth), ro)
+        if depth == 1:
+            assert mgr.table.subset_count == 2
+        out[depth] = mgr.render(cam)
+        mgr.close()
+    (rgb0, t0), (rgb1, t1) = out[0], out[1]
+    assert t0.min() < 0.5  # the view sees the scene
+    assert np.abs(rgb1 - rgb0).max() <= 1e-4, float(np.abs(rgb1 - rgb0).max())
+    assert np.abs(t1 - t0).max() <= 1e-4, float(np.abs(t1 - t0).max())
