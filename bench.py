@@ -330,8 +330,11 @@ def b200_arm(a, world, rank, local_rank):
     achieved = alg_bytes[roof_kernel] / (t_kernel_ms / 1e3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(roof_kernel)
+    tj = json.loads(tf.read_text()) if tf.exists() else {}
+    # ncu bytes are only meaningful for the workload they were captured on
+    if any(tj.get(k) not in (None, v) for k, v in (("gaussians", a.count), ("width", a.width), ("height", a.height))):
+        tj = {}
+    traffic = tj.get(roof_kernel)
 
     # ---- CPU baseline (rank 0, N = 1) ------------------------------------------------
     cpu = None
@@ -372,7 +375,6 @@ def b200_arm(a, world, rank, local_rank):
         "adam": ("hbm", alg_bytes["adam"]),
     }
     kernels = {}
-    tj = json.loads(tf.read_text()) if tf.exists() else {}
     for k, (bound, amount) in algo.items():
         t = per_stage.get(k, 0.0)
         if t <= 0:

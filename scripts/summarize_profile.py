@@ -96,6 +96,9 @@ print("full-set kernels:", ", ".join(last))
 key_map = {"k_adam_stream4": "adam", "k_preprocess": "preprocess", "k_grad_record": "project_bwd"}
 out = {"note": f"dram__bytes_read.sum + dram__bytes_write.sum per launch from one ncu --set full capture "
                f"({tag}_ncu_full_summary.csv)"}
+if (src / "bench.json").exists():  # the workload these bytes belong to (bench.py matches it)
+    cfg = json.loads((src / "bench.json").read_text()).get("config", {})
+    out.update({k: cfg.get(k) for k in ("gaussians", "width", "height", "batch", "kd_subsets")})
 for k, v in traffic.items():
     for pre, name in key_map.items():
         if k.startswith(pre):
