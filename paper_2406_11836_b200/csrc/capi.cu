@@ -16,6 +16,7 @@
 #include <memory>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dgs_capi.h"
@@ -226,6 +227,12 @@ struct Ctx {
     DevBuf<float> tgt_stage;                  // host targets prefetched on copy_stream (HWC windows, all views)
     cudaStream_t copy_stream = nullptr;       // H2D of host targets, overlapped with the forward
     cudaEvent_t copy_done = nullptr;
+    // pageable host targets: a helper thread copies them into this pinned
+    // buffer chunk by chunk and queues each chunk's H2D, while the forward runs
+    float* pin_stage = nullptr;
+    size_t pin_cap = 0;
+    std::thread stager;
+    std::string stager_err;
     DevBuf<double> block_sums, sums;
     DevBuf<const float4*> partial_ptrs;
     DevBuf<float4*> grad_ptrs;
@@ -1096,7 +1103,10 @@ int dgs_ctx_destroy(dgs_ctx* ctx) {
     return dgs_guard([&] {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
+        if (ctx->stager.joinable()) ctx->stager.join();
         cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->copy_stream);
+        if (ctx->pin_stage) cudaFreeHost(ctx->pin_stage);
         if (ctx->comm) nccl().CommDestroy(ctx->comm);
         ctx->subsets.clear();
         cudaStreamDestroy(ctx->stream);
@@ -1990,12 +2000,69 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             ctx->tgt_stage.ensure(tgt_win * batch);
             CK(cudaEventRecord(ctx->copy_done, ctx->stream));  // staging reuse: previous step's readers are done
             CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_done, 0));
-            for (int v = 0; v < batch; ++v)
-                CK(cudaMemcpyAsync(ctx->tgt_stage.p + (size_t)v * tgt_win,
-                                   targets + (size_t)v * 3 * Wd0 * H0 + (size_t)h0 * Wd0 * 3, tgt_win * 4,
-                                   cudaMemcpyHostToDevice, ctx->copy_stream));
-            CK(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+            cudaPointerAttributes at{};
+            const bool pinned = cudaPointerGetAttributes(&at, targets) == cudaSuccess && at.type == cudaMemoryTypeHost;
+            cudaGetLastError();  // unregistered pointers may leave an error on older runtimes
+            if (pinned) {
+                for (int v = 0; v < batch; ++v)
+                    CK(cudaMemcpyAsync(ctx->tgt_stage.p + (size_t)v * tgt_win,
+                                       targets + (size_t)v * 3 * Wd0 * H0 + (size_t)h0 * Wd0 * 3, tgt_win * 4,
+                                       cudaMemcpyHostToDevice, ctx->copy_stream));
+                CK(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+            } else {
+                // pageable: cudaMemcpyAsync would stage synchronously on this thread
+                // (the GPU idles meanwhile); copy through pinned memory on a helper
+                // thread instead, overlapped with the forward (the previous step's
+                // H2D from pin_stage completed before its loss)
+                if (ctx->pin_cap < tgt_win * batch) {
+                    if (ctx->pin_stage) CK(cudaFreeHost(ctx->pin_stage));
+                    ctx->pin_stage = nullptr;
+                    CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pin_stage), tgt_win * batch * 4,
+                                     cudaHostAllocDefault));
+                    ctx->pin_cap = tgt_win * batch;
+                }
+                const size_t plane_all = (size_t)3 * Wd0 * H0, row0 = (size_t)h0 * Wd0 * 3;
+                Ctx* cx = ctx;
+                ctx->stager_err.clear();
+                ctx->stager = std::thread([cx, targets, batch, tgt_win, plane_all, row0] {
+                    // host memcpy bandwidth per core is the limit: split the copy over a
+                    // few threads, each queueing the H2D of its 1 MB pieces as they land
+                    const unsigned hw = std::thread::hardware_concurrency();
+                    const int nt = (int)std::max(1u, std::min(8u, hw ? hw / 2 : 1u));
+                    const size_t total = tgt_win * (size_t)batch, per = (total + nt - 1) / nt;
+                    std::vector<std::thread> ws;
+                    std::vector<int> bad(nt, 0);
+                    for (int w = 0; w < nt; ++w)
+                        ws.emplace_back([&, w] {
+                            cudaSetDevice(cx->device);
+                            constexpr size_t kPiece = (size_t)1 << 18;  // floats (1 MB)
+                            const size_t b = std::min(total, (size_t)w * per), e = std::min(total, b + per);
+                            for (size_t o = b; o < e;) {
+                                const size_t v = o / tgt_win, in_v = o - v * tgt_win;
+                                const size_t len = std::min({kPiece, e - o, tgt_win - in_v});
+                                std::memcpy(cx->pin_stage + o, targets + v * plane_all + row0 + in_v, len * 4);
+                                if (cudaMemcpyAsync(cx->tgt_stage.p + o, cx->pin_stage + o, len * 4,
+                                                    cudaMemcpyHostToDevice, cx->copy_stream) != cudaSuccess)
+                                    bad[w] = 1;
+                                o += len;
+                            }
+                        });
+                    for (auto& t : ws) t.join();
+                    cudaSetDevice(cx->device);
+                    for (int w = 0; w < nt; ++w)
+                        if (bad[w]) cx->stager_err = "train_step: target upload failed";
+                    if (cudaEventRecord(cx->copy_done, cx->copy_stream) != cudaSuccess)
+                        cx->stager_err = "train_step: target upload event failed";
+                });
+            }
         }
+        // the stager (if any) is joined before the loss waits for the copy, and on every exit
+        struct JoinStager {
+            Ctx* c;
+            ~JoinStager() {
+                if (c->stager.joinable()) c->stager.join();
+            }
+        } join_stager{ctx};
         bool waited_copy = false;
         for (int v = 0; v < batch; ++v) {
             const ViewParams& vp = vps[v];
@@ -2064,6 +2131,8 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                     tgt = ctx->targets_win.p;
                 } else {
                     if (!waited_copy) {
+                        if (ctx->stager.joinable()) ctx->stager.join();
+                        if (!ctx->stager_err.empty()) throw std::runtime_error(ctx->stager_err);
                         CK(cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
                         waited_copy = true;
                     }
