@@ -8,6 +8,8 @@
 * C2 — 1M splats, 1920x1080, 2-way KD split: the merged partial maps equal
   the unsplit render (the reference's merge == monolithic check,
   test_engine.cpp:171-203, 1e-4 in float) with oracle options.
+* The three ways targets reach the step (pageable host, pinned host,
+  device-resident) give the same loss.
 """
 import ctypes as C
 
@@ -102,3 +104,31 @@ def test_c2_kd_split_merge_equals_unsplit_render():
     assert t0.min() < 0.5  # the view sees the scene
     assert np.abs(rgb1 - rgb0).max() <= 1e-4, float(np.abs(rgb1 - rgb0).max())
     assert np.abs(t1 - t0).max() <= 1e-4, float(np.abs(t1 - t0).max())
+
+
+def test_host_target_paths_agree():
+    """Pinned host targets (direct H2D) and pageable ones (staged through
+    pinned memory by helper threads) give the same step as device-resident
+    targets: the forward and the loss are deterministic, so the loss is
+    bit-identical."""
+    import torch
+
+    s = engine.synth_splats(20_000, seed=3, sh_degree=3)
+    cam = engine.ring_camera(320, 180, 2, n_views=64)
+    rng = np.random.default_rng(1)
+    target = rng.random((1, 180, 320, 3), dtype=np.float32)
+    pinned = torch.empty(target.size, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = target.reshape(-1)
+    losses = []
+    for mode in ("pageable", "pinned", "device"):
+        mgr = engine.Manager(s, engine.train_config(kd_depth=1), engine.render_options())
+        if mode == "pageable":
+            r = mgr.train_step([cam], target)
+        elif mode == "pinned":
+            r = mgr.train_step([cam], pinned.numpy().reshape(target.shape))
+        else:
+            tdev = mgr.ctx.upload_targets(target)
+            r = mgr.train_step([cam], None, targets_device_ptr=tdev)
+        losses.append(r["loss"])
+        mgr.close()
+    assert losses[0] == losses[1] == losses[2], losses
