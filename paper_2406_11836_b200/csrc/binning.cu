@@ -113,6 +113,42 @@ __device__ __forceinline__ uint32_t lower_bound_u16(const uint16_t* __restrict__
     return lo;
 }
 
+/// Longest lists first: the blends take tiles in this order, so the long
+/// tiles start in the first waves instead of setting the kernel's tail.  One
+/// CTA: tiles are bucketed by list length on a half-octave scale (64 buckets,
+/// longest first), the order within a bucket is arbitrary (scheduling only:
+/// every tile's work is independent of the block order).
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int tiles,
+                                                     uint32_t* __restrict__ order) {
+    __shared__ uint32_t cnt[64], start[64];
+    const int tid = threadIdx.x;
+    if (tid < 64) cnt[tid] = 0;
+    __syncthreads();
+    auto bucket = [](uint32_t len) -> uint32_t {  // 63 = longest
+        if (len == 0) return 0;
+        const uint32_t lg = 31u - __clz(len);
+        const uint32_t half = lg > 0 ? (len >> (lg - 1)) & 1u : 0u;
+        return min(2u * lg + half + 1u, 63u);
+    };
+    for (int t = tid; t < tiles; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        atomicAdd(&cnt[bucket(r.y - r.x)], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t acc = 0;
+        for (int b = 63; b >= 0; --b) {
+            start[b] = acc;
+            acc += cnt[b];
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < tiles; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        order[atomicAdd(&start[bucket(r.y - r.x)], 1u)] = (uint32_t)t;
+    }
+}
+
 /// Per-tile [start, end) by binary search over the sorted tile keys (one thread per tile).
 __global__ void k_tile_ranges(const uint16_t* __restrict__ tile, uint32_t P, int tiles, uint2* __restrict__ ranges) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -225,6 +261,8 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     }
     // 5) per-tile [start, end)
     k_tile_ranges<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(vb.pair_tile, (uint32_t)P, tiles, vb.ranges);
+    // 6) block order for the blends: tiles by decreasing list length
+    if (vb.tile_order) k_tile_order<<<1, 1024, 0, s>>>(vb.ranges, tiles, vb.tile_order);
     return P;
 }
 

@@ -187,8 +187,10 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                                                              const uint8_t* __restrict__ ovf_flag,
                                                              const uint8_t* __restrict__ tile_replay,
                                                              float* __restrict__ g2d, size_t ld2,
-                                                             BlendStats* __restrict__ stats) {
-    if (tile_replay != nullptr && tile_replay[blockIdx.x] == 0) return;  // handled by k_blend_bwd_rec
+                                                             BlendStats* __restrict__ stats,
+                                                             const uint32_t* __restrict__ tile_order) {
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+    if (tile_replay != nullptr && tile_replay[tile] == 0) return;  // handled by k_blend_bwd_rec
     extern __shared__ float4 smem4[];
     float4* sA = smem4;
     float4* sB = sA + kBlendThreads;
@@ -205,7 +207,6 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                                                 (kBlendThreads / 32) * kBlendThreads);
 
     const int tid = threadIdx.x, lane = tid & 31;
-    const int tile = blockIdx.x;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
     int px, py;
     tile_pixel(tid, tx, ty, px, py);
@@ -419,8 +420,9 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
                                                                  const float4* __restrict__ grad_ct,
                                                                  const uint8_t* __restrict__ ovf_flag,
                                                                  CompRecords crec, float* __restrict__ g2d,
-                                                                 size_t ld2, BlendStats* __restrict__ stats) {
-    const int tile = blockIdx.x;
+                                                                 size_t ld2, BlendStats* __restrict__ stats,
+                                                                 const uint32_t* __restrict__ tile_order) {
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     if (crec.tile_replay[tile]) return;  // handled by the replay kernel
     const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
@@ -618,20 +620,24 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
     if (rec.pos != nullptr) {
         if (stats)
             k_blend_bwd_rec<true><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
-                                                                  fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats);
+                                                                  fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats,
+                                                                   vb.tile_order);
         else
             k_blend_bwd_rec<false><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
-                                                                   fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats);
+                                                                   fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats,
+                                                                   vb.tile_order);
     }
     // replay: flagged tiles only (every tile without records)
     if (stats)
         k_blend_bwd<true><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
                                                                  vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
-                                                                 ovf_flag, rec.tile_replay, g2d, ld2, stats);
+                                                                 ovf_flag, rec.tile_replay, g2d, ld2, stats,
+                                                                  vb.tile_order);
     else
         k_blend_bwd<false><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
                                                                   vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
-                                                                  ovf_flag, rec.tile_replay, g2d, ld2, stats);
+                                                                  ovf_flag, rec.tile_replay, g2d, ld2, stats,
+                                                                  vb.tile_order);
 }
 
 void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,

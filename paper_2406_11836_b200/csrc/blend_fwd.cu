@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                                                              uint32_t* __restrict__ dbg_ids,
                                                              uint32_t* __restrict__ dbg_cnt, int dbg_cap,
                                                              BlendStats* __restrict__ stats,
-                                                             double* __restrict__ out_cd, CompRecords crec) {
+                                                             double* __restrict__ out_cd, CompRecords crec,
+                                                             const uint32_t* __restrict__ tile_order) {
     extern __shared__ float4 smem4[];
     float4* sA = smem4;
     float4* sB = sA + kBlendThreads;
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                                                 (kBlendThreads / 32) * kBlendThreads);
 
     const int tid = threadIdx.x;
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
     int px, py;
     tile_pixel(tid, tx, ty, px, py);
@@ -395,7 +396,7 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
 #define DGS_FWD(D, S)                                                                                              \
     k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, vb.dmax_bits, \
                                                          onorm, out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids,       \
-                                                         dbg_cnt, dbg_cap, stats, out_cd, rec)
+                                                         dbg_cnt, dbg_cap, stats, out_cd, rec, vb.tile_order)
     if (dbg_ids != nullptr && dbg_cnt != nullptr) DGS_FWD(true, true);
     else if (stats != nullptr) DGS_FWD(false, true);
     else DGS_FWD(false, false);

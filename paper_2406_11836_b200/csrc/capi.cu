@@ -99,6 +99,7 @@ struct ViewSlot {
     DevBuf<uint32_t> sort_keys_alt, sort_vals, sort_vals_alt, scan, ovf_list, ovf_count;
     DevBuf<int> err;
     DevBuf<uint2> ranges;
+    DevBuf<uint32_t> tile_order;
     DevBuf<uint8_t> temp, ovf_flag;
     DevBuf<float4> ct, grad_ct;
     DevBuf<double> cd;  // double colour sums for the backward suffix
@@ -365,6 +366,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vb.dmax_bits = vs.dmax.ensure(4);
     vb.err_index = vs.err.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);
+    vb.tile_order = vs.tile_order.ensure(tiles);
     vs.sort_keys_alt.ensure(n);
     vs.sort_vals.ensure(n);
     vs.sort_vals_alt.ensure(n);

@@ -25,6 +25,7 @@ struct ViewBins {
     uint16_t* pair_tile = nullptr;   // [cap] tile key of each (splat, tile) pair
     uint32_t* pair_val = nullptr;    // [cap] member index
     uint2* ranges = nullptr;         // [tiles] (start, end) into the sorted pair list
+    uint32_t* tile_order = nullptr;  // [tiles] tiles by decreasing list length (the blends' block order)
     int64_t pairs = 0;
     int64_t visible = 0;
 };
