@@ -43,11 +43,6 @@ __global__ void k_gather_sorted_rects(const uint32_t* __restrict__ sorted_idx, c
     cnt_sorted[j] = (x1 >= x0 && y1 >= y0) ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
 }
 
-__global__ void k_gather_counts(const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ counts,
-                                uint32_t* __restrict__ out, int n) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < n) out[j] = counts[sorted_idx[j]];
-}
 
 /// Pair emission, warp-cooperative: the warp's 32 members (in range order)
 /// own a contiguous run of output slots; lane l writes slots l, l+32, ...
@@ -184,10 +179,6 @@ struct MemberSortHub {
 };
 using MemberSort = cub::DispatchRadixSort<false, uint32_t, uint32_t, int, MemberSortHub>;
 
-struct CountOf {
-    const uint32_t* counts;
-    __host__ __device__ uint32_t operator()(uint32_t i) const { return counts[i]; }
-};
 
 int bits_for(uint32_t v) {
     int b = 1;
@@ -206,11 +197,7 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
     cub::DoubleBuffer<uint16_t> dk;
     cub::DoubleBuffer<uint32_t> dv;
     cub::DeviceRadixSort::SortPairs(nullptr, b, dk, dv, (int)pair_cap, 0, 16);
-    cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it((const uint32_t*)nullptr, CountOf{nullptr});
-    cub::DeviceScan::InclusiveSum(nullptr, c, it, (uint32_t*)nullptr, n);
-    size_t c2 = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, c2, (const uint32_t*)nullptr, (uint32_t*)nullptr, n);
-    c = c > c2 ? c : c2;
+    cub::DeviceScan::InclusiveSum(nullptr, c, (const uint32_t*)nullptr, (uint32_t*)nullptr, n);
     size_t m = a > b ? a : b;
     return (m > c ? m : c) + 256;
 }
