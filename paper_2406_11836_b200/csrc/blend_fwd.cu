@@ -80,6 +80,14 @@ __device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint
     D = __ldg(r4 + 3);
 }
 
+/// Forward blend of one tile (CTA, 256 pixel slots).  Candidates are staged in
+/// list batches of 256; every warp composites the candidates its pixels can
+/// see through a per-pixel (t, id) ring.  Pixels terminate at very different
+/// depths, so warps soon run at a few live lanes: at a batch boundary, once the
+/// live pixels fit in fewer warps, they are re-packed (slot order kept, so a
+/// warp's pixels stay close) and every warp culls candidates against the
+/// bounding box of its own pixels.  Per-pixel state moves through shared
+/// memory; the ring stays in place (indexed by pixel slot).
 template <bool DBG, bool STATS>
 __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, RenderOpts ro, Subspace gate,
                                                              const SplatRec* __restrict__ recs,
@@ -110,34 +118,53 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     uint16_t* wlist = reinterpret_cast<uint16_t*>(bpos + KBUF) + (threadIdx.x >> 5) * kBlendThreads;
     uint8_t* smask = reinterpret_cast<uint8_t*>(reinterpret_cast<uint16_t*>(bpos + KBUF) +
                                                 (kBlendThreads / 32) * kBlendThreads);
+    __shared__ float4 wbox[kBlendThreads / 32];  // per warp: pixel-centre x range, y range of its slots
+    __shared__ int s_woff[kBlendThreads / 32];
+    __shared__ int s_short;
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
-    int px, py;
-    tile_pixel(tid, tx, ty, px, py);
-    const bool inside = px < vp.width && py < vp.height;
-    const size_t pix = (size_t)py * vp.width + px;
-    PixelRay pr;
-    pixel_ray_dir(vp, px, py, pr.d);
-    pr.pxf = fadd((float)px, 0.5f);
-    pr.pyf = fadd((float)py, 0.5f);
     const float dmax = __uint_as_float(dmax_bits[0]);
     // tile lists are ordered by 16-bit range bucket (binning.cu): an entry's
     // bound is the lower edge of its bucket
     const uint32_t r_lo_bits = dmax_bits[1];
     const int r_shift = range_key_shift(r_lo_bits, dmax_bits[3]);
+    const uint2 rg = ranges[tile];
+    const bool record = crec.pos != nullptr && rg.y - rg.x <= 65535u;
 
+    // ---- per-slot pixel state (the slot travels with the pixel when re-packed) ----
+    int q = tid;  // pixel slot: tile_pixel order
+    bool valid = true;
+    int px, py;
+    size_t pix;
+    bool inside;
+    PixelRay pr;
+    uint16_t* rec16;
+    auto bind_slot = [&]() {
+        tile_pixel(q, tx, ty, px, py);
+        inside = px < vp.width && py < vp.height;
+        pix = (size_t)py * vp.width + px;
+        pixel_ray_dir(vp, px, py, pr.d);
+        pr.pxf = fadd((float)px, 0.5f);
+        pr.pyf = fadd((float)py, 0.5f);
+        rec16 = record ? crec.pos + (size_t)tile * kRecCap * kBlendThreads + 4 * q : nullptr;
+    };
+    bind_slot();
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     double D0 = 0.0, D1 = 0.0, D2 = 0.0;  // exact-ish sum of c*sigma*A for the backward suffix
     bool done = !inside, ovf = false;
     int head = 0, cnt = 0, nemit = 0;
     float head_t = kInf;
-    unsigned long long n_eval = 0;
-    const uint2 rg = ranges[tile];
+    unsigned long long n_eval = 0, n_contrib = 0, n_ovf = 0;
     uint32_t cur_base = rg.x, cur_nb = 0;  // batch currently staged in shared memory
-    const bool record = crec.pos != nullptr && rg.y - rg.x <= 65535u;
-    uint16_t* rec16 = record ? crec.pos + (size_t)tile * kRecCap * kBlendThreads + 4 * tid : nullptr;
+    if (tid < kBlendThreads / 32) {  // the fixed 8x4 blocks
+        const float x0 = fadd((float)(tx * kTileSize + (tid & 1) * 8), 0.5f);
+        const float y0 = fadd((float)(ty * kTileSize + (tid >> 1) * 4), 0.5f);
+        wbox[tid] = make_float4(x0, fadd(x0, 7.0f), y0, fadd(y0, 3.0f));
+    }
+    if (tid == 0) s_short = 0;
+    int live_warps = kBlendThreads / 32;
 
     auto emit_head = [&]() {
         if (ro.stop > 0.0f && T < ro.stop) {  // raster.hpp:183
@@ -147,8 +174,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             return;
         }
         const int sl = head & (KBUF - 1);
-        const float sg = bs[sl][tid];
-        const uint32_t lp = bpos[sl][tid];
+        const float sg = bs[sl][q];
+        const uint32_t lp = bpos[sl][q];
         const float4 col = (lp - cur_base < cur_nb) ? sD[lp - cur_base]
                                                     : __ldg(reinterpret_cast<const float4*>(recs + pair_val[lp]) + 3);
         if (record && nemit < kRecCap) rec16[(nemit >> 2) * (4 * kBlendThreads) + (nemit & 3)] = (uint16_t)(lp - rg.x);
@@ -163,17 +190,109 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             D2 += (double)col.z * wd;
         }
         T = fmul(T, fsub(1.0f, sg));
-        if (DBG && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][tid];
+        if (DBG && nemit < dbg_cap) dbg_ids[pix * dbg_cap + nemit] = bid[sl][q];
         ++nemit;
         ++head;
         --cnt;
-        head_t = cnt ? bt[head & (KBUF - 1)][tid] : kInf;
+        head_t = cnt ? bt[head & (KBUF - 1)][q] : kInf;
+    };
+    // final values of this slot's pixel (once it is done, or at the end)
+    auto write_out = [&]() {
+        if (!inside) return;
+        if (crec.pos != nullptr) {
+            if (!ovf && nemit > kRecCap) s_short = 1;  // records incomplete: the backward replays the tile
+            crec.cnt[pix] = (uint16_t)min(nemit, kRecCap);
+        }
+        if (ovf) {
+            ovf_flag[pix] = 1;
+            ovf_list[atomicAdd(ovf_count, 1u)] = (uint32_t)pix;
+        } else {
+            ovf_flag[pix] = 0;
+            out_ct[pix] = make_float4(C0, C1, C2, T);
+            if (out_cd != nullptr) {
+                out_cd[3 * pix] = D0;
+                out_cd[3 * pix + 1] = D1;
+                out_cd[3 * pix + 2] = D2;
+            }
+            if (DBG) dbg_cnt[pix] = (uint32_t)nemit;
+        }
+        if (STATS) {
+            n_contrib += (unsigned long long)nemit;
+            n_ovf += ovf ? 1ull : 0ull;
+        }
     };
 
     // the member index of this thread's entry in the next batch is loaded one batch ahead
     uint32_t m_next = rg.x + tid < rg.y ? pair_val[rg.x + tid] : 0u;
     for (uint32_t base = rg.x; base < rg.y; base += kBlendThreads) {
-        if (__syncthreads_count(!done) == 0) break;
+        const int nact = __syncthreads_count(valid && !done);
+        if (nact == 0) break;
+        if ((nact + 31) / 32 < live_warps) {
+            // ---- re-pack the live pixels into the first warps (slot order kept) ----
+            if (valid && done) {
+                write_out();
+                valid = false;
+            }
+            const bool live = valid && !done;
+            const unsigned bm = __ballot_sync(0xffffffffu, live);
+            if (lane == 0) s_woff[wid] = __popc(bm);
+            __syncthreads();
+            int rank = __popc(bm & ((1u << lane) - 1u));
+            for (int w = 0; w < wid; ++w) rank += s_woff[w];
+            // state through the staging area (its batch is fully consumed)
+            // (16 KB: 5 float rows at 0, 4 int rows at 5 KB, 3 double rows at 9 KB)
+            char* st = reinterpret_cast<char*>(sA);
+            float* fs = reinterpret_cast<float*>(st);
+            int* is = reinterpret_cast<int*>(st + 5 * kBlendThreads * sizeof(float));
+            double* ds = reinterpret_cast<double*>(st + 9 * kBlendThreads * sizeof(float));
+            if (live) {
+                fs[rank] = T;
+                fs[kBlendThreads + rank] = C0;
+                fs[2 * kBlendThreads + rank] = C1;
+                fs[3 * kBlendThreads + rank] = C2;
+                fs[4 * kBlendThreads + rank] = head_t;
+                ds[rank] = D0;
+                ds[kBlendThreads + rank] = D1;
+                ds[2 * kBlendThreads + rank] = D2;
+                is[rank] = q;
+                is[kBlendThreads + rank] = head;
+                is[2 * kBlendThreads + rank] = cnt;
+                is[3 * kBlendThreads + rank] = nemit;
+            }
+            __syncthreads();
+            valid = tid < nact;
+            done = !valid;
+            if (valid) {
+                T = fs[tid];
+                C0 = fs[kBlendThreads + tid];
+                C1 = fs[2 * kBlendThreads + tid];
+                C2 = fs[3 * kBlendThreads + tid];
+                head_t = fs[4 * kBlendThreads + tid];
+                D0 = ds[tid];
+                D1 = ds[kBlendThreads + tid];
+                D2 = ds[2 * kBlendThreads + tid];
+                q = is[tid];
+                head = is[kBlendThreads + tid];
+                cnt = is[2 * kBlendThreads + tid];
+                nemit = is[3 * kBlendThreads + tid];
+                ovf = false;
+                bind_slot();
+            }
+            live_warps = (nact + 31) / 32;
+            {
+                const float bx = valid ? pr.pxf : kInf, by = valid ? pr.pyf : kInf;
+                const float ex = valid ? pr.pxf : -kInf, ey = valid ? pr.pyf : -kInf;
+                float x0 = bx, y0 = by, x1 = ex, y1 = ey;
+                for (int off = 16; off > 0; off >>= 1) {
+                    x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+                    y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+                    x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+                    y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+                }
+                if (lane == 0) wbox[wid] = make_float4(x0, x1, y0, y1);  // empty warps: an empty box
+            }
+            __syncthreads();  // boxes visible; the staging area is free again
+        }
         cur_base = base;
         cur_nb = min((uint32_t)kBlendThreads, rg.y - base);
         const uint32_t p = base + tid;
@@ -187,15 +306,22 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             sB[tid] = B;
             sC[tid] = C;
             sD[tid] = D;
-            // which warps (8x4 pixel blocks of this tile) can see m^2 <= 9
-            const uint32_t wm = warp_block_mask(__ldg(ext + m), A.x, A.y, tx, ty);
+            // which warps' pixel boxes can see m^2 <= 9 (the same conservative float
+            // test as warp_block_mask: the nearest column / row already beyond the extent)
+            const float2 e = __ldg(ext + m);
+            uint32_t wm = 0;
+            for (int w = 0; w < live_warps; ++w) {
+                const float4 bx = wbox[w];
+                if (!(fsub(bx.x, A.x) > e.x || fsub(A.x, bx.y) > e.x || fsub(bx.z, A.y) > e.y ||
+                      fsub(A.y, bx.w) > e.y))
+                    wm |= 1u << w;
+            }
             smask[tid] = (uint8_t)wm;
         }
         __syncthreads();
         // this warp's candidates of the batch, in list order
         int nlist = 0;
-        {
-            const int wid = tid >> 5, lane = tid & 31;
+        if (wid < live_warps) {
             const int nbb = (int)min((uint32_t)kBlendThreads, rg.y - base);
             for (int c0 = 0; c0 < nbb; c0 += 32) {
                 const int jj = c0 + lane;
@@ -206,9 +332,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             }
             __syncwarp();
         }
-        const int nb = (int)min((uint32_t)kBlendThreads, rg.y - base);
-        for (int q = 0; q < nlist && !done; ++q) {
-            const int j = wlist[q];
+        for (int qq = 0; qq < nlist && !done; ++qq) {
+            const int j = wlist[qq];
             const float4 D = sD[j];
             while (head_t < D.w && !done) emit_head();
             if (done) break;
@@ -225,54 +350,38 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             int pos = head + cnt;
             while (pos > head) {
                 const int pl = (pos - 1) & (KBUF - 1);
-                const float tp = bt[pl][tid];
-                const uint32_t ip = bid[pl][tid];
+                const float tp = bt[pl][q];
+                const uint32_t ip = bid[pl][q];
                 if (t < tp || (t == tp && id < ip)) {
                     const int ps = pos & (KBUF - 1);
-                    bt[ps][tid] = tp;
-                    bid[ps][tid] = ip;
-                    bs[ps][tid] = bs[pl][tid];
-                    bpos[ps][tid] = bpos[pl][tid];
+                    bt[ps][q] = tp;
+                    bid[ps][q] = ip;
+                    bs[ps][q] = bs[pl][q];
+                    bpos[ps][q] = bpos[pl][q];
                     --pos;
                 } else {
                     break;
                 }
             }
             const int ps = pos & (KBUF - 1);
-            bt[ps][tid] = t;
-            bid[ps][tid] = id;
-            bs[ps][tid] = sigma;
-            bpos[ps][tid] = base + (uint32_t)j;
+            bt[ps][q] = t;
+            bid[ps][q] = id;
+            bs[ps][q] = sigma;
+            bpos[ps][q] = base + (uint32_t)j;
             ++cnt;
             if (pos == head) head_t = t;
         }
     }
-    while (cnt > 0 && !done) emit_head();
-
-    if (crec.pos != nullptr) {
-        // tiles whose records are incomplete are replayed by the backward
-        const bool short_rec = inside && !ovf && nemit > kRecCap;
-        const int rep = __syncthreads_or(short_rec || !record);
-        if (inside) crec.cnt[pix] = (uint16_t)min(nemit, kRecCap);
-        if (tid == 0) crec.tile_replay[tile] = (uint8_t)(rep != 0);
+    if (valid) {
+        while (cnt > 0 && !done) emit_head();
+        write_out();
     }
-    if (inside) {
-        if (ovf) {
-            ovf_flag[pix] = 1;
-            ovf_list[atomicAdd(ovf_count, 1u)] = (uint32_t)pix;
-        } else {
-            ovf_flag[pix] = 0;
-            out_ct[pix] = make_float4(C0, C1, C2, T);
-            if (out_cd != nullptr) {
-                out_cd[3 * pix] = D0;
-                out_cd[3 * pix + 1] = D1;
-                out_cd[3 * pix + 2] = D2;
-            }
-            if (DBG) dbg_cnt[pix] = (uint32_t)nemit;
-        }
+    if (crec.pos != nullptr) {
+        __syncthreads();
+        if (tid == 0) crec.tile_replay[tile] = (uint8_t)(s_short != 0 || !record);
     }
     if (STATS && stats != nullptr) {
-        unsigned long long e = n_eval, c = (unsigned long long)nemit, o = ovf ? 1ull : 0ull;
+        unsigned long long e = n_eval, c = n_contrib, o = n_ovf;
         for (int off = 16; off > 0; off >>= 1) {
             e += __shfl_xor_sync(0xffffffffu, e, off);
             c += __shfl_xor_sync(0xffffffffu, c, off);
