@@ -25,7 +25,31 @@ constexpr int KBUF = 8;  // ring capacity (power of two); must equal blend_bwd.c
 constexpr float kInf = __builtin_huge_valf();
 // 4 staged float4 record fields + 4 ring fields per pixel (t, id, sigma, member).
 constexpr size_t kFwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float) +
-                            kBlendThreads + (kBlendThreads / 32) * kBlendThreads * sizeof(uint16_t);
+                            kBlendThreads * sizeof(uint16_t) + (kBlendThreads / 32) * kBlendThreads * sizeof(uint16_t);
+
+/// 16-bit mask of the 4x4 pixel sub-blocks of tile (tx, ty) that may contain a
+/// pixel with m^2 <= trunc^2 (the conservative test of warp_block_mask at 4x4
+/// granularity).  Bit (row * 4 + col).
+__device__ __forceinline__ uint32_t subblock_mask(float2 ext, float mx, float my, int tx, int ty) {
+    uint32_t cm = 0, rm = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const float xlo = fadd((float)(tx * kTileSize + b * 4), 0.5f), xhi = fadd(xlo, 3.0f);
+        if (!(fsub(xlo, mx) > ext.x || fsub(mx, xhi) > ext.x)) cm |= 1u << b;
+        const float ylo = fadd((float)(ty * kTileSize + b * 4), 0.5f), yhi = fadd(ylo, 3.0f);
+        if (!(fsub(ylo, my) > ext.y || fsub(my, yhi) > ext.y)) rm |= 1u << b;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if ((rm >> r) & 1u) m |= cm << (4 * r);
+    return m;
+}
+/// The 4x4 sub-block of a pixel slot (tile_pixel order).
+__device__ __forceinline__ int slot_subblock(int q) {
+    const int w = q >> 5, l = q & 31;
+    return (w >> 1) * 4 + (w & 1) * 2 + ((l & 7) >> 2);  // row = 4-pixel row group, col = 4-pixel column group
+}
 
 /// Lower bound on t for every candidate at or after a list position whose
 /// range is r (t >= sqrt(r^2 - D^2), with margins ≫ float
@@ -89,7 +113,7 @@ __device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint
 /// bounding box of its own pixels.  Per-pixel state moves through shared
 /// memory; the ring stays in place (indexed by pixel slot).
 template <bool DBG, bool STATS>
-__global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, RenderOpts ro, Subspace gate,
+__global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fwd(ViewParams vp, RenderOpts ro, Subspace gate,
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
                                                              const uint2* __restrict__ ranges,
@@ -116,9 +140,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     // entries accepted in an earlier batch, through pair_val; also recorded)
     uint32_t(*bpos)[kBlendThreads] = reinterpret_cast<uint32_t(*)[kBlendThreads]>(bs + KBUF);
     uint16_t* wlist = reinterpret_cast<uint16_t*>(bpos + KBUF) + (threadIdx.x >> 5) * kBlendThreads;
-    uint8_t* smask = reinterpret_cast<uint8_t*>(reinterpret_cast<uint16_t*>(bpos + KBUF) +
-                                                (kBlendThreads / 32) * kBlendThreads);
-    __shared__ float4 wbox[kBlendThreads / 32];  // per warp: pixel-centre x range, y range of its slots
+    uint16_t* smask = reinterpret_cast<uint16_t*>(bpos + KBUF) + (kBlendThreads / 32) * kBlendThreads;
     __shared__ int s_woff[kBlendThreads / 32];
     __shared__ int s_short;
 
@@ -158,13 +180,11 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
     float head_t = kInf;
     unsigned long long n_eval = 0, n_contrib = 0, n_ovf = 0;
     uint32_t cur_base = rg.x, cur_nb = 0;  // batch currently staged in shared memory
-    if (tid < kBlendThreads / 32) {  // the fixed 8x4 blocks
-        const float x0 = fadd((float)(tx * kTileSize + (tid & 1) * 8), 0.5f);
-        const float y0 = fadd((float)(ty * kTileSize + (tid >> 1) * 4), 0.5f);
-        wbox[tid] = make_float4(x0, fadd(x0, 7.0f), y0, fadd(y0, 3.0f));
-    }
     if (tid == 0) s_short = 0;
     int live_warps = kBlendThreads / 32;
+    // the 4x4 sub-blocks this warp's pixels lie in: a staged candidate concerns
+    // the warp only if its sub-block mask meets this one
+    uint32_t wsub = __reduce_or_sync(0xffffffffu, 1u << slot_subblock(q));
 
     auto emit_head = [&]() {
         if (ro.stop > 0.0f && T < ro.stop) {  // raster.hpp:183
@@ -279,19 +299,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
                 bind_slot();
             }
             live_warps = (nact + 31) / 32;
-            {
-                const float bx = valid ? pr.pxf : kInf, by = valid ? pr.pyf : kInf;
-                const float ex = valid ? pr.pxf : -kInf, ey = valid ? pr.pyf : -kInf;
-                float x0 = bx, y0 = by, x1 = ex, y1 = ey;
-                for (int off = 16; off > 0; off >>= 1) {
-                    x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
-                    y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, off));
-                    x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
-                    y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, off));
-                }
-                if (lane == 0) wbox[wid] = make_float4(x0, x1, y0, y1);  // empty warps: an empty box
-            }
-            __syncthreads();  // boxes visible; the staging area is free again
+            wsub = __reduce_or_sync(0xffffffffu, valid ? 1u << slot_subblock(q) : 0u);
+            __syncthreads();  // the staging area is free again
         }
         cur_base = base;
         cur_nb = min((uint32_t)kBlendThreads, rg.y - base);
@@ -306,17 +315,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             sB[tid] = B;
             sC[tid] = C;
             sD[tid] = D;
-            // which warps' pixel boxes can see m^2 <= 9 (the same conservative float
-            // test as warp_block_mask: the nearest column / row already beyond the extent)
-            const float2 e = __ldg(ext + m);
-            uint32_t wm = 0;
-            for (int w = 0; w < live_warps; ++w) {
-                const float4 bx = wbox[w];
-                if (!(fsub(bx.x, A.x) > e.x || fsub(A.x, bx.y) > e.x || fsub(bx.z, A.y) > e.y ||
-                      fsub(A.y, bx.w) > e.y))
-                    wm |= 1u << w;
-            }
-            smask[tid] = (uint8_t)wm;
+            // which 4x4 pixel sub-blocks of this tile can see m^2 <= 9
+            smask[tid] = (uint16_t)subblock_mask(__ldg(ext + m), A.x, A.y, tx, ty);
         }
         __syncthreads();
         // this warp's candidates of the batch, in list order
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(ViewParams vp, Rend
             const int nbb = (int)min((uint32_t)kBlendThreads, rg.y - base);
             for (int c0 = 0; c0 < nbb; c0 += 32) {
                 const int jj = c0 + lane;
-                const bool hit = jj < nbb && ((smask[jj] >> wid) & 1u);
+                const bool hit = jj < nbb && (smask[jj] & wsub);
                 const unsigned bm = __ballot_sync(0xffffffffu, hit);
                 if (hit) wlist[nlist + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)jj;
                 nlist += __popc(bm);
