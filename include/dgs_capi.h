@@ -148,6 +148,9 @@ int dgs_perturb_splats(dgs_splats* s, uint64_t seed);
 /* One context per GPU (rank).  world > 1 requires a 128-byte ncclUniqueId
  * made by dgs_nccl_unique_id on rank 0 and shared by the caller. */
 int dgs_nccl_unique_id(void* out128);
+/* Grouped send/recv and an all-reduce on a one-rank NCCL communicator on
+ * `device`: checks the run-time NCCL binding the rank exchange uses. */
+int dgs_nccl_selftest(int32_t device);
 int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl_id, dgs_ctx** out);
 /* Test transport for the multi-rank step: the exchanges and the loss
  * all-reduce go through host callbacks instead of NCCL (NCCL refuses two

@@ -111,6 +111,7 @@ _SIGS = {
                                   C.POINTER(Camera)]),
     "dgs_perturb_splats": (C.c_int, [C.POINTER(SplatsC), C.c_uint64]),
     "dgs_nccl_unique_id": (C.c_int, [_P]),
+    "dgs_nccl_selftest": (C.c_int, [C.c_int32]),
     "dgs_ctx_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
     "dgs_ctx_create_host_transport": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(HostTransportC),
                                               C.POINTER(_P)]),

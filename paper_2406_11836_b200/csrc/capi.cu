@@ -1058,6 +1058,45 @@ int dgs_nccl_unique_id(void* out128) {
     });
 }
 
+int dgs_nccl_selftest(int32_t device) {
+    return dgs_guard([&] {
+        // the calls the rank exchange makes (grouped send/recv, all-reduce of the
+        // loss sums), on a one-rank communicator: checks the run-time NCCL binding
+        CK(cudaSetDevice(device));
+        ncclUniqueId id;
+        NK(nccl().GetUniqueId(&id));
+        ncclComm_t comm = nullptr;
+        NK(nccl().CommInitRank(&comm, 1, id, 0));
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const size_t n = 4099;
+        std::vector<float> h(n), back(n);
+        for (size_t i = 0; i < n; ++i) h[i] = (float)i * 0.5f - 7.0f;
+        DevBuf<float> a, b;
+        DevBuf<double> d;
+        a.ensure(n);
+        b.ensure(n);
+        d.ensure(3);
+        const double dh[3] = {1.5, -2.0, 3.25};
+        CK(cudaMemcpy(a.p, h.data(), n * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d.p, dh, sizeof(dh), cudaMemcpyHostToDevice));
+        NK(nccl().GroupStart());
+        NK(nccl().Send(a.p, n, ncclFloat, 0, comm, s));
+        NK(nccl().Recv(b.p, n, ncclFloat, 0, comm, s));
+        NK(nccl().GroupEnd());
+        NK(nccl().AllReduce(d.p, d.p, 3, ncclDouble, ncclSum, comm, s));
+        CK(cudaStreamSynchronize(s));
+        double dr[3];
+        CK(cudaMemcpy(back.data(), b.p, n * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dr, d.p, sizeof(dr), cudaMemcpyDeviceToHost));
+        nccl().CommDestroy(comm);
+        cudaStreamDestroy(s);
+        if (std::memcmp(back.data(), h.data(), n * 4) != 0) throw std::runtime_error("nccl selftest: send/recv mismatch");
+        if (dr[0] != dh[0] || dr[1] != dh[1] || dr[2] != dh[2])
+            throw std::runtime_error("nccl selftest: all-reduce mismatch");
+    });
+}
+
 int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl_id, dgs_ctx** out) {
     return dgs_guard([&] {
         int ndev = 0;

@@ -235,3 +235,13 @@ def test_multi_rank_grad_sync_keeps_replicas_identical(tmp_path, world):
     want = p0[[row_of[i] for i in sids]].astype(np.float64) - lr_row * want_g / (np.abs(want_g) + cfg.adam_eps)
     ok, e, noisy = post_adam_ok(got_p, want, want_g, np.broadcast_to(lr_row, want.shape))
     assert ok.all(), int((~ok).sum())
+
+
+def test_nccl_binding_self_communicator():
+    """The NCCL entry points the rank exchange uses (grouped send/recv, the
+    loss all-reduce), through the library's run-time binding, on a one-rank
+    communicator (one GPU here; the multi-rank exchange logic itself is
+    covered above with the host transport)."""
+    from paper_2406_11836_b200 import capi
+
+    capi.check(capi.lib().dgs_nccl_selftest(0))
