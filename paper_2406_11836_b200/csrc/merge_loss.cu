@@ -161,6 +161,10 @@ __global__ void k_merge_bwd_ordered(int px, int kcount, int kstride, const uint1
 // ---------------------------------------------------------------------------
 // Fused L1 + D-SSIM (loss.hpp:94-177), one channel plane per blockIdx.z.
 // ---------------------------------------------------------------------------
+#ifndef DGS_LOSS_THREADS
+#define DGS_LOSS_THREADS 384
+#endif
+constexpr int kLT = DGS_LOSS_THREADS;  // threads per loss CTA
 constexpr int kOT = 32;             // output tile
 constexpr int kR = 5;               // blur radius
 constexpr int kIn = kOT + 4 * kR;   // 52: input tile with 10-pixel halo
@@ -188,11 +192,11 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
     // stage 0: inputs with zero padding outside the image / provided window;
     // all of a thread's loads are issued before any is stored (memory-level parallelism)
     {
-        constexpr int NIT = (kIn * kIn + 255) / 256;
+        constexpr int NIT = (kIn * kIn + kLT - 1) / kLT;
         float xr[NIT], yr[NIT];
 #pragma unroll
         for (int u = 0; u < NIT; ++u) {
-            const int i = tid + u * 256;
+            const int i = tid + u * kLT;
             xr[u] = yr[u] = 0.0f;
             if (i < kIn * kIn) {
                 const int r = i / kIn, c = i % kIn;
@@ -207,7 +211,7 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
         }
 #pragma unroll
         for (int u = 0; u < NIT; ++u) {
-            const int i = tid + u * 256;
+            const int i = tid + u * kLT;
             if (i < kIn * kIn) {
                 X[i] = xr[u];
                 Y[i] = yr[u];
@@ -216,7 +220,7 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
     }
     __syncthreads();
     // stage 1: horizontal blur of x, y, x*x, y*y, x*y (rows -10..+41, cols -5..+36)
-    for (int it = tid; it < kIn * (kMid / kR1); it += 256) {
+    for (int it = tid; it < kIn * (kMid / kR1); it += kLT) {
         const int r = it / (kMid / kR1), c0 = (it % (kMid / kR1)) * kR1;
         float xv[kR1 + 10], yv[kR1 + 10];
 #pragma unroll
@@ -247,7 +251,7 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
     __syncthreads();
     // stage 2: vertical blur -> mu_x, mu_y, E[xx], E[yy], E[xy] at tile +-5;
     // then the per-pixel SSIM partials A, B, B mu_x, C, C mu_y (zero outside the image).
-    for (int it = tid; it < kMid * (kMid / kR2); it += 256) {
+    for (int it = tid; it < kMid * (kMid / kR2); it += kLT) {
         const int c = it % kMid, r0 = (it / kMid) * kR2;
         const int gx = ox - kR + c;
         const int gyb = oy - 2 * kR + r0;  // image row of input i = gyb + i
@@ -301,7 +305,7 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
     __syncthreads();
     // stage 3: horizontal blur of the five maps (rows -5..+36, cols 0..31)
     float* H2 = Hb;  // [5][kMid][kOT]
-    for (int it = tid; it < 5 * (kOT / kR3) * kMid; it += 256) {
+    for (int it = tid; it < 5 * (kOT / kR3) * kMid; it += kLT) {
         const int r = it % kMid, qc = it / kMid;
         const int q = qc / (kOT / kR3), c0 = (qc % (kOT / kR3)) * kR3;
         const int gxb = ox - kR + c0;
@@ -321,7 +325,7 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
     }
     __syncthreads();
     // stage 4: vertical blur -> gradient (loss.hpp:138-140, 160-175)
-    for (int it = tid; it < kOT * (kOT / kR4); it += 256) {
+    for (int it = tid; it < kOT * (kOT / kR4); it += kLT) {
         const int c = it % kOT, r0 = (it / kOT) * kR4;
         const int gx = ox + c;
         const int gyb = oy + r0 - kR;
@@ -363,7 +367,7 @@ __device__ __forceinline__ void loss_tile(int W, int H, int row0, int row1, int 
     }
 }
 
-__global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, int in_base, int in_rows,
+__global__ void __launch_bounds__(kLT, 2) k_loss(int W, int H, int row0, int row1, int in_base, int in_rows,
                                               const float* __restrict__ xs, const float* __restrict__ ys, float lam,
                                               float c1, float c2, float nf, float inv_batch,
                                               const float* __restrict__ kern_g, float* __restrict__ grad,
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, 
     float* Hb = Y + kIn * kIn;           // [5][kIn][kMid] horizontal stage (reused as [5][kMid][kOT])
     float* Vb = Hb + 5 * kIn * kMid;     // [5][kMid][kMid]
     __shared__ float kern[11];
-    __shared__ double red[3][8];
+    __shared__ double red[3][kLT / 32];
     const int tid = threadIdx.x;
     if (tid < 11) kern[tid] = kern_g[tid];
     const int ox = blockIdx.x * kOT, oy = row0 + blockIdx.y * kOT;
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(256) k_loss(int W, int H, int row0, int row1, 
     __syncthreads();
     if (tid < 3) {
         double x = 0.0;
-        for (int w = 0; w < 8; ++w) x += red[tid][w];
+        for (int w = 0; w < kLT / 32; ++w) x += red[tid][w];
         const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         block_sums[(size_t)b * 3 + tid] = x;
     }
@@ -481,7 +485,7 @@ void launch_loss(int W, int H, int row0, int row1, int in_base, int in_rows, con
     // loss.hpp:16-17: C1 = (0.01)^2, C2 = (0.03)^2 evaluated in double, then T(.)
     const float c1 = (float)(0.01 * 0.01), c2 = (float)(0.03 * 0.03);
     const float nf = (float)((size_t)W * H * 3);
-    k_loss<<<grid, 256, kLossSmem, s>>>(W, H, row0, row1, in_base, in_rows, x, y, lambda, c1, c2, nf, inv_batch,
+    k_loss<<<grid, kLT, kLossSmem, s>>>(W, H, row0, row1, in_base, in_rows, x, y, lambda, c1, c2, nf, inv_batch,
                                         kernel, grad, block_sums);
 }
 
