@@ -209,7 +209,14 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     const int tiles = vp.tiles_x * vp.tiles_y;
     cudaMemsetAsync(vb.ranges, 0, sizeof(uint2) * tiles, s);
     vb.pairs = 0;
-    if (n <= 0) return 0;
+    // the blends' block order (tiles longest list first) is a permutation on every path
+    auto tile_order = [&]() {
+        if (vb.tile_order) k_tile_order<<<1, 1024, 0, s>>>(vb.ranges, tiles, vb.tile_order);
+    };
+    if (n <= 0) {
+        tile_order();
+        return 0;
+    }
     const int blk = 256, grid = (n + blk - 1) / blk;
     // 1) members by range bucket: 16-bit keys (2 radix passes)
     k_key16<<<grid, blk, 0, s>>>(vb.rkey, vb.dmax_bits, scan_buf, sort_vals, n);
@@ -233,7 +240,10 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     const int64_t P = (int64_t)*pairs_host;
     if (P > cap) return -P;
     vb.pairs = P;
-    if (P == 0) return 0;
+    if (P == 0) {
+        tile_order();
+        return 0;
+    }
     // 3) emit (tile, member) pairs, range-ordered within every tile
     k_emit_pairs<<<grid, blk, 0, s>>>(sorted_idx, scan_buf, cnt_sorted, rect_sorted, vp.tiles_x, n, vb.pair_tile,
                                       vb.pair_val);  // scan_buf holds inclusive ends: start = end - count
@@ -249,7 +259,7 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     // 5) per-tile [start, end)
     k_tile_ranges<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(vb.pair_tile, (uint32_t)P, tiles, vb.ranges);
     // 6) block order for the blends: tiles by decreasing list length
-    if (vb.tile_order) k_tile_order<<<1, 1024, 0, s>>>(vb.ranges, tiles, vb.tile_order);
+    tile_order();
     return P;
 }
 

@@ -495,7 +495,8 @@ class Manager:
     def snapshot(self):
         """manager.hpp:390-418: the replica held by the subspace containing the centre wins."""
         if self.world > 1:
-            raise NotImplementedError("snapshot/repartition across ranks is SURVEY §8(f) row 1 (not built)")
+            raise NotImplementedError("snapshot() gathers a single rank's subsets; across ranks use "
+                                      "repartition(device=True) (dgs_repartition)")
         parts = [self.ctx.store_subset(k, self.sh_coeffs) for k in range(self.table.subset_count)]
         chosen: dict[int, tuple[int, int]] = {}
         for k, (p, _, _, _) in enumerate(parts):

@@ -1,0 +1,102 @@
+"""GPU: edge cases of the training step — a view that culls every splat,
+KD leaves with no members, image sizes that are not multiples of the 16-pixel
+tile, a single splat, and the reference's zero-quaternion error
+(math.hpp:36-37 -> std::domain_error)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_binding as ob
+from paper_2406_11836_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("mu", "log_scale", "rotation", "opacity_logit", "sh")
+
+
+def _away(cam):
+    """The same camera moved 100 units back along its axis: every splat lies behind it."""
+    c = engine.Camera.from_record(cam.record())
+    c.t_wc[2] = c.t_wc[2] - 100.0
+    return c
+
+
+def test_view_that_culls_everything():
+    s = engine.synth_splats(3000, seed=4, sh_degree=3)
+    cam = _away(engine.ring_camera(96, 64, 1, n_views=64))
+    mgr = engine.Manager(s, engine.train_config(kd_depth=1), engine.render_options())
+    rgb, t = mgr.render(cam, bg=(0.25, 0.5, 0.75))
+    np.testing.assert_array_equal(t, np.ones_like(t))
+    np.testing.assert_array_equal(rgb, np.broadcast_to(np.float32([0.25, 0.5, 0.75]), rgb.shape))
+    before = [mgr.ctx.store_subset(k, s.sh_coeffs)[0] for k in range(mgr.table.subset_count)]
+    target = np.random.default_rng(0).random((1, 64, 96, 3), dtype=np.float32)
+    res = mgr.train_step([cam], target)
+    assert np.isfinite(res["loss"]) and res["loss"] > 0
+    # no gradient anywhere: the first Adam step leaves every parameter as it was (m = v = 0)
+    for k in range(mgr.table.subset_count):
+        p, _, _, step = mgr.ctx.store_subset(k, s.sh_coeffs)
+        assert step == 1
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(p, f), getattr(before[k], f), err_msg=f)
+    mgr.close()
+
+
+def test_empty_kd_leaves():
+    """Three small splats split 8 ways: some KD leaves get no members; the
+    merged render still equals the unsplit one and the step runs."""
+    s = engine.synth_splats(1_000_000, seed=9, sh_degree=3).take(np.arange(3))
+    cam = engine.ring_camera(80, 60, 0, n_views=64)
+    ro = engine.render_options(oracle=True)
+    out = {}
+    for depth in (0, 3):
+        mgr = engine.Manager(s, engine.train_config(kd_depth=depth), ro)
+        out[depth] = mgr.render(cam)
+        if depth == 3:
+            sizes = [int(engine.lib().dgs_subset_size(mgr.ctx.handle, k)) for k in range(8)]
+            assert min(sizes) == 0, sizes  # the case under test: leaves without members
+            res = mgr.train_step([cam], out[0][0][None])
+            assert np.isfinite(res["loss"])
+        mgr.close()
+    (rgb0, t0), (rgb3, t3) = out[0], out[3]
+    assert (t0 < 1).any()
+    assert np.abs(rgb3 - rgb0).max() <= 1e-4
+    assert np.abs(t3 - t0).max() <= 1e-4
+
+
+@pytest.mark.parametrize("count,wh", [(4000, (257, 131)), (4000, (17, 15)), (1, (64, 48))])
+def test_ragged_sizes_and_single_splat_match_oracle(count, wh):
+    W, H = wh
+    s = engine.synth_splats(10_000, seed=12, sh_degree=3)
+    cam = engine.ring_camera(W, H, 3, n_views=64)
+    if count == 1:  # the splat nearest the view centre
+        s = s.take(np.array([int(np.argmin(np.linalg.norm(s.mu, axis=1)))]))
+    else:
+        s = s.take(np.arange(count))
+    ctx = engine.Context(0)
+    ctx.set_table(engine.build_kdtree(s.mu, 0))
+    ctx.set_options(engine.render_options(), engine.train_config())
+    ctx.load_subset(0, s)
+    ct = ctx.render_partial(0, cam)
+    ctx.close()
+    sc = ob.Scene(s)
+    sub = ob.Sub()
+    sub.n = 0
+    ref = np.zeros((H, W, 4), np.float32)
+    assert ob.lib().orc_partial_render(C.byref(sc.c), C.byref(sub), C.byref(ob.cam_of(cam.record())),
+                                       C.byref(ob.opts(False)), ob.p(ref), 0, None, None) == 0
+    assert (ref[..., 3] < 1).any()
+    assert np.abs(ct - ref).max() <= 1e-4
+
+
+def test_zero_quaternion_raises_domain_error():
+    s = engine.synth_splats(500, seed=2, sh_degree=3)
+    cam = engine.ring_camera(64, 48, 0, n_views=64)
+    s.rotation[:, :] = 0.0
+    ctx = engine.Context(0)
+    ctx.set_table(engine.build_kdtree(s.mu, 0))
+    ctx.set_options(engine.render_options(), engine.train_config())
+    ctx.load_subset(0, s)
+    with pytest.raises(ArithmeticError, match="quaternion"):
+        ctx.render_partial(0, cam)
+    ctx.close()
