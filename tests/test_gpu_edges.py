@@ -100,3 +100,78 @@ def test_zero_quaternion_raises_domain_error():
     with pytest.raises(ArithmeticError, match="quaternion"):
         ctx.render_partial(0, cam)
     ctx.close()
+
+
+def _ring_overflow_scene(cam, n=64, seed=7):
+    """n translucent splats at one distance from the camera centre, clustered
+    around the view axis: their ranges share one bucket, so the (t, id) ring
+    can emit none of them before the list ends and overflows after 8."""
+    rng = np.random.default_rng(seed)
+    q = np.asarray(cam.q_wc, np.float64)
+    w, x, y, z = q / np.linalg.norm(q)
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                  [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                  [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    t = np.asarray(cam.t_wc, np.float64)
+    o = -R.T @ t
+    fwd = R.T @ np.array([0.0, 0.0, 1.0])
+    right, up = R.T @ np.array([1.0, 0.0, 0.0]), R.T @ np.array([0.0, 1.0, 0.0])
+    s = engine.Splats.empty(n, 16)
+    s.id[:] = np.arange(n, dtype=np.uint64)
+    for j in range(n):
+        d = fwd + 0.004 * (rng.standard_normal() * right + rng.standard_normal() * up)
+        s.mu[j] = o + 3.2 * d / np.linalg.norm(d)
+    s.log_scale[:] = np.log(0.2 * rng.uniform(0.6, 1.4, (n, 3)))  # anisotropic: rotation gradients are not noise
+    s.rotation[:] = rng.standard_normal((n, 4))
+    s.opacity_logit[:] = -2.2  # alpha ~ 0.1: no early termination within 64
+    s.sh[:, 0, :] = rng.uniform(-1.0, 1.0, (n, 3))
+    return s
+
+
+def test_ring_overflow_fallbacks_match_oracle():
+    """Pixels whose reorder ring overflows take the exact fallback kernels
+    (forward and backward): the composite and the gradients still match the
+    oracle."""
+    cam = engine.ring_camera(48, 40, 0, n_views=64)
+    s = _ring_overflow_scene(cam)
+    ro, o = engine.render_options(grad_skip_eps=0.0), ob.opts(False, grad_skip_eps=0.0)
+    mgr = engine.Manager(s, engine.train_config(kd_depth=0), ro)
+    mgr.ctx.set_collect_stats(True)
+    target = np.zeros((1, 40, 48, 3), np.float32)
+    res = mgr.train_step([cam], target)
+    mgr.close()
+    assert res["overflow_pixels"] > 0, "the scene did not overflow the ring"
+
+    ctx = engine.Context(0)
+    ctx.set_table(engine.build_kdtree(s.mu, 0))
+    ctx.set_options(ro, engine.train_config())
+    ctx.load_subset(0, s)
+    ct, ids, cnt = ctx.render_partial(0, cam, dbg_cap=128)
+    sc = ob.Scene(s)
+    sub = ob.Sub()
+    sub.n = 0
+    ocam = ob.cam_of(cam.record())
+    ref = np.zeros((40, 48, 4), np.float32)
+    rids = np.zeros((40 * 48, 128), np.uint32)
+    rcnt = np.zeros(40 * 48, np.uint32)
+    assert ob.lib().orc_partial_render(C.byref(sc.c), C.byref(sub), C.byref(ocam), C.byref(o), ob.p(ref), 128,
+                                       ob.p(rids), ob.p(rcnt)) == 0
+    assert rcnt.max() > 8
+    assert np.abs(ct - ref).max() <= 1e-4
+    np.testing.assert_array_equal(cnt, rcnt)
+    for p in np.nonzero(rcnt)[0]:
+        np.testing.assert_array_equal(ids[p, :cnt[p]], rids[p, :rcnt[p]], err_msg=f"pixel {p}")
+    # backward through the fallback: gradients against the oracle's
+    g = (np.random.default_rng(5).standard_normal((40, 48, 4)) * 1e-2).astype(np.float32)
+    got = ctx.render_partial_backward(0, cam, g, s.sh_coeffs)
+    order = np.argsort(ctx.store_subset(0, s.sh_coeffs)[0].id)  # storage order -> id order
+    ctx.close()
+    gr, want = ob.empty_grads(s.n, s.sh_coeffs)
+    assert ob.lib().orc_partial_backward(C.byref(sc.c), C.byref(sub), C.byref(ocam), C.byref(o), ob.p(g),
+                                         C.byref(gr)) == 0
+    for f in ("mu", "log_scale", "rotation", "opacity_logit"):
+        a = getattr(got, f)[order].astype(np.float64)
+        b = want["d_" + f].astype(np.float64)
+        floor = 1e-3 * np.abs(b).max()
+        err = np.abs(a - b) / np.maximum(np.abs(b), floor)
+        assert err.max() <= 1e-3, (f, float(err.max()))
