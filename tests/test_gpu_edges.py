@@ -1,7 +1,9 @@
 """GPU: edge cases of the training step — a view that culls every splat,
 KD leaves with no members, image sizes that are not multiples of the 16-pixel
-tile, a single splat, and the reference's zero-quaternion error
-(math.hpp:36-37 -> std::domain_error)."""
+tile, a single splat, the reference's zero-quaternion error
+(math.hpp:36-37 -> std::domain_error), and the two capacity fallbacks: the
+exact kernels for pixels whose (t, id) reorder ring overflows, and the
+ordered-ring replay for tiles whose composite records overflow."""
 import ctypes as C
 
 import numpy as np
@@ -175,3 +177,54 @@ def test_ring_overflow_fallbacks_match_oracle():
         floor = 1e-3 * np.abs(b).max()
         err = np.abs(a - b) / np.maximum(np.abs(b), floor)
         assert err.max() <= 1e-3, (f, float(err.max()))
+
+
+def test_record_capacity_overflow_replays_tile():
+    """Pixels with more composited contributions than the record holds
+    (kRecCap = 256) mark their tile for the ordered-ring replay in the
+    backward; the gradients still match the oracle's."""
+    cam = engine.ring_camera(40, 32, 0, n_views=64)
+    n = 400
+    s = _ring_overflow_scene(cam, n=n, seed=8)
+    # spread along the view axis (distinct ranges, so the ring drains) and faint (no termination)
+    s.mu[:] = (s.mu + np.linspace(-0.6, 0.6, n)[:, None] * _view_axis(cam)).astype(np.float32)
+    s.opacity_logit[:] = -4.6  # alpha ~ 0.01
+    # small splats: the order slack (~ D^2 / 2r) stays below the range spacing, so no ring overflow
+    s.log_scale[:] = np.log(0.03 * np.random.default_rng(4).uniform(0.6, 1.4, (n, 3))).astype(np.float32)
+    ro, o = engine.render_options(grad_skip_eps=0.0), ob.opts(False, grad_skip_eps=0.0)
+    mgr = engine.Manager(s, engine.train_config(kd_depth=0), ro)
+    mgr.ctx.set_collect_stats(True)
+    res = mgr.train_step([cam], np.zeros((1, 32, 40, 3), np.float32))
+    mgr.close()
+    assert res["overflow_pixels"] == 0
+    assert res["replay_tiles_bwd"] > 0, "no tile exceeded the record capacity"
+    ctx = engine.Context(0)
+    ctx.set_table(engine.build_kdtree(s.mu, 0))
+    ctx.set_options(ro, engine.train_config())
+    ctx.load_subset(0, s)
+    ctx.render_partial(0, cam)
+    g = (np.random.default_rng(6).standard_normal((32, 40, 4)) * 1e-2).astype(np.float32)
+    got = ctx.render_partial_backward(0, cam, g, s.sh_coeffs)
+    order = np.argsort(ctx.store_subset(0, s.sh_coeffs)[0].id)
+    ctx.close()
+    sc = ob.Scene(s)
+    sub = ob.Sub()
+    sub.n = 0
+    gr, want = ob.empty_grads(s.n, s.sh_coeffs)
+    assert ob.lib().orc_partial_backward(C.byref(sc.c), C.byref(sub), C.byref(ob.cam_of(cam.record())), C.byref(o),
+                                         ob.p(g), C.byref(gr)) == 0
+    for f in ("mu", "log_scale", "rotation", "opacity_logit"):
+        a = getattr(got, f)[order].astype(np.float64)
+        b = want["d_" + f].astype(np.float64)
+        floor = 1e-3 * np.abs(b).max()
+        err = np.abs(a - b) / np.maximum(np.abs(b), floor)
+        assert err.max() <= 1e-3, (f, float(err.max()))
+
+
+def _view_axis(cam):
+    q = np.asarray(cam.q_wc, np.float64)
+    w, x, y, z = q / np.linalg.norm(q)
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                  [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                  [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    return R.T @ np.array([0.0, 0.0, 1.0])
