@@ -228,3 +228,24 @@ def _view_axis(cam):
                   [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
                   [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
     return R.T @ np.array([0.0, 0.0, 1.0])
+
+
+def test_device_repartition_into_empty_leaves():
+    """dgs_repartition to a depth with more leaves than splats: the device
+    path still equals the host path (planes, members, migrated p/m/v)."""
+    from test_gpu_repartition import _check, _host_reference
+
+    s = engine.synth_splats(1_000_000, seed=9, sh_degree=3).take(np.arange(3))
+    cam = engine.ring_camera(48, 40, 0, n_views=64)
+    mgr = engine.Manager(s, engine.train_config(kd_depth=0), engine.render_options())
+    mgr.train_step([cam], np.zeros((1, 40, 48, 3), np.float32))
+    mgr.config.kd_depth = 3
+    ref = _host_reference(mgr, 3)
+    mgr.repartition(device=True)
+    assert mgr.table.subset_count == 8
+    sizes = [int(engine.lib().dgs_subset_size(mgr.ctx.handle, k)) for k in range(8)]
+    assert min(sizes) == 0, sizes
+    _check(mgr, ref)
+    res = mgr.train_step([cam], np.zeros((1, 40, 48, 3), np.float32))
+    assert np.isfinite(res["loss"])
+    mgr.close()
