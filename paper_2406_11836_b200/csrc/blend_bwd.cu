@@ -100,13 +100,14 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     ps.a1 += (double)D.y * wd;
     ps.a2 += (double)D.z * wd;
     ps.T = fmul(ps.T, fsub(1.0f, sigma));
-    // suffix_i = sum_{j>i} c_j sigma_j A_j = C - prefix_i, evaluated in double so
-    // the difference keeps full relative accuracy (raster.hpp:212-224).
-    const double s0 = ps.Cf0 - ps.a0, s1 = ps.Cf1 - ps.a1, s2 = ps.Cf2 - ps.a2;
-    const double gdc = (double)ps.gc0 * D.x + (double)ps.gc1 * D.y + (double)ps.gc2 * D.z;
-    const double num = (double)ps.gc0 * s0 + (double)ps.gc1 * s1 + (double)ps.gc2 * s2 + (double)ps.gT * (double)ps.Tf;
+    // suffix_i = sum_{j>i} c_j sigma_j A_j = C - prefix_i: the subtraction in double keeps
+    // its full relative accuracy (raster.hpp:212-224 accumulates it backwards in float);
+    // the rest is float, as in the reference.
+    const float s0 = (float)(ps.Cf0 - ps.a0), s1 = (float)(ps.Cf1 - ps.a1), s2 = (float)(ps.Cf2 - ps.a2);
+    const float gdc = ps.gc0 * D.x + ps.gc1 * D.y + ps.gc2 * D.z;
+    const float num = ps.gc0 * s0 + ps.gc1 * s1 + ps.gc2 * s2 + ps.gT * ps.Tf;
     const float inv_om = __frcp_rn(1.0f - sigma);  // 1/(1-sigma), sigma <= 0.99
-    const float d_sigma = (float)(gdc * a_i - num * (double)inv_om);
+    const float d_sigma = gdc * a_i - num * inv_om;
     v[5] = ps.gc0 * w;
     v[6] = ps.gc1 * w;
     v[7] = ps.gc2 * w;
