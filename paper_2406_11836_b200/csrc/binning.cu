@@ -91,7 +91,10 @@ __global__ void k_emit_pairs(const uint32_t* __restrict__ sorted_idx, const uint
         const uint32_t my0 = __shfl_sync(0xffffffffu, y0, lo);
         if (q < total) {
             const uint32_t r = q - ex;
-            const uint32_t ty = my0 + r / mw, tx = mx0 + r % mw;
+            // r / mw by a float reciprocal: (r + 0.5) / mw <= tiles_y stays >= 0.5 / mw away from
+            // an integer, far beyond the float error (r, mw < 2^16)
+            const uint32_t dy = (uint32_t)(((float)r + 0.5f) * __frcp_rn((float)mw));
+            const uint32_t ty = my0 + dy, tx = mx0 + (r - dy * mw);
             pair_tile[base + q] = (uint16_t)(ty * (uint32_t)tiles_x + tx);
             pair_val[base + q] = mi;
         }
