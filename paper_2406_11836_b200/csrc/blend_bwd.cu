@@ -81,9 +81,11 @@ __device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint
 /// Per-pixel backward state.
 struct PixState {
     float T;                 // replayed transmittance (bitwise the forward's sequence)
-    double a0, a1, a2;       // running prefix sum of c*sigma*A (double, as the forward's D)
+    // suffix_i = sum_{j>i} c_j sigma_j A_j, kept as the forward's double total C minus the
+    // running prefix (raster.hpp:212-224 accumulates it backwards in float): double keeps
+    // its relative accuracy however much of C is already spent
+    double r0, r1, r2;
     float gc0, gc1, gc2, gT;
-    double Cf0, Cf1, Cf2;    // total sum from the forward (double)
     float Tf;
     float pxf, pyf;
 };
@@ -96,14 +98,12 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     const float a_i = ps.T;
     const float w = fmul(sigma, a_i);
     const double wd = (double)sigma * (double)a_i;
-    ps.a0 += (double)D.x * wd;
-    ps.a1 += (double)D.y * wd;
-    ps.a2 += (double)D.z * wd;
+    ps.r0 -= (double)D.x * wd;
+    ps.r1 -= (double)D.y * wd;
+    ps.r2 -= (double)D.z * wd;
     ps.T = fmul(ps.T, fsub(1.0f, sigma));
-    // suffix_i = sum_{j>i} c_j sigma_j A_j = C - prefix_i: the subtraction in double keeps
-    // its full relative accuracy (raster.hpp:212-224 accumulates it backwards in float);
-    // the rest is float, as in the reference.
-    const float s0 = (float)(ps.Cf0 - ps.a0), s1 = (float)(ps.Cf1 - ps.a1), s2 = (float)(ps.Cf2 - ps.a2);
+    // the rest in float, as in the reference
+    const float s0 = (float)ps.r0, s1 = (float)ps.r1, s2 = (float)ps.r2;
     const float gdc = ps.gc0 * D.x + ps.gc1 * D.y + ps.gc2 * D.z;
     const float num = ps.gc0 * s0 + ps.gc1 * s1 + ps.gc2 * s2 + ps.gT * ps.Tf;
     const float inv_om = __frcp_rn(1.0f - sigma);  // 1/(1-sigma), sigma <= 0.99
@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
 
     PixState ps;
     ps.T = 1.0f;
-    ps.a0 = ps.a1 = ps.a2 = 0.0;
     ps.pxf = pr.pxf;
     ps.pyf = pr.pyf;
     bool done = !inside;
@@ -236,9 +235,9 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
         ps.gc1 = g.y;
         ps.gc2 = g.z;
         ps.gT = g.w;
-        ps.Cf0 = fwd_cd[3 * pix];
-        ps.Cf1 = fwd_cd[3 * pix + 1];
-        ps.Cf2 = fwd_cd[3 * pix + 2];
+        ps.r0 = fwd_cd[3 * pix];
+        ps.r1 = fwd_cd[3 * pix + 1];
+        ps.r2 = fwd_cd[3 * pix + 2];
         ps.Tf = f.w;
         const float e = ro.grad_skip_eps;
         const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
@@ -433,7 +432,6 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
     const size_t pix = (size_t)py * vp.width + px;
     PixState ps;
     ps.T = 1.0f;
-    ps.a0 = ps.a1 = ps.a2 = 0.0;
     ps.pxf = fadd((float)px, 0.5f);
     ps.pyf = fadd((float)py, 0.5f);
     int n = 0;
@@ -444,9 +442,9 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
         ps.gc1 = g.y;
         ps.gc2 = g.z;
         ps.gT = g.w;
-        ps.Cf0 = fwd_cd[3 * pix];
-        ps.Cf1 = fwd_cd[3 * pix + 1];
-        ps.Cf2 = fwd_cd[3 * pix + 2];
+        ps.r0 = fwd_cd[3 * pix];
+        ps.r1 = fwd_cd[3 * pix + 1];
+        ps.r2 = fwd_cd[3 * pix + 2];
         ps.Tf = f.w;
         const float e = ro.grad_skip_eps;
         const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
@@ -536,7 +534,6 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
     pr.pyf = fadd((float)py, 0.5f);
     PixState ps;
     ps.T = 1.0f;
-    ps.a0 = ps.a1 = ps.a2 = 0.0;
     ps.pxf = pr.pxf;
     ps.pyf = pr.pyf;
     const float4 gg = grad_ct[pix], ff = fwd_ct[pix];
@@ -544,9 +541,9 @@ __global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate
     ps.gc1 = gg.y;
     ps.gc2 = gg.z;
     ps.gT = gg.w;
-    ps.Cf0 = fwd_cd[3 * (size_t)pix];
-    ps.Cf1 = fwd_cd[3 * (size_t)pix + 1];
-    ps.Cf2 = fwd_cd[3 * (size_t)pix + 2];
+    ps.r0 = fwd_cd[3 * (size_t)pix];
+    ps.r1 = fwd_cd[3 * (size_t)pix + 1];
+    ps.r2 = fwd_cd[3 * (size_t)pix + 2];
     ps.Tf = ff.w;
     const float e = ro.grad_skip_eps;
     if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) continue;
