@@ -25,20 +25,32 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir):
+def _tiny_case():
+    """Three small splats split 8 ways: most KD subsets (and so some ranks' blocks) are empty."""
+    from paper_2406_11836_b200 import engine
+    s = engine.synth_splats(1_000_000, seed=9, sh_degree=3).take(np.arange(3))
+    cam = engine.ring_camera(48, 40, 0, n_views=64)
+    target = np.random.default_rng(2).random((1, 40, 48, 3), dtype=np.float32)
+    return s, 3, False, cam, target, (0.0, 0.0, 0.0)
+
+
+def _golden_case():
+    from conftest import Golden
+    g = Golden(NAME)
+    return g.splats(), g.args["kd"], g.oracle_mode, g.camera(), g["step_target"][None], g.bg
+
+
+def _worker(rank, world, port, out_dir, case="golden"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from conftest import Golden
         from host_transport import GlooTransport
         from paper_2406_11836_b200 import engine
-        g = Golden(NAME)
-        s = g.splats()
-        cfg = engine.train_config(kd_depth=g.args["kd"])
-        mgr = engine.Manager(s, cfg, engine.render_options(oracle=g.oracle_mode), device=0, rank=rank, world=world,
+        s, kd, oracle, cam, target, bg = _tiny_case() if case == "tiny" else _golden_case()
+        cfg = engine.train_config(kd_depth=kd)
+        mgr = engine.Manager(s, cfg, engine.render_options(oracle=oracle), device=0, rank=rank, world=world,
                              transport=GlooTransport())
-        cam = g.camera()
-        res = mgr.train_step([cam], g["step_target"][None], g.bg)
+        res = mgr.train_step([cam], target, bg)
         K = mgr.table.subset_count
         maps = {}
         for k in range(K):
@@ -52,17 +64,14 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_multi_rank_step_matches_single_rank_virtual_slices(tmp_path, world):
-    from conftest import Golden
+@pytest.mark.parametrize("world,case", [(2, "golden"), (4, "golden"), (2, "tiny")])
+def test_multi_rank_step_matches_single_rank_virtual_slices(tmp_path, world, case):
     from paper_2406_11836_b200 import engine
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    g = Golden(NAME)
-    s = g.splats()
-    cam = g.camera()
-    mgr = engine.Manager(s, engine.train_config(kd_depth=g.args["kd"]), engine.render_options(oracle=g.oracle_mode))
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), case), nprocs=world, join=True)
+    s, kd, oracle, cam, target, bg = _tiny_case() if case == "tiny" else _golden_case()
+    mgr = engine.Manager(s, engine.train_config(kd_depth=kd), engine.render_options(oracle=oracle))
     mgr.ctx.set_virtual_slices(world)
-    ref = mgr.train_step([cam], g["step_target"][None], g.bg)
+    ref = mgr.train_step([cam], target, bg)
     K = mgr.table.subset_count
     got = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
     for r in range(world):
