@@ -19,6 +19,7 @@
 // (shared-memory float atomics are CAS loops on sm_100).  Pixels skipped by
 // the reference rule (gc.isZero() && gT == 0, raster.hpp:285) never emit.
 #include "kernels.h"
+#include "fallback_select.cuh"
 
 namespace dgs_b200 {
 
@@ -513,92 +514,65 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
     }
 }
 
-// Exact fallback for pixels that overflowed the ring in the forward pass:
-// watermark selection (as in blend_fwd.cu) with global atomics.
-constexpr int FB = 16;
-
-__global__ void k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate, const SplatRec* __restrict__ recs,
-                                     const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
-                                     const float4* __restrict__ fwd_ct, const double* __restrict__ fwd_cd,
-                                     const float4* __restrict__ grad_ct, const uint32_t* __restrict__ ovf_list,
-                                     const uint32_t* __restrict__ n_ovf_dev, float* __restrict__ g2d, size_t ld2) {
+// Exact fallback for ring-overflow pixels: one warp per pixel walks the tile
+// list in (t, id) order (fallback_select.cuh), accumulating as it goes.
+__global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate,
+                                                           const SplatRec* __restrict__ recs,
+                                                           const uint32_t* __restrict__ pair_val,
+                                                           const uint2* __restrict__ ranges,
+                                                           const float2* __restrict__ ext,
+                                                           const float4* __restrict__ fwd_ct,
+                                                           const double* __restrict__ fwd_cd,
+                                                           const float4* __restrict__ grad_ct,
+                                                           const uint32_t* __restrict__ ovf_list,
+                                                           const uint32_t* __restrict__ n_ovf_dev, float* __restrict__ g2d,
+                                                           size_t ld2) {
     // grid-stride over the device-side overflow count (no host round trip)
     const uint32_t n_ovf = *n_ovf_dev;
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_ovf; w += gridDim.x * blockDim.x) {
-    const uint32_t pix = ovf_list[w];
-    const int px = pix % vp.width, py = pix / vp.width;
-    const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
-    PixelRay pr;
-    pixel_ray_dir(vp, px, py, pr.d);
-    pr.pxf = fadd((float)px, 0.5f);
-    pr.pyf = fadd((float)py, 0.5f);
-    PixState ps;
-    ps.T = 1.0f;
-    ps.pxf = pr.pxf;
-    ps.pyf = pr.pyf;
-    const float4 gg = grad_ct[pix], ff = fwd_ct[pix];
-    ps.gc0 = gg.x;
-    ps.gc1 = gg.y;
-    ps.gc2 = gg.z;
-    ps.gT = gg.w;
-    ps.r0 = fwd_cd[3 * (size_t)pix];
-    ps.r1 = fwd_cd[3 * (size_t)pix + 1];
-    ps.r2 = fwd_cd[3 * (size_t)pix + 2];
-    ps.Tf = ff.w;
-    const float e = ro.grad_skip_eps;
-    if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) continue;
-    const uint2 rg = ranges[tile];
-    float wt = -kInf;
-    uint32_t wid = 0;
-    bool have_w = false, done = false;
-    float bt[FB], bs[FB], bgv[FB];
-    uint32_t bi[FB], bm[FB];
-    while (!done) {
-        int m = 0;
-        for (uint32_t p = rg.x; p < rg.y; ++p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_ovf; w += nw) {
+        const uint32_t pix = ovf_list[w];
+        const int px = pix % vp.width, py = pix / vp.width;
+        const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
+        PixelRay pr;
+        pixel_ray_dir(vp, px, py, pr.d);
+        pr.pxf = fadd((float)px, 0.5f);
+        pr.pyf = fadd((float)py, 0.5f);
+        PixState ps;
+        ps.T = 1.0f;
+        ps.pxf = pr.pxf;
+        ps.pyf = pr.pyf;
+        const float4 gg = grad_ct[pix], ff = fwd_ct[pix];
+        ps.gc0 = gg.x;
+        ps.gc1 = gg.y;
+        ps.gc2 = gg.z;
+        ps.gT = gg.w;
+        ps.r0 = fwd_cd[3 * (size_t)pix];
+        ps.r1 = fwd_cd[3 * (size_t)pix + 1];
+        ps.r2 = fwd_cd[3 * (size_t)pix + 2];
+        ps.Tf = ff.w;
+        const float e = ro.grad_skip_eps;
+        if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) continue;
+        auto eval = [&](uint32_t mem, float& t, float& sigma, float& g, uint32_t& id) {
             float4 A, B, C, D;
-            const uint32_t mem = pair_val[p];
             load_rec(recs, mem, A, B, C, D);
-            float t, sigma, g;
-            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
-            const uint32_t id = __float_as_uint(C.w);
-            if (have_w && !(t > wt || (t == wt && id > wid))) continue;
-            if (m == FB && !(t < bt[FB - 1] || (t == bt[FB - 1] && id < bi[FB - 1]))) continue;
-            int pos = m < FB ? m : FB - 1;
-            while (pos > 0 && (t < bt[pos - 1] || (t == bt[pos - 1] && id < bi[pos - 1]))) {
-                bt[pos] = bt[pos - 1];
-                bi[pos] = bi[pos - 1];
-                bs[pos] = bs[pos - 1];
-                bgv[pos] = bgv[pos - 1];
-                bm[pos] = bm[pos - 1];
-                --pos;
-            }
-            bt[pos] = t;
-            bi[pos] = id;
-            bs[pos] = sigma;
-            bgv[pos] = g;
-            bm[pos] = mem;
-            if (m < FB) ++m;
-        }
-        for (int k = 0; k < m; ++k) {
-            if (ro.stop > 0.0f && ps.T < ro.stop) {
-                done = true;
-                break;
-            }
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) return false;
+            id = __float_as_uint(C.w);
+            return true;
+        };
+        auto emit = [&](float, uint32_t, float sigma, float g, uint32_t mem) {
+            if (ro.stop > 0.0f && ps.T < ro.stop) return false;
             float4 A, B, C, D;
-            load_rec(recs, bm[k], A, B, C, D);
+            load_rec(recs, mem, A, B, C, D);
             float v[9];
-            contribution_grad(ps, bs[k], bgv[k], A, B, D, ro.sigma_clamp, v);
-            for (int f = 0; f < 9; ++f)
-                if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + bm[k], v[f]);
-        }
-        if (m < FB) done = true;
-        if (m > 0) {
-            wt = bt[m - 1];
-            wid = bi[m - 1];
-            have_w = true;
-        }
-    }
+            contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
+            if (lane == 0)
+                for (int f = 0; f < 9; ++f)
+                    if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+            return true;
+        };
+        warp_ordered_walk(pr.pxf, pr.pyf, ranges[tile], pair_val, recs, ext, eval, emit);
     }
 }
 
@@ -642,8 +616,8 @@ void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
                                const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
                                const uint32_t* ovf_list, const uint32_t* n_ovf_dev, float* g2d, size_t ld2,
                                cudaStream_t s) {
-    k_blend_bwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, fwd_ct, fwd_cd, grad_ct,
-                                               ovf_list, n_ovf_dev, g2d, ld2);
+    k_blend_bwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, fwd_ct, fwd_cd,
+                                               grad_ct, ovf_list, n_ovf_dev, g2d, ld2);
 }
 
 }  // namespace dgs_b200

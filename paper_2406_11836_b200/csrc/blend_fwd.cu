@@ -16,6 +16,7 @@
 // order is therefore exactly the reference's per-pixel std::sort order.  A
 // pixel whose ring would overflow is handed to an exact O(n^2/16) fallback.
 #include "kernels.h"
+#include "fallback_select.cuh"
 
 namespace dgs_b200 {
 
@@ -396,93 +397,65 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fwd(ViewParams vp, R
     }
 }
 
-// Exact fallback for ring-overflow pixels: repeatedly selects the next 16
-// contributions above a (t, id) watermark by scanning the whole tile list.
-constexpr int FB = 16;
-
-__global__ void k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate, const SplatRec* __restrict__ recs,
-                                     const uint32_t* __restrict__ pair_val, const uint2* __restrict__ ranges,
-                                     float4* __restrict__ out_ct, const uint32_t* __restrict__ ovf_list,
-                                     const uint32_t* __restrict__ n_ovf_dev, uint32_t* __restrict__ dbg_ids, uint32_t* __restrict__ dbg_cnt,
-                                     int dbg_cap, double* __restrict__ out_cd) {
+// Exact fallback for ring-overflow pixels: one warp per pixel walks the tile
+// list in (t, id) order (fallback_select.cuh) and composites as it goes.
+__global__ void __launch_bounds__(64) k_blend_fwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate,
+                                                           const SplatRec* __restrict__ recs,
+                                                           const uint32_t* __restrict__ pair_val,
+                                                           const uint2* __restrict__ ranges,
+                                                           const float2* __restrict__ ext, float4* __restrict__ out_ct,
+                                                           const uint32_t* __restrict__ ovf_list,
+                                                           const uint32_t* __restrict__ n_ovf_dev,
+                                                           uint32_t* __restrict__ dbg_ids, uint32_t* __restrict__ dbg_cnt,
+                                                           int dbg_cap, double* __restrict__ out_cd) {
     // grid-stride over the device-side overflow count (no host round trip)
     const uint32_t n_ovf = *n_ovf_dev;
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_ovf; w += gridDim.x * blockDim.x) {
-    const uint32_t pix = ovf_list[w];
-    const int px = pix % vp.width, py = pix / vp.width;
-    const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
-    PixelRay pr;
-    pixel_ray_dir(vp, px, py, pr.d);
-    pr.pxf = fadd((float)px, 0.5f);
-    pr.pyf = fadd((float)py, 0.5f);
-    const uint2 rg = ranges[tile];
-    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-    double D0 = 0.0, D1 = 0.0, D2 = 0.0;
-    float wt = -kInf;
-    uint32_t wid = 0;
-    bool have_w = false, done = false;
-    int nemit = 0;
-    float bt[FB], bs[FB], c0[FB], c1[FB], c2[FB];
-    uint32_t bi[FB];
-    while (!done) {
-        int m = 0;
-        for (uint32_t p = rg.x; p < rg.y; ++p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_ovf; w += nw) {
+        const uint32_t pix = ovf_list[w];
+        const int px = pix % vp.width, py = pix / vp.width;
+        const int tile = (py / kTileSize) * vp.tiles_x + px / kTileSize;
+        PixelRay pr;
+        pixel_ray_dir(vp, px, py, pr.d);
+        pr.pxf = fadd((float)px, 0.5f);
+        pr.pyf = fadd((float)py, 0.5f);
+        float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+        double D0 = 0.0, D1 = 0.0, D2 = 0.0;
+        int nemit = 0;
+        auto eval = [&](uint32_t mem, float& t, float& sigma, float& g, uint32_t& id) {
             float4 A, B, C, D;
-            load_rec(recs, pair_val[p], A, B, C, D);
-            float t, sigma, g;
-            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
-            const uint32_t id = __float_as_uint(C.w);
-            if (have_w && !(t > wt || (t == wt && id > wid))) continue;
-            if (m == FB && !(t < bt[FB - 1] || (t == bt[FB - 1] && id < bi[FB - 1]))) continue;
-            int pos = m < FB ? m : FB - 1;
-            while (pos > 0 && (t < bt[pos - 1] || (t == bt[pos - 1] && id < bi[pos - 1]))) {
-                bt[pos] = bt[pos - 1];
-                bi[pos] = bi[pos - 1];
-                bs[pos] = bs[pos - 1];
-                c0[pos] = c0[pos - 1];
-                c1[pos] = c1[pos - 1];
-                c2[pos] = c2[pos - 1];
-                --pos;
-            }
-            bt[pos] = t;
-            bi[pos] = id;
-            bs[pos] = sigma;
-            c0[pos] = D.x;
-            c1[pos] = D.y;
-            c2[pos] = D.z;
-            if (m < FB) ++m;
-        }
-        for (int k = 0; k < m; ++k) {
-            if (ro.stop > 0.0f && T < ro.stop) {
-                done = true;
-                break;
-            }
-            const float wgt = fmul(bs[k], T);
-            C0 = fadd(C0, fmul(c0[k], wgt));
-            C1 = fadd(C1, fmul(c1[k], wgt));
-            C2 = fadd(C2, fmul(c2[k], wgt));
-            const double wd = (double)bs[k] * (double)T;
-            D0 += (double)c0[k] * wd;
-            D1 += (double)c1[k] * wd;
-            D2 += (double)c2[k] * wd;
-            T = fmul(T, fsub(1.0f, bs[k]));
-            if (dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[(size_t)pix * dbg_cap + nemit] = bi[k];
+            load_rec(recs, mem, A, B, C, D);
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) return false;
+            id = __float_as_uint(C.w);
+            return true;
+        };
+        auto emit = [&](float, uint32_t id, float sigma, float, uint32_t mem) {
+            if (ro.stop > 0.0f && T < ro.stop) return false;  // raster.hpp:183
+            const float4 col = __ldg(reinterpret_cast<const float4*>(recs + mem) + 3);
+            const float wgt = fmul(sigma, T);
+            C0 = fadd(C0, fmul(col.x, wgt));
+            C1 = fadd(C1, fmul(col.y, wgt));
+            C2 = fadd(C2, fmul(col.z, wgt));
+            const double wd = (double)sigma * (double)T;
+            D0 += (double)col.x * wd;
+            D1 += (double)col.y * wd;
+            D2 += (double)col.z * wd;
+            T = fmul(T, fsub(1.0f, sigma));
+            if (lane == 0 && dbg_ids != nullptr && nemit < dbg_cap) dbg_ids[(size_t)pix * dbg_cap + nemit] = id;
             ++nemit;
+            return true;
+        };
+        warp_ordered_walk(pr.pxf, pr.pyf, ranges[tile], pair_val, recs, ext, eval, emit);
+        if (lane == 0) {
+            out_ct[pix] = make_float4(C0, C1, C2, T);
+            if (out_cd != nullptr) {
+                out_cd[3 * (size_t)pix] = D0;
+                out_cd[3 * (size_t)pix + 1] = D1;
+                out_cd[3 * (size_t)pix + 2] = D2;
+            }
+            if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
         }
-        if (m < FB) done = true;
-        if (m > 0) {
-            wt = bt[m - 1];
-            wid = bi[m - 1];
-            have_w = true;
-        }
-    }
-    out_ct[pix] = make_float4(C0, C1, C2, T);
-    if (out_cd != nullptr) {
-        out_cd[3 * (size_t)pix] = D0;
-        out_cd[3 * (size_t)pix + 1] = D1;
-        out_cd[3 * (size_t)pix + 2] = D2;
-    }
-    if (dbg_cnt != nullptr) dbg_cnt[pix] = (uint32_t)nemit;
     }
 }
 
@@ -516,8 +489,8 @@ void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
                                float4* out_ct, const uint32_t* ovf_list, const uint32_t* n_ovf_dev, uint32_t* dbg_ids,
                                uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s) {
     // fixed grid, device-side count: launched unconditionally (exits at once when nothing overflowed)
-    k_blend_fwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, out_ct, ovf_list,
-                                               n_ovf_dev, dbg_ids, dbg_cnt, dbg_cap, out_cd);
+    k_blend_fwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, out_ct,
+                                               ovf_list, n_ovf_dev, dbg_ids, dbg_cnt, dbg_cap, out_cd);
 }
 
 }  // namespace dgs_b200
