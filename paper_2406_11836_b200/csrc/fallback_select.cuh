@@ -11,7 +11,7 @@
 
 namespace dgs_b200 {
 
-constexpr int kFbBatch = 16;
+constexpr int kFbBatch = 64;
 
 /// Returns when `emit` returns false (the pixel terminated) or the list is exhausted.
 template <class Eval, class Emit>
