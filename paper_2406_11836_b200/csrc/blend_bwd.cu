@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, Render
                                                            const uint32_t* __restrict__ pair_val,
                                                            const uint2* __restrict__ ranges,
                                                            const float2* __restrict__ ext,
+                                                           const uint32_t* __restrict__ dmax_bits, float onorm,
                                                            const float4* __restrict__ fwd_ct,
                                                            const double* __restrict__ fwd_cd,
                                                            const float4* __restrict__ grad_ct,
@@ -572,7 +573,13 @@ __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, Render
                     if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
             return true;
         };
-        warp_ordered_walk(pr.pxf, pr.pyf, ranges[tile], pair_val, recs, ext, eval, emit);
+        __shared__ FbRing rings[2];  // one per warp of the 64-thread block
+        const float dmax = __uint_as_float(dmax_bits[0]);
+        const uint32_t r_lo_bits = dmax_bits[1];
+        const int r_shift = range_key_shift(r_lo_bits, dmax_bits[3]);
+        auto bound = [&](float range) { return order_bound(range_bucket_lo(range, r_lo_bits, r_shift), dmax, onorm); };
+        warp_ring_walk(pr.pxf, pr.pyf, ranges[tile], pair_val, recs, ext, rings[(threadIdx.x >> 5) & 1], bound, eval,
+                       emit);
     }
 }
 
@@ -616,8 +623,9 @@ void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
                                const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
                                const uint32_t* ovf_list, const uint32_t* n_ovf_dev, float* g2d, size_t ld2,
                                cudaStream_t s) {
-    k_blend_bwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, fwd_ct, fwd_cd,
-                                               grad_ct, ovf_list, n_ovf_dev, g2d, ld2);
+    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
+    k_blend_bwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, vb.dmax_bits,
+                                               onorm, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, g2d, ld2);
 }
 
 }  // namespace dgs_b200

@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(64) k_blend_fwd_fallback(ViewParams vp, Render
                                                            const SplatRec* __restrict__ recs,
                                                            const uint32_t* __restrict__ pair_val,
                                                            const uint2* __restrict__ ranges,
-                                                           const float2* __restrict__ ext, float4* __restrict__ out_ct,
+                                                           const float2* __restrict__ ext,
+                                                           const uint32_t* __restrict__ dmax_bits, float onorm, float4* __restrict__ out_ct,
                                                            const uint32_t* __restrict__ ovf_list,
                                                            const uint32_t* __restrict__ n_ovf_dev,
                                                            uint32_t* __restrict__ dbg_ids, uint32_t* __restrict__ dbg_cnt,
@@ -446,7 +447,13 @@ __global__ void __launch_bounds__(64) k_blend_fwd_fallback(ViewParams vp, Render
             ++nemit;
             return true;
         };
-        warp_ordered_walk(pr.pxf, pr.pyf, ranges[tile], pair_val, recs, ext, eval, emit);
+        __shared__ FbRing rings[2];  // one per warp of the 64-thread block
+        const float dmax = __uint_as_float(dmax_bits[0]);
+        const uint32_t r_lo_bits = dmax_bits[1];
+        const int r_shift = range_key_shift(r_lo_bits, dmax_bits[3]);
+        auto bound = [&](float range) { return order_bound(range_bucket_lo(range, r_lo_bits, r_shift), dmax, onorm); };
+        warp_ring_walk(pr.pxf, pr.pyf, ranges[tile], pair_val, recs, ext, rings[(threadIdx.x >> 5) & 1], bound, eval,
+                       emit);
         if (lane == 0) {
             out_ct[pix] = make_float4(C0, C1, C2, T);
             if (out_cd != nullptr) {
@@ -489,8 +496,9 @@ void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
                                float4* out_ct, const uint32_t* ovf_list, const uint32_t* n_ovf_dev, uint32_t* dbg_ids,
                                uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s) {
     // fixed grid, device-side count: launched unconditionally (exits at once when nothing overflowed)
-    k_blend_fwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, out_ct,
-                                               ovf_list, n_ovf_dev, dbg_ids, dbg_cnt, dbg_cap, out_cd);
+    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
+    k_blend_fwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, vb.dmax_bits,
+                                               onorm, out_ct, ovf_list, n_ovf_dev, dbg_ids, dbg_cnt, dbg_cap, out_cd);
 }
 
 }  // namespace dgs_b200

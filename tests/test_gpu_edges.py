@@ -130,12 +130,14 @@ def _ring_overflow_scene(cam, n=64, seed=7):
     return s
 
 
-def test_ring_overflow_fallbacks_match_oracle():
+@pytest.mark.parametrize("n", [64, 300])
+def test_ring_overflow_fallbacks_match_oracle(n):
     """Pixels whose reorder ring overflows take the exact fallback kernels
     (forward and backward): the composite and the gradients still match the
-    oracle."""
+    oracle.  n = 300 also fills the fallback's own 256-entry ring, whose walk
+    then continues from the last emitted contribution."""
     cam = engine.ring_camera(48, 40, 0, n_views=64)
-    s = _ring_overflow_scene(cam)
+    s = _ring_overflow_scene(cam, n=n)
     ro, o = engine.render_options(grad_skip_eps=0.0), ob.opts(False, grad_skip_eps=0.0)
     mgr = engine.Manager(s, engine.train_config(kd_depth=0), ro)
     mgr.ctx.set_collect_stats(True)
@@ -148,15 +150,16 @@ def test_ring_overflow_fallbacks_match_oracle():
     ctx.set_table(engine.build_kdtree(s.mu, 0))
     ctx.set_options(ro, engine.train_config())
     ctx.load_subset(0, s)
-    ct, ids, cnt = ctx.render_partial(0, cam, dbg_cap=128)
+    cap = 512
+    ct, ids, cnt = ctx.render_partial(0, cam, dbg_cap=cap)
     sc = ob.Scene(s)
     sub = ob.Sub()
     sub.n = 0
     ocam = ob.cam_of(cam.record())
     ref = np.zeros((40, 48, 4), np.float32)
-    rids = np.zeros((40 * 48, 128), np.uint32)
+    rids = np.zeros((40 * 48, cap), np.uint32)
     rcnt = np.zeros(40 * 48, np.uint32)
-    assert ob.lib().orc_partial_render(C.byref(sc.c), C.byref(sub), C.byref(ocam), C.byref(o), ob.p(ref), 128,
+    assert ob.lib().orc_partial_render(C.byref(sc.c), C.byref(sub), C.byref(ocam), C.byref(o), ob.p(ref), cap,
                                        ob.p(rids), ob.p(rcnt)) == 0
     assert rcnt.max() > 8
     assert np.abs(ct - ref).max() <= 1e-4
