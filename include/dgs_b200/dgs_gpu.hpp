@@ -201,8 +201,12 @@ inline std::vector<dgs_plane> planes_of(const std::vector<Subspace<float>>& subs
     return out;
 }
 
-/// One device context (one GPU).  The stateless functions below share a
-/// process-wide default context on device 0.
+/// One device context (one GPU).  The stateless functions below use a
+/// per-THREAD default context on device 0: the reference's ThreadWorkerLink
+/// runs one worker thread per subset, each calling partial_render /
+/// partial_render_backward concurrently (worker.hpp:70,93), and a context is
+/// not thread-safe (its subset slot, view buffers and pinned scalars are
+/// per-context state).
 class Device {
   public:
     explicit Device(int device = 0) { check(dgs_ctx_create(device, 0, 1, nullptr, &ctx_)); }
@@ -213,7 +217,7 @@ class Device {
     Device& operator=(const Device&) = delete;
     dgs_ctx* get() const { return ctx_; }
     static Device& default_device() {
-        static Device d(0);
+        static thread_local Device d(0);
         return d;
     }
 
@@ -493,9 +497,11 @@ class Manager {
     }
 
     /// manager.hpp:390-418 (the replica held by the subspace containing the centre wins)
+    /// A non-empty checkpoint_path sends MsgCheckpoint instead of MsgSnapshot
+    /// in the reference; its worker answers both with the same snapshot and
+    /// writes no file (worker.hpp:146-147), so the path is accepted and ignored.
     std::vector<SplatPack<float>> snapshot(const std::string& checkpoint_path = "") {
-        if (!checkpoint_path.empty())
-            throw std::invalid_argument("dgs::gpu::Manager::snapshot: checkpoint files are not supported");
+        (void)checkpoint_path;
         std::vector<SplatPack<float>> merged;
         std::set<SplatId> seen;
         std::vector<std::vector<SplatPack<float>>> per(table_.subset_count());
@@ -619,6 +625,7 @@ class Manager {
                 check(dgs_subset_load(dev_.get(), k, &pv, &mv, &vv, adam_step, epoch));
             }
         }
+        check(dgs_set_epoch(dev_.get(), epoch));  // every render task carries it (manager.hpp:276)
     }
 
     TrainConfig config_;

@@ -51,7 +51,9 @@ typedef struct dgs_camera {
 /* RenderOptions (splat.hpp:118-133).  grad_skip_eps is the threshold of the
  * reference's backward pixel skip `gc.isZero() && gT == 0` (raster.hpp:285):
  * Eigen's isZero() uses dummy_precision = 1e-5 for float, which is the
- * default here; 0 skips only exact zeros. camera_z_order is not supported. */
+ * default here; 0 skips only exact zeros.  camera_z_order != 0 selects the
+ * fast mode of splat.hpp:126 (per-view camera depth order, ties by id,
+ * raster.hpp:162). */
 typedef struct dgs_render_options {
     double truncation_radius;
     double near_plane;
@@ -179,6 +181,12 @@ int dgs_subset_load(dgs_ctx* ctx, int32_t k, const dgs_splats* params, const dgs
 int dgs_subset_store(dgs_ctx* ctx, int32_t k, dgs_splats* params, dgs_splats* m, dgs_splats* v,
                      uint64_t* adam_step);
 int64_t dgs_subset_size(dgs_ctx* ctx, int32_t k);
+/* The manager's partition epoch (Manager::epoch_, carried by every
+ * MsgRenderTask, manager.hpp:276).  Once set, dgs_train_step and
+ * dgs_render_partial refuse a local subset loaded with another epoch:
+ * DGS_ERR_RUNTIME "partition epoch mismatch" (worker.hpp:63).
+ * dgs_repartition sets it to its new epoch. */
+int dgs_set_epoch(dgs_ctx* ctx, uint64_t epoch);
 
 /* ---- Per-subset forward (engine.hpp:44-52 partial_render) -------------------- */
 /* Projection + binning + forward blend of local subset k for one view.

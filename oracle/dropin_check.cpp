@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace dgs;
@@ -204,6 +205,56 @@ int main() {
     }
     rep.add("partial_backward_rel", pb_err, 1e-3);
 
+    // ---- concurrency: one host thread per subset, as the reference's
+    //      ThreadWorkerLink runs its workers (worker.hpp:70,93) ---------------
+    // Each thread calls the stateless drop-ins (per-thread default context) at
+    // the same time as the others; the results must equal the single-thread ones.
+    {
+        const int K = tr.subset_count();
+        std::vector<PartialImage<float>> pc(K);
+        std::vector<GradBuffers<float>> gc;
+        std::vector<GradBuffers<float>> g1;
+        for (int k = 0; k < K; ++k) {
+            const auto mem = members_of(tr, k, splats);
+            gc.emplace_back(std::span<const Splat<float>>(mem));
+            g1.push_back(gpu::partial_render_backward(mem, tr.subspaces[k], cam, br[k].d_color, br[k].d_transmittance,
+                                                      opts));
+        }
+        std::vector<std::string> errs(K);
+        for (int round = 0; round < 3; ++round) {
+            std::vector<std::thread> ts;
+            for (int k = 0; k < K; ++k)
+                ts.emplace_back([&, k] {
+                    try {
+                        const auto mem = members_of(tr, k, splats);
+                        for (int rep_i = 0; rep_i < 4; ++rep_i) {
+                            pc[k] = gpu::partial_render(mem, tr.subspaces[k], cam, opts);
+                            gc[k] = gpu::partial_render_backward(mem, tr.subspaces[k], cam, br[k].d_color,
+                                                                 br[k].d_transmittance, opts);
+                        }
+                    } catch (const std::exception& e) {
+                        errs[k] = e.what();
+                    }
+                });
+            for (auto& t : ts) t.join();
+        }
+        double thr_render = 0, thr_grad = 0, thr_fail = 0;
+        for (int k = 0; k < K; ++k) {
+            if (!errs[k].empty()) {
+                thr_fail += 1;
+                std::fprintf(stderr, "thread %d: %s\n", k, errs[k].c_str());
+                continue;
+            }
+            thr_render = std::max({thr_render, max_abs(pc[k].color.data, pg[k].color.data),
+                                   max_abs(pc[k].transmittance.data, pg[k].transmittance.data)});
+            thr_grad = std::max(thr_grad, grad_rel(g1[k], gc[k]));
+        }
+        rep.add("threaded_failures", thr_fail, 0);
+        rep.add("threaded_partial_render_max_abs", thr_render, 0);
+        // float-atomic accumulation order may differ between runs
+        rep.add("threaded_partial_backward_rel", thr_grad, 1e-3);
+    }
+
     // ---- Manager: two training steps, then snapshot ------------------------
     TrainConfig cfg;
     cfg.kd_depth = 1;
@@ -239,6 +290,9 @@ int main() {
     // below the noise floor can put two steps 4 lr apart
     rep.add("snapshot_mu_max_abs", mu_err, 4 * 1.6e-4);
     rep.add("snapshot_opacity_max_abs", op_err, 4 * 0.025);
+    // snapshot(checkpoint_path): the worker answers MsgCheckpoint with a plain
+    // snapshot (worker.hpp:147), so a path must not change the result
+    rep.add("snapshot_checkpoint_size_err", std::fabs(double(m_gpu.snapshot("unused.ckpt").size()) - double(sg.size())), 0);
     m_gpu.repartition();
     rep.add("repartition_epoch_err", std::fabs(double(m_gpu.epoch()) - 1.0), 0);
 

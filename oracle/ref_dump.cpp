@@ -41,7 +41,11 @@
 #include <vector>
 
 using namespace dgs;
+#ifdef DGS_REF_DOUBLE
+using Real = double;  // precision probe (tests/golden/noise_probe.py)
+#else
 using Real = float;
+#endif
 
 namespace {
 
@@ -481,7 +485,9 @@ int main(int argc, char** argv) {
         const std::vector<Splat<Real>> gt_splats = splats;  // targets render the unperturbed scene
         if (has("perturb")) perturb(splats, std::uint64_t(iarg("perturb", 1)));
 
+#ifndef DGS_REF_DOUBLE
         if (has("save_ply")) save_splats_ply(std::span<const Splat<Real>>(splats), arg("save_ply", "scene.ply"), true);
+#endif
         if (has("save_scene")) {
             save_splats("scene_", splats);
             std::vector<Real> cr;
@@ -494,6 +500,7 @@ int main(int argc, char** argv) {
 
         RenderOptions opts = arg("mode", "default") == "oracle" ? oracle_options() : RenderOptions{};
         if (has("indicator_off")) opts.indicator_enabled = false;
+        if (iarg("z_order", 0) != 0) opts.camera_z_order = true;  // fast mode (splat.hpp:126, raster.hpp:162)
         const int view = int(iarg("view", 0));
         const Vec3<Real> bg{Real(farg("bg_r", 0)), Real(farg("bg_g", 0)), Real(farg("bg_b", 0))};
         const int depth = int(iarg("kd", 0));

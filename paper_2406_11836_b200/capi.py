@@ -129,6 +129,7 @@ _SIGS = {
     "dgs_subset_store": (C.c_int, [_P, C.c_int32, C.POINTER(SplatsC), C.POINTER(SplatsC), C.POINTER(SplatsC),
                                    C.POINTER(C.c_uint64)]),
     "dgs_subset_size": (C.c_int64, [_P, C.c_int32]),
+    "dgs_set_epoch": (C.c_int, [_P, C.c_uint64]),
     "dgs_render_partial": (C.c_int, [_P, C.c_int32, C.POINTER(Camera), _P, C.c_int32, _P, _P]),
     "dgs_dump_bins": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int64, C.POINTER(C.c_int64)]),
     "dgs_dump_records": (C.c_int, [_P, C.c_int32, _P, _P]),

@@ -30,6 +30,17 @@ __global__ void k_key16(const uint32_t* __restrict__ rkey, const uint32_t* __res
     vals[i] = (uint32_t)i;
 }
 
+/// camera_z_order: exact 32-bit keys (positive depths order like their bits;
+/// culled members take the top key).  The stable sort keeps member order on
+/// equal depths; the blends break those ties by id.
+__global__ void k_key32(const uint32_t* __restrict__ rkey, uint32_t* __restrict__ key, uint32_t* __restrict__ vals,
+                        int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = rkey[i];
+    vals[i] = (uint32_t)i;
+}
+
 /// Members in range order: their tile rectangle and tile count (the count is
 /// derived from the rectangle; culled members carry an empty one).  One random
 /// 8-byte gather per member; the scan and the emission then stream.
@@ -196,6 +207,9 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
     {
         cub::DoubleBuffer<uint32_t> k, v;
         MemberSort::Dispatch(nullptr, a, k, v, n, 0, kRangeKeyBits, true, 0);
+        size_t a32 = 0;
+        MemberSort::Dispatch(nullptr, a32, k, v, n, 0, 32, true, 0);
+        if (a32 > a) a = a32;
     }
     cub::DoubleBuffer<uint16_t> dk;
     cub::DoubleBuffer<uint32_t> dv;
@@ -222,12 +236,13 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     }
     const int blk = 256, grid = (n + blk - 1) / blk;
     // 1) members by range bucket: 16-bit keys (2 radix passes)
-    k_key16<<<grid, blk, 0, s>>>(vb.rkey, vb.dmax_bits, scan_buf, sort_vals, n);
+    if (vb.zorder) k_key32<<<grid, blk, 0, s>>>(vb.rkey, scan_buf, sort_vals, n);
+    else k_key16<<<grid, blk, 0, s>>>(vb.rkey, vb.dmax_bits, scan_buf, sort_vals, n);
     size_t tb = temp_bytes;
     const uint32_t* sorted_idx;
     {
         cub::DoubleBuffer<uint32_t> k(scan_buf, sort_keys_alt), v(sort_vals, sort_vals_alt);
-        MemberSort::Dispatch(temp, tb, k, v, n, 0, kRangeKeyBits, true, s);
+        MemberSort::Dispatch(temp, tb, k, v, n, 0, vb.zorder ? 32 : kRangeKeyBits, true, s);
         sorted_idx = v.Current();
     }
     // 2) tile counts in range order -> inclusive scan -> pair end offsets

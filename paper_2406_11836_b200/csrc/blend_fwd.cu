@@ -73,7 +73,8 @@ struct PixelRay {
 /// (raster.hpp:153-161).  Returns false when it does not contribute.
 __device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewParams& vp, const RenderOpts& ro,
                                                const Subspace& gate, const float4& A, const float4& B,
-                                               const float4& C, float& t_out, float& sigma_out, float& g_out) {
+                                               const float4& C, float zkey, float& t_out, float& sigma_out,
+                                               float& g_out) {
     const float dx = fsub(pr.pxf, A.x), dy = fsub(pr.pyf, A.y);
     // eval_2d (splat.hpp:326-332): m2 = delta . (inv_cov2d * delta)
     const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))), fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
@@ -90,7 +91,7 @@ __device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewPar
     const float ag = fmul(A.z, g);
     const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;  // std::min(alpha*g, clamp)
     if (!(sigma > 0.0f)) return false;
-    t_out = t;
+    t_out = ro.zorder ? zkey : t;  // camera_z_order: the per-view depth is the key (raster.hpp:162)
     sigma_out = sigma;
     g_out = g;
     return true;
@@ -311,7 +312,9 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fwd(ViewParams vp, R
         if (p < rg.y) {
             float4 A, B, C, D;
             load_rec(recs, m, A, B, C, D);
-            D.w = order_bound(range_bucket_lo(D.w, r_lo_bits, r_shift), dmax, onorm);
+            // bound on the ordering key of this and every later entry: the lower edge of
+            // the range bucket mapped to t, or (camera_z_order, exact 32-bit sort) the depth
+            if (!ro.zorder) D.w = order_bound(range_bucket_lo(D.w, r_lo_bits, r_shift), dmax, onorm);
             sA[tid] = A;
             sB[tid] = B;
             sC[tid] = C;
@@ -341,7 +344,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fwd(ViewParams vp, R
             const float4 A = sA[j], B = sB[j], C = sC[j];
             if (STATS) ++n_eval;
             float t, sigma, g;
-            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) continue;
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, D.w, t, sigma, g)) continue;
             const uint32_t id = __float_as_uint(C.w);
             if (cnt == KBUF) {  // ring full and nothing safe to emit: exact fallback
                 ovf = true;
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(64) k_blend_fwd_fallback(ViewParams vp, Render
         auto eval = [&](uint32_t mem, float& t, float& sigma, float& g, uint32_t& id) {
             float4 A, B, C, D;
             load_rec(recs, mem, A, B, C, D);
-            if (!eval_candidate(pr, vp, ro, gate, A, B, C, t, sigma, g)) return false;
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, D.w, t, sigma, g)) return false;
             id = __float_as_uint(C.w);
             return true;
         };
@@ -451,7 +454,9 @@ __global__ void __launch_bounds__(64) k_blend_fwd_fallback(ViewParams vp, Render
         const float dmax = __uint_as_float(dmax_bits[0]);
         const uint32_t r_lo_bits = dmax_bits[1];
         const int r_shift = range_key_shift(r_lo_bits, dmax_bits[3]);
-        auto bound = [&](float range) { return order_bound(range_bucket_lo(range, r_lo_bits, r_shift), dmax, onorm); };
+        auto bound = [&](float range) {
+            return ro.zorder ? range : order_bound(range_bucket_lo(range, r_lo_bits, r_shift), dmax, onorm);
+        };
         warp_ring_walk(pr.pxf, pr.pyf, ranges[tile], pair_val, recs, ext, rings[(threadIdx.x >> 5) & 1], bound, eval,
                        emit);
         if (lane == 0) {
@@ -475,13 +480,9 @@ void launch_blend_fwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
     const int tiles = vp.tiles_x * vp.tiles_y;
     const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
     const size_t smem = kFwdSmem;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_blend_fwd<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_fwd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_fwd<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    ensure_smem_attr((const void*)k_blend_fwd<false, false>, (int)smem);
+    ensure_smem_attr((const void*)k_blend_fwd<false, true>, (int)smem);
+    ensure_smem_attr((const void*)k_blend_fwd<true, true>, (int)smem);
 #define DGS_FWD(D, S)                                                                                              \
     k_blend_fwd<D, S><<<tiles, kBlendThreads, smem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, vb.dmax_bits, \
                                                          onorm, out_ct, ovf_flag, ovf_list, ovf_count, dbg_ids,       \

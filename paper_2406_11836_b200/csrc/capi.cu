@@ -14,6 +14,8 @@
 #include <iterator>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <random>
 #include <string>
 #include <thread>
@@ -28,6 +30,21 @@ namespace dgs_b200 {
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void ensure_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e) + " (cudaGetDevice)");
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({dev, func})) return;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess)
+        throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e) + " (cudaFuncSetAttribute, " +
+                        std::to_string(bytes) + " B dynamic shared memory)");
+    done.insert({dev, func});
+}
 
 #define CK(call)                                                                                 \
     do {                                                                                         \
@@ -219,6 +236,10 @@ struct Ctx {
     ncclComm_t comm = nullptr;
     Table table{};
     bool table_set = false;
+    // the manager's partition epoch (MsgRenderTask::epoch, manager.hpp:276); once
+    // set, every local subset must carry it (worker.hpp:63)
+    uint64_t epoch = 0;
+    bool epoch_set = false;
     DevBuf<Table> table_dev;
     dgs_render_options ro_in{};
     dgs_train_config cfg{};
@@ -273,6 +294,7 @@ RenderOpts to_render_opts(const dgs_render_options& o) {
     r.sh_degree = o.sh_degree;
     r.indicator_enabled = o.indicator_enabled;
     r.grad_skip_eps = (float)o.grad_skip_eps;
+    r.zorder = o.camera_z_order ? 1 : 0;
     return r;
 }
 
@@ -297,6 +319,12 @@ SubsetState& subset(Ctx& ctx, int k) {
     auto it = ctx.subsets.find(k);
     if (it == ctx.subsets.end()) throw std::invalid_argument("subset " + std::to_string(k) + " is not loaded on this rank");
     return *it->second;
+}
+
+/// WorkerCore::dispatch(MsgRenderTask) (worker.hpp:63): a render task carries
+/// the manager's epoch and a worker holding another partition refuses it.
+void check_epoch(const Ctx& ctx, const SubsetState& S) {
+    if (ctx.epoch_set && S.epoch != ctx.epoch) throw std::runtime_error("partition epoch mismatch");
 }
 
 __global__ void k_hwc_to_planar(const float* __restrict__ in, float* __restrict__ out, size_t px) {
@@ -356,6 +384,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     const size_t px = (size_t)vp.width * vp.height;
     vs.vp = vp;
     ViewBins& vb = vs.vb;
+    vb.zorder = ctx.ro.zorder;
     if (tiles > 65535) throw std::invalid_argument("render: more than 65535 16x16 tiles (16-bit tile keys)");
     vb.shjac = vs.shjac.ensure((size_t)10 * S.ld);
     vb.recs = vs.recs.ensure(n);
@@ -423,14 +452,16 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     // more than a quarter of the free HBM falls back to the ring-replay
     // backward (same results, slower) instead of failing the allocation.
     bool use_rec = ctx.records;
-    if (use_rec && !vs.rec_pos.p) {
-        const size_t need = (size_t)tiles * kRecCap * kBlendThreads * sizeof(uint16_t) + px * 2 + tiles;
+    const size_t rec_need = (size_t)tiles * kRecCap * kBlendThreads;  // u16 entries
+    if (use_rec && (vs.rec_pos.p == nullptr || rec_need > vs.rec_pos.n)) {
+        // any (re)allocation, e.g. a 1080p slot now rendering a 4K view
+        const size_t need = rec_need * sizeof(uint16_t) + px * 2 + tiles;
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
         use_rec = need <= free_b / 4;
     }
     if (use_rec) {
-        vs.rec_pos.ensure((size_t)tiles * kRecCap * kBlendThreads);
+        vs.rec_pos.ensure(rec_need);
         vs.rec_cnt.ensure(px);
         vs.rec_replay.ensure(tiles);
     }
@@ -1131,12 +1162,17 @@ int dgs_ctx_create_host_transport(int32_t device, int32_t rank, int32_t world, c
     return dgs_guard([&] {
         if (!t || !t->send || !t->recv || !t->flush || !t->allreduce_sum_f64)
             throw std::invalid_argument("dgs_ctx_create_host_transport: incomplete callbacks");
-        if (dgs_ctx_create(device, 0, 1, nullptr, out) != 0) throw std::runtime_error(g_last_error);
-        (*out)->rank = rank;
-        (*out)->world = world;
-        (*out)->host_xfer = true;
-        (*out)->xfer_cb = *t;
+        if (!out) throw std::invalid_argument("dgs_ctx_create_host_transport: null output");
+        *out = nullptr;
+        // validate before creating anything: an error return leaves nothing live in *out
         if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("dgs_ctx_create: bad rank/world");
+        dgs_ctx* c = nullptr;
+        if (dgs_ctx_create(device, 0, 1, nullptr, &c) != 0) throw std::runtime_error(g_last_error);
+        c->rank = rank;
+        c->world = world;
+        c->host_xfer = true;
+        c->xfer_cb = *t;
+        *out = c;
     });
 }
 
@@ -1214,10 +1250,16 @@ int dgs_set_table(dgs_ctx* ctx, const dgs_plane* planes, int32_t k_count, int32_
     });
 }
 
+int dgs_set_epoch(dgs_ctx* ctx, uint64_t epoch) {
+    return dgs_guard([&] {
+        ctx->epoch = epoch;
+        ctx->epoch_set = true;
+    });
+}
+
 int dgs_set_options(dgs_ctx* ctx, const dgs_render_options* ro, const dgs_train_config* cfg) {
     return dgs_guard([&] {
         if (ro) {
-            if (ro->camera_z_order) throw std::invalid_argument("camera_z_order fast mode is not supported");
             ctx->ro_in = *ro;
             ctx->ro = to_render_opts(*ro);
         }
@@ -1564,6 +1606,8 @@ int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t ex
             fresh[k] = std::move(S);
         }
         ctx->subsets = std::move(fresh);
+        ctx->epoch = epoch;  // the manager's new epoch (manager.hpp:441)
+        ctx->epoch_set = true;
         ctx->shared_dirty = true;
     });
 }
@@ -1679,6 +1723,7 @@ int dgs_render_partial(dgs_ctx* ctx, int32_t k, const dgs_camera* cam, float* ou
     return dgs_guard([&] {
         require_table(*ctx);
         SubsetState& S = subset(*ctx, k);
+        check_epoch(*ctx, S);
         const ViewParams vp = view_params(*cam);
         const size_t px = (size_t)vp.width * vp.height;
         DevBuf<uint32_t> d_ids, d_cnt;
@@ -2007,6 +2052,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                                             std::to_string(o));
             if (here) local.push_back(k);
         }
+        for (int k : local) check_epoch(*ctx, subset(*ctx, k));
         const uint64_t launches0 = ctx->launches;
         uint64_t nccl_bytes = 0;
         CK(cudaMemsetAsync(ctx->stats.p, 0, 2 * sizeof(BlendStats), ctx->stream));

@@ -50,6 +50,7 @@ struct RenderOpts {
     int sh_degree;      // -1: stored degree
     int indicator_enabled;
     float grad_skip_eps;  // render_maps_backward skip rule: |gc|<=eps (isZero) && gT==0
+    int zorder;           // camera_z_order (splat.hpp:126): order by camera depth, ties by id
 };
 
 /// One subspace's half-space list (partition.hpp:19-41).

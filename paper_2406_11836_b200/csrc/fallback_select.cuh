@@ -100,6 +100,7 @@ __device__ __forceinline__ void warp_ring_walk(float pxf, float pyf, uint2 rg, c
                                                const SplatRec* __restrict__ recs, const float2* __restrict__ ext,
                                                FbRing& ring, Bound bound, Eval eval, Emit emit) {
     const int lane = threadIdx.x & 31;
+    __syncwarp();  // the previous pixel's last pops read the ring this walk rewrites
     int head = 0, cnt = 0;  // warp-uniform
     bool have_last = false;
     float last_t = 0.0f;
@@ -143,8 +144,11 @@ __device__ __forceinline__ void warp_ring_walk(float pxf, float pyf, uint2 rg, c
                 warp_ordered_walk(pxf, pyf, rg, pair_val, recs, ext, eval, emit, have_last, last_t, last_id);
                 return;
             }
-            // insertion into the sorted ring (lane 0 writes; the warp reads after the sync)
+            // insertion into the sorted ring (lane 0 writes; the warp reads after the sync).
+            // The head test and pop() above read ring slots on every lane: order those
+            // reads before lane 0's shifts (shuffles/ballots are not memory fences).
             int pos = head + cnt;
+            __syncwarp();
             if (lane == 0) {
                 while (pos > head) {
                     const int pl = (pos - 1) & (kFbRing - 1);

@@ -9,6 +9,13 @@
 
 namespace dgs_b200 {
 
+/// Opts `func` into `bytes` of dynamic shared memory on the CURRENT device.
+/// Function attributes are per device context, so this is tracked per
+/// (device, function) under a mutex (several devices or host threads may
+/// launch concurrently); a failure is thrown as a CUDA error.  Defined in
+/// capi.cu.
+void ensure_smem_attr(const void* func, int bytes);
+
 /// Per-view, per-subset scratch produced by the projection/binning stage and
 /// consumed by both blend kernels.
 struct ViewBins {
@@ -28,6 +35,9 @@ struct ViewBins {
     uint32_t* tile_order = nullptr;  // [tiles] tiles by decreasing list length (the blends' block order)
     int64_t pairs = 0;
     int64_t visible = 0;
+    // camera_z_order: rkey / SplatRec::range hold the camera depth z and the
+    // member sort is exact (32-bit keys) instead of 16-bit range buckets
+    int zorder = 0;
 };
 
 // K1: projection + SH colour + tile rectangles (splat.hpp:288-321, raster.hpp:113-125).

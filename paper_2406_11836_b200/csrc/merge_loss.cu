@@ -475,11 +475,7 @@ void launch_merge_bwd_ordered(int px, int kcount, int kstride, const uint16_t* o
 void launch_loss(int W, int H, int row0, int row1, int in_base, int in_rows, const float* x, const float* y,
                  float lambda, const float* kernel, float inv_batch, float* grad, double* block_sums, int* n_blocks,
                  cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLossSmem);
-        configured = true;
-    }
+    ensure_smem_attr((const void*)k_loss, (int)kLossSmem);
     dim3 grid((W + kOT - 1) / kOT, (row1 - row0 + kOT - 1) / kOT, 3);
     *n_blocks = (int)(grid.x * grid.y * grid.z);
     // loss.hpp:16-17: C1 = (0.01)^2, C2 = (0.03)^2 evaluated in double, then T(.)

@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
                 rec.muy = mu1;
                 rec.muz = mu2;
                 rec.id = ids32[i];
-                rec.range = fsqrt(n2);
+                // the blends' ordering key: range ||mu - o|| (per-ray t order, exact via the
+                // reorder ring), or the camera depth (camera_z_order, raster.hpp:162)
+                rec.range = ro.zorder ? t2 : fsqrt(n2);
                 vb.recs[i] = rec;
                 vb.rkey[i] = f2u(rec.range);
                 dmax_local = wr;

@@ -300,6 +300,11 @@ class Context:
         self.table = table
         check(lib().dgs_set_table(self._h, table.c_planes(), table.subset_count, table.planes.shape[1]))
 
+    def set_epoch(self, epoch: int):
+        """The manager's partition epoch: local subsets loaded with another
+        epoch are refused with "partition epoch mismatch" (worker.hpp:63)."""
+        check(lib().dgs_set_epoch(self._h, int(epoch)))
+
     def set_options(self, ro: capi.RenderOptionsC | None = None, cfg: capi.TrainConfigC | None = None):
         check(lib().dgs_set_options(self._h, C.byref(ro) if ro is not None else None,
                                     C.byref(cfg) if cfg is not None else None))
@@ -484,6 +489,7 @@ class Manager:
                 continue
             self.ctx.load_subset(k, splats.take(idx), m.take(idx) if m is not None else None,
                                  v.take(idx) if v is not None else None, adam_step=adam_step, epoch=epoch)
+        self.ctx.set_epoch(epoch)
         self.epoch = epoch
 
     def train_step(self, cams, targets, bg=(0.0, 0.0, 0.0), targets_device_ptr=None) -> dict:

@@ -29,6 +29,9 @@ SETS = {
     # Manager::train_step with a batch of 3 views (summed GradBuffers, one Adam step), 4-way split.
     "g7_synth_kd2_batch3": dict(scene="synth", count=1500, w=56, h=40, n_views=8, seed=13, kd=2, mode="default",
                                 view=0, perturb=6, dump_batch=1, batch_views="0,3,5"),
+    # camera_z_order fast mode (splat.hpp:126, raster.hpp:162): per-view depth order, ties by id.
+    "g8_synth_kd1_zorder": dict(scene="synth", count=2000, w=64, h=48, n_views=8, seed=19, kd=1, mode="oracle",
+                                view=5, perturb=8, z_order=1),
     # non-zero background, 8-way split, default options.
     "g4_synth_kd3_bg": dict(scene="synth", count=2000, w=48, h=48, n_views=6, seed=23, kd=3, mode="default",
                             view=2, perturb=4, bg_r=0.2, bg_g=0.5, bg_b=0.9),

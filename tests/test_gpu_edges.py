@@ -104,6 +104,27 @@ def test_zero_quaternion_raises_domain_error():
     ctx.close()
 
 
+def test_partition_epoch_mismatch_raises():
+    """WorkerCore::dispatch(MsgRenderTask) refuses a task from another
+    partition epoch (worker.hpp:63, std::runtime_error)."""
+    s = engine.synth_splats(800, seed=3, sh_degree=3)
+    cam = engine.ring_camera(64, 48, 0, n_views=64)
+    target = np.zeros((1, 48, 64, 3), np.float32)
+    mgr = engine.Manager(s, engine.train_config(kd_depth=1), engine.render_options())
+    mgr.train_step([cam], target)  # epoch 0 everywhere: fine
+    mgr.ctx.set_epoch(1)  # the manager moved on; subsets still hold epoch 0
+    with pytest.raises(RuntimeError, match="partition epoch mismatch"):
+        mgr.train_step([cam], target)
+    with pytest.raises(RuntimeError, match="partition epoch mismatch"):
+        mgr.ctx.render_partial(0, cam)
+    mgr.ctx.set_epoch(0)
+    mgr.train_step([cam], target)
+    mgr.repartition()  # device repartition: subsets and manager both at epoch 1
+    assert mgr.epoch == 1
+    mgr.train_step([cam], target)
+    mgr.close()
+
+
 def _ring_overflow_scene(cam, n=64, seed=7):
     """n translucent splats at one distance from the camera centre, clustered
     around the view axis: their ranges share one bucket, so the (t, id) ring
