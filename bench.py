@@ -35,6 +35,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "train steps/s and Mpixel/s (fwd+bwd+merge+Adam), 10M Gaussians 1080p, 1/2/4/8 GPU"
 REF_DUMP = ROOT / "oracle" / "_ref" / "ref_dump"
+PARITY_ROW_STEP = 64  # merged-image rows compared with the reference: 0, 64, 128, ...
 
 
 def parse():
@@ -47,16 +48,30 @@ def parse():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--view", type=int, default=0)
+    ap.add_argument("--views", type=int, default=8,
+                    help="training cycles over this many ring views (every 64/views-th of the 64), one per step")
+    ap.add_argument("--iterations", type=int, default=30000, help="TrainConfig.iterations (position-LR schedule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=120.0)
     return ap.parse_args()
 
 
+def train_views(a):
+    """The ring views the B200 arm cycles through, one per step (a training run visits every view)."""
+    stride = max(1, 64 // max(1, a.views))
+    return [(a.view + i * stride) % 64 for i in range(max(1, a.views))]
+
+
 def workload_config(a, world):
     return {
-        "workload": f"C3: {a.count / 1e6:g}M synthetic Gaussians (synth_scene seed 11, SH3), {a.width}x{a.height} "
-                    f"ring view {a.view}, KD split into {world} subset(s), batch 1, fwd+bwd+merge+loss+Adam",
+        "workload": f"C3: {a.count / 1e6:g}M synthetic Gaussians (synth_scene seed 11, SH3, perturbed seed 5), "
+                    f"{a.width}x{a.height}, KD split into {world} subset(s), batch 1, fwd+bwd+merge+loss+Adam",
         "gaussians": a.count, "width": a.width, "height": a.height, "batch": 1, "kd_subsets": world,
+        "views": {"b200": f"cycles ring views {train_views(a)} (of 64), one per step, targets = GT rendered in "
+                          f"oracle mode per view (io.hpp:540-541)",
+                  "reference": f"ring view {a.view}, target = GT rendered in oracle mode by the reference "
+                               f"(untimed setup); a step's cost does not depend on which ring view it renders"},
+        "iterations": a.iterations,
         "render_options": "default (per-ray t order, stop 1e-4, 3-sigma, near 0.01)",
         "backward_skip": "exact-zero (grad_skip_eps=0): the reference's Eigen isZero() threshold would skip "
                          "every pixel's backward at 1080p (DESIGN.md)",
@@ -135,13 +150,20 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref: the unmodified reference headers)
 # ---------------------------------------------------------------------------
-def run_reference_steps(a, steps: int, budget_s: float, target_path: str | None, kd: int = 0):
+def run_reference_steps(a, steps: int, budget_s: float, target_path: str | None, kd: int = 0,
+                        parity_dir: str | None = None):
+    """`target_path` None: the reference renders the GT target itself (oracle
+    mode, untimed).  `parity_dir`: also dump the step-0 bins hashes, sampled
+    merged rows and loss there (untimed, oracle/ref_dump.cpp parity=1)."""
     if not REF_DUMP.exists():
         return None, "oracle/_ref/ref_dump not built (needs /root/reference at build time)"
     threads = os.cpu_count() or 1
+    out = parity_dir or "/tmp/dgs_ref_bench"
     argv = [str(REF_DUMP), "scene=synth", f"count={a.count}", f"w={a.width}", f"h={a.height}", "n_views=64",
             "seed=11", f"kd={kd}", "perturb=5", f"view={a.view}", f"time_direct={steps}", f"budget_s={budget_s}",
-            f"target={target_path or 'zeros'}", "out=/tmp/dgs_ref_bench"]
+            f"iterations={a.iterations}", f"target={target_path or 'gt'}", f"out={out}"]
+    if parity_dir:
+        argv += ["parity=1", f"parity_row_step={PARITY_ROW_STEP}"]
     t0 = time.time()
     p = subprocess.run(argv, capture_output=True, text=True, env={**os.environ, "DGS_THREADS": str(threads)})
     if p.returncode != 0:
@@ -149,8 +171,68 @@ def run_reference_steps(a, steps: int, budget_s: float, target_path: str | None,
     rows = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
     step_rows = [r for r in rows if "step" in r]
     setup = next((r["setup_s"] for r in rows if "setup_s" in r), None)
-    return {"steps": step_rows, "setup_s": setup, "wall_s": time.time() - t0, "threads": threads,
-            "effective_threads": min(threads, 16)}, None
+    trs = next((r["target_render_s"] for r in rows if "target_render_s" in r), None)
+    return {"steps": step_rows, "setup_s": setup, "target_render_s": trs, "wall_s": time.time() - t0,
+            "threads": threads, "effective_threads": min(threads, 16)}, None
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """oracle/ref_dump.cpp splitmix64 (uint64 wrap-around arithmetic)."""
+    with np.errstate(over="ignore"):
+        x = x.astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def bins_hash(off: np.ndarray, ent: np.ndarray) -> dict:
+    """Per tile: entry count, wrapping sum and xor of splitmix64(member index)
+    — an order-independent fingerprint of each tile's bin set (the reference's
+    bins are in projection order, ours in range order)."""
+    counts = np.diff(off).astype(np.int64)
+    h = splitmix64(ent)
+    hsum = np.zeros(len(counts), np.uint64)
+    hxor = np.zeros(len(counts), np.uint64)
+    nz = counts > 0
+    if nz.any():
+        starts = off[:-1][nz]
+        with np.errstate(over="ignore"):
+            hsum[nz] = np.add.reduceat(h, starts)
+        hxor[nz] = np.bitwise_xor.reduceat(h, starts)
+    return {"count": counts, "hsum": hsum, "hxor": hxor}
+
+
+def compare_parity(gpu: dict, first_step: dict, pdir: str, ref_step: dict) -> dict:
+    """GPU vs the reference on the benchmarked workload's step-0 inputs
+    (north_star tolerances: bins bit-exact, pixels <= 1e-4 absolute)."""
+    p = Path(pdir)
+    ref_rows = np.load(p / "parity_rows.npy")
+    rows = gpu["rows"][: len(ref_rows)]
+    max_abs = float(np.abs(rows.astype(np.float64) - ref_rows).max())
+    cnt = np.load(p / "k0_parity_tile_count.npy")
+    hs = np.load(p / "k0_parity_tile_hsum.npy")
+    hx = np.load(p / "k0_parity_tile_hxor.npy")
+    b = gpu["bins"]
+    same = (cnt == b["count"]) & (hs == b["hsum"]) & (hx == b["hxor"]) if len(cnt) == len(b["count"]) else None
+    pl = np.load(p / "parity_loss.npy")
+    ref_loss, ref_loss_f64 = float(pl[0]), float(pl[2])
+    ref_vis = int(np.load(p / "k0_parity_visible.npy")[0])
+    loss_rel = abs(first_step["loss"] - ref_loss_f64) / max(abs(ref_loss_f64), 1e-30)
+    out = {
+        "inputs": "step 0 of the timed workload: perturbed scene, view 0, target 0 (identical bytes on both sides)",
+        "loss_gpu": first_step["loss"], "loss_ref_f64": ref_loss_f64, "loss_rel": loss_rel,
+        "loss_ref_f32": ref_loss, "loss_rel_vs_ref_f32": abs(first_step["loss"] - ref_loss) / max(abs(ref_loss), 1e-30),
+        "loss_note": "loss_ref_f64 = the reference's loss<T> instantiated with double on the reference's own float "
+                     "image and target; its float instantiation sums 6.2M terms sequentially in float",
+        "max_abs_px": max_abs, "rows_checked": int(len(ref_rows)), "px_checked": int(ref_rows.size // 3),
+        "bins_equal": bool(same is not None and same.all()), "tiles_checked": int(len(cnt)),
+        "tiles_differing": None if same is None else int((~same).sum()),
+        "pairs_gpu": int(b["count"].sum()), "pairs_ref": int(cnt.sum()),
+        "visible_gpu": gpu["visible"], "visible_ref": ref_vis,
+        "tolerance": {"max_abs_px": 1e-4, "bins": "bit-exact", "loss_rel": 1e-5},
+    }
+    out["pass"] = bool(out["bins_equal"] and max_abs <= 1e-4 and gpu["visible"] == ref_vis and loss_rel <= 1e-5)
+    return out
 
 
 def cpu_model():
@@ -185,7 +267,8 @@ def reference_arm(a, world, rank):
                          "sample": f"{len(timed)} full-frame C3 step(s) of the unmodified reference (oracle/_ref/ref_dump "
                                    f"time_direct: Manager::train_step call sequence, no IPC copies), DGS_THREADS="
                                    f"{res['threads']} (parallel_chunks caps at 16 chunks), budget {a.cpu_budget_s:.0f}s, "
-                                   f"scene setup {res['setup_s']}s untimed, host {cpu_model()}"},
+                                   f"scene setup {res['setup_s']}s and GT target render {res['target_render_s']}s "
+                                   f"untimed, host {cpu_model()}"},
         "e2e": {"value": mpx, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -232,26 +315,51 @@ def b200_arm(a, world, rank, local_rank):
 
     t_setup = time.time()
     gt = engine.synth_splats(a.count, seed=11, sh_degree=3)
-    cam = engine.ring_camera(a.width, a.height, a.view, n_views=64)
+    views = train_views(a)
+    cams = [engine.ring_camera(a.width, a.height, v, n_views=64) for v in views]
+    V = len(cams)
     init = engine.perturb(gt, 5)
-    # targets: GT rendered in oracle mode by this path (io.hpp:540-541); every
-    # rank renders the same full target on its own GPU (bitwise identical)
+    # targets: GT rendered in oracle mode by this path, one per view (io.hpp:540-541);
+    # every rank renders the same full targets on its own GPU (bitwise identical)
     tmgr = engine.Manager(gt, engine.train_config(kd_depth=0), engine.render_options(oracle=True), device=local_rank)
-    target, _ = tmgr.render(cam)
+    targets = np.stack([tmgr.render(c)[0] for c in cams])
     tmgr.close()
     del gt
-    cfg = engine.train_config(kd_depth=int(math.log2(world)), iterations=30000, deterministic=0)
+    cfg = engine.train_config(kd_depth=int(math.log2(world)), iterations=a.iterations, deterministic=0)
     ro = engine.render_options(grad_skip_eps=0.0)
     mgr = engine.Manager(init, cfg, ro, device=local_rank, rank=rank, world=world, nccl_id=nccl_id)
     ctx = mgr.ctx
     n_local = sum(int(engine.lib().dgs_subset_size(ctx.handle, k)) for k in range(mgr.table.subset_count)
                   if engine.subset_owner(k, mgr.table.subset_count, world) == rank)
-    tdev = ctx.upload_targets(target[None])
+    tdev = ctx.upload_targets(targets)
+    view_bytes = a.width * a.height * 3 * 4
     setup_s = time.time() - t_setup
 
+    # ---- parity capture: the step-0 inputs the reference leg is given (N = 1) ----
+    do_cpu = rank == 0 and world == 1 and not a.no_cpu_baseline
+    gpu_parity = None
+    if do_cpu:
+        rgb0, _ = mgr.render(cams[0])
+        off, ent = ctx.dump_bins(0, cams[0])
+        cnt = np.zeros(n_local, np.uint32)
+        engine.check(engine.lib().dgs_dump_records(ctx.handle, 0, None, engine.ptr(cnt)))
+        gpu_parity = {"rows": rgb0[::PARITY_ROW_STEP].copy(), "bins": bins_hash(off, ent),
+                      "visible": int((cnt > 0).sum())}
+        del rgb0, off, ent, cnt
+
+    def step(i, host=None):
+        v = i % V
+        if host is not None:
+            return mgr.train_step([cams[v]], host[v:v + 1])
+        return mgr.train_step([cams[v]], None, targets_device_ptr=tdev + v * view_bytes)
+
     stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+    it = 0
+    first = None
     for _ in range(a.warmup):
-        mgr.train_step([cam], None, targets_device_ptr=tdev)
+        r = step(it)
+        first = first or r
+        it += 1
     barrier()
 
     # ---- device-resident timed region (no per-stage events inside) ------------
@@ -262,7 +370,8 @@ def b200_arm(a, world, rank, local_rank):
     e0.record(stream)
     results = []
     for _ in range(a.steps):
-        results.append(mgr.train_step([cam], None, targets_device_ptr=tdev))
+        results.append(step(it))
+        it += 1
     e1.record(stream)
     torch.cuda.synchronize()
     ms_local = e0.elapsed_time(e1)
@@ -271,37 +380,60 @@ def b200_arm(a, world, rank, local_rank):
     rank_ms = gather_ranks(ms_local)
 
     # ---- per-stage breakdown (separate run: CUDA events around every stage) ----
-    n_prof = max(1, min(a.steps, 10))
+    n_prof = max(V, min(a.steps, 2 * V))
     ctx.set_profiling(True)
     for _ in range(n_prof):
-        mgr.train_step([cam], None, targets_device_ptr=tdev)
+        step(it)
+        it += 1
     stages = ctx.stage_times()
     ctx.set_profiling(False)
     rank_blend_ms = gather_ranks((stages["blend_fwd"][0] + stages["blend_bwd"][0]) / n_prof)
     rank_members = gather_ranks(float(n_local))
 
-    # ---- counters (separate short run: the stats variants of the blends are slower) ----
+    # ---- counters (separate short run over every view: the stats variants are slower) ----
     ctx.set_collect_stats(True)
-    results_stats = [mgr.train_step([cam], None, targets_device_ptr=tdev) for _ in range(2)]
+    results_stats = []
+    for _ in range(V):
+        results_stats.append(step(it))
+        it += 1
     ctx.set_collect_stats(False)
 
     # ---- e2e: public call with host (pinned) targets, result read back --------
-    pinned = torch.empty(target.size, dtype=torch.float32, pin_memory=True)
-    pinned.numpy()[:] = target.reshape(-1)
-    host_target = pinned.numpy().reshape(1, a.height, a.width, 3)
-    mgr.train_step([cam], host_target)
+    pinned = torch.empty(targets.size, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = targets.reshape(-1)
+    host_targets = pinned.numpy().reshape(V, a.height, a.width, 3)
+    step(it, host_targets)
+    it += 1
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     w0 = time.perf_counter()
     e2e_losses = []
     for _ in range(a.steps):
-        r = mgr.train_step([cam], host_target)
+        r = step(it, host_targets)
+        it += 1
         e2e_losses.append(r["loss"])
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     e2e_wall = max_over_ranks((time.perf_counter() - w0) * 1e3)
+
+    # ---- deterministic = 1 (the reference default: IEEE Adam, int64 fixed-point backward sums) ----
+    cfg_det = engine.train_config(kd_depth=int(math.log2(world)), iterations=a.iterations, deterministic=1)
+    ctx.set_options(ro, cfg_det)
+    n_det = max(V, min(a.steps, 2 * V))
+    step(it)  # allocates the fixed-point accumulators
+    it += 1
+    barrier()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for _ in range(n_det):
+        step(it)
+        it += 1
+    d1.record(stream)
+    torch.cuda.synchronize()
+    det_ms = max_over_ranks(d0.elapsed_time(d1)) / n_det
+    ctx.set_options(ro, cfg)
 
     px = a.width * a.height
     step_ms = ms / a.steps
@@ -336,58 +468,84 @@ def b200_arm(a, world, rank, local_rank):
         tj = {}
     traffic = tj.get(roof_kernel)
 
-    # ---- CPU baseline (rank 0, N = 1) ------------------------------------------------
+    # ---- CPU baseline + parity (rank 0, N = 1): the reference's own step on the
+    # identical inputs (scene, perturbation, view 0, target 0); its step-0 bins,
+    # merged rows and loss are compared with the GPU's (captured before warm-up)
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    parity = None
+    if do_cpu:
         tpath = "/tmp/dgs_bench_target.npy"
-        np.save(tpath, target.astype(np.float32).reshape(-1))
-        res, err = run_reference_steps(a, 1, 1.0, tpath)
+        np.save(tpath, targets[0].astype(np.float32).reshape(-1))
+        pdir = "/tmp/dgs_ref_parity"
+        os.makedirs(pdir, exist_ok=True)
+        for f in Path(pdir).glob("*.npy"):
+            f.unlink()
+        res, err = run_reference_steps(a, 1, 1.0, tpath, parity_dir=pdir)
         if res is not None and res["steps"]:
             t = res["steps"][0]["seconds"]
             cpu = {"value": px / 1e6 / t, "unit": "Mpixel/s", "cores": res["effective_threads"], "kind": "reference",
-                   "sample": f"1 full-frame step of the same C3 workload through the unmodified reference "
-                             f"(oracle/_ref/ref_dump time_direct = Manager::train_step call sequence), "
-                             f"{t:.1f} s, DGS_THREADS={res['threads']} (parallel_chunks uses <=16), host {cpu_model()}",
+                   "sample": f"1 full-frame step of the same C3 workload (view {a.view}, its GPU-rendered GT target) "
+                             f"through the unmodified reference (oracle/_ref/ref_dump time_direct = "
+                             f"Manager::train_step call sequence), {t:.1f} s, DGS_THREADS={res['threads']} "
+                             f"(parallel_chunks uses <=16), host {cpu_model()}",
                    "seconds_per_step": t, "forward_s": res["steps"][0]["forward_s"],
                    "backward_adam_s": res["steps"][0]["backward_adam_s"]}
+            parity = compare_parity(gpu_parity, first, pdir, res["steps"][0])
         else:
             cpu = {"value": None, "unit": "Mpixel/s", "cores": 0, "kind": "reference", "sample": err}
+            parity = {"unavailable": err}
 
     last = dict(results[-1])
-    last_stats = results_stats[-1]
-    for key in ("evals_fwd", "contribs_fwd", "evals_bwd", "contribs_bwd", "overflow_pixels", "subrounds_bwd",
-                "small_subrounds_bwd", "tiles_work_fwd", "replay_tiles_bwd", "visible"):
-        last[key] = results_stats[-1][key]
+    # counters averaged over one pass of the views (the stage times average over the same views)
+    avg = {k: float(np.mean([r[k] for r in results_stats])) for k in
+           ("evals_fwd", "contribs_fwd", "evals_bwd", "contribs_bwd", "subrounds_bwd", "small_subrounds_bwd",
+            "tiles_work_fwd", "replay_tiles_bwd", "visible", "pairs")}
     # ---- per-kernel roofline (algorithmic bytes / FLOPs per launch) ----
-    nv, npairs = last["visible"], last["pairs"]
-    ef, nc = last_stats["evals_fwd"], last_stats["contribs_fwd"]
+    nv, npairs = avg["visible"], avg["pairs"]
+    ef, nc = avg["evals_fwd"], avg["contribs_fwd"]
     fp32_peak = 148 * 128 * 2 * (clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # TFLOP/s, FMA = 2
+    K_sub = mgr.table.subset_count
     algo = {
         # params in; record 64 + rect 8 + count 4 + key 4 + ext_y 4 + SH Jacobian 40 out per visible member
         "preprocess": ("hbm", n_all * rows * 4 + nv * 124 + (n_all - nv) * 8),
-        # 24-bit key + 3 radix passes over members, count scan, pair emission, 2 radix passes over pairs
+        # 16-bit key + 2 radix passes over members, count scan, pair emission, 2 radix passes over pairs
         "binning": ("hbm", 88 * n_all + 30 * npairs),
         "blend_fwd": ("fp32", 50 * ef + 15 * nc),
+        # K partial maps (float4) in, merged RGB out, per owned pixel (engine.hpp:152-182)
+        "merge": ("hbm", (16 * K_sub + 12) * px / world),
+        "loss": ("fp32", 678 * 3 * px / world),
+        # K partial maps + the loss gradient in, K gradient maps out (engine.hpp:195-234)
+        "merge_bwd": ("hbm", (32 * K_sub + 12) * px / world),
         "blend_bwd": ("fp32", 110 * nc),
-        "loss": ("fp32", 678 * 3 * px),
         # 11 param rows + 10 Jacobian rows + 9 adjoint rows in per visible member, 17-float record out
         "project_bwd": ("hbm", nv * 120 + n_all * 68),
         "adam": ("hbm", alg_bytes["adam"]),
     }
     kernels = {}
+    t_roof = 0.0
     for k, (bound, amount) in algo.items():
         t = per_stage.get(k, 0.0)
         if t <= 0:
             continue
         if bound == "hbm":
             ach = amount / (t / 1e3) / 1e9
-            kernels[k] = {"bound": "hbm", "ms": round(t, 4), "algorithmic_bytes": int(amount),
-                          "achieved_gbs": round(ach, 1), "frac": round(ach / hbm_peak, 3),
-                          "traffic_ncu": tj.get(k)}
+            tr = amount / (hbm_peak * 1e9) * 1e3
+            kernels[k] = {"bound": "hbm", "ms": round(t, 4), "roofline_ms": round(tr, 4),
+                          "algorithmic_bytes": int(amount), "achieved_gbs": round(ach, 1),
+                          "frac": round(ach / hbm_peak, 3), "traffic_ncu": tj.get(k)}
         else:
             ach = amount / (t / 1e3) / 1e12
-            kernels[k] = {"bound": "fp32-issue", "ms": round(t, 4), "algorithmic_flop": int(amount),
-                          "achieved_tflops": round(ach, 2), "frac_of_fp32_peak": round(ach / fp32_peak, 3)}
+            tr = amount / (fp32_peak * 1e12) * 1e3
+            kernels[k] = {"bound": "fp32", "ms": round(t, 4), "roofline_ms": round(tr, 4),
+                          "algorithmic_flop": int(amount), "achieved_tflops": round(ach, 2),
+                          "frac": round(ach / fp32_peak, 3)}
+        t_roof += tr
+    # the step's roofline fraction = sum of the kernels' roofline times / measured step
+    step_roofline = {"sum_kernel_roofline_ms": round(t_roof, 4), "ms_per_step": step_ms,
+                     "frac": t_roof / step_ms,
+                     "definition": "sum over kernels of max(bytes/HBM peak, FLOP/FP32 peak) / ms_per_step "
+                                   "(HBM peak measured, FP32 nominal at the sampled SM clock)"}
+    ovf_timed = [int(r["overflow_pixels"]) for r in results]
     line = {
         "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True,
@@ -401,6 +559,12 @@ def b200_arm(a, world, rank, local_rank):
         "e2e": {"value": e2e_value, "unit": "Mpixel/s", "h2d_bytes_per_step": px * 3 * 4,
                 "d2h_bytes_per_step": 3 * 8 + 16 * 4, "ms_per_step_events": e2e_ms / a.steps,
                 "ms_per_step_wall": e2e_wall / a.steps},
+        "step_roofline": step_roofline,
+        "deterministic_mode": {"ms_per_step": det_ms, "value": px / 1e6 / (det_ms / 1e3),
+                               "unit": "Mpixel/s", "steps": n_det,
+                               "what": "TrainConfig::deterministic=1 (reference default): IEEE Adam op sequence and "
+                                       "int64 fixed-point backward sums (bitwise reproducible); the headline "
+                                       "uses deterministic=0 (fast Adam, float RED atomics)"},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes[roof_kernel], "launch_ms": t_kernel_ms},
@@ -409,14 +573,13 @@ def b200_arm(a, world, rank, local_rank):
         "fp32_peak_tflops_nominal": round(fp32_peak, 1),
         "dominant_stage": dom,
         "cpu_baseline": cpu,
+        "parity": parity,
         "clocks": clk,
         "gpu_launches": int(sum(r["kernel_launches"] for r in results)),
         "step_stats": {"loss_first": results[0]["loss"], "loss_last": last["loss"], "psnr_last": last["psnr"],
-                       "pairs": last["pairs"], "evals_fwd": last["evals_fwd"], "contribs_fwd": last["contribs_fwd"],
-                       "evals_bwd": last["evals_bwd"], "contribs_bwd": last["contribs_bwd"],
-                       "overflow_pixels": last["overflow_pixels"], "subrounds_bwd": last["subrounds_bwd"],
-                       "small_subrounds_bwd": last["small_subrounds_bwd"], "tiles_work_fwd": last["tiles_work_fwd"],
-                       "replay_tiles_bwd": last["replay_tiles_bwd"],
+                       "per_view_avg": {k: round(v, 1) for k, v in avg.items()},
+                       "overflow_pixels_timed_steps": ovf_timed,
+                       "overflow_steps_timed": int(sum(1 for o in ovf_timed if o)),
                        "comm_bytes_reference_accounting":
                            last["comm_bytes"]},
         "setup_s": setup_s,

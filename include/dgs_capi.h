@@ -111,7 +111,8 @@ typedef struct dgs_step_result {
     uint64_t comm_bytes;      /* reference accounting: partial-map payload, both directions */
     uint64_t nccl_bytes;      /* bytes this rank actually sent over NCCL */
     uint64_t pairs;           /* (splat, tile) pairs over all local subsets and views */
-    uint64_t evals_fwd, contribs_fwd, evals_bwd, contribs_bwd, overflow_pixels;
+    uint64_t evals_fwd, contribs_fwd, evals_bwd, contribs_bwd; /* stats mode only */
+    uint64_t overflow_pixels; /* ring-overflow pixels (exact fallback kernels), every step */
     uint64_t kernel_launches; /* kernels this call launched */
     uint64_t subrounds_bwd, small_subrounds_bwd, tiles_work_fwd; /* blend work counters (stats mode) */
     uint64_t replay_tiles_bwd; /* tiles the backward replayed (records incomplete; stats mode) */

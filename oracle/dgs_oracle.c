@@ -679,6 +679,97 @@ static void composite_backward(const contrib_t* cb, int64_t n, const scene_t* sc
     }
 }
 
+/* Exact-accumulation probe (NOT the reference's arithmetic): the same
+ * per-contribution float values as composite_backward, but the suffix and the
+ * per-splat sums (within and across the 16 chunks) in double, rounded to float
+ * once before the pullback.  Its difference from the float path is the
+ * reference's own accumulation rounding; tests/conftest.py grad_ok accepts a
+ * GPU gradient that matches either (the GPU's deterministic mode sums exactly,
+ * in int64 fixed point). */
+typedef struct {
+    double dm[2], dc[4], dcol[3], da;
+} g2dx_t;
+
+static int g_exact_acc = 0;
+void orc_set_exact_accumulation(int on) { g_exact_acc = on; }
+
+static void composite_backward_x(const contrib_t* cb, int64_t n, const scene_t* sc, const orc_opts* o, float px,
+                                 float py, const float gc[3], float gt, g2dx_t* pg, float* prefix) {
+    const float stop = o->stop;
+    float trans = 1.0f;
+    int64_t done = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        if (stop > 0.0f && trans < stop) break;
+        prefix[done++] = trans;
+        trans *= (1.0f - cb[k].sigma);
+    }
+    const float t_final = trans;
+    double suffix[3] = {0.0, 0.0, 0.0};
+    for (int64_t k = done; k-- > 0;) {
+        const splat2d_t* s = &sc->sp[cb[k].proj];
+        const float a_i = prefix[k], sig = cb[k].sigma, one_minus = 1.0f - sig;
+        g2dx_t* g = &pg[cb[k].proj];
+        const float ws = sig * a_i;
+        for (int ch = 0; ch < 3; ++ch) g->dcol[ch] += (double)(gc[ch] * ws);
+        const float sf[3] = {(float)suffix[0], (float)suffix[1], (float)suffix[2]};
+        const float d_sigma = dot3(gc, s->col) * a_i - dot3(gc, sf) / one_minus - gt * t_final / one_minus;
+        for (int ch = 0; ch < 3; ++ch) suffix[ch] += (double)(s->col[ch] * ws);
+        const float gval = eval_2d(s, px, py, o);
+        if (s->alpha * gval >= o->sigma_clamp) continue;
+        g->da += (double)(d_sigma * gval);
+        const float d_g = d_sigma * s->alpha;
+        const float d0 = px - s->mx, d1 = py - s->my;
+        const float w0 = s->inv[0] * d0 + s->inv[1] * d1, w1 = s->inv[2] * d0 + s->inv[3] * d1;
+        const float m = d_g * gval;
+        g->dm[0] += (double)(m * w0);
+        g->dm[1] += (double)(m * w1);
+        const float hh = d_g * gval * 0.5f;
+        const float ww[4] = {w0 * w0, w0 * w1, w1 * w0, w1 * w1};
+        for (int a = 0; a < 4; ++a) g->dc[a] += (double)(hh * ww[a]);
+    }
+}
+
+/* Magnitude probe for the rounding bound (orc_partial_backward_bound): per
+ * contribution, the absolute size of every term the 10 adjoint fields are
+ * formed from (d_sigma = gc.c A - gc.suffix/(1-s) - gT T_f/(1-s) counted term
+ * by term), summed without cancellation. */
+static void composite_backward_mass(const contrib_t* cb, int64_t n, const scene_t* sc, const orc_opts* o, float px,
+                                    float py, const float gc[3], float gt, g2dx_t* am, float* prefix) {
+    const float stop = o->stop;
+    float trans = 1.0f;
+    int64_t done = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        if (stop > 0.0f && trans < stop) break;
+        prefix[done++] = trans;
+        trans *= (1.0f - cb[k].sigma);
+    }
+    const double t_final = trans;
+    const double agc[3] = {fabs(gc[0]), fabs(gc[1]), fabs(gc[2])}, agt = fabs(gt);
+    double suffix[3] = {0.0, 0.0, 0.0};
+    for (int64_t k = done; k-- > 0;) {
+        const splat2d_t* s = &sc->sp[cb[k].proj];
+        const double a_i = prefix[k], sig = cb[k].sigma, one_minus = 1.0 - sig, ws = sig * a_i;
+        g2dx_t* g = &am[cb[k].proj];
+        for (int ch = 0; ch < 3; ++ch) g->dcol[ch] += agc[ch] * ws;
+        const double dsig = (agc[0] * s->col[0] + agc[1] * s->col[1] + agc[2] * s->col[2]) * a_i +
+                            (agc[0] * suffix[0] + agc[1] * suffix[1] + agc[2] * suffix[2]) / one_minus +
+                            agt * t_final / one_minus;
+        for (int ch = 0; ch < 3; ++ch) suffix[ch] += s->col[ch] * ws;
+        const float gval = eval_2d(s, px, py, o);
+        if (s->alpha * gval >= o->sigma_clamp) continue;
+        g->da += dsig * gval;
+        const double d0 = px - s->mx, d1 = py - s->my;
+        const double w0 = fabs(s->inv[0] * d0) + fabs(s->inv[1] * d1), w1 = fabs(s->inv[2] * d0) + fabs(s->inv[3] * d1);
+        const double m = dsig * s->alpha * gval;
+        g->dm[0] += m * w0;
+        g->dm[1] += m * w1;
+        g->dc[0] += 0.5 * m * w0 * w0;
+        g->dc[1] += 0.5 * m * w0 * w1;
+        g->dc[2] += 0.5 * m * w1 * w0;
+        g->dc[3] += 0.5 * m * w1 * w1;
+    }
+}
+
 /* project_splat_backward (splat.hpp:363-437) into the GradBuffers slot of member i */
 static void project_backward(const orc_splats* sp, int64_t i, const view_t* v, const orc_opts* o, const g2d_t* g,
                              orc_grads* out) {
@@ -820,6 +911,7 @@ int orc_partial_backward(const orc_splats* s, const orc_subspace* sub, const orc
     float* prefix = (float*)malloc(sizeof(float) * maxlen);
     g2d_t* merged = (g2d_t*)calloc(np ? np : 1, sizeof(g2d_t));
     g2d_t* pg = (g2d_t*)malloc(sizeof(g2d_t) * (np ? np : 1));
+    g2dx_t* mx = g_exact_acc ? (g2dx_t*)calloc(np ? np : 1, sizeof(g2dx_t)) : NULL;
     /* parallel_chunks(H, 16) decomposition (parallel.hpp:30-55), merged in chunk order */
     const int chunks = v.h < 16 ? v.h : 16;
     const int per = (v.h + chunks - 1) / chunks;
@@ -839,14 +931,25 @@ int orc_partial_backward(const orc_splats* s, const orc_subspace* sub, const orc
                 const float px = (float)x + 0.5f, py = (float)y + 0.5f;
                 const int64_t tile = (int64_t)(y / 16) * v.tx + x / 16;
                 const int64_t n = collect(&sc, s->id, tile, &v, d, px, py, o, sub, buf);
-                composite_backward(buf, n, &sc, o, px, py, gc, gt, pg, prefix);
+                if (mx) composite_backward_x(buf, n, &sc, o, px, py, gc, gt, mx, prefix);
+                else composite_backward(buf, n, &sc, o, px, py, gc, gt, pg, prefix);
             }
+        if (mx) continue; /* exact: one double accumulator across all chunks */
         for (int64_t p = 0; p < np; ++p) {
             for (int a = 0; a < 2; ++a) merged[p].dm[a] += pg[p].dm[a];
             for (int a = 0; a < 4; ++a) merged[p].dc[a] += pg[p].dc[a];
             for (int a = 0; a < 3; ++a) merged[p].dcol[a] += pg[p].dcol[a];
             merged[p].da += pg[p].da;
         }
+    }
+    if (mx) {
+        for (int64_t p = 0; p < np; ++p) {
+            for (int a = 0; a < 2; ++a) merged[p].dm[a] = (float)mx[p].dm[a];
+            for (int a = 0; a < 4; ++a) merged[p].dc[a] = (float)mx[p].dc[a];
+            for (int a = 0; a < 3; ++a) merged[p].dcol[a] = (float)mx[p].dcol[a];
+            merged[p].da = (float)mx[p].da;
+        }
+        free(mx);
     }
     const size_t nsh = (size_t)s->n * s->sh_coeffs * 3;
     memset(out->d_mu, 0, sizeof(float) * 3 * s->n);
@@ -859,6 +962,188 @@ int orc_partial_backward(const orc_splats* s, const orc_subspace* sub, const orc
     free(prefix);
     free(merged);
     free(pg);
+    scene_free(&sc);
+    return 0;
+}
+
+/* project_backward with every signed operation replaced by its magnitude
+ * (running-error style): inputs are the cancellation-free adjoint magnitudes,
+ * numerators are summed in absolute value, denominators (t_z, |q|, |mu - o|)
+ * keep their actual values.  Accumulates into b* (double). */
+static void project_backward_abs(const orc_splats* sp, int64_t i, const view_t* v, const orc_opts* o,
+                                 const double g[10], double* bmu, double* bls, double* brot, double* bop,
+                                 double* bsh) {
+    const float* W = v->R;
+    const float* mu = sp->mu + 3 * i;
+    double t[3], at[3];
+    for (int a = 0; a < 3; ++a) {
+        t[a] = (double)(dot3(W + 3 * a, mu) + v->t[a]);
+        at[a] = fabs(W[3 * a]) * fabs(mu[0]) + fabs(W[3 * a + 1]) * fabs(mu[1]) + fabs(W[3 * a + 2]) * fabs(mu[2]) +
+                fabs(v->t[a]);
+    }
+    const double iz = 1.0 / fabs(t[2]), fx = v->fx, fy = v->fy;
+    const double AJ[6] = {fx * iz, 0.0, fx * at[0] * iz * iz, 0.0, fy * iz, fy * at[1] * iz * iz};
+    const double gm[2] = {g[0], g[1]}, gc[4] = {g[2], g[3], g[4], g[5]}, gcol[3] = {g[6], g[7], g[8]};
+    double d_t[3];
+    for (int a = 0; a < 3; ++a) d_t[a] = AJ[a] * gm[0] + AJ[3 + a] * gm[1];
+    float r[9];
+    rotation_from_quat(sp->rotation + 4 * i, r);
+    const float* ls = sp->log_scale + 3 * i;
+    const double sc[3] = {exp(ls[0]), exp(ls[1]), exp(ls[2])};
+    double m[9], sigma[9], V[6];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) m[a * 3 + b] = fabs(r[a * 3 + b]) * sc[b];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            sigma[a * 3 + b] = m[a * 3] * m[b * 3] + m[a * 3 + 1] * m[b * 3 + 1] + m[a * 3 + 2] * m[b * 3 + 2];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+            V[a * 3 + b] = AJ[a * 3] * fabs(W[b]) + AJ[a * 3 + 1] * fabs(W[3 + b]) + AJ[a * 3 + 2] * fabs(W[6 + b]);
+    const double g2[4] = {gc[0], 0.5 * (gc[1] + gc[2]), 0.5 * (gc[2] + gc[1]), gc[3]};
+    double vtg[6];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 2; ++b) vtg[a * 2 + b] = V[a] * g2[b] + V[3 + a] * g2[2 + b];
+    double dS[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dS[a * 3 + b] = vtg[a * 2] * V[b] + vtg[a * 2 + 1] * V[3 + b];
+    const double gs[4] = {2.0 * g2[0], g2[1] + g2[2], g2[2] + g2[1], 2.0 * g2[3]};
+    double gv[6], dv[6], dj[6];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b) gv[a * 3 + b] = gs[a * 2] * V[b] + gs[a * 2 + 1] * V[3 + b];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+            dv[a * 3 + b] = gv[a * 3] * sigma[b] + gv[a * 3 + 1] * sigma[3 + b] + gv[a * 3 + 2] * sigma[6 + b];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+            dj[a * 3 + b] = dv[a * 3] * fabs(W[b * 3]) + dv[a * 3 + 1] * fabs(W[b * 3 + 1]) + dv[a * 3 + 2] * fabs(W[b * 3 + 2]);
+    d_t[0] += dj[2] * fx * iz * iz;
+    d_t[1] += dj[5] * fy * iz * iz;
+    d_t[2] += dj[0] * fx * iz * iz + dj[2] * 2.0 * fx * at[0] * iz * iz * iz + dj[4] * fy * iz * iz +
+              dj[5] * 2.0 * fy * at[1] * iz * iz * iz;
+    for (int a = 0; a < 3; ++a) bmu[a] += fabs(W[a]) * d_t[0] + fabs(W[3 + a]) * d_t[1] + fabs(W[6 + a]) * d_t[2];
+    double dsym[9], dm[9], dr[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dsym[a * 3 + b] = dS[a * 3 + b] + dS[b * 3 + a];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            dm[a * 3 + b] = dsym[a * 3] * m[b] + dsym[a * 3 + 1] * m[3 + b] + dsym[a * 3 + 2] * m[6 + b];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dr[a * 3 + b] = dm[a * 3 + b] * sc[b];
+    for (int a = 0; a < 3; ++a)
+        bls[a] += (fabs(r[a]) * dm[a] + fabs(r[3 + a]) * dm[3 + a] + fabs(r[6 + a]) * dm[6 + a]) * sc[a];
+    const float* q = sp->rotation + 4 * i;
+    const double n = sqrt((double)dot4(q, q));
+    const double qw = fabs(q[0]) / n, qx = fabs(q[1]) / n, qy = fabs(q[2]) / n, qz = fabs(q[3]) / n;
+    double dq[4] = {0.0, 0.0, 0.0, 0.0};
+#define ADDQA(rr, cc, a, b, c, d)              \
+    do {                                       \
+        const double gg_ = dr[(rr) * 3 + (cc)]; \
+        dq[0] += gg_ * (a);                    \
+        dq[1] += gg_ * (b);                    \
+        dq[2] += gg_ * (c);                    \
+        dq[3] += gg_ * (d);                    \
+    } while (0)
+    ADDQA(0, 0, 0.0, 0.0, 4.0 * qy, 4.0 * qz);
+    ADDQA(0, 1, 2.0 * qz, 2.0 * qy, 2.0 * qx, 2.0 * qw);
+    ADDQA(0, 2, 2.0 * qy, 2.0 * qz, 2.0 * qw, 2.0 * qx);
+    ADDQA(1, 0, 2.0 * qz, 2.0 * qy, 2.0 * qx, 2.0 * qw);
+    ADDQA(1, 1, 0.0, 4.0 * qx, 0.0, 4.0 * qz);
+    ADDQA(1, 2, 2.0 * qx, 2.0 * qw, 2.0 * qz, 2.0 * qy);
+    ADDQA(2, 0, 2.0 * qy, 2.0 * qz, 2.0 * qw, 2.0 * qx);
+    ADDQA(2, 1, 2.0 * qx, 2.0 * qw, 2.0 * qz, 2.0 * qy);
+    ADDQA(2, 2, 0.0, 4.0 * qx, 4.0 * qy, 0.0);
+#undef ADDQA
+    const double qn[4] = {qw, qx, qy, qz};
+    const double qd = qn[0] * dq[0] + qn[1] * dq[1] + qn[2] * dq[2] + qn[3] * dq[3];
+    for (int a = 0; a < 4; ++a) brot[a] += (dq[a] + qn[a] * qd) / n;
+    const int deg = eval_degree(o, sp->sh_coeffs);
+    const float rel[3] = {mu[0] - v->o[0], mu[1] - v->o[1], mu[2] - v->o[2]};
+    const float dist = sqrtf(dot3(rel, rel));
+    const float dir[3] = {rel[0] / dist, rel[1] / dist, rel[2] / dist};
+    float b[16], jb[16][3];
+    sh_basis(dir, deg, b);
+    sh_basis_jac(dir, deg, jb);
+    const int nb = (deg + 1) * (deg + 1);
+    const float* co = sp->sh + (size_t)i * sp->sh_coeffs * 3;
+    float pre[3] = {0.5f, 0.5f, 0.5f};
+    for (int k = 0; k < nb; ++k)
+        for (int ch = 0; ch < 3; ++ch) pre[ch] = pre[ch] + b[k] * co[k * 3 + ch];
+    double gg[3] = {gcol[0], gcol[1], gcol[2]};
+    for (int ch = 0; ch < 3; ++ch)
+        if (pre[ch] < 0.0f) gg[ch] = 0.0;
+    double ddir[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < nb; ++k) {
+        for (int ch = 0; ch < 3; ++ch) bsh[k * 3 + ch] += fabs(b[k]) * gg[ch];
+        const double gd = gg[0] * fabs(co[k * 3]) + gg[1] * fabs(co[k * 3 + 1]) + gg[2] * fabs(co[k * 3 + 2]);
+        for (int a = 0; a < 3; ++a) ddir[a] += fabs(jb[k][a]) * gd;
+    }
+    const double dd = fabs(dir[0]) * ddir[0] + fabs(dir[1]) * ddir[1] + fabs(dir[2]) * ddir[2];
+    for (int a = 0; a < 3; ++a) bmu[a] += (ddir[a] + fabs(dir[a]) * dd) / dist;
+    const double al = sigmoidf_ref(sp->opacity_logit[i]);
+    *bop += g[9] * al * (1.0 - al);
+}
+
+/* Rounding-sensitivity bound of every parameter gradient (TEST
+ * INFRASTRUCTURE): B_j = the gradient evaluated with every term in absolute
+ * value — the cancellation-free magnitudes of the 10 pixel-space adjoint sums
+ * (composite_backward_mass) pulled back by project_backward_abs.
+ * A float evaluation of the same chain in any order differs from the exact
+ * value by at most ~ c u B_j (u = 2^-24, c ~ the op-chain length): the
+ * entry-wise scale a gradient comparison between two float implementations
+ * has to allow for (tests/conftest.py grad_ok). */
+int orc_partial_backward_bound(const orc_splats* s, const orc_subspace* sub, const orc_camera* cam, const orc_opts* o,
+                               const float* grad_ct, orc_grads* out) {
+    view_t v;
+    if (!make_view(cam, &v)) return -1;
+    scene_t sc;
+    if (project_scene(s, &v, o, &sc) < 0) {
+        scene_free(&sc);
+        return -1;
+    }
+    const int64_t np = sc.np;
+    int64_t maxlen = 1;
+    for (int t = 0; t < v.tx * v.ty; ++t)
+        if (sc.off[t + 1] - sc.off[t] > maxlen) maxlen = sc.off[t + 1] - sc.off[t];
+    contrib_t* buf = (contrib_t*)malloc(sizeof(contrib_t) * maxlen);
+    float* prefix = (float*)malloc(sizeof(float) * maxlen);
+    g2dx_t* am = (g2dx_t*)calloc(np ? np : 1, sizeof(g2dx_t));
+    for (int y = 0; y < v.h; ++y)
+        for (int x = 0; x < v.w; ++x) {
+            const size_t pix = (size_t)y * v.w + x;
+            const float gc[3] = {grad_ct[4 * pix], grad_ct[4 * pix + 1], grad_ct[4 * pix + 2]};
+            const float gt = grad_ct[4 * pix + 3];
+            const float e = o->grad_skip_eps;
+            if (fabsf(gc[0]) <= e && fabsf(gc[1]) <= e && fabsf(gc[2]) <= e && gt == 0.0f) continue;
+            float d[3];
+            pixel_ray(&v, x, y, d);
+            const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+            const int64_t tile = (int64_t)(y / 16) * v.tx + x / 16;
+            const int64_t n = collect(&sc, s->id, tile, &v, d, px, py, o, sub, buf);
+            composite_backward_mass(buf, n, &sc, o, px, py, gc, gt, am, prefix);
+        }
+    const size_t nsh = (size_t)s->n * s->sh_coeffs * 3;
+    double* acc = (double*)calloc((size_t)s->n * 11 + nsh + 1, sizeof(double));
+    double* bmu = acc;
+    double* bls = acc + 3 * s->n;
+    double* brot = acc + 6 * s->n;
+    double* bop = acc + 10 * s->n;
+    double* bsh = acc + 11 * s->n;
+    for (int64_t p = 0; p < np; ++p) {
+        const int64_t i = sc.src[p];
+        const double mass[10] = {am[p].dm[0], am[p].dm[1], am[p].dc[0], am[p].dc[1], am[p].dc[2],
+                                 am[p].dc[3], am[p].dcol[0], am[p].dcol[1], am[p].dcol[2], am[p].da};
+        project_backward_abs(s, i, &v, o, mass, bmu + 3 * i, bls + 3 * i, brot + 4 * i, bop + i,
+                             bsh + (size_t)i * s->sh_coeffs * 3);
+    }
+    for (int64_t i = 0; i < 3 * s->n; ++i) out->d_mu[i] = (float)bmu[i];
+    for (int64_t i = 0; i < 3 * s->n; ++i) out->d_log_scale[i] = (float)bls[i];
+    for (int64_t i = 0; i < 4 * s->n; ++i) out->d_rotation[i] = (float)brot[i];
+    for (int64_t i = 0; i < s->n; ++i) out->d_opacity_logit[i] = (float)bop[i];
+    for (size_t i = 0; i < nsh; ++i) out->d_sh[i] = (float)bsh[i];
+    free(acc);
+    free(am);
+    free(buf);
+    free(prefix);
     scene_free(&sc);
     return 0;
 }

@@ -74,6 +74,16 @@ int orc_merge_backward(const float* partials, const uint16_t* order, const uint1
  * reference's 16 row chunks merged in chunk order, then the per-splat pullback. */
 int orc_partial_backward(const orc_splats* s, const orc_subspace* sub, const orc_camera* cam, const orc_opts* o,
                          const float* grad_ct, orc_grads* out);
+/* 1: orc_partial_backward sums the suffix and every per-splat adjoint in double
+ * (the same per-contribution float values), rounding once: a probe of the
+ * reference's own accumulation rounding, not the reference's arithmetic. */
+void orc_set_exact_accumulation(int on);
+/* Per-gradient-entry rounding-sensitivity scale B (same layout as the
+ * gradients): sum over the 10 adjoint fields of |pullback Jacobian| x the
+ * cancellation-free magnitude each field sums.  Two float evaluations of the
+ * backward differ by O(u B) entry-wise (tests/conftest.py grad_ok). */
+int orc_partial_backward_bound(const orc_splats* s, const orc_subspace* sub, const orc_camera* cam, const orc_opts* o,
+                               const float* grad_ct, orc_grads* out);
 /* adam_apply over every member (optim.hpp:104-126, worker.hpp:162-167); p/m/v
  * are mutable field arrays; lr as float per group. */
 int orc_adam(int64_t n, int32_t sh_coeffs, float* mu, float* ls, float* rot, float* op, float* sh, float* m_all,

@@ -64,6 +64,16 @@ template <> const char* npy_descr<std::uint8_t>() { return "|u1"; }
 
 std::string g_out = ".";
 
+/// Order-independent set hashing of tile bins (bench.py parity fields): each
+/// member index is mixed by SplitMix64's finaliser, a bin hashes to the
+/// wrapping sum and the xor of its members' mixes.
+std::uint64_t splitmix64(std::uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
 template <typename U>
 void save_npy(const std::string& name, const std::vector<U>& v, std::vector<std::size_t> shape = {}) {
     if (shape.empty()) shape = {v.size()};
@@ -530,6 +540,68 @@ int main(int argc, char** argv) {
             for (int k = 0; k < table.subset_count(); ++k)
                 dump_partial("k" + std::to_string(k) + "_", members[k], table.subspaces[k], cam, opts,
                              has("contributors"));
+        if (has("dump_rows")) {
+            // Sampled rows of render_view, of every subset's partial_render and of
+            // their merge (engine.hpp:44-52, 152-182; raster.hpp:241-263, 333-344):
+            // the per-pixel body of render_maps run on the listed rows only, so a
+            // 1M-splat 1080p comparison costs seconds (tests/test_gpu_configs.py C2).
+            const std::vector<int> rows = ilist("rows");
+            const std::size_t R = rows.size(), Wd = std::size_t(cam.width);
+            auto render_rows = [&](std::span<const Splat<Real>> sp, auto gate, std::vector<Real>& C,
+                                   std::vector<Real>& Tm) {
+                const auto scene = detail::project_scene<Real>(sp, cam, opts);
+                C.assign(R * Wd * 3, Real(0));
+                Tm.assign(R * Wd, Real(1));
+                parallel_chunks(R, std::min<std::size_t>(R, 16), [&](std::size_t, std::size_t r0, std::size_t r1) {
+                    std::vector<detail::Contribution<Real>> contribs;
+                    for (std::size_t r = r0; r < r1; ++r) {
+                        const int y = rows[r];
+                        for (int x = 0; x < cam.width; ++x) {
+                            const Ray<Real> ray = pixel_ray(cam, x, y);
+                            const Vec2<Real> pix{Real(x) + Real(0.5), Real(y) + Real(0.5)};
+                            detail::collect_contributions(scene, scene.candidates(x, y), ray, pix, opts, gate, contribs);
+                            const auto acc = detail::composite_ray<Real>(contribs, scene, opts);
+                            for (int c = 0; c < 3; ++c) C[(r * Wd + x) * 3 + c] = acc.color[c];
+                            Tm[r * Wd + x] = acc.transmittance;
+                        }
+                    }
+                });
+            };
+            std::vector<Real> C, Tm;
+            render_rows(std::span<const Splat<Real>>(splats), detail::AcceptAll<Real>{}, C, Tm);
+            for (std::size_t i = 0; i < R * Wd; ++i)  // render_view composes over the background
+                for (int c = 0; c < 3; ++c) C[i * 3 + c] = C[i * 3 + c] + Tm[i] * bg[c];
+            save_npy("rows_render_C", C, {R, Wd, 3});
+            save_npy("rows_render_T", Tm, {R, Wd});
+            std::vector<PartialImage<Real>> partials;
+            for (int k = 0; k < table.subset_count(); ++k) {
+                render_rows(std::span<const Splat<Real>>(members[k]),
+                            detail::SubspaceGate<Real>{&table.subspaces[k], opts.indicator_enabled}, C, Tm);
+                const std::string t = "rows_k" + std::to_string(k) + "_";
+                save_npy(t + "C", C, {R, Wd, 3});
+                save_npy(t + "T", Tm, {R, Wd});
+                PartialImage<Real> p;
+                p.k = table.subspaces[k].k;
+                p.color = Image<Real>(cam.width, cam.height, 3);
+                p.transmittance = Image<Real>(cam.width, cam.height, 1, Real(1));
+                for (std::size_t r = 0; r < R; ++r)
+                    for (std::size_t x = 0; x < Wd; ++x) {
+                        for (int c = 0; c < 3; ++c) p.color.at(rows[r], int(x), c) = C[(r * Wd + x) * 3 + c];
+                        p.transmittance.at(rows[r], int(x), 0) = Tm[r * Wd + x];
+                    }
+                partials.push_back(std::move(p));
+            }
+            const PixelOrders orders = compute_pixel_orders(table, cam);
+            const RenderedImage<Real> img = merge<Real>(partials, orders, bg);
+            std::vector<Real> mc, mt;
+            for (std::size_t r = 0; r < R; ++r)
+                for (std::size_t x = 0; x < Wd; ++x) {
+                    for (int c = 0; c < 3; ++c) mc.push_back(img.color.at(rows[r], int(x), c));
+                    mt.push_back(img.transmittance.at(rows[r], int(x), 0));
+                }
+            save_npy("rows_merged_C", mc, {R, Wd, 3});
+            save_npy("rows_merged_T", mt, {R, Wd});
+        }
         if (has("dump_render")) {
             const auto rv = render_view<Real>(splats, cam, bg, opts);
             save_npy("render_C", flat(rv.color), {std::size_t(cam.height), std::size_t(cam.width), 3});
@@ -678,18 +750,58 @@ int main(int argc, char** argv) {
         if (has("time_direct")) {
             TrainConfig cfg;
             cfg.kd_depth = depth;
+            cfg.iterations = std::uint64_t(iarg("iterations", 2000));
             Image<Real> target(cam.width, cam.height, 3);
-            if (has("target") && arg("target", "") != "zeros") target.data = load_npy<Real>(arg("target", ""));
+            if (has("target") && arg("target", "") != "zeros") {
+                target.data = load_npy<Real>(arg("target", ""));
+            } else if (arg("target", "") == "gt") {
+                // GT splats (unperturbed) rendered in oracle mode, as synth_scene
+                // renders its targets (io.hpp:540-541): the target the B200 arm
+                // renders on the GPU (bench.py); untimed setup
+                const double tr0 = now_s();
+                target = render_view<Real>(gt_splats, cam, bg, oracle_options()).color;
+                std::printf("{\"target_render_s\": %.3f}\n", now_s() - tr0);
+            }
             std::vector<std::vector<AdamMoments<Real>>> moments(table.subset_count());
             std::vector<std::vector<Splat<Real>>> mem = members;
             for (int k = 0; k < table.subset_count(); ++k)
                 for (const auto& sp : mem[k]) moments[k].push_back(AdamMoments<Real>::like(sp));
+            // parity=1: the step-0 inputs' bins (per tile: entry count and an
+            // order-independent hash of the member indices, raster.hpp:113-125)
+            // and sampled rows of the merged image, untimed, for bench.py's
+            // GPU-vs-reference check on the benchmarked workload itself
+            const bool parity = iarg("parity", 0) != 0;
+            const int parity_row_step = int(iarg("parity_row_step", 64));
+            if (parity) {
+                for (int k = 0; k < table.subset_count(); ++k) {
+                    const auto scene = detail::project_scene<Real>(mem[k], cam, opts);
+                    std::vector<std::int64_t> cnt(scene.bins.size());
+                    std::vector<std::uint64_t> hsum(scene.bins.size()), hxor(scene.bins.size());
+                    for (std::size_t t = 0; t < scene.bins.size(); ++t) {
+                        std::uint64_t s = 0, x = 0;
+                        for (int p : scene.bins[t]) {
+                            const std::uint64_t h = splitmix64(std::uint64_t(scene.source_index[p]));
+                            s += h;
+                            x ^= h;
+                        }
+                        cnt[t] = std::int64_t(scene.bins[t].size());
+                        hsum[t] = s;
+                        hxor[t] = x;
+                    }
+                    const std::string t = "k" + std::to_string(k) + "_";
+                    save_npy(t + "parity_tile_count", cnt);
+                    save_npy(t + "parity_tile_hsum", hsum);
+                    save_npy(t + "parity_tile_hxor", hxor);
+                    save_npy(t + "parity_visible", std::vector<std::int64_t>{std::int64_t(scene.splats2d.size())});
+                }
+            }
             const int steps = int(iarg("time_direct", 1));
             const double budget = farg("budget_s", 1e30);
             double total = 0.0;
             std::uint64_t adam_step = 0;
             for (int st = 0; st < steps; ++st) {
                 const double t0 = now_s();
+                double excl = 0.0;
                 std::vector<PartialImage<Real>> partials;
                 for (int k = 0; k < table.subset_count(); ++k)
                     partials.push_back(partial_render<Real>(mem[k], table.subspaces[k], cam, opts));
@@ -701,6 +813,30 @@ int main(int argc, char** argv) {
                 const Image<Real> gt0(cam.width, cam.height, 1, Real(0));
                 auto per = merge_backward<Real>(partials, orders, l.grad, gt0, bg);
                 const double t2 = now_s();
+                if (parity && st == 0) {
+                    // untimed: excluded from this step's seconds below
+                    const double tp0 = now_s();
+                    std::vector<Real> rows;
+                    std::vector<std::int32_t> row_idx;
+                    for (int y = 0; y < cam.height; y += parity_row_step) {
+                        row_idx.push_back(y);
+                        for (int x = 0; x < cam.width; ++x)
+                            for (int c = 0; c < 3; ++c) rows.push_back(img.color.at(y, x, c));
+                    }
+                    save_npy("parity_rows", rows, {row_idx.size(), std::size_t(cam.width), 3});
+                    save_npy("parity_row_idx", row_idx);
+                    // the reference's own loss template instantiated in double on the same
+                    // float image and target: its float loss accumulates 6.2M terms in one
+                    // sequential float sum (loss.hpp:160-164), ~1e-3 relative off at 1080p
+                    Image<double> xd(cam.width, cam.height, 3), yd(cam.width, cam.height, 3);
+                    for (std::size_t i = 0; i < xd.data.size(); ++i) {
+                        xd.data[i] = double(img.color.data[i]);
+                        yd.data[i] = double(target.data[i]);
+                    }
+                    const double loss_d = loss<double>(xd, yd, cfg.lambda_ssim).value;
+                    save_npy("parity_loss", std::vector<double>{double(l.value), double(mse_v), loss_d});
+                    excl = now_s() - tp0;
+                }
                 for (int k = 0; k < table.subset_count(); ++k) {
                     GradBuffers<Real> g = partial_render_backward<Real>(mem[k], table.subspaces[k], cam,
                                                                         per[k].d_color, per[k].d_transmittance, opts);
@@ -709,7 +845,7 @@ int main(int argc, char** argv) {
                         adam_apply(mem[k][i], g, i, moments[k][i], cfg, lr_pos, adam_step + 1);
                 }
                 ++adam_step;
-                const double t3 = now_s();
+                const double t3 = now_s() - excl;
                 total += t3 - t0;
                 std::printf("{\"step\": %d, \"seconds\": %.6f, \"forward_s\": %.6f, \"merge_loss_s\": %.6f, "
                             "\"backward_adam_s\": %.6f, \"loss\": %.9g, \"mse\": %.9g, \"threads\": %u}\n",

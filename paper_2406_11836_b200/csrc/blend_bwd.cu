@@ -18,6 +18,11 @@
 // a 5-step butterfly and added by one lane with native red.global.add.f32
 // (shared-memory float atomics are CAS loops on sm_100).  Pixels skipped by
 // the reference rule (gc.isZero() && gT == 0, raster.hpp:285) never emit.
+// TrainConfig::deterministic (fixed-order reductions, optim.hpp:33;
+// parallel.hpp:23-55): the same sub-round sums are added as int64 fixed point
+// (red.global.add.u64) at a power-of-two scale per member, taken from a first
+// pass that records each member's largest adjoint and its contribution count, so every member's total is an exact integer independent
+// of the atomics' order, at a resolution relative to its own terms.
 #include "kernels.h"
 #include "fallback_select.cuh"
 
@@ -61,7 +66,7 @@ __device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewPar
     const float e0 = fsub(x0, C.x), e1 = fsub(x1, C.y), e2 = fsub(x2, C.z);
     if (dot3(e0, e1, e2, e0, e1, e2) > A.w) return false;
     if (ro.indicator_enabled && !subspace_contains(gate, x0, x1, x2)) return false;
-    const float g = __expf(fmul(-0.5f, m2));
+    const float g = glibc_expf(fmul(-0.5f, m2));  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
     const float ag = fmul(A.z, g);
     const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
     if (!(sigma > 0.0f)) return false;
@@ -130,24 +135,101 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     v[4] = h * (w1 * w1);
 }
 
+// Accumulation modes of the backward kernels:
+//   kAccFloat  float RED atomics into acc.f (TrainConfig::deterministic = 0)
+//   kAccMax    deterministic pass 1: per member the largest |adjoint| of any of
+//              its contributions (RED.MAX on the float bits) and the number of
+//              its contributions
+//   kAccFixed  deterministic pass 2: int64 fixed point into acc.q at the member's
+//              own power-of-two scale (fixed_scale), exact integer sums in any order
+constexpr int kAccFloat = 0, kAccMax = 1, kAccFixed = 2;
+
+/// Member m's fixed-point scale: S = 2^(62 - e) with count(m) * max|adjoint|(m)
+/// < 2^e.  Every value added for m (a sum of some of its contributions, one
+/// field) is below count x max in total, so its int64 sums cannot overflow,
+/// and their resolution is 2^-62 count of its own largest adjoint — however
+/// small the member's gradient is.
+__device__ __forceinline__ float fixed_scale(uint32_t amax_bits, uint32_t count) {
+    const float b = __uint_as_float(amax_bits) * (float)count * 1.0001f;
+    if (!(b > 0.0f) || !(b < kInf)) return 1.0f;
+    int e;
+    frexpf(b, &e);  // b < 2^e
+    return ldexpf(1.0f, max(-126, min(127, 62 - e)));
+}
+
+/// Pass 2's scale of member m (1 in the other modes: unused).
+template <int MODE>
+__device__ __forceinline__ float member_scale(const GradAcc& a, uint32_t m) {
+    if constexpr (MODE == kAccFixed) return fixed_scale(__ldg(a.amax + m), __ldg(a.cnt + m));
+    return 1.0f;
+}
+
+template <int MODE>
+__device__ __forceinline__ void acc_add(const GradAcc& a, int f, uint32_t mem, float v, float scale) {
+    const size_t o = (size_t)f * a.ld + mem;
+    if constexpr (MODE == kAccFloat) {
+        if (v != 0.0f) atomicAdd(a.f + o, v);
+    } else if constexpr (MODE == kAccFixed) {
+        const long long qv = __float2ll_rn(v * scale);
+        if (qv != 0) atomicAdd(a.q + o, (unsigned long long)qv);
+    }
+}
+
+/// Pass 1 for one contribution (or a group of `n` lanes of the same member):
+/// the largest |adjoint| and the count; a non-finite adjoint flags the member.
+__device__ __forceinline__ float abs_max9(const float v[9], bool& finite) {
+    float m = 0.0f;
+    finite = true;
+#pragma unroll
+    for (int f = 0; f < 9; ++f) {
+        finite = finite && isfinite(v[f]);
+        m = fmaxf(m, fabsf(v[f]));
+    }
+    return m;
+}
+
 /// One emission sub-round's accumulation: all `go` lanes hold adjoints of the
 /// same member `mem`.  One or two lanes: direct atomics.  Otherwise a
 /// transposed butterfly (every exchange halves the values a lane still
 /// carries: 4 + 2 + 1 + 1 + 1 shuffles for fields 0-7 instead of 8 x 5)
 /// leaves the full sum of field (lane >> 2) & 7 in every lane; lanes 0, 4,
 /// ..., 28 issue the eight reductions with one RED instruction.  Field 8
-/// (d_alpha) takes a plain 5-step butterfly.
+/// (d_alpha) takes a plain 5-step butterfly.  Pass 1 (kAccMax) instead takes
+/// the warp max of the lanes' largest |adjoint| (one RED.MAX per sub-round).
+/// Pass 2: `scale` is the go lanes' member scale (member_scale), fetched by the
+/// caller ahead of the sub-round so its load latency stays off this path.
+template <int MODE>
 __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint32_t mem, const float v[9],
-                                            float* __restrict__ g2d, size_t ld2) {
-    if (__popc(gm) <= 2) {
-        if (go) {
-#pragma unroll
-            for (int f = 0; f < 9; ++f)
-                if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+                                            const GradAcc& acc, float scale) {
+    const int n = __popc(gm);
+    if constexpr (MODE == kAccMax) {
+        bool finite = true;
+        float m = go ? abs_max9(v, finite) : 0.0f;
+        if (go && !finite) atomicMin(acc.bad, (int)mem);
+        if (n <= 2) {
+            if (go) {
+                atomicAdd(acc.cnt + mem, 1u);
+                if (m > 0.0f && finite) atomicMax(acc.amax + mem, __float_as_uint(m));
+            }
+            return;
+        }
+        m = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(finite ? m : 0.0f)));
+        if (lane == __ffs(gm) - 1) {
+            atomicAdd(acc.cnt + mem, (uint32_t)n);
+            if (m > 0.0f) atomicMax(acc.amax + mem, __float_as_uint(m));
         }
         return;
     }
-    const uint32_t mem_w = __shfl_sync(kFull, mem, __ffs(gm) - 1);
+    if (n <= 2) {
+        if (go) {
+#pragma unroll
+            for (int f = 0; f < 9; ++f) acc_add<MODE>(acc, f, mem, v[f], scale);
+        }
+        return;
+    }
+    const int lead = __ffs(gm) - 1;
+    const uint32_t mem_w = __shfl_sync(kFull, mem, lead);
+    if constexpr (MODE == kAccFixed) scale = __shfl_sync(kFull, scale, lead);
     float a0 = v[0], a1 = v[1], a2 = v[2], a3 = v[3];
     {
         const bool hi = lane & 16;
@@ -173,11 +255,11 @@ __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint
     float a8 = v[8];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) a8 += __shfl_xor_sync(kFull, a8, off);
-    if ((lane & 3) == 0 && a0 != 0.0f) atomicAdd(g2d + ((lane >> 2) & 7) * ld2 + mem_w, a0);
-    if (lane == 0 && a8 != 0.0f) atomicAdd(g2d + 8 * ld2 + mem_w, a8);
+    if ((lane & 3) == 0) acc_add<MODE>(acc, (lane >> 2) & 7, mem_w, a0, scale);
+    if (lane == 0) acc_add<MODE>(acc, 8, mem_w, a8, scale);
 }
 
-template <bool STATS>
+template <bool STATS, int MODE>
 __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, RenderOpts ro, Subspace gate,
                                                              const SplatRec* __restrict__ recs,
                                                              const uint32_t* __restrict__ pair_val,
@@ -189,8 +271,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                                                              const float4* __restrict__ grad_ct,
                                                              const uint8_t* __restrict__ ovf_flag,
                                                              const uint8_t* __restrict__ tile_replay,
-                                                             float* __restrict__ g2d, size_t ld2,
-                                                             BlendStats* __restrict__ stats,
+                                                             GradAcc acc, BlendStats* __restrict__ stats,
                                                              const uint32_t* __restrict__ tile_order) {
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     if (tile_replay != nullptr && tile_replay[tile] == 0) return;  // handled by k_blend_bwd_rec
@@ -276,10 +357,12 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
 #pragma unroll
             for (int f = 0; f < 9; ++f) v[f] = 0.0f;
             uint32_t mem = 0;
+            float msc = 1.0f;
             if (go) {
                 const int sl = head & (KBUF - 1);
                 const float sigma = bs[sl][tid];
                 mem = pair_val[pmin];
+                msc = member_scale<MODE>(acc, mem);
                 float4 A, B, C, D;
                 if (pmin >= base && pmin < base + (uint32_t)nb) {
                     const int j = (int)(pmin - base);
@@ -293,7 +376,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                 const float dx = fsub(pr.pxf, A.x), dy = fsub(pr.pyf, A.y);
                 const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
                                       fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
-                const float g = __expf(fmul(-0.5f, m2));
+                const float g = glibc_expf(fmul(-0.5f, m2));  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
                 contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
                 if (STATS) ++nemit;
                 ++head;
@@ -307,7 +390,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                 ++n_rounds;
                 if (__popc(gm) <= 2) ++n_small;
             }
-            reduce_emit(gm, go, lane, mem, v, g2d, ld2);
+            reduce_emit<MODE>(gm, go, lane, mem, v, acc, msc);
         }
     };
 
@@ -414,7 +497,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
 // kernel, and the adjoint of each sub-round is reduced once.  The next
 // contribution's record is fetched right after an emission, so its L2 latency
 // overlaps the reduction and the other lanes' sub-rounds.
-template <bool STATS>
+template <bool STATS, int MODE>
 __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams vp, RenderOpts ro,
                                                                  const SplatRec* __restrict__ recs,
                                                                  const uint32_t* __restrict__ pair_val,
@@ -423,8 +506,8 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
                                                                  const double* __restrict__ fwd_cd,
                                                                  const float4* __restrict__ grad_ct,
                                                                  const uint8_t* __restrict__ ovf_flag,
-                                                                 CompRecords crec, float* __restrict__ g2d,
-                                                                 size_t ld2, BlendStats* __restrict__ stats,
+                                                                 CompRecords crec, GradAcc acc,
+                                                                 BlendStats* __restrict__ stats,
                                                                  const uint32_t* __restrict__ tile_order) {
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     if (crec.tile_replay[tile]) return;  // handled by the replay kernel
@@ -459,6 +542,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
     ushort4 q4 = make_ushort4(0, 0, 0, 0);
     int k = 0;
     uint32_t key = 0xffffffffu, m = 0;
+    float nsc = 1.0f;  // pass 2: the next contribution's member scale, loaded with its record
     float4 A, B, D;
     auto fetch = [&]() {
         if (k < n) {
@@ -471,6 +555,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
             A = __ldg(r4 + 0);
             B = __ldg(r4 + 1);
             D = __ldg(r4 + 3);
+            nsc = member_scale<MODE>(acc, m);
         } else {
             key = 0xffffffffu;
         }
@@ -486,16 +571,18 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
 #pragma unroll
         for (int f = 0; f < 9; ++f) v[f] = 0.0f;
         uint32_t mem = 0;
+        float msc = 1.0f;
         if (go) {
             // sigma and g exactly as the forward computed them (eval_candidate)
             const float dx = fsub(ps.pxf, A.x), dy = fsub(ps.pyf, A.y);
             const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
                                   fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
-            const float g = __expf(fmul(-0.5f, m2));
+            const float g = glibc_expf(fmul(-0.5f, m2));  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
             const float ag = fmul(A.z, g);
             const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
             contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
             mem = m;
+            msc = nsc;
             ++k;
             fetch();
         }
@@ -504,7 +591,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
             ++n_rounds;
             if (__popc(gm) <= 2) ++n_small;
         }
-        reduce_emit(gm, go, lane, mem, v, g2d, ld2);
+        reduce_emit<MODE>(gm, go, lane, mem, v, acc, msc);
     }
     if (STATS && stats != nullptr) {
         unsigned long long c = (unsigned long long)k;
@@ -519,6 +606,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
 
 // Exact fallback for ring-overflow pixels: one warp per pixel walks the tile
 // list in (t, id) order (fallback_select.cuh), accumulating as it goes.
+template <int MODE>
 __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, RenderOpts ro, Subspace gate,
                                                            const SplatRec* __restrict__ recs,
                                                            const uint32_t* __restrict__ pair_val,
@@ -529,8 +617,7 @@ __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, Render
                                                            const double* __restrict__ fwd_cd,
                                                            const float4* __restrict__ grad_ct,
                                                            const uint32_t* __restrict__ ovf_list,
-                                                           const uint32_t* __restrict__ n_ovf_dev, float* __restrict__ g2d,
-                                                           size_t ld2) {
+                                                           const uint32_t* __restrict__ n_ovf_dev, GradAcc acc) {
     // grid-stride over the device-side overflow count (no host round trip)
     const uint32_t n_ovf = *n_ovf_dev;
     const int lane = threadIdx.x & 31;
@@ -571,9 +658,18 @@ __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, Render
             load_rec(recs, mem, A, B, C, D);
             float v[9];
             contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
-            if (lane == 0)
-                for (int f = 0; f < 9; ++f)
-                    if (v[f] != 0.0f) atomicAdd(g2d + f * ld2 + mem, v[f]);
+            if (lane == 0) {
+                if constexpr (MODE == kAccMax) {
+                    bool finite = true;
+                    const float m = abs_max9(v, finite);
+                    if (!finite) atomicMin(acc.bad, (int)mem);
+                    atomicAdd(acc.cnt + mem, 1u);
+                    if (finite && m > 0.0f) atomicMax(acc.amax + mem, __float_as_uint(m));
+                } else {
+                    const float scale = MODE == kAccFixed ? fixed_scale(acc.amax[mem], acc.cnt[mem]) : 0.0f;
+                    for (int f = 0; f < 9; ++f) acc_add<MODE>(acc, f, mem, v[f], scale);
+                }
+            }
             return true;
         };
         __shared__ FbRing rings[2];  // one per warp of the 64-thread block
@@ -588,45 +684,80 @@ __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, Render
     }
 }
 
+
+template <int MODE>
+void blend_bwd_impl(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                    const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
+                    const CompRecords& rec, const GradAcc& acc, BlendStats* stats, cudaStream_t s) {
+    const int tiles = vp.tiles_x * vp.tiles_y;
+    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
+    ensure_smem_attr((const void*)k_blend_bwd<true, MODE>, (int)kBwdSmem);
+    ensure_smem_attr((const void*)k_blend_bwd<false, MODE>, (int)kBwdSmem);
+    if (rec.pos != nullptr) {
+        if (stats)
+            k_blend_bwd_rec<true, MODE><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
+                                                                        fwd_cd, grad_ct, ovf_flag, rec, acc, stats,
+                                                                        vb.tile_order);
+        else
+            k_blend_bwd_rec<false, MODE><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges,
+                                                                         fwd_ct, fwd_cd, grad_ct, ovf_flag, rec, acc,
+                                                                         stats, vb.tile_order);
+    }
+    // replay: flagged tiles only (every tile without records)
+    if (stats)
+        k_blend_bwd<true, MODE><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
+                                                                       vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd,
+                                                                       grad_ct, ovf_flag, rec.tile_replay, acc, stats,
+                                                                       vb.tile_order);
+    else
+        k_blend_bwd<false, MODE><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
+                                                                        vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd,
+                                                                        grad_ct, ovf_flag, rec.tile_replay, acc, stats,
+                                                                        vb.tile_order);
+}
+
+template <int MODE>
+void blend_bwd_fallback_impl(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
+                             const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
+                             const uint32_t* ovf_list, const uint32_t* n_ovf_dev, const GradAcc& acc, cudaStream_t s) {
+    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
+    k_blend_bwd_fallback<MODE><<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext,
+                                                      vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct, ovf_list,
+                                                      n_ovf_dev, acc);
+}
+
+/// Deterministic mode, after pass 2: g2d = q / S (S recomputed per member
+/// from pass 1's max and count; a power of two, so the division is exact
+/// before the final rounding to float).
+__global__ void k_fixed_to_float(GradAcc acc, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // member; blockIdx.y = field
+    if (i >= n) return;
+    const size_t j = (size_t)blockIdx.y * acc.ld + i;
+    const long long q = (long long)acc.q[j];
+    acc.f[j] = q == 0 ? 0.0f : (float)(__ll2double_rn(q) / (double)fixed_scale(acc.amax[i], acc.cnt[i]));
+}
+
 }  // namespace
 
 void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
-                      const CompRecords& rec, float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s) {
-    const int tiles = vp.tiles_x * vp.tiles_y;
-    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
-    ensure_smem_attr((const void*)k_blend_bwd<true>, (int)kBwdSmem);
-    ensure_smem_attr((const void*)k_blend_bwd<false>, (int)kBwdSmem);
-    if (rec.pos != nullptr) {
-        if (stats)
-            k_blend_bwd_rec<true><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
-                                                                  fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats,
-                                                                   vb.tile_order);
-        else
-            k_blend_bwd_rec<false><<<tiles, kBlendThreads, 0, s>>>(vp, ro, vb.recs, vb.pair_val, vb.ranges, fwd_ct,
-                                                                   fwd_cd, grad_ct, ovf_flag, rec, g2d, ld2, stats,
-                                                                   vb.tile_order);
+                      const CompRecords& rec, const GradAcc& acc, const uint32_t* ovf_list,
+                      const uint32_t* n_ovf_dev, BlendStats* stats, cudaStream_t s) {
+    if (acc.q == nullptr) {
+        blend_bwd_impl<kAccFloat>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_flag, rec, acc, stats, s);
+        blend_bwd_fallback_impl<kAccFloat>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, acc, s);
+        return;
     }
-    // replay: flagged tiles only (every tile without records)
-    if (stats)
-        k_blend_bwd<true><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
-                                                                 vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
-                                                                 ovf_flag, rec.tile_replay, g2d, ld2, stats,
-                                                                  vb.tile_order);
-    else
-        k_blend_bwd<false><<<tiles, kBlendThreads, kBwdSmem, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges,
-                                                                  vb.ext, vb.dmax_bits, onorm, fwd_ct, fwd_cd, grad_ct,
-                                                                  ovf_flag, rec.tile_replay, g2d, ld2, stats,
-                                                                  vb.tile_order);
+    // deterministic: pass 1 (max |term| and counts), pass 2 (fixed point); then launch_fixed_to_float
+    blend_bwd_impl<kAccMax>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_flag, rec, acc, nullptr, s);
+    blend_bwd_fallback_impl<kAccMax>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, acc, s);
+    blend_bwd_impl<kAccFixed>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_flag, rec, acc, stats, s);
+    blend_bwd_fallback_impl<kAccFixed>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, acc, s);
 }
 
-void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
-                               const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
-                               const uint32_t* ovf_list, const uint32_t* n_ovf_dev, float* g2d, size_t ld2,
-                               cudaStream_t s) {
-    const float onorm = sqrtf(vp.o[0] * vp.o[0] + vp.o[1] * vp.o[1] + vp.o[2] * vp.o[2]);
-    k_blend_bwd_fallback<<<148 * 8, 64, 0, s>>>(vp, ro, gate, vb.recs, vb.pair_val, vb.ranges, vb.ext, vb.dmax_bits,
-                                               onorm, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, g2d, ld2);
+void launch_fixed_to_float(const GradAcc& acc, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    k_fixed_to_float<<<dim3((unsigned)((n + 255) / 256), 9), 256, 0, s>>>(acc, n);
 }
 
 }  // namespace dgs_b200

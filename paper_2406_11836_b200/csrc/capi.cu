@@ -124,6 +124,7 @@ struct ViewSlot {
     DevBuf<float> shjac;       // [10][ld] SH colour Jacobian + clamp mask (ViewBins::shjac)
     DevBuf<uint16_t> rec_cnt;
     DevBuf<uint8_t> rec_replay;
+    DevBuf<uint32_t> blkp;     // K1 per-block partials (ViewBins::blk_part)
     bool rec_valid = false;  // the last forward of this slot wrote records
     CompRecords crec() const {
         CompRecords r;
@@ -145,6 +146,8 @@ struct SubsetState {
     int rows = 59;
     size_t ld = 0;
     DevBuf<float> P, M, V, G, g2d, rec;
+    DevBuf<unsigned long long> g2q;  // deterministic mode: fixed-point adjoint sums [9][ld]
+    DevBuf<uint32_t> amax, cnt;      // deterministic mode: per member max |adjoint|, contributions [ld]
     DevBuf<uint32_t> ids32;
     std::vector<uint64_t> ids64;
     uint64_t adam_step = 0, epoch = 0;
@@ -393,6 +396,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vb.rkey = vs.rkey.ensure(n);
     vb.ext = vs.ext.ensure(n);
     vb.dmax_bits = vs.dmax.ensure(4);
+    vb.blk_part = vs.blkp.ensure(preprocess_partials((int)n));
     vb.err_index = vs.err.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);
     vb.tile_order = vs.tile_order.ensure(tiles);
@@ -425,7 +429,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         Stage st(ctx.timer, kStPre, ctx.stream);
         launch_preprocess((int)n, S.P.p, S.ld, S.sh_coeffs, S.ids32.p, vp, ctx.ro, vb, ctx.stream);
     }
-    ++ctx.launches;
+    ctx.launches += 2;
     // zero-quaternion flag: rides along with the binning's pair-count readback
     CK(cudaMemcpyAsync(&ctx.hs->err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
     CK(cudaMemcpyAsync(&ctx.hs->visible, vb.dmax_bits + 2, 4, cudaMemcpyDeviceToHost, ctx.stream));
@@ -483,19 +487,42 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
 
 /// partial_render_backward for subset S, view slot v (engine.hpp:74-88) up to
 /// the pixel-space adjoints g2d (K8 + fallback).
+/// TrainConfig::deterministic ("fixed-order reductions", optim.hpp:33): the
+/// adjoints are summed as int64 fixed point in two passes (kernels.h GradAcc),
+/// then converted; a non-finite contribution is reported through ctx.bad like
+/// K9's check.
 void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     ViewSlot& vs = S.slot(v);
     S.g2d.ensure(9 * S.ld);
-    CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
+    const bool det = ctx.cfg.deterministic != 0;
+    GradAcc acc;
+    acc.f = S.g2d.p;
+    acc.ld = S.ld;
+    if (det) {
+        S.g2q.ensure(9 * S.ld);
+        S.amax.ensure(S.ld);
+        S.cnt.ensure(S.ld);
+        ctx.bad.ensure(1);
+        CK(cudaMemsetAsync(S.g2q.p, 0, 9 * S.ld * sizeof(unsigned long long), ctx.stream));
+        CK(cudaMemsetAsync(S.amax.p, 0, S.ld * sizeof(uint32_t), ctx.stream));
+        CK(cudaMemsetAsync(S.cnt.p, 0, S.ld * sizeof(uint32_t), ctx.stream));
+        acc.q = S.g2q.p;
+        acc.amax = S.amax.p;
+        acc.cnt = S.cnt.p;
+        acc.bad = ctx.bad.p;
+    } else {
+        CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
+    }
     Stage st(ctx.timer, kStBwd, ctx.stream);
     CompRecords crec;
     if (ctx.records && vs.rec_valid) crec = vs.crec();
     launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, crec,
-                     S.g2d.p, S.ld, stats, ctx.stream);
-    ++ctx.launches;
-    launch_blend_bwd_fallback(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p,
-                              vs.ovf_list.p, vs.ovf_count.p, S.g2d.p, S.ld, ctx.stream);
-    ++ctx.launches;
+                     acc, vs.ovf_list.p, vs.ovf_count.p, stats, ctx.stream);
+    ctx.launches += det ? 6 : 3;
+    if (det) {
+        launch_fixed_to_float(acc, (int)S.n, ctx.stream);
+        ++ctx.launches;
+    }
 }
 
 AdamParams adam_params(const Ctx& ctx, const SubsetState& S, uint64_t step_after) {
@@ -1956,10 +1983,10 @@ int dgs_render_partial_backward(dgs_ctx* ctx, int32_t k, const dgs_camera* cam, 
         ViewSlot& vs = S.slot(0);
         vs.grad_ct.ensure(px);
         CK(cudaMemcpyAsync(vs.grad_ct.p, grad_ct, px * sizeof(float4), cudaMemcpyHostToDevice, ctx->stream));
+        reset_bad(*ctx);
         backward_blend(*ctx, S, 0, nullptr);
         S.G.ensure(S.rows * S.ld);
         CK(cudaMemsetAsync(S.G.p, 0, S.rows * S.ld * sizeof(float), ctx->stream));
-        reset_bad(*ctx);
         launch_project_bwd((int)S.n, S.P.p, S.ld, S.sh_coeffs, vp, ctx->ro, vs.vb.counts, S.g2d.p, S.ld, S.G.p,
                            ctx->bad.p, ctx->stream);
         check_bad(*ctx, S);
@@ -2383,6 +2410,12 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         CK(cudaMemcpyAsync(st, ctx->stats.p, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
         int bad = INT_MAX;
         CK(cudaMemcpyAsync(&bad, ctx->bad.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        // ring-overflow pixels of every (subset, view): the fallback kernels' device counts
+        std::vector<uint32_t> ovf(local.size() * (size_t)batch, 0u);
+        for (size_t i = 0; i < local.size(); ++i)
+            for (int v = 0; v < batch; ++v)
+                CK(cudaMemcpyAsync(&ovf[i * batch + v], subset(*ctx, local[i]).slot(v).ovf_count.p, 4,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaGetLastError());
         ctx->timer.resolve();
@@ -2411,7 +2444,8 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             out->pairs = pairs;
             out->evals_fwd = st[0].evals;
             out->contribs_fwd = st[0].contribs;
-            out->overflow_pixels = st[0].overflow;
+            out->overflow_pixels = 0;
+            for (uint32_t o : ovf) out->overflow_pixels += o;
             out->evals_bwd = st[1].evals;
             out->contribs_bwd = st[1].contribs;
             out->subrounds_bwd = st[1].subrounds;

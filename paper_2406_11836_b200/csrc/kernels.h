@@ -26,6 +26,7 @@ struct ViewBins {
     float2* ext = nullptr;           // [n] conservative (x, y) half-extents of the m^2 <= 9 region (warp culling)
     uint32_t* dmax_bits = nullptr;   // [4] max world_radius over visible members, min range (float bits),
                                      //     visible member count, max range (float bits)
+    uint32_t* blk_part = nullptr;    // [preprocess_partials(n)] K1's per-block partials of dmax_bits
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
     float* shjac = nullptr;          // [10][ld] (optional): d colour_ch / d dir_a (row 3 ch + a) and the
                                      //     pre-clamp sign mask (row 9, bits) for the gradient record (K9)
@@ -40,7 +41,9 @@ struct ViewBins {
     int zorder = 0;
 };
 
-// K1: projection + SH colour + tile rectangles (splat.hpp:288-321, raster.hpp:113-125).
+// K1: projection + SH colour + tile rectangles (splat.hpp:288-321, raster.hpp:113-125),
+// then the fold of its per-block partials into vb.dmax_bits (2 launches).
+size_t preprocess_partials(int n);
 void launch_preprocess(int n, const float* P, size_t ld, int sh_coeffs, const uint32_t* ids32, const ViewParams& vp,
                        const RenderOpts& ro, const ViewBins& vb, cudaStream_t s);
 
@@ -86,17 +89,36 @@ void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
                                float4* out_ct, const uint32_t* ovf_list, const uint32_t* n_ovf_dev, uint32_t* dbg_ids,
                                uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s);
 
-// K8: backward blend; accumulates 9 pixel-space adjoints per member into g2d (SoA [9][ld2]).
+/// Where K8 accumulates the 9 pixel-space adjoints of each member (SoA [9][ld]).
+/// q == nullptr: float RED atomics into f (order-dependent rounding).
+/// q != nullptr (TrainConfig::deterministic, "fixed-order reductions",
+/// optim.hpp:33): two passes over the same emission sub-rounds — the first
+/// records per member the largest |adjoint| of any of its contributions (amax,
+/// float bits) and its contribution count (cnt), the second adds int64 fixed
+/// point at the member's own power-of-two scale (no overflow by construction),
+/// so the totals are exact integers whatever order the atomics land in;
+/// launch_fixed_to_float converts them into f.  A non-finite contribution sets
+/// bad = min(member index).  amax, cnt and q must be zeroed by the caller.
+struct GradAcc {
+    float* f = nullptr;
+    unsigned long long* q = nullptr;  // [9][ld]
+    uint32_t* amax = nullptr;         // [ld]
+    uint32_t* cnt = nullptr;          // [ld]
+    int* bad = nullptr;
+    size_t ld = 0;
+};
+
+// K8: backward blend (+ the exact fallback for ring-overflow pixels);
+// accumulates 9 pixel-space adjoints per member into acc (SoA [9][ld]).
 // fwd_cd: the forward's double-precision colour sums (suffix = C - prefix without cancellation loss).
 // With records (rec.pos != nullptr): the record walk for unflagged tiles plus
 // the ordered-ring replay for flagged tiles; without: replay everywhere.
 void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate, const ViewBins& vb,
                       const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
-                      const CompRecords& rec, float* g2d, size_t ld2, BlendStats* stats, cudaStream_t s);
-void launch_blend_bwd_fallback(const ViewParams& vp, const RenderOpts& ro, const Subspace& gate,
-                               const ViewBins& vb, const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct,
-                               const uint32_t* ovf_list, const uint32_t* n_ovf_dev, float* g2d, size_t ld2,
-                               cudaStream_t s);
+                      const CompRecords& rec, const GradAcc& acc, const uint32_t* ovf_list,
+                      const uint32_t* n_ovf_dev, BlendStats* stats, cudaStream_t s);
+// Deterministic mode: the fixed-point sums converted to float (acc.q -> acc.f, 9 rows).
+void launch_fixed_to_float(const GradAcc& acc, int n, cudaStream_t s);
 
 // Row windows: an array "with base b and rows r" holds image rows [b, b + r)
 // (planar arrays: plane = r * W).  partials[k] / grad_out[k] hold float4

@@ -228,20 +228,46 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
     }
     const int nvis = __syncthreads_count(dmax_local > 0.0f);
     if (threadIdx.x == 0) {
-        if (nvis) atomicAdd(vb.dmax_bits + 2, (uint32_t)nvis);
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
             m = fmaxf(m, s_max[w]);
             lo = fminf(lo, s_min[w]);
             hi = fmaxf(hi, s_hi[w]);
         }
-        // non-negative floats order like their bit patterns
-        if (m > 0.0f) atomicMax(vb.dmax_bits, __float_as_uint(m));
-        atomicMin(vb.dmax_bits + 1, __float_as_uint(lo));
-        if (hi > 0.0f) atomicMax(vb.dmax_bits + 3, __float_as_uint(hi));
+        // one 16-byte partial per block (non-negative floats order like their bit
+        // patterns); k_pre_reduce folds them instead of same-address atomics from
+        // every one of the ~78k blocks, which serialise in L2
+        reinterpret_cast<uint4*>(vb.blk_part)[blockIdx.x] =
+            make_uint4(__float_as_uint(m), __float_as_uint(lo), (uint32_t)nvis, __float_as_uint(hi));
+    }
+}
+
+/// Folds K1's per-block partials into dmax_bits (max D, min range, visible
+/// count, max range): one atomic per quantity per warp here.
+__global__ void __launch_bounds__(256) k_pre_reduce(const uint32_t* __restrict__ part, int nblk,
+                                                    uint32_t* __restrict__ dmax_bits) {
+    uint32_t m = 0, lo = 0x7f7fffffu, hi = 0, nv = 0;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x) {
+        const uint4 a = reinterpret_cast<const uint4*>(part)[b];
+        m = max(m, a.x);
+        lo = min(lo, a.y);
+        nv += a.z;
+        hi = max(hi, a.w);
+    }
+    m = __reduce_max_sync(0xffffffffu, m);
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    nv = __reduce_add_sync(0xffffffffu, nv);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if ((threadIdx.x & 31) == 0) {
+        if (nv) atomicAdd(dmax_bits + 2, nv);
+        if (m) atomicMax(dmax_bits, m);
+        atomicMin(dmax_bits + 1, lo);
+        if (hi) atomicMax(dmax_bits + 3, hi);
     }
 }
 
 }  // namespace
+
+size_t preprocess_partials(int n) { return n > 0 ? 4 * (size_t)((n + kPreTB - 1) / kPreTB) : 1; }
 
 void launch_preprocess(int n, const float* P, size_t ld, int sh_coeffs, const uint32_t* ids32, const ViewParams& vp,
                        const RenderOpts& ro, const ViewBins& vb, cudaStream_t s) {
@@ -253,6 +279,7 @@ void launch_preprocess(int n, const float* P, size_t ld, int sh_coeffs, const ui
         case 9: k_preprocess<9><<<grid, kPreTB, 0, s>>>(n, P, ld, ids32, vp, ro, vb); break;
         default: k_preprocess<16><<<grid, kPreTB, 0, s>>>(n, P, ld, ids32, vp, ro, vb); break;
     }
+    k_pre_reduce<<<64, 256, 0, s>>>(vb.blk_part, (int)grid, vb.dmax_bits);
 }
 
 }  // namespace dgs_b200

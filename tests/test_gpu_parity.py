@@ -14,7 +14,8 @@ compared bit for bit.
 import numpy as np
 import pytest
 
-from conftest import GRAD_RTOL, Golden, adam_lr_rows, grad_errors, post_adam_ok, rel_err
+from conftest import (GRAD_RTOL, K_ROUND, Golden, adam_lr_rows, golden_bounds, grad_ok, oracle_gradients,
+                      oracle_step_bounds, post_adam_ok, rel_err)
 from paper_2406_11836_b200 import engine
 
 pytestmark = pytest.mark.gpu
@@ -158,20 +159,42 @@ def _grad_check(got, g, prefix, fields, tol=1e-3):
     return worst
 
 
+@pytest.mark.parametrize("det", [1, 0], ids=["fixed-point", "float-atomic"])
 @pytest.mark.parametrize("records", [True, False], ids=["record-walk", "ring-replay"])
-def test_partial_backward_gradients(golden, records):
+def test_partial_backward_gradients(golden, records, det):
+    """partial_render_backward (engine.hpp:74-88) against the reference's
+    gradients with its own 1e-8 floor and no noise mask (conftest.grad_ok:
+    1e-3 relative, or of the exact-accumulation probe, or within 16 u B of the
+    rounding-sensitivity scale).  deterministic = 1 (int64 fixed-point sums)
+    is also bitwise reproducible; deterministic = 0 uses float RED atomics."""
     g = golden
     ctx, table, s = make_ctx(g, members_of(g))
+    ctx.set_options(engine.render_options(oracle=g.oracle_mode), engine.train_config(deterministic=det))
     ctx.set_backward_records(records)
     cam = g.camera()
+    rec = g["scene_cameras"][g.args["view"]]
+    members = members_of(g)
+    bounds = golden_bounds(g, members)
+    n2 = n3 = 0
+    worst = 0.0
     for k in range(g.subsets()):
         grad_ct = np.concatenate([g[f"k{k}_dC"], g[f"k{k}_dT"][..., None]], axis=-1)
         got = ctx.render_partial_backward(k, cam, grad_ct, s.sh_coeffs)
+        if det:
+            again = ctx.render_partial_backward(k, cam, grad_ct, s.sh_coeffs)
+        exact = oracle_gradients(s.take(members[k]), table.planes[k], rec, g.oracle_mode, grad_ct, exact=True)
         for f in GRAD_FIELDS:
             want = g[f"k{k}_grad_{f}"]
             a = getattr(got, f[2:]).reshape(want.shape)
-            e = grad_errors(a, want)
-            assert e.max() <= GRAD_RTOL, (k, f, float(e.max()), np.unravel_index(e.argmax(), e.shape))
+            if det:
+                np.testing.assert_array_equal(a, getattr(again, f[2:]).reshape(want.shape))
+            ok, e, c2, c3, ratio = grad_ok(a, want, exact[f].reshape(want.shape), bounds[k][f].reshape(want.shape))
+            n2, n3, worst = n2 + c2, n3 + c3, max(worst, ratio)
+            bad = np.nonzero(~ok.reshape(-1))[0]
+            assert ok.all(), (k, f, int((~ok).sum()), [(int(i), float(e.reshape(-1)[i]), float(want.reshape(-1)[i]),
+                                                         float(a.reshape(-1)[i])) for i in bad[:4]])
+    print(f"{g.name}: beyond 1e-3: {n2} within 1e-3 of exact sums, {n3} within {K_ROUND} u B "
+          f"(max {worst:.2f} u B)")
     ctx.close()
 
 
@@ -224,12 +247,14 @@ def test_full_train_step_matches_reference(golden):
     res = mgr.train_step([cam], g["step_target"][None], g.bg)
     assert abs(res["loss"] - float(g["step_loss"][0])) <= 1e-4 * max(1.0, abs(float(g["step_loss"][0])))
     lrs = adam_lr_rows(cfg, s.sh_coeffs)
+    bounds = golden_bounds(g, members_of(g))
     for k in range(g.subsets()):
         p, _, _, step = mgr.ctx.store_subset(k, s.sh_coeffs)
         assert step == 1
         for f in PARAM_FIELDS:
             want = g[f"k{k}_adam_{f}"]
-            ok, e, noisy = post_adam_ok(getattr(p, f).reshape(want.shape), want, g[f"k{k}_grad_d_{f}"], lrs[f])
+            ok, e, noisy = post_adam_ok(getattr(p, f).reshape(want.shape), want, g[f"k{k}_grad_d_{f}"], lrs[f],
+                                        bound=bounds[k]["d_" + f])
             assert ok.all(), (k, f, float(e[~noisy].max()) if (~noisy).any() else 0.0, int((~ok).sum()))
     mgr.close()
 
@@ -249,11 +274,15 @@ def test_batch_train_step_matches_reference():
     want_loss = float(g["batch_loss"][0])
     assert abs(res["loss"] - want_loss) <= 1e-4 * max(1.0, abs(want_loss)), (res["loss"], want_loss)
     lrs = adam_lr_rows(cfg, s.sh_coeffs)
+    table = engine.build_kdtree(s.mu, g.args["kd"])
+    bounds = oracle_step_bounds(s, members_of(g), table.planes, g["batch_cameras"], g["batch_targets"],
+                                g.oracle_mode, g.bg)
     for k in range(g.subsets()):
         p, _, _, step = mgr.ctx.store_subset(k, s.sh_coeffs)
         assert step == 1
         for f in PARAM_FIELDS:
             want = g[f"k{k}_batch_adam_{f}"]
-            ok, e, noisy = post_adam_ok(getattr(p, f).reshape(want.shape), want, g[f"k{k}_batch_grad_d_{f}"], lrs[f])
+            ok, e, noisy = post_adam_ok(getattr(p, f).reshape(want.shape), want, g[f"k{k}_batch_grad_d_{f}"], lrs[f],
+                                        bound=bounds[k]["d_" + f])
             assert ok.all(), (k, f, int((~ok).sum()))
     mgr.close()
