@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--views", type=int, default=8,
                     help="training cycles over this many ring views (every 64/views-th of the 64), one per step")
     ap.add_argument("--iterations", type=int, default=30000, help="TrainConfig.iterations (position-LR schedule)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="N > 1 exchange: NCCL over NVLink (one GPU per rank), or the host-staged gloo transport "
+                         "(every rank on GPU 0: runs the N > 1 harness end to end on a single-GPU box)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=120.0)
     return ap.parse_args()
@@ -79,6 +82,7 @@ def workload_config(a, world):
                      "MUFU sqrt/divide, <= few ulp from the reference's IEEE sequence)",
         "l2": "no flush needed: params + Adam moments (7.1 GB) and per-view buffers exceed the 126 MB L2",
         "parallelism": f"kd-model-parallel x{world}",
+        "transport": a.transport if world > 1 else None,
     }
 
 
@@ -282,35 +286,48 @@ def b200_arm(a, world, rank, local_rank):
     import torch.distributed as dist
     from paper_2406_11836_b200 import engine
 
+    host_xfer = a.transport == "host" and world > 1
+    if host_xfer:
+        local_rank = 0  # every rank shares GPU 0; exchanges staged through host memory over gloo
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     nccl_id = None
+    transport = None
     if world > 1:
         if world & (world - 1):
             raise SystemExit("--gpus must be a power of two (one KD subset per rank, K = 2^depth)")
-        dist.init_process_group("nccl", device_id=dev)
-        obj = [engine.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        if host_xfer:
+            from paper_2406_11836_b200.host_transport import GlooTransport
+            dist.init_process_group("gloo")
+            transport = GlooTransport()
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            obj = [engine.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
+    cdev = torch.device("cpu") if host_xfer else dev
 
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def gather_ranks(x: float) -> list:
         if world == 1:
             return [x]
-        t = torch.zeros(world, dtype=torch.float64, device=dev)
+        t = torch.zeros(world, dtype=torch.float64, device=cdev)
         t[rank] = x
         dist.all_reduce(t)
         return [float(v) for v in t.tolist()]
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            if host_xfer:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize()
 
     t_setup = time.time()
@@ -327,7 +344,8 @@ def b200_arm(a, world, rank, local_rank):
     del gt
     cfg = engine.train_config(kd_depth=int(math.log2(world)), iterations=a.iterations, deterministic=0)
     ro = engine.render_options(grad_skip_eps=0.0)
-    mgr = engine.Manager(init, cfg, ro, device=local_rank, rank=rank, world=world, nccl_id=nccl_id)
+    mgr = engine.Manager(init, cfg, ro, device=local_rank, rank=rank, world=world, nccl_id=nccl_id,
+                         transport=transport)
     ctx = mgr.ctx
     n_local = sum(int(engine.lib().dgs_subset_size(ctx.handle, k)) for k in range(mgr.table.subset_count)
                   if engine.subset_owner(k, mgr.table.subset_count, world) == rank)

@@ -243,7 +243,7 @@ class Context:
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  transport=None):
         """transport: an object with send/recv/flush/allreduce methods (e.g.
-        tests/host_transport.py) replacing NCCL for the multi-rank exchange."""
+        paper_2406_11836_b200/host_transport.py) replacing NCCL for the multi-rank exchange."""
         self._h = C.c_void_p()
         self._transport = None
         if transport is not None:
@@ -499,37 +499,51 @@ class Manager:
         return self.ctx.render(cam, bg)
 
     def snapshot(self):
-        """manager.hpp:390-418: the replica held by the subspace containing the centre wins."""
+        """manager.hpp:390-418: gather every subset's (p, m, v); a shared splat
+        resolves to the replica held by the subspace containing its centre, else
+        to the lowest subset index.  Returned in id order (the reference returns
+        owner-resolved packs first, then the rest).  world > 1: every rank sends
+        its owned subsets to rank 0 over torch.distributed (the process group
+        the caller initialised, NCCL or gloo); rank 0 returns the snapshot and
+        the other ranks None (the reference's snapshot lives on the manager)."""
+        parts = {k: self.ctx.store_subset(k, self.sh_coeffs) for k in range(self.table.subset_count)
+                 if subset_owner(k, self.table.subset_count, self.world) == self.rank}
         if self.world > 1:
-            raise NotImplementedError("snapshot() gathers a single rank's subsets; across ranks use "
-                                      "repartition(device=True) (dgs_repartition)")
-        parts = [self.ctx.store_subset(k, self.sh_coeffs) for k in range(self.table.subset_count)]
-        chosen: dict[int, tuple[int, int]] = {}
-        for k, (p, _, _, _) in enumerate(parts):
-            owner = self.table.locate(p.mu)
-            for i in np.nonzero(owner == k)[0]:
-                chosen.setdefault(int(p.id[i]), (k, int(i)))
-        for k, (p, _, _, _) in enumerate(parts):
-            for i in range(p.n):
-                chosen.setdefault(int(p.id[i]), (k, i))
-        if len(chosen) != len(self.ids):
+            import torch.distributed as dist
+            if not dist.is_initialized():
+                raise RuntimeError("snapshot: world > 1 needs the torch.distributed process group of the ranks")
+            got = [None] * self.world if self.rank == 0 else None
+            dist.gather_object(parts, got, dst=0)
+            if self.rank != 0:
+                return None
+            parts = {k: v for d in got for k, v in d.items()}
+        K = self.table.subset_count
+        if sorted(parts) != list(range(K)):
+            raise RuntimeError("snapshot: missing subsets " + str(sorted(set(range(K)) - set(parts))))
+        ids = np.concatenate([parts[k][0].id for k in range(K)])
+        kk = np.concatenate([np.full(parts[k][0].n, k, np.int64) for k in range(K)])
+        owner = np.concatenate([self.table.locate(parts[k][0].mu) == k for k in range(K)])
+        pri = np.where(owner, kk, K + kk)  # owner-held replica first, then the lowest k
+        order = np.lexsort((pri, ids))
+        first = np.ones(len(order), bool)
+        first[1:] = ids[order][1:] != ids[order][:-1]
+        chosen = order[first]
+        if len(chosen) != len(self.ids) or not np.array_equal(ids[chosen], self.ids):
             raise RuntimeError("snapshot lost splats")
-        order = sorted(chosen)
+
         def gather(which):
-            out = Splats.empty(len(order), self.sh_coeffs)
-            for j, sid in enumerate(order):
-                k, i = chosen[sid]
-                src = parts[k][which]
-                for f in ("id", "mu", "log_scale", "rotation", "opacity_logit", "sh"):
-                    getattr(out, f)[j] = getattr(src, f)[i]
+            out = Splats.empty(len(chosen), self.sh_coeffs)
+            for f in ("id", "mu", "log_scale", "rotation", "opacity_logit", "sh"):
+                getattr(out, f)[...] = np.concatenate([getattr(parts[k][which], f) for k in range(K)])[chosen]
             return out
         return gather(0), gather(1), gather(2), parts[0][3]
 
     def checkpoint(self, path: str) -> None:
         """snapshot(checkpoint_path) (manager.hpp:390-396): the merged splats as a
-        3DGS PLY (Adam moments are not part of the file format)."""
-        p, _, _, _ = self.snapshot()
-        save_splats_ply(p, path)
+        3DGS PLY (Adam moments are not part of the file format); written by rank 0."""
+        snap = self.snapshot()
+        if snap is not None:
+            save_splats_ply(snap[0], path)
 
     def repartition(self, device: bool = True):
         """Manager::repartition (manager.hpp:421-430).  device=True (default):

@@ -1,7 +1,8 @@
-"""Test transport for the multi-rank step (dgs_host_transport): the C-ABI's
-exchanges and loss all-reduce go through torch.distributed (gloo) between
-processes that share one GPU (NCCL refuses two ranks on one device).  Test
-infrastructure only."""
+"""Host-staged transport for the multi-rank step (dgs_host_transport): the
+C-ABI's exchanges and loss all-reduce go through torch.distributed (gloo)
+between processes that may share one GPU (NCCL refuses two ranks on one
+device).  Used by the multi-rank tests and `bench.py --transport host`; the
+production path is the context's NCCL communicator."""
 import ctypes as C
 
 import numpy as np

@@ -44,7 +44,7 @@ def _worker(rank, world, port, out_dir, case="golden"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from host_transport import GlooTransport
+        from paper_2406_11836_b200.host_transport import GlooTransport
         from paper_2406_11836_b200 import engine
         s, kd, oracle, cam, target, bg = _tiny_case() if case == "tiny" else _golden_case()
         cfg = engine.train_config(kd_depth=kd)
@@ -108,7 +108,7 @@ def _rep_worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from conftest import Golden
-        from host_transport import GlooTransport
+        from paper_2406_11836_b200.host_transport import GlooTransport
         from paper_2406_11836_b200 import engine
         g = Golden(NAME)
         s = g.splats()
@@ -170,7 +170,7 @@ def _sync_worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from conftest import Golden
-        from host_transport import GlooTransport
+        from paper_2406_11836_b200.host_transport import GlooTransport
         from paper_2406_11836_b200 import engine
         g = Golden(NAME)
         s = g.splats()
@@ -254,3 +254,51 @@ def test_nccl_binding_self_communicator():
     from paper_2406_11836_b200 import capi
 
     capi.check(capi.lib().dgs_nccl_selftest(0))
+
+
+def _snap_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2406_11836_b200.host_transport import GlooTransport
+        from paper_2406_11836_b200 import engine
+        s, kd, oracle, cam, target, bg = _golden_case()
+        cfg = engine.train_config(kd_depth=kd)
+        mgr = engine.Manager(s, cfg, engine.render_options(oracle=oracle), device=0, rank=rank, world=world,
+                             transport=GlooTransport())
+        mgr.train_step([cam], target, bg)
+        snap = mgr.snapshot()
+        mgr.checkpoint(os.path.join(out_dir, "ckpt.ply"))
+        if rank == 0:
+            p, m, v, step = snap
+            np.savez(os.path.join(out_dir, "snap.npz"), step=np.array([step]),
+                     **{f"{w}_{f}": getattr(x, f) for w, x in (("p", p), ("m", m), ("v", v))
+                        for f in ("id", "mu", "log_scale", "rotation", "opacity_logit", "sh")})
+        else:
+            assert snap is None
+        mgr.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_snapshot_and_checkpoint_match_single_rank(tmp_path, world):
+    """Manager::snapshot / checkpoint across ranks (manager.hpp:390-418,
+    trainer.hpp:184): every rank's subsets gathered to rank 0 with the
+    reference's replica rule; equals the single-rank snapshot after the same
+    step bit for bit, and rank 0's PLY equals the single-rank PLY byte for byte."""
+    from paper_2406_11836_b200 import engine
+    mp.spawn(_snap_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    s, kd, oracle, cam, target, bg = _golden_case()
+    mgr = engine.Manager(s, engine.train_config(kd_depth=kd), engine.render_options(oracle=oracle))
+    mgr.ctx.set_virtual_slices(world)
+    mgr.train_step([cam], target, bg)
+    p, m, v, step = mgr.snapshot()
+    mgr.checkpoint(str(tmp_path / "ref.ply"))
+    mgr.close()
+    got = np.load(tmp_path / "snap.npz")
+    assert int(got["step"][0]) == step == 1
+    for w, x in (("p", p), ("m", m), ("v", v)):
+        for f in ("id", "mu", "log_scale", "rotation", "opacity_logit", "sh"):
+            np.testing.assert_array_equal(got[f"{w}_{f}"], getattr(x, f), err_msg=f"{w}.{f}")
+    assert (tmp_path / "ckpt.ply").read_bytes() == (tmp_path / "ref.ply").read_bytes()
