@@ -388,6 +388,94 @@ int64_t orc_project(const orc_splats* s, const orc_camera* cam, const orc_opts* 
 }
 
 /* render_maps with the subspace gate (raster.hpp:241-263, engine.hpp:31-52) */
+/* Row-parallel driver for the oracle's embarrassingly parallel loops (the
+ * reference's own parallel_chunks is order-sensitive only in its reductions,
+ * which stay serial here): fn(arg, y0, y1, thread) on blocks of rows. */
+#include <pthread.h>
+#include <unistd.h>
+typedef struct {
+    void (*fn)(void*, int, int, int);
+    void* arg;
+    int n, next, tid;
+    pthread_mutex_t mu;
+} par_t;
+static void* par_worker(void* p) {
+    par_t* q = (par_t*)p;
+    pthread_mutex_lock(&q->mu);
+    const int tid = q->tid++;
+    pthread_mutex_unlock(&q->mu);
+    for (;;) {
+        pthread_mutex_lock(&q->mu);
+        const int y0 = q->next;
+        q->next += 4;
+        pthread_mutex_unlock(&q->mu);
+        if (y0 >= q->n) break;
+        q->fn(q->arg, y0, y0 + 4 < q->n ? y0 + 4 : q->n, tid);
+    }
+    return NULL;
+}
+static int par_threads(void) {
+    long c = sysconf(_SC_NPROCESSORS_ONLN);
+    return c < 1 ? 1 : (c > 64 ? 64 : (int)c);
+}
+static void par_rows(int n, void (*fn)(void*, int, int, int), void* arg) {
+    const int nt = par_threads();
+    par_t q = {fn, arg, n, 0, 0, PTHREAD_MUTEX_INITIALIZER};
+    pthread_t th[64];
+    for (int t = 0; t < nt; ++t) pthread_create(&th[t], NULL, par_worker, &q);
+    for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
+typedef struct {
+    const orc_splats* s;
+    const orc_subspace* sub;
+    const orc_opts* o;
+    const view_t* v;
+    const scene_t* sc;
+    int64_t maxlen;
+    float* out_ct;
+    int32_t dbg_cap;
+    uint32_t* dbg_ids;
+    uint32_t* dbg_cnt;
+} render_job_t;
+
+/* composite_ray (raster.hpp:177-189) for the rows [y0, y1) */
+static void render_rows(void* arg, int y0, int y1, int tid) {
+    (void)tid;
+    const render_job_t* j = (const render_job_t*)arg;
+    const view_t* v = j->v;
+    const float stop = j->o->stop;
+    contrib_t* buf = (contrib_t*)malloc(sizeof(contrib_t) * j->maxlen);
+    for (int y = y0; y < y1; ++y)
+        for (int x = 0; x < v->w; ++x) {
+            float d[3];
+            pixel_ray(v, x, y, d);
+            const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+            const int64_t tile = (int64_t)(y / 16) * v->tx + x / 16;
+            const int64_t n = collect(j->sc, j->s->id, tile, v, d, px, py, j->o, j->sub, buf);
+            float C[3] = {0.0f, 0.0f, 0.0f}, T = 1.0f;
+            int32_t ne = 0;
+            const size_t pix = (size_t)y * v->w + x;
+            for (int64_t k = 0; k < n; ++k) {
+                if (stop > 0.0f && T < stop) break;
+                const splat2d_t* q = &j->sc->sp[buf[k].proj];
+                const float wgt = buf[k].sigma * T;
+                for (int ch = 0; ch < 3; ++ch) C[ch] = C[ch] + q->col[ch] * wgt;
+                T = T * (1.0f - buf[k].sigma);
+                if (j->dbg_ids && ne < j->dbg_cap) j->dbg_ids[pix * j->dbg_cap + ne] = (uint32_t)buf[k].id;
+                ++ne;
+            }
+            if (j->out_ct) {
+                j->out_ct[4 * pix] = C[0];
+                j->out_ct[4 * pix + 1] = C[1];
+                j->out_ct[4 * pix + 2] = C[2];
+                j->out_ct[4 * pix + 3] = T;
+            }
+            if (j->dbg_cnt) j->dbg_cnt[pix] = (uint32_t)ne;
+        }
+    free(buf);
+}
+
 int orc_partial_render(const orc_splats* s, const orc_subspace* sub, const orc_camera* cam, const orc_opts* o,
                        float* out_ct, int32_t dbg_cap, uint32_t* dbg_ids, uint32_t* dbg_cnt) {
     view_t v;
@@ -400,36 +488,9 @@ int orc_partial_render(const orc_splats* s, const orc_subspace* sub, const orc_c
     int64_t maxlen = 1;
     for (int t = 0; t < v.tx * v.ty; ++t)
         if (sc.off[t + 1] - sc.off[t] > maxlen) maxlen = sc.off[t + 1] - sc.off[t];
-    contrib_t* buf = (contrib_t*)malloc(sizeof(contrib_t) * maxlen);
-    const float stop = o->stop;
-    for (int y = 0; y < v.h; ++y)
-        for (int x = 0; x < v.w; ++x) {
-            float d[3];
-            pixel_ray(&v, x, y, d);
-            const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-            const int64_t tile = (int64_t)(y / 16) * v.tx + x / 16;
-            const int64_t n = collect(&sc, s->id, tile, &v, d, px, py, o, sub, buf);
-            float C[3] = {0.0f, 0.0f, 0.0f}, T = 1.0f;
-            int32_t ne = 0;
-            const size_t pix = (size_t)y * v.w + x;
-            for (int64_t k = 0; k < n; ++k) { /* composite_ray (raster.hpp:177-189) */
-                if (stop > 0.0f && T < stop) break;
-                const splat2d_t* q = &sc.sp[buf[k].proj];
-                const float wgt = buf[k].sigma * T;
-                for (int ch = 0; ch < 3; ++ch) C[ch] = C[ch] + q->col[ch] * wgt;
-                T = T * (1.0f - buf[k].sigma);
-                if (dbg_ids && ne < dbg_cap) dbg_ids[pix * dbg_cap + ne] = (uint32_t)buf[k].id;
-                ++ne;
-            }
-            if (out_ct) {
-                out_ct[4 * pix] = C[0];
-                out_ct[4 * pix + 1] = C[1];
-                out_ct[4 * pix + 2] = C[2];
-                out_ct[4 * pix + 3] = T;
-            }
-            if (dbg_cnt) dbg_cnt[pix] = (uint32_t)ne;
-        }
-    free(buf);
+    /* pixels are independent: row blocks on threads give the serial loop's results */
+    render_job_t job = {s, sub, o, &v, &sc, maxlen, out_ct, dbg_cap, dbg_ids, dbg_cnt};
+    par_rows(v.h, render_rows, &job);
     scene_free(&sc);
     return 0;
 }
@@ -1083,6 +1144,43 @@ static void project_backward_abs(const orc_splats* sp, int64_t i, const view_t* 
     *bop += g[9] * al * (1.0 - al);
 }
 
+typedef struct {
+    const orc_splats* s;
+    const orc_subspace* sub;
+    const orc_opts* o;
+    const view_t* v;
+    const scene_t* sc;
+    int64_t maxlen;
+    const float* grad_ct;
+    g2dx_t* mine;  /* [threads][np] */
+    int64_t np;
+} mass_job_t;
+
+static void mass_rows(void* arg, int y0, int y1, int tid) {
+    const mass_job_t* j = (const mass_job_t*)arg;
+    const view_t* v = j->v;
+    contrib_t* buf = (contrib_t*)malloc(sizeof(contrib_t) * j->maxlen);
+    float* prefix = (float*)malloc(sizeof(float) * j->maxlen);
+    g2dx_t* am = j->mine + (size_t)tid * j->np;
+    for (int y = y0; y < y1; ++y)
+        for (int x = 0; x < v->w; ++x) {
+            const size_t pix = (size_t)y * v->w + x;
+            const float* g = j->grad_ct + 4 * pix;
+            const float gc[3] = {g[0], g[1], g[2]};
+            const float gt = g[3];
+            const float e = j->o->grad_skip_eps;
+            if (fabsf(gc[0]) <= e && fabsf(gc[1]) <= e && fabsf(gc[2]) <= e && gt == 0.0f) continue;
+            float d[3];
+            pixel_ray(v, x, y, d);
+            const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+            const int64_t tile = (int64_t)(y / 16) * v->tx + x / 16;
+            const int64_t n = collect(j->sc, j->s->id, tile, v, d, px, py, j->o, j->sub, buf);
+            composite_backward_mass(buf, n, j->sc, j->o, px, py, gc, gt, am, prefix);
+        }
+    free(buf);
+    free(prefix);
+}
+
 /* Rounding-sensitivity bound of every parameter gradient (TEST
  * INFRASTRUCTURE): B_j = the gradient evaluated with every term in absolute
  * value — the cancellation-free magnitudes of the 10 pixel-space adjoint sums
@@ -1104,23 +1202,21 @@ int orc_partial_backward_bound(const orc_splats* s, const orc_subspace* sub, con
     int64_t maxlen = 1;
     for (int t = 0; t < v.tx * v.ty; ++t)
         if (sc.off[t + 1] - sc.off[t] > maxlen) maxlen = sc.off[t + 1] - sc.off[t];
-    contrib_t* buf = (contrib_t*)malloc(sizeof(contrib_t) * maxlen);
-    float* prefix = (float*)malloc(sizeof(float) * maxlen);
     g2dx_t* am = (g2dx_t*)calloc(np ? np : 1, sizeof(g2dx_t));
-    for (int y = 0; y < v.h; ++y)
-        for (int x = 0; x < v.w; ++x) {
-            const size_t pix = (size_t)y * v.w + x;
-            const float gc[3] = {grad_ct[4 * pix], grad_ct[4 * pix + 1], grad_ct[4 * pix + 2]};
-            const float gt = grad_ct[4 * pix + 3];
-            const float e = o->grad_skip_eps;
-            if (fabsf(gc[0]) <= e && fabsf(gc[1]) <= e && fabsf(gc[2]) <= e && gt == 0.0f) continue;
-            float d[3];
-            pixel_ray(&v, x, y, d);
-            const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-            const int64_t tile = (int64_t)(y / 16) * v.tx + x / 16;
-            const int64_t n = collect(&sc, s->id, tile, &v, d, px, py, o, sub, buf);
-            composite_backward_mass(buf, n, &sc, o, px, py, gc, gt, am, prefix);
+    /* rows on threads, one mass array per thread, summed after (a bound: order free) */
+    const int nt = par_threads();
+    g2dx_t* mine = (g2dx_t*)calloc((size_t)nt * (np ? np : 1), sizeof(g2dx_t));
+    mass_job_t job = {s, sub, o, &v, &sc, maxlen, grad_ct, mine, np ? np : 1};
+    par_rows(v.h, mass_rows, &job);
+    for (int t = 0; t < nt; ++t)
+        for (int64_t p = 0; p < np; ++p) {
+            const g2dx_t* m = &mine[(size_t)t * np + p];
+            for (int a = 0; a < 2; ++a) am[p].dm[a] += m->dm[a];
+            for (int a = 0; a < 4; ++a) am[p].dc[a] += m->dc[a];
+            for (int a = 0; a < 3; ++a) am[p].dcol[a] += m->dcol[a];
+            am[p].da += m->da;
         }
+    free(mine);
     const size_t nsh = (size_t)s->n * s->sh_coeffs * 3;
     double* acc = (double*)calloc((size_t)s->n * 11 + nsh + 1, sizeof(double));
     double* bmu = acc;
@@ -1142,8 +1238,6 @@ int orc_partial_backward_bound(const orc_splats* s, const orc_subspace* sub, con
     for (size_t i = 0; i < nsh; ++i) out->d_sh[i] = (float)bsh[i];
     free(acc);
     free(am);
-    free(buf);
-    free(prefix);
     scene_free(&sc);
     return 0;
 }
