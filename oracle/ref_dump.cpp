@@ -704,7 +704,7 @@ int main(int argc, char** argv) {
             std::vector<GradBuffers<Real>> acc;
             for (int k = 0; k < table.subset_count(); ++k)
                 acc.emplace_back(std::span<const Splat<Real>>(members[k]));
-            double loss_acc = 0.0;
+            double loss_acc = 0.0, loss_acc64 = 0.0;
             std::vector<Real> cams_rec, tgts;
             for (std::size_t v = 0; v < B; ++v) {
                 const Camera<Real>& c = cams[views[v]];
@@ -719,6 +719,16 @@ int main(int argc, char** argv) {
                 const RenderedImage<Real> img = merge<Real>(partials, orders, bg);
                 LossResult<Real> l = loss<Real>(img.color, target, cfg.lambda_ssim);
                 loss_acc += double(l.value) / double(B);
+                {
+                    // the same loss template in double on the same float images: the float
+                    // instantiation's sequential sum drifts by percent at 1e6+ terms
+                    Image<double> xd(c.width, c.height, 3), yd(c.width, c.height, 3);
+                    for (std::size_t i = 0; i < xd.data.size(); ++i) {
+                        xd.data[i] = double(img.color.data[i]);
+                        yd.data[i] = double(target.data[i]);
+                    }
+                    loss_acc64 += loss<double>(xd, yd, cfg.lambda_ssim).value / double(B);
+                }
                 for (auto& g : l.grad.data) g *= inv_batch;
                 const Image<Real> gt0(c.width, c.height, 1, Real(0));
                 auto per = merge_backward<Real>(partials, orders, l.grad, gt0, bg);
@@ -726,7 +736,7 @@ int main(int argc, char** argv) {
                     acc[k].add(partial_render_backward<Real>(members[k], table.subspaces[k], c, per[k].d_color,
                                                              per[k].d_transmittance, opts));
             }
-            save_npy("batch_loss", std::vector<double>{loss_acc});
+            save_npy("batch_loss", std::vector<double>{loss_acc, loss_acc64});
             save_npy("batch_cameras", cams_rec, {B, 13});
             save_npy("batch_targets", tgts, {B, std::size_t(cams[views[0]].height), std::size_t(cams[views[0]].width), 3});
             for (int k = 0; k < table.subset_count(); ++k) {

@@ -42,8 +42,12 @@ def test_batch4_4k_train_step_matches_reference(tmp_path):
     cfg = engine.train_config(kd_depth=ARGS["kd"], batch_size=B)
     mgr = engine.Manager(s, cfg, engine.render_options(oracle=True))
     res = mgr.train_step(cams, targets)
-    want_loss = float(z["batch_loss"][0])
-    assert abs(res["loss"] - want_loss) <= 1e-5 * abs(want_loss), (res["loss"], want_loss)
+    # [1]: the reference's loss template in double on its own float images (its float
+    # instantiation sums 8.3M terms per view sequentially in float: ~4x off at 4K).  The GPU
+    # sums the reference's own float per-pixel terms (bit-exact) in double; the double
+    # template also evaluates the SSIM maps in double: 2e-5 relative.
+    want_loss = float(z["batch_loss"][1])
+    assert abs(res["loss"] - want_loss) <= 2e-5 * abs(want_loss), (res["loss"], want_loss, float(z["batch_loss"][0]))
     off, ids = z["kd_member_off"], z["kd_member_ids"]
     members = [ids[off[k]:off[k + 1]].astype(np.int64) for k in range(len(off) - 1)]
     bounds = oracle_step_bounds(s, members, mgr.table.planes, z["batch_cameras"], targets, True)
