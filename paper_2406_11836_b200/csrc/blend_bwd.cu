@@ -538,17 +538,24 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
         if (!((gc_zero && g.w == 0.0f) || ovf_flag[pix])) n = crec.cnt[pix];
     }
     const uint32_t base = ranges[tile].x;
-    const ushort4* rp = reinterpret_cast<const ushort4*>(crec.pos) + (size_t)tile * (kRecCap / 4) * kBlendThreads + tid;
-    ushort4 q4 = make_ushort4(0, 0, 0, 0);
+    // records of 4 contributions per load: 4 u16 list positions in one 64-bit
+    // word, consumed by shifts; the next group of 4 is loaded while the current
+    // one is walked, so the DRAM latency stays off the sub-rounds
+    const unsigned long long* rp =
+        reinterpret_cast<const unsigned long long*>(crec.pos) + (size_t)tile * (kRecCap / 4) * kBlendThreads + tid;
+    unsigned long long q4 = 0, q4n = n > 0 ? rp[0] : 0ull;
     int k = 0;
     uint32_t key = 0xffffffffu, m = 0;
     float nsc = 1.0f;  // pass 2: the next contribution's member scale, loaded with its record
     float4 A, B, D;
     auto fetch = [&]() {
         if (k < n) {
-            if ((k & 3) == 0) q4 = rp[(k >> 2) * kBlendThreads];
-            const int sel = k & 3;
-            const uint32_t r = sel == 0 ? q4.x : (sel == 1 ? q4.y : (sel == 2 ? q4.z : q4.w));
+            if ((k & 3) == 0) {
+                q4 = q4n;
+                if (k + 4 < n) q4n = rp[((k >> 2) + 1) * kBlendThreads];
+            }
+            const uint32_t r = (uint32_t)(q4 & 0xffffu);
+            q4 >>= 16;
             key = r;
             m = pair_val[base + r];
             const float4* r4 = reinterpret_cast<const float4*>(recs + m);
