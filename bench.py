@@ -436,7 +436,7 @@ def b200_arm(a, world, rank, local_rank):
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     e2e_wall = max_over_ranks((time.perf_counter() - w0) * 1e3)
 
-    # ---- deterministic = 1 (the reference default: IEEE Adam, int64 fixed-point backward sums) ----
+    # ---- deterministic = 1 (the reference default: IEEE Adam, fixed-point backward sums) ----
     cfg_det = engine.train_config(kd_depth=int(math.log2(world)), iterations=a.iterations, deterministic=1)
     ctx.set_options(ro, cfg_det)
     n_det = max(V, min(a.steps, 2 * V))
@@ -581,7 +581,7 @@ def b200_arm(a, world, rank, local_rank):
         "deterministic_mode": {"ms_per_step": det_ms, "value": px / 1e6 / (det_ms / 1e3),
                                "unit": "Mpixel/s", "steps": n_det,
                                "what": "TrainConfig::deterministic=1 (reference default): IEEE Adam op sequence and "
-                                       "int64 fixed-point backward sums (bitwise reproducible); the headline "
+                                       "fixed-point (2^-72) backward sums in one pass (bitwise reproducible); the headline "
                                        "uses deterministic=0 (fast Adam, float RED atomics)"},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,

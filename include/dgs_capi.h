@@ -76,11 +76,14 @@ typedef struct dgs_train_config {
     double lr_sh_dc, lr_sh_rest, lr_opacity, lr_scale, lr_rotation;
     double adam_beta1, adam_beta2, adam_eps;
     int32_t grad_sync;
-    /* TrainConfig::deterministic (default 1): the optimizer uses the
-     * reference's exact IEEE op sequence (bit-identical given identical
-     * gradients).  0 selects the fast Adam (reciprocal bias corrections,
-     * approximate sqrt/divide; within 2 ulp of the exact step).  Gradient
-     * accumulation uses float atomics in both modes. */
+    /* TrainConfig::deterministic (default 1, "fixed-order reductions"): the
+     * backward sums every member's pixel-space adjoints as fixed point in
+     * units of 2^-72 (order-independent integer atomics: bitwise reproducible
+     * steps; |adjoint sum| < 2^22 per member and view)
+     * and the optimizer uses the reference's exact IEEE op sequence
+     * (bit-identical given identical gradients).  0 selects float RED
+     * atomics and the fast Adam (reciprocal bias corrections, approximate
+     * sqrt/divide; within 2 ulp of the exact step). */
     int32_t deterministic;
 } dgs_train_config;
 

@@ -19,10 +19,11 @@
 // (shared-memory float atomics are CAS loops on sm_100).  Pixels skipped by
 // the reference rule (gc.isZero() && gT == 0, raster.hpp:285) never emit.
 // TrainConfig::deterministic (fixed-order reductions, optim.hpp:33;
-// parallel.hpp:23-55): the same sub-round sums are added as int64 fixed point
-// (red.global.add.u64) at a power-of-two scale per member, taken from a first
-// pass that records each member's largest adjoint and its contribution count, so every member's total is an exact integer independent
-// of the atomics' order, at a resolution relative to its own terms.
+// parallel.hpp:23-55): the same sub-round sums are added as fixed point
+// (units of 2^-72, two 64-bit words) with integer atomics (acc_add), so every member's total is an exact
+// integer independent of the atomics' order.
+#include <algorithm>
+
 #include "kernels.h"
 #include "fallback_select.cuh"
 
@@ -137,55 +138,57 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
 
 // Accumulation modes of the backward kernels:
 //   kAccFloat  float RED atomics into acc.f (TrainConfig::deterministic = 0)
-//   kAccMax    deterministic pass 1: per member the largest |adjoint| of any of
-//              its contributions (RED.MAX on the float bits) and the number of
-//              its contributions
-//   kAccFixed  deterministic pass 2: int64 fixed point into acc.q at the member's
-//              own power-of-two scale (fixed_scale), exact integer sums in any order
-constexpr int kAccFloat = 0, kAccMax = 1, kAccFixed = 2;
+//   kAccFixed  TrainConfig::deterministic = 1 ("fixed-order reductions",
+//              optim.hpp:33): every value added to a member (one sub-round's
+//              butterfly sum, itself a fixed-order float sum) is rounded once
+//              to an integer V = round(v 2^72) and added as two words with
+//              plain integer REDs: V mod 2^32 into an unsigned 64-bit word and
+//              floor(V / 2^32) into a signed one.  Integer addition is
+//              associative (the low word cannot overflow below 2^32 terms, the
+//              high word's wrap-around cancels), so every member's total is the
+//              same integer whatever order the atomics land in: bitwise
+//              reproducible, one pass, |value| < 2^22 per (member, view, field),
+//              resolution 2^-72.
+constexpr int kAccFloat = 0, kAccFixed = 2;
+constexpr int kFixedFrac = 72;
+constexpr float kFixedMax = 4194304.0f;  // 2^22
 
-/// Member m's fixed-point scale: S = 2^(62 - e) with count(m) * max|adjoint|(m)
-/// < 2^e.  Every value added for m (a sum of some of its contributions, one
-/// field) is below count x max in total, so its int64 sums cannot overflow,
-/// and their resolution is 2^-62 count of its own largest adjoint — however
-/// small the member's gradient is.
-__device__ __forceinline__ float fixed_scale(uint32_t amax_bits, uint32_t count) {
-    const float b = __uint_as_float(amax_bits) * (float)count * 1.0001f;
-    if (!(b > 0.0f) || !(b < kInf)) return 1.0f;
-    int e;
-    frexpf(b, &e);  // b < 2^e
-    return ldexpf(1.0f, max(-126, min(127, 62 - e)));
+/// v (|v| < 2^22) -> V = round(v 2^72) split as V = hi32 2^32 + lo32,
+/// lo32 in [0, 2^32), hi32 = floor(V / 2^32).  With x = |v| 2^40 (exact),
+/// H = floor(x) and L = (x - H) 2^32 are exact float operations for x >= 0
+/// (the conversion of L rounds only below 2^-72); a negative v is
+/// -(H 2^32 + L) = (-H - 1) 2^32 + (2^32 - L) for L > 0.
+__device__ __forceinline__ void to_fixed(float v, unsigned long long& lo32, long long& hi32) {
+    const float x = fabsf(v) * 0x1p40f;
+    const float fl = floorf(x);
+    const long long H = __float2ll_rn(fl);
+    const unsigned long long L = __float2ull_rn((x - fl) * 0x1p32f);  // <= 2^32
+    if (v >= 0.0f) {
+        hi32 = H + (long long)(L >> 32);
+        lo32 = L & 0xffffffffull;
+    } else {
+        hi32 = L ? -H - 1 : -H;
+        lo32 = L ? (0x100000000ull - L) : 0ull;
+    }
 }
 
-/// Pass 2's scale of member m (1 in the other modes: unused).
 template <int MODE>
-__device__ __forceinline__ float member_scale(const GradAcc& a, uint32_t m) {
-    if constexpr (MODE == kAccFixed) return fixed_scale(__ldg(a.amax + m), __ldg(a.cnt + m));
-    return 1.0f;
-}
-
-template <int MODE>
-__device__ __forceinline__ void acc_add(const GradAcc& a, int f, uint32_t mem, float v, float scale) {
-    const size_t o = (size_t)f * a.ld + mem;
+__device__ __forceinline__ void acc_add(const GradAcc& a, int f, uint32_t mem, float v, float) {
     if constexpr (MODE == kAccFloat) {
-        if (v != 0.0f) atomicAdd(a.f + o, v);
-    } else if constexpr (MODE == kAccFixed) {
-        const long long qv = __float2ll_rn(v * scale);
-        if (qv != 0) atomicAdd(a.q + o, (unsigned long long)qv);
+        if (v != 0.0f) atomicAdd(a.f + (size_t)f * a.ld + mem, v);
+    } else {
+        if (v == 0.0f) return;
+        if (!(fabsf(v) < kFixedMax)) {  // non-finite (or beyond the fixed-point range): reported
+            atomicMin(a.bad, (int)mem);
+            return;
+        }
+        unsigned long long lo;
+        long long hi;
+        to_fixed(v, lo, hi);
+        unsigned long long* q = a.q + (size_t)(2 * f) * a.ld + mem;  // [f][lo | hi][ld]
+        atomicAdd(q, lo);
+        atomicAdd(q + a.ld, (unsigned long long)hi);
     }
-}
-
-/// Pass 1 for one contribution (or a group of `n` lanes of the same member):
-/// the largest |adjoint| and the count; a non-finite adjoint flags the member.
-__device__ __forceinline__ float abs_max9(const float v[9], bool& finite) {
-    float m = 0.0f;
-    finite = true;
-#pragma unroll
-    for (int f = 0; f < 9; ++f) {
-        finite = finite && isfinite(v[f]);
-        m = fmaxf(m, fabsf(v[f]));
-    }
-    return m;
 }
 
 /// One emission sub-round's accumulation: all `go` lanes hold adjoints of the
@@ -194,32 +197,13 @@ __device__ __forceinline__ float abs_max9(const float v[9], bool& finite) {
 /// carries: 4 + 2 + 1 + 1 + 1 shuffles for fields 0-7 instead of 8 x 5)
 /// leaves the full sum of field (lane >> 2) & 7 in every lane; lanes 0, 4,
 /// ..., 28 issue the eight reductions with one RED instruction.  Field 8
-/// (d_alpha) takes a plain 5-step butterfly.  Pass 1 (kAccMax) instead takes
-/// the warp max of the lanes' largest |adjoint| (one RED.MAX per sub-round).
-/// Pass 2: `scale` is the go lanes' member scale (member_scale), fetched by the
-/// caller ahead of the sub-round so its load latency stays off this path.
+/// (d_alpha) takes a plain 5-step butterfly.  The butterfly's order is fixed
+/// by the lanes, so in deterministic mode the sums it hands to acc_add are
+/// reproducible too.
 template <int MODE>
 __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint32_t mem, const float v[9],
                                             const GradAcc& acc, float scale) {
     const int n = __popc(gm);
-    if constexpr (MODE == kAccMax) {
-        bool finite = true;
-        float m = go ? abs_max9(v, finite) : 0.0f;
-        if (go && !finite) atomicMin(acc.bad, (int)mem);
-        if (n <= 2) {
-            if (go) {
-                atomicAdd(acc.cnt + mem, 1u);
-                if (m > 0.0f && finite) atomicMax(acc.amax + mem, __float_as_uint(m));
-            }
-            return;
-        }
-        m = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(finite ? m : 0.0f)));
-        if (lane == __ffs(gm) - 1) {
-            atomicAdd(acc.cnt + mem, (uint32_t)n);
-            if (m > 0.0f) atomicMax(acc.amax + mem, __float_as_uint(m));
-        }
-        return;
-    }
     if (n <= 2) {
         if (go) {
 #pragma unroll
@@ -229,7 +213,6 @@ __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint
     }
     const int lead = __ffs(gm) - 1;
     const uint32_t mem_w = __shfl_sync(kFull, mem, lead);
-    if constexpr (MODE == kAccFixed) scale = __shfl_sync(kFull, scale, lead);
     float a0 = v[0], a1 = v[1], a2 = v[2], a3 = v[3];
     {
         const bool hi = lane & 16;
@@ -362,7 +345,6 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                 const int sl = head & (KBUF - 1);
                 const float sigma = bs[sl][tid];
                 mem = pair_val[pmin];
-                msc = member_scale<MODE>(acc, mem);
                 float4 A, B, C, D;
                 if (pmin >= base && pmin < base + (uint32_t)nb) {
                     const int j = (int)(pmin - base);
@@ -546,7 +528,6 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
     unsigned long long q4 = 0, q4n = n > 0 ? rp[0] : 0ull;
     int k = 0;
     uint32_t key = 0xffffffffu, m = 0;
-    float nsc = 1.0f;  // pass 2: the next contribution's member scale, loaded with its record
     float4 A, B, D;
     auto fetch = [&]() {
         if (k < n) {
@@ -562,7 +543,6 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
             A = __ldg(r4 + 0);
             B = __ldg(r4 + 1);
             D = __ldg(r4 + 3);
-            nsc = member_scale<MODE>(acc, m);
         } else {
             key = 0xffffffffu;
         }
@@ -589,7 +569,6 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
             const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
             contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
             mem = m;
-            msc = nsc;
             ++k;
             fetch();
         }
@@ -665,18 +644,8 @@ __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, Render
             load_rec(recs, mem, A, B, C, D);
             float v[9];
             contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
-            if (lane == 0) {
-                if constexpr (MODE == kAccMax) {
-                    bool finite = true;
-                    const float m = abs_max9(v, finite);
-                    if (!finite) atomicMin(acc.bad, (int)mem);
-                    atomicAdd(acc.cnt + mem, 1u);
-                    if (finite && m > 0.0f) atomicMax(acc.amax + mem, __float_as_uint(m));
-                } else {
-                    const float scale = MODE == kAccFixed ? fixed_scale(acc.amax[mem], acc.cnt[mem]) : 0.0f;
-                    for (int f = 0; f < 9; ++f) acc_add<MODE>(acc, f, mem, v[f], scale);
-                }
-            }
+            if (lane == 0)
+                for (int f = 0; f < 9; ++f) acc_add<MODE>(acc, f, mem, v[f], 1.0f);
             return true;
         };
         __shared__ FbRing rings[2];  // one per warp of the 64-thread block
@@ -733,15 +702,31 @@ void blend_bwd_fallback_impl(const ViewParams& vp, const RenderOpts& ro, const S
                                                       n_ovf_dev, acc);
 }
 
-/// Deterministic mode, after pass 2: g2d = q / S (S recomputed per member
-/// from pass 1's max and count; a power of two, so the division is exact
-/// before the final rounding to float).
-__global__ void k_fixed_to_float(GradAcc acc, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // member; blockIdx.y = field
-    if (i >= n) return;
-    const size_t j = (size_t)blockIdx.y * acc.ld + i;
-    const long long q = (long long)acc.q[j];
-    acc.f[j] = q == 0 ? 0.0f : (float)(__ll2double_rn(q) / (double)fixed_scale(acc.amax[i], acc.cnt[i]));
+/// Deterministic mode: g2d = (hi 2^32 + lo) 2^-72 (acc.q [9][lo | hi][ld]),
+/// then the accumulators are zeroed for the next backward (they stay zero
+/// between uses).  Two members per thread (16-byte words, ld is a multiple of
+/// 32), all 9 fields' loads issued before any store: HBM-bound.
+__global__ void __launch_bounds__(256) k_fixed_to_float(GradAcc acc, int n) {
+    const size_t ld = acc.ld;
+    const int pairs = (n + 1) >> 1;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < pairs; p += gridDim.x * blockDim.x) {
+        const size_t i = 2 * (size_t)p;
+        ulonglong2 lo[9], hi[9];
+#pragma unroll
+        for (int f = 0; f < 9; ++f) {
+            lo[f] = *reinterpret_cast<const ulonglong2*>(acc.q + (2 * f) * ld + i);
+            hi[f] = *reinterpret_cast<const ulonglong2*>(acc.q + (2 * f + 1) * ld + i);
+        }
+        const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+#pragma unroll
+        for (int f = 0; f < 9; ++f) {
+            *reinterpret_cast<ulonglong2*>(acc.q + (2 * f) * ld + i) = z;
+            *reinterpret_cast<ulonglong2*>(acc.q + (2 * f + 1) * ld + i) = z;
+            const float a = (float)(fma((double)(long long)hi[f].x, 0x1p32, (double)lo[f].x) * 0x1p-72);
+            const float b = (float)(fma((double)(long long)hi[f].y, 0x1p32, (double)lo[f].y) * 0x1p-72);
+            *reinterpret_cast<float2*>(acc.f + f * ld + i) = make_float2(a, b);
+        }
+    }
 }
 
 }  // namespace
@@ -755,16 +740,18 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
         blend_bwd_fallback_impl<kAccFloat>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, acc, s);
         return;
     }
-    // deterministic: pass 1 (max |term| and counts), pass 2 (fixed point); then launch_fixed_to_float
-    blend_bwd_impl<kAccMax>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_flag, rec, acc, nullptr, s);
-    blend_bwd_fallback_impl<kAccMax>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, acc, s);
+    // deterministic: one pass of fixed-point sums; then launch_fixed_to_float
     blend_bwd_impl<kAccFixed>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_flag, rec, acc, stats, s);
     blend_bwd_fallback_impl<kAccFixed>(vp, ro, gate, vb, fwd_ct, fwd_cd, grad_ct, ovf_list, n_ovf_dev, acc, s);
 }
 
 void launch_fixed_to_float(const GradAcc& acc, int n, cudaStream_t s) {
     if (n <= 0) return;
-    k_fixed_to_float<<<dim3((unsigned)((n + 255) / 256), 9), 256, 0, s>>>(acc, n);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pairs = (n + 1) / 2;
+    k_fixed_to_float<<<std::min((pairs + 255) / 256, sms * 8), 256, 0, s>>>(acc, n);
 }
 
 }  // namespace dgs_b200

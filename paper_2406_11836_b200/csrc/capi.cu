@@ -146,8 +146,7 @@ struct SubsetState {
     int rows = 59;
     size_t ld = 0;
     DevBuf<float> P, M, V, G, g2d, rec;
-    DevBuf<unsigned long long> g2q;  // deterministic mode: fixed-point adjoint sums [9][ld]
-    DevBuf<uint32_t> amax, cnt;      // deterministic mode: per member max |adjoint|, contributions [ld]
+    DevBuf<unsigned long long> g2q;  // deterministic mode: fixed-point adjoint sums [9][lo|hi][ld], zero between uses
     DevBuf<uint32_t> ids32;
     std::vector<uint64_t> ids64;
     uint64_t adam_step = 0, epoch = 0;
@@ -488,7 +487,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
 /// partial_render_backward for subset S, view slot v (engine.hpp:74-88) up to
 /// the pixel-space adjoints g2d (K8 + fallback).
 /// TrainConfig::deterministic ("fixed-order reductions", optim.hpp:33): the
-/// adjoints are summed as int64 fixed point in two passes (kernels.h GradAcc),
+/// adjoints are summed as fixed point (2^-72 units) in one pass (kernels.h GradAcc),
 /// then converted; a non-finite contribution is reported through ctx.bad like
 /// K9's check.
 void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
@@ -499,16 +498,12 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     acc.f = S.g2d.p;
     acc.ld = S.ld;
     if (det) {
-        S.g2q.ensure(9 * S.ld);
-        S.amax.ensure(S.ld);
-        S.cnt.ensure(S.ld);
+        if (S.g2q.p == nullptr || S.g2q.n < 18 * S.ld) {
+            S.g2q.ensure(18 * S.ld);  // launch_fixed_to_float re-zeroes it after every use
+            CK(cudaMemsetAsync(S.g2q.p, 0, 18 * S.ld * sizeof(unsigned long long), ctx.stream));
+        }
         ctx.bad.ensure(1);
-        CK(cudaMemsetAsync(S.g2q.p, 0, 9 * S.ld * sizeof(unsigned long long), ctx.stream));
-        CK(cudaMemsetAsync(S.amax.p, 0, S.ld * sizeof(uint32_t), ctx.stream));
-        CK(cudaMemsetAsync(S.cnt.p, 0, S.ld * sizeof(uint32_t), ctx.stream));
         acc.q = S.g2q.p;
-        acc.amax = S.amax.p;
-        acc.cnt = S.cnt.p;
         acc.bad = ctx.bad.p;
     } else {
         CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));

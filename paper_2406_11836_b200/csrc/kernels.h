@@ -92,18 +92,15 @@ void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
 /// Where K8 accumulates the 9 pixel-space adjoints of each member (SoA [9][ld]).
 /// q == nullptr: float RED atomics into f (order-dependent rounding).
 /// q != nullptr (TrainConfig::deterministic, "fixed-order reductions",
-/// optim.hpp:33): two passes over the same emission sub-rounds — the first
-/// records per member the largest |adjoint| of any of its contributions (amax,
-/// float bits) and its contribution count (cnt), the second adds int64 fixed
-/// point at the member's own power-of-two scale (no overflow by construction),
-/// so the totals are exact integers whatever order the atomics land in;
-/// launch_fixed_to_float converts them into f.  A non-finite contribution sets
-/// bad = min(member index).  amax, cnt and q must be zeroed by the caller.
+/// optim.hpp:33): one pass; every sub-round sum is rounded to an integer
+/// V = round(v 2^72) and added as V mod 2^32 and floor(V / 2^32) into two
+/// 64-bit words (q = [9][lo|hi][ld]), so the totals are exact integers
+/// whatever order the atomics land in; launch_fixed_to_float converts them
+/// into f and re-zeroes q.  A non-finite value (or |value| >= 2^22) sets
+/// bad = min(member index).  q must be zero on the first use.
 struct GradAcc {
     float* f = nullptr;
-    unsigned long long* q = nullptr;  // [9][ld]
-    uint32_t* amax = nullptr;         // [ld]
-    uint32_t* cnt = nullptr;          // [ld]
+    unsigned long long* q = nullptr;  // [9][2][ld]
     int* bad = nullptr;
     size_t ld = 0;
 };
@@ -117,7 +114,7 @@ void launch_blend_bwd(const ViewParams& vp, const RenderOpts& ro, const Subspace
                       const float4* fwd_ct, const double* fwd_cd, const float4* grad_ct, const uint8_t* ovf_flag,
                       const CompRecords& rec, const GradAcc& acc, const uint32_t* ovf_list,
                       const uint32_t* n_ovf_dev, BlendStats* stats, cudaStream_t s);
-// Deterministic mode: the fixed-point sums converted to float (acc.q -> acc.f, 9 rows).
+// Deterministic mode: the fixed-point sums converted to float (acc.q -> acc.f, 9 rows); q re-zeroed.
 void launch_fixed_to_float(const GradAcc& acc, int n, cudaStream_t s);
 
 // Row windows: an array "with base b and rows r" holds image rows [b, b + r)

@@ -2,11 +2,11 @@
 parallel.hpp:23-55: the reference's per-chunk GradBuffers merged in chunk
 order, so a step is bitwise reproducible).
 
-The B200 backward sums every member's 9 pixel-space adjoints as int64 fixed
-point (blend_bwd.cu GradAcc / det_scale): integer addition is associative, so
-the totals do not depend on the order the atomics land in, and they are exact
-up to one rounding per warp sub-round at a scale of ~1e-13 of the view's
-largest possible sum.
+The B200 backward sums every member's 9 pixel-space adjoints as fixed point
+in units of 2^-72 (blend_bwd.cu acc_add / to_fixed: two 64-bit words per
+value, plain integer atomics): integer addition is associative, so the totals
+do not depend on the order the atomics land in, and they are exact up to one
+rounding (2^-73) per warp sub-round.
 
 * Two runs of the same training steps are bitwise identical (gradients,
   post-Adam parameters and moments), on a scene large enough for heavy atomic
