@@ -55,6 +55,8 @@ def parse():
                     help="N > 1 exchange: NCCL over NVLink (one GPU per rank), or the host-staged gloo transport "
                          "(every rank on GPU 0: runs the N > 1 harness end to end on a single-GPU box)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-deterministic", action="store_true",
+                    help="skip the deterministic=1 timing (profiling runs: the last step is then a headline step)")
     ap.add_argument("--cpu-budget-s", type=float, default=120.0)
     return ap.parse_args()
 
@@ -437,21 +439,23 @@ def b200_arm(a, world, rank, local_rank):
     e2e_wall = max_over_ranks((time.perf_counter() - w0) * 1e3)
 
     # ---- deterministic = 1 (the reference default: IEEE Adam, fixed-point backward sums) ----
-    cfg_det = engine.train_config(kd_depth=int(math.log2(world)), iterations=a.iterations, deterministic=1)
-    ctx.set_options(ro, cfg_det)
-    n_det = max(V, min(a.steps, 2 * V))
-    step(it)  # allocates the fixed-point accumulators
-    it += 1
-    barrier()
-    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    d0.record(stream)
-    for _ in range(n_det):
-        step(it)
+    det_ms = None
+    if not a.no_deterministic:
+        cfg_det = engine.train_config(kd_depth=int(math.log2(world)), iterations=a.iterations, deterministic=1)
+        ctx.set_options(ro, cfg_det)
+        n_det = max(V, min(a.steps, 2 * V))
+        step(it)  # allocates the fixed-point accumulators
         it += 1
-    d1.record(stream)
-    torch.cuda.synchronize()
-    det_ms = max_over_ranks(d0.elapsed_time(d1)) / n_det
-    ctx.set_options(ro, cfg)
+        barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for _ in range(n_det):
+            step(it)
+            it += 1
+        d1.record(stream)
+        torch.cuda.synchronize()
+        det_ms = max_over_ranks(d0.elapsed_time(d1)) / n_det
+        ctx.set_options(ro, cfg)
 
     px = a.width * a.height
     step_ms = ms / a.steps
@@ -578,11 +582,11 @@ def b200_arm(a, world, rank, local_rank):
                 "d2h_bytes_per_step": 3 * 8 + 16 * 4, "ms_per_step_events": e2e_ms / a.steps,
                 "ms_per_step_wall": e2e_wall / a.steps},
         "step_roofline": step_roofline,
-        "deterministic_mode": {"ms_per_step": det_ms, "value": px / 1e6 / (det_ms / 1e3),
-                               "unit": "Mpixel/s", "steps": n_det,
-                               "what": "TrainConfig::deterministic=1 (reference default): IEEE Adam op sequence and "
-                                       "fixed-point (2^-72) backward sums in one pass (bitwise reproducible); the headline "
-                                       "uses deterministic=0 (fast Adam, float RED atomics)"},
+        "deterministic_mode": None if det_ms is None else {
+            "ms_per_step": det_ms, "value": px / 1e6 / (det_ms / 1e3), "unit": "Mpixel/s", "steps": n_det,
+            "what": "TrainConfig::deterministic=1 (reference default): IEEE Adam op sequence and "
+                    "fixed-point (2^-72) backward sums in one pass (bitwise reproducible); the headline "
+                    "uses deterministic=0 (fast Adam, float RED atomics)"},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes[roof_kernel], "launch_ms": t_kernel_ms},

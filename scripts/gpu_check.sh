@@ -14,6 +14,6 @@ except Exception as e:
 print(round(d["ms_per_step"], 3), "ms/step", round(d["value"], 1), "Mpx/s", "e2e", round(d["e2e"]["value"], 1))
 print(d["stages_ms_per_step"])
 s = d["step_stats"]
-print({k: s[k] for k in ("loss_last", "evals_fwd", "contribs_bwd", "overflow_pixels", "subrounds_bwd", "replay_tiles_bwd")})
+print({k: s["per_view_avg"].get(k) for k in ("evals_fwd", "contribs_bwd", "subrounds_bwd", "replay_tiles_bwd")}, s.get("loss_last"))
 PY
 tail -3 $OUT/bench.err
