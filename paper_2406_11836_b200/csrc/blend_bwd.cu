@@ -67,7 +67,7 @@ __device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewPar
     const float e0 = fsub(x0, C.x), e1 = fsub(x1, C.y), e2 = fsub(x2, C.z);
     if (dot3(e0, e1, e2, e0, e1, e2) > A.w) return false;
     if (ro.indicator_enabled && !subspace_contains(gate, x0, x1, x2)) return false;
-    const float g = glibc_expf(fmul(-0.5f, m2));  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
+    const float g = gauss_expf(m2, ro.trunc < 13.0f);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
     const float ag = fmul(A.z, g);
     const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
     if (!(sigma > 0.0f)) return false;
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
                 const float dx = fsub(pr.pxf, A.x), dy = fsub(pr.pyf, A.y);
                 const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
                                       fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
-                const float g = glibc_expf(fmul(-0.5f, m2));  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
+                const float g = gauss_expf(m2, ro.trunc < 13.0f);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
                 contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);
                 if (STATS) ++nemit;
                 ++head;
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
             const float dx = fsub(ps.pxf, A.x), dy = fsub(ps.pyf, A.y);
             const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
                                   fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
-            const float g = glibc_expf(fmul(-0.5f, m2));  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
+            const float g = gauss_expf(m2, ro.trunc < 13.0f);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
             const float ag = fmul(A.z, g);
             const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
             contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);

@@ -87,7 +87,7 @@ __device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewPar
     const float e0 = fsub(x0, C.x), e1 = fsub(x1, C.y), e2 = fsub(x2, C.z);
     if (dot3(e0, e1, e2, e0, e1, e2) > A.w) return false;
     if (ro.indicator_enabled && !subspace_contains(gate, x0, x1, x2)) return false;
-    const float g = glibc_expf(fmul(-0.5f, m2));  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
+    const float g = gauss_expf(m2, ro.trunc < 13.0f);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
     const float ag = fmul(A.z, g);
     const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;  // std::min(alpha*g, clamp)
     if (!(sigma > 0.0f)) return false;

@@ -79,15 +79,10 @@ static const uint64_t kExp2fTab[32] = {
     0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull,
 };
 
-DGS_HD float glibc_expf(float x) {
-    const uint32_t ux = f2u(x);
-    const uint32_t abstop = (ux >> 20) & 0x7ff;
-    if (abstop >= 0x42b) {  // top12(88.0f)
-        if (ux == 0xff800000u) return 0.0f;       // -inf
-        if (abstop >= 0x7f8) return x + x;       // inf or nan
-        if (x > 0x1.62e42ep6f) return u2f(0x7f800000u);  // x > log(0x1p128): overflow
-        if (x < -0x1.9fe368p6f) return 0.0f;            // x < log(0x1p-150): underflow
-    }
+/// glibc_expf's evaluation without its special cases: bit-identical to
+/// glibc_expf for |x| < 88 (top12(x) < 0x42b), the range of the blends'
+/// eval_2d argument -m^2/2 whenever truncation_radius < 13.
+DGS_HD float glibc_expf_core(float x) {
     const double N = 32.0;
     const double InvLn2N = 0x1.71547652b82fep+0 * N;
     const double SHIFT = 0x1.8p+52;
@@ -112,6 +107,25 @@ DGS_HD float glibc_expf(float x) {
     y = dfma(z, r2, y);
     y = y * s;
     return (float)y;
+}
+
+DGS_HD float glibc_expf(float x) {
+    const uint32_t ux = f2u(x);
+    const uint32_t abstop = (ux >> 20) & 0x7ff;
+    if (abstop >= 0x42b) {  // top12(88.0f)
+        if (ux == 0xff800000u) return 0.0f;       // -inf
+        if (abstop >= 0x7f8) return x + x;       // inf or nan
+        if (x > 0x1.62e42ep6f) return u2f(0x7f800000u);  // x > log(0x1p128): overflow
+        if (x < -0x1.9fe368p6f) return 0.0f;            // x < log(0x1p-150): underflow
+    }
+    return glibc_expf_core(x);
+}
+
+/// eval_2d's g = exp(-m^2/2) for 0 <= m^2 <= trunc^2: the special-case-free
+/// core when the whole range stays below |x| < 88 (the flag is uniform).
+DGS_HD float gauss_expf(float m2, bool core_ok) {
+    const float x = fmul(-0.5f, m2);
+    return core_ok ? glibc_expf_core(x) : glibc_expf(x);
 }
 
 /// math.hpp:21-24: 1/(1+exp(-x)).
