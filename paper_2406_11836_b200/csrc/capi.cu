@@ -271,6 +271,8 @@ struct Ctx {
     DevBuf<uint64_t> sh_keys;
     DevBuf<uint32_t> sh_reps, sh_starts;
     int sh_slots = 0, sh_nrep = 0;
+    DevBuf<float*> gsync_G, gsync_G2;  // grad_sync: per-subset gradient rows (by subset id / by local order)
+    DevBuf<size_t> gsync_ld, gsync_ld2;
     // cross-rank variant (world > 1): the globally sorted shared replicas
     DevBuf<uint64_t> xs_keys;                 // [S] id << 8 | k
     DevBuf<uint32_t> xs_g, xs_src, xs_pos;    // [S] global replica index, row in the gathered rows; my entries
@@ -2291,14 +2293,13 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             std::vector<size_t> gl;
             for (int k : local) {
                 SubsetState& S_ = subset(*ctx, k);
-                S_.G.ensure(S_.rows * S_.ld);
-                CK(cudaMemsetAsync(S_.G.p, 0, S_.rows * S_.ld * sizeof(float), ctx->stream));
+                S_.G.ensure(S_.rows * S_.ld);  // the first view's pullback overwrites every row
                 for (int v = 0; v < batch; ++v) {
                     ViewSlot& vs = S_.slot(v);
                     backward_blend(*ctx, S_, v, ctx->collect_stats ? ctx->stats.p + 1 : nullptr);
                     Stage st(ctx->timer, kStProjBwd, ctx->stream);
                     launch_project_bwd((int)S_.n, S_.P.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro, vs.vb.counts, S_.g2d.p,
-                                       S_.ld, S_.G.p, ctx->bad.p, ctx->stream);
+                                       S_.ld, S_.G.p, ctx->bad.p, ctx->stream, v == 0);
                     ++ctx->launches;
                 }
             }
@@ -2311,12 +2312,12 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                 gp[k] = subset(*ctx, k).G.p;
                 gl[k] = subset(*ctx, k).ld;
             }
-            DevBuf<float*> dG;
-            DevBuf<size_t> dL;
-            dG.ensure(kmax + 1);
-            dL.ensure(kmax + 1);
-            CK(cudaMemcpyAsync(dG.p, gp.data(), (kmax + 1) * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
-            CK(cudaMemcpyAsync(dL.p, gl.data(), (kmax + 1) * sizeof(size_t), cudaMemcpyHostToDevice, ctx->stream));
+            // pointer tables persist in the context (stream-ordered uploads from pageable
+            // vectors: the runtime stages them before returning, no sync needed)
+            float** dG = ctx->gsync_G.ensure(kmax + 1);
+            size_t* dL = ctx->gsync_ld.ensure(kmax + 1);
+            CK(cudaMemcpyAsync(dG, gp.data(), (kmax + 1) * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(dL, gl.data(), (kmax + 1) * sizeof(size_t), cudaMemcpyHostToDevice, ctx->stream));
             const int rows = subset(*ctx, local[0]).rows;
             if (W > 1) {
                 // G pointers in ascending local k (the order of the cross-rank replica numbering)
@@ -2326,16 +2327,14 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                     gl2.push_back(subset(*ctx, k).G.p);
                     ll2.push_back(subset(*ctx, k).ld);
                 }
-                DevBuf<float*> dG2;
-                DevBuf<size_t> dL2;
-                dG2.ensure(gl2.size());
-                dL2.ensure(ll2.size());
-                CK(cudaMemcpy(dG2.p, gl2.data(), gl2.size() * sizeof(float*), cudaMemcpyHostToDevice));
-                CK(cudaMemcpy(dL2.p, ll2.data(), ll2.size() * sizeof(size_t), cudaMemcpyHostToDevice));
-                grad_sync_multi(*ctx, rows, dG2.p, dL2.p, (int)local.size());
+                float** dG2 = ctx->gsync_G2.ensure(gl2.size());
+                size_t* dL2 = ctx->gsync_ld2.ensure(ll2.size());
+                CK(cudaMemcpyAsync(dG2, gl2.data(), gl2.size() * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
+                CK(cudaMemcpyAsync(dL2, ll2.data(), ll2.size() * sizeof(size_t), cudaMemcpyHostToDevice, ctx->stream));
+                grad_sync_multi(*ctx, rows, dG2, dL2, (int)local.size());
             } else {
-                grad_sync(ctx->sh_slots, rows, ctx->sh_starts.p, ctx->sh_nrep, ctx->sh_keys.p, ctx->sh_reps.p, dG.p,
-                          dL.p, ctx->stream);
+                grad_sync(ctx->sh_slots, rows, ctx->sh_starts.p, ctx->sh_nrep, ctx->sh_keys.p, ctx->sh_reps.p, dG, dL,
+                          ctx->stream);
             }
             ++ctx->launches;
             for (int k : local) {
@@ -2346,7 +2345,6 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                 ++ctx->launches;
                 ++S_.adam_step;
             }
-            CK(cudaStreamSynchronize(ctx->stream));  // dG / dL scoped to this block
         }
         for (int k : (sync ? std::vector<int>{} : local)) {
             SubsetState& S_ = subset(*ctx, k);

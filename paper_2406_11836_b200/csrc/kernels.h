@@ -215,9 +215,11 @@ struct AdamParams {
 // K9 (+K10): projection backward (splat.hpp:363-437) fused with dense Adam
 // (optim.hpp:104-126) when `adam` is non-null; otherwise accumulates the
 // parameter gradients into G (SoA rows).
+// overwrite: G = this view's gradients (every row of every member written, so G
+// needs no clearing); otherwise G += them.
 void launch_project_bwd(int n, const float* P, size_t ld, int sh_coeffs, const ViewParams& vp,
                         const RenderOpts& ro, const uint32_t* counts, const float* g2d, size_t ld2, float* G,
-                        int* bad_index, cudaStream_t s);
+                        int* bad_index, cudaStream_t s, bool overwrite = false);
 // g_rec: scratch of kGradRecordRows(nviews) rows x ld floats (the per-member gradient record:
 // 11 non-SH gradient rows summed over the views, then colour adjoint + direction per view).
 // shjac: the preprocess's SH colour Jacobian rows ([10][ld], ViewBins::shjac) or nullptr (read the SH rows).
