@@ -251,6 +251,11 @@ struct Ctx {
     DevBuf<float> tgt_stage;                  // host targets prefetched on copy_stream (HWC windows, all views)
     cudaStream_t copy_stream = nullptr;       // H2D of host targets, overlapped with the forward
     cudaEvent_t copy_done = nullptr;
+    // batch > 1: view v's exchange / merge / loss / merge adjoint / exchange-back
+    // chain runs on xstream while view v+1 renders on `stream`
+    cudaStream_t xstream = nullptr;
+    std::vector<cudaEvent_t> view_done;       // forward of view v finished (stream -> xstream)
+    cudaEvent_t chain_done = nullptr;         // every view's chain finished (xstream -> stream)
     // pageable host targets: a helper thread copies them into this pinned
     // buffer chunk by chunk and queues each chunk's H2D, while the forward runs
     float* pin_stage = nullptr;
@@ -603,13 +608,13 @@ int subset_owner(int k, int K, int W) { return (int)((int64_t)k * W / K); }
 /// without blocking, flush() completes every posted send and receive).
 class Xfer {
   public:
-    explicit Xfer(Ctx& ctx) : ctx_(ctx) {
-        if (ctx_.host_xfer) CK(cudaStreamSynchronize(ctx_.stream));
+    Xfer(Ctx& ctx, cudaStream_t s) : ctx_(ctx), s_(s) {
+        if (ctx_.host_xfer) CK(cudaStreamSynchronize(s_));
         else NK(nccl().GroupStart());
     }
     void send(const float* dev, size_t floats, int peer) {
         if (!ctx_.host_xfer) {
-            NK(nccl().Send(dev, floats, ncclFloat, peer, ctx_.comm, ctx_.stream));
+            NK(nccl().Send(dev, floats, ncclFloat, peer, ctx_.comm, s_));
             return;
         }
         stage_.emplace_back(floats);
@@ -619,7 +624,7 @@ class Xfer {
     }
     void recv(float* dev, size_t floats, int peer) {
         if (!ctx_.host_xfer) {
-            NK(nccl().Recv(dev, floats, ncclFloat, peer, ctx_.comm, ctx_.stream));
+            NK(nccl().Recv(dev, floats, ncclFloat, peer, ctx_.comm, s_));
             return;
         }
         stage_.emplace_back(floats);
@@ -639,6 +644,7 @@ class Xfer {
 
   private:
     Ctx& ctx_;
+    cudaStream_t s_;
     std::vector<std::vector<float>> stage_;
     std::vector<std::pair<float*, size_t>> pending_;
 };
@@ -648,13 +654,14 @@ class Xfer {
 /// all-to-all of manager.hpp:280-293's gather, sliced); single rank
 /// (virtual slices): device copies with the same layout.  Returns bytes sent
 /// over NCCL.
-uint64_t exchange_forward(Ctx& ctx, int v, const std::vector<int>& local, int Wd, int H, int S, int sl) {
+uint64_t exchange_forward(Ctx& ctx, int v, const std::vector<int>& local, int Wd, int H, int S, int sl,
+                          cudaStream_t s) {
     const int K = ctx.table.k_count, W = ctx.world, rank = ctx.rank;
     const SliceRows me = slice_rows(H, S, sl);
     const size_t hr = (size_t)(me.h1 - me.h0);
     uint64_t sent = 0;
     if (W > 1) {
-        Xfer x(ctx);
+        Xfer x(ctx, s);
         for (int k : local) {
             const float4* src = subset(ctx, k).slot(v).ct.p;
             for (int j = 0; j < W; ++j) {
@@ -674,20 +681,21 @@ uint64_t exchange_forward(Ctx& ctx, int v, const std::vector<int>& local, int Wd
     }
     for (int k : local)  // own subsets: local copy
         CK(cudaMemcpyAsync(ctx.xrecv.p + (size_t)k * hr * Wd, subset(ctx, k).slot(v).ct.p + (size_t)me.h0 * Wd,
-                           hr * Wd * sizeof(float4), cudaMemcpyDeviceToDevice, ctx.stream));
+                           hr * Wd * sizeof(float4), cudaMemcpyDeviceToDevice, s));
     return sent;
 }
 
 /// Backward exchange for slice `sl`: (dL/dC_k, dL/dT_k) rows [r0, r1) from
 /// ctx.xgrad[k] to the rank holding subset k (manager.hpp:336-343's
 /// scatter, sliced).
-uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int Wd, int H, int S, int sl) {
+uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int Wd, int H, int S, int sl,
+                           cudaStream_t s) {
     const int K = ctx.table.k_count, W = ctx.world, rank = ctx.rank;
     const SliceRows me = slice_rows(H, S, sl);
     const size_t orows = (size_t)(me.r1 - me.r0);
     uint64_t sent = 0;
     if (W > 1) {
-        Xfer x(ctx);
+        Xfer x(ctx, s);
         for (int k = 0; k < K; ++k) {
             const int o = subset_owner(k, K, W);
             if (o == rank) continue;
@@ -706,7 +714,7 @@ uint64_t exchange_backward(Ctx& ctx, int v, const std::vector<int>& local, int W
     }
     for (int k : local)
         CK(cudaMemcpyAsync(subset(ctx, k).slot(v).grad_ct.p + (size_t)me.r0 * Wd, ctx.xgrad.p + (size_t)k * orows * Wd,
-                           orows * Wd * sizeof(float4), cudaMemcpyDeviceToDevice, ctx.stream));
+                           orows * Wd * sizeof(float4), cudaMemcpyDeviceToDevice, s));
     return sent;
 }
 
@@ -869,7 +877,7 @@ std::vector<uint64_t> xfer_counts(Ctx& ctx, const std::vector<uint64_t>& send) {
     dr.ensure(W);
     CK(cudaMemcpy(ds.p, send.data(), 8 * W, cudaMemcpyHostToDevice));
     {
-        Xfer x(ctx);
+        Xfer x(ctx, ctx.stream);
         for (int d = 0; d < W; ++d)
             if (d != me) x.send(reinterpret_cast<const float*>(ds.p + d), 2, d);
         for (int r = 0; r < W; ++r)
@@ -887,7 +895,7 @@ std::vector<uint64_t> xfer_counts(Ctx& ctx, const std::vector<uint64_t>& send) {
 void xfer_alltoallv(Ctx& ctx, const std::vector<const float*>& sp, const std::vector<size_t>& sn,
                     const std::vector<float*>& rp, const std::vector<size_t>& rn) {
     const int W = ctx.world, me = ctx.rank;
-    Xfer x(ctx);
+    Xfer x(ctx, ctx.stream);
     for (int d = 0; d < W; ++d)
         if (d != me && sn[d]) x.send(sp[d], sn[d], d);
     for (int r = 0; r < W; ++r)
@@ -1167,6 +1175,8 @@ int dgs_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl
         CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hs), sizeof(HostScalars), cudaHostAllocDefault));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->chain_done, cudaEventDisableTiming));
         if (world > 1) {
             if (nccl_id == nullptr) throw std::invalid_argument("dgs_ctx_create: world > 1 needs an nccl id");
             ncclUniqueId id;
@@ -1213,6 +1223,12 @@ int dgs_ctx_destroy(dgs_ctx* ctx) {
         cudaStreamDestroy(ctx->stream);
         if (ctx->hs) cudaFreeHost(ctx->hs);
         if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+        if (ctx->xstream) {
+            cudaStreamSynchronize(ctx->xstream);
+            cudaStreamDestroy(ctx->xstream);
+        }
+        if (ctx->chain_done) cudaEventDestroy(ctx->chain_done);
+        for (cudaEvent_t e : ctx->view_done) cudaEventDestroy(e);
         if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
         delete ctx;
     });
@@ -2086,6 +2102,13 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         const float inv_batch = 1.0f / (float)batch;  // manager.hpp:329
         const int S = W > 1 ? W : std::max(1, ctx->virtual_slices);
         const bool zero_copy = (W == 1 && S == 1);
+        static const bool no_overlap = getenv("DGS_NO_VIEW_OVERLAP") != nullptr;  // A/B switch
+        const bool overlap = batch > 1 && !ctx->host_xfer && !no_overlap;
+        while (overlap && (int)ctx->view_done.size() < batch) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ctx->view_done.push_back(e);
+        }
         ctx->partial_ptrs.ensure((size_t)K);
         ctx->grad_ptrs.ensure((size_t)K);
         ctx->sums.ensure((size_t)3 * batch * S);
@@ -2189,6 +2212,15 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             }
             const int owner = table_locate(ctx->table, vp.o);
             const float* kern = ensure_kernel(*ctx);
+            // the view's exchange / merge / loss / merge-adjoint chain: on xstream when
+            // a later view's forward can run meanwhile (batch > 1; not with the
+            // host-staged test transport, whose exchanges synchronise the stream)
+            cudaStream_t cs = ctx->stream;
+            if (overlap) {
+                cs = ctx->xstream;
+                CK(cudaEventRecord(ctx->view_done[v], ctx->stream));
+                CK(cudaStreamWaitEvent(cs, ctx->view_done[v], 0));
+            }
             const std::vector<int> slices = W > 1 ? std::vector<int>{rank} : [&] {
                 std::vector<int> a(S);
                 for (int i = 0; i < S; ++i) a[i] = i;
@@ -2215,19 +2247,19 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                     }
                     prow0 = R.h0;
                     grow0 = R.r0;
-                    Stage st(ctx->timer, kStExchange, ctx->stream);
-                    nccl_bytes += exchange_forward(*ctx, v, local, Wd, H, S, sl);
+                    Stage st(ctx->timer, kStExchange, cs);
+                    nccl_bytes += exchange_forward(*ctx, v, local, Wd, H, S, sl, cs);
                 }
                 CK(cudaMemcpyAsync(ctx->partial_ptrs.p, ptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice,
-                                   ctx->stream));
+                                   cs));
                 CK(cudaMemcpyAsync(ctx->grad_ptrs.p, gptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice,
-                                   ctx->stream));
+                                   cs));
                 // ---- merge (engine.hpp:152-182) over rows [h0, h1) ----
                 ctx->merged.ensure((size_t)3 * hr * Wd);
                 {
-                    Stage st(ctx->timer, kStMerge, ctx->stream);
+                    Stage st(ctx->timer, kStMerge, cs);
                     launch_merge(vp, ctx->table_dev.p, owner, R.h0, R.h1, ctx->partial_ptrs.p, prow0, bg,
-                                 ctx->merged.p, nullptr, R.h0, hr, ctx->stream);
+                                 ctx->merged.p, nullptr, R.h0, hr, cs);
                 }
                 // ---- target window ----
                 ctx->targets_win.ensure((size_t)3 * hr * Wd);
@@ -2238,20 +2270,20 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                     for (int c = 0; c < 3; ++c)
                         CK(cudaMemcpyAsync(ctx->targets_win.p + (size_t)c * hr * Wd,
                                            targets + (size_t)v * 3 * px + (size_t)c * px + (size_t)R.h0 * Wd,
-                                           (size_t)hr * Wd * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+                                           (size_t)hr * Wd * 4, cudaMemcpyDeviceToDevice, cs));
                     tgt = ctx->targets_win.p;
                 } else {
                     if (!waited_copy) {
                         if (ctx->stager.joinable()) ctx->stager.join();
                         if (!ctx->stager_err.empty()) throw std::runtime_error(ctx->stager_err);
-                        CK(cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
+                        CK(cudaStreamWaitEvent(cs, ctx->copy_done, 0));
                         waited_copy = true;
                     }
                     // window rows [h0, h1) inside the prefetched window (which starts at
                     // row 0 for a single rank, at this rank's halo start otherwise)
                     const int base_row = my_slice >= 0 ? slice_rows(H, S, my_slice).h0 : 0;
                     const float* src = ctx->tgt_stage.p + (size_t)v * tgt_win + (size_t)(R.h0 - base_row) * Wd * 3;
-                    k_hwc_to_planar<<<(unsigned)(((size_t)hr * Wd + 255) / 256), 256, 0, ctx->stream>>>(
+                    k_hwc_to_planar<<<(unsigned)(((size_t)hr * Wd + 255) / 256), 256, 0, cs>>>(
                         src, ctx->targets_win.p, (size_t)hr * Wd);
                     ++ctx->launches;
                     tgt = ctx->targets_win.p;
@@ -2262,24 +2294,28 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                 ctx->block_sums.ensure((size_t)max_blocks * 3);
                 int nb = 0;
                 {
-                    Stage st(ctx->timer, kStLoss, ctx->stream);
+                    Stage st(ctx->timer, kStLoss, cs);
                     launch_loss(Wd, H, R.r0, R.r1, R.h0, hr, ctx->merged.p, tgt, lam, kern, inv_batch,
-                                ctx->grad_rgb.p, ctx->block_sums.p, &nb, ctx->stream);
-                    launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p + (size_t)3 * (v * S + sl), ctx->stream);
+                                ctx->grad_rgb.p, ctx->block_sums.p, &nb, cs);
+                    launch_reduce_sums(ctx->block_sums.p, nb, ctx->sums.p + (size_t)3 * (v * S + sl), cs);
                 }
                 // ---- merge_backward (engine.hpp:195-234) on owned rows ----
                 {
-                    Stage st(ctx->timer, kStMergeBwd, ctx->stream);
+                    Stage st(ctx->timer, kStMergeBwd, cs);
                     launch_merge_bwd(vp, ctx->table_dev.p, owner, R.r0, R.r1, ctx->partial_ptrs.p, prow0,
-                                     ctx->grad_rgb.p, R.h0, hr, bg, ctx->grad_ptrs.p, grow0, ctx->stream);
+                                     ctx->grad_rgb.p, R.h0, hr, bg, ctx->grad_ptrs.p, grow0, cs);
                 }
                 ctx->launches += 4;
                 // ---- backward exchange: (dL/dC_k, dL/dT_k) rows [r0, r1) -> subset owners ----
                 if (!zero_copy) {
-                    Stage st(ctx->timer, kStExchange, ctx->stream);
-                    nccl_bytes += exchange_backward(*ctx, v, local, Wd, H, S, sl);
+                    Stage st(ctx->timer, kStExchange, cs);
+                    nccl_bytes += exchange_backward(*ctx, v, local, Wd, H, S, sl, cs);
                 }
             }
+        }
+        if (overlap) {  // every view's chain precedes the backward
+            CK(cudaEventRecord(ctx->chain_done, ctx->xstream));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->chain_done, 0));
         }
         // ---- MsgBackwardTask x B, then apply_step (worker.hpp:86-127, 162-167) ----
         reset_bad(*ctx);
