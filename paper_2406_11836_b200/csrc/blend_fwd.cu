@@ -23,6 +23,10 @@ namespace dgs_b200 {
 namespace {
 
 constexpr int KBUF = 8;  // ring capacity (power of two); must equal blend_bwd.cu
+#ifndef DGS_EMIT_EVERY
+#define DGS_EMIT_EVERY 4
+#endif
+constexpr int kEmitEvery = DGS_EMIT_EVERY;  // candidates between emission checks (power of two)
 constexpr float kInf = __builtin_huge_valf();
 // 4 staged float4 record fields + 4 ring fields per pixel (t, id, sigma, member).
 constexpr size_t kFwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float) +
@@ -339,13 +343,24 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fwd(ViewParams vp, R
         for (int qq = 0; qq < nlist && !done; ++qq) {
             const int j = wlist[qq];
             const float4 D = sD[j];
-            while (head_t < D.w && !done) emit_head();
+            // Emission is deferred to every kEmitEvery-th candidate (qq is uniform over the
+            // warp, so the lanes emit together instead of one divergent loop per candidate)
+            // or to a (nearly) full ring.  Emitting later is exact: an entry with t below the
+            // bound of a list position stays below every later bound, and nothing inserted
+            // later can precede it; the sequence, its termination point and the overflow
+            // decision (full ring with nothing emittable) are those of eager emission.
+            if ((qq & (kEmitEvery - 1)) == 0 || cnt >= KBUF - 1)
+                while (head_t < D.w && !done) emit_head();
             if (done) break;
             const float4 A = sA[j], B = sB[j], C = sC[j];
             if (STATS) ++n_eval;
             float t, sigma, g;
             if (!eval_candidate(pr, vp, ro, gate, A, B, C, D.w, t, sigma, g)) continue;
             const uint32_t id = __float_as_uint(C.w);
+            if (cnt == KBUF) {
+                while (head_t < D.w && !done) emit_head();
+                if (done) break;
+            }
             if (cnt == KBUF) {  // ring full and nothing safe to emit: exact fallback
                 ovf = true;
                 done = true;
