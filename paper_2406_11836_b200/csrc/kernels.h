@@ -212,6 +212,11 @@ struct AdamParams {
     int exact;                // 1: reference IEEE op sequence (TrainConfig::deterministic)
 };
 
+// K10: the streaming dense Adam over the gradient record (launch_project_bwd_adam
+// runs it after the last view's K9).
+void launch_adam_record(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, int deg, int nviews,
+                        const AdamParams& ap, const float* rec, cudaStream_t s);
+
 // K9 (+K10): projection backward (splat.hpp:363-437) fused with dense Adam
 // (optim.hpp:104-126) when `adam` is non-null; otherwise accumulates the
 // parameter gradients into G (SoA rows).
