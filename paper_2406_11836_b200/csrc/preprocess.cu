@@ -27,22 +27,27 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
     constexpr int ROWS = kRowSh + 3 * SHC;
     constexpr int sh_coeffs = SHC;
     __shared__ __align__(128) float tile[ROWS * kPreTB];
-    __shared__ uint64_t bar;
+    // two mbarriers: the 11 geometry rows, then the SH rows, so the projection
+    // math starts while the SH rows (81 % of the bytes) are still in flight
+    __shared__ uint64_t bar[2];
     const int tid = threadIdx.x;
     const int i0 = blockIdx.x * kPreTB;
     const int i = i0 + tid;
     const int cnt = min(kPreTB, n - i0);
     const uint32_t bytes = (uint32_t)((cnt + 3) / 4) * 16u;
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (tid == 0) {
-        mbar_expect_tx(&bar, (uint32_t)ROWS * bytes);
-        for (int r = 0; r < ROWS; ++r) bulk_g2s(tile + r * kPreTB, P + (size_t)r * ld + i0, bytes, &bar);
+        mbar_expect_tx(&bar[0], (uint32_t)kRowSh * bytes);
+        for (int r = 0; r < kRowSh; ++r) bulk_g2s(tile + r * kPreTB, P + (size_t)r * ld + i0, bytes, &bar[0]);
+        mbar_expect_tx(&bar[1], (uint32_t)(ROWS - kRowSh) * bytes);
+        for (int r = kRowSh; r < ROWS; ++r) bulk_g2s(tile + r * kPreTB, P + (size_t)r * ld + i0, bytes, &bar[1]);
     }
-    mbar_wait(&bar, 0);
+    mbar_wait(&bar[0], 0);
     float dmax_local = 0.0f, rmin_local = __int_as_float(0x7f7fffff);
     if (i < n) {
         auto row = [&](int r) { return tile[r * kPreTB + tid]; };
@@ -140,6 +145,7 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
                 vb.rect[2 * (size_t)i] = (uint32_t)x0 | ((uint32_t)x1 << 16);
                 vb.rect[2 * (size_t)i + 1] = (uint32_t)y0 | ((uint32_t)y1 << 16);
                 vb.counts[i] = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+                mbar_wait(&bar[1], 0);  // the SH rows
                 // SH colour toward the camera centre (splat.hpp:315-317)
                 const float v0 = fsub(mu0, vp.o[0]), v1 = fsub(mu1, vp.o[1]), v2 = fsub(mu2, vp.o[2]);
                 const float n2 = dot3(v0, v1, v2, v0, v1, v2);
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
             vb.rkey[i] = 0xffffffffu;
         }
     }
+    mbar_wait(&bar[1], 0);  // no CTA exits with its bulk copy in flight
     // block max of D and min of the range over visible members -> one atomic each per block
     // (and the max range, which sizes the binning's 16-bit range buckets)
     __shared__ float s_max[kPreTB / 32], s_min[kPreTB / 32], s_hi[kPreTB / 32];
