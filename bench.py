@@ -55,6 +55,9 @@ def parse():
                     help="N > 1 exchange: NCCL over NVLink (one GPU per rank), or the host-staged gloo transport "
                          "(every rank on GPU 0: runs the N > 1 harness end to end on a single-GPU box)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="on", choices=["on", "off"],
+                    help="train steps as CUDA graph replays (single rank; dgs_set_graph_mode); the eager step is "
+                         "timed beside it")
     ap.add_argument("--no-deterministic", action="store_true",
                     help="skip the deterministic=1 timing (profiling runs: the last step is then a headline step)")
     ap.add_argument("--cpu-budget-s", type=float, default=120.0)
@@ -380,6 +383,20 @@ def b200_arm(a, world, rank, local_rank):
         r = step(it)
         first = first or r
         it += 1
+    # CUDA graph mode (single rank): every view's step is captured once it has run
+    # eagerly (the capture needs its pair counts); priming = two untimed steps per view
+    use_graph = a.graph == "on" and world == 1 and hasattr(engine.lib(), "dgs_set_graph_mode")
+    n_prime = 2 * V if use_graph else 0
+
+    def prime(host=None):
+        nonlocal it
+        for _ in range(n_prime):
+            step(it, host)
+            it += 1
+
+    if use_graph:
+        ctx.set_graph_mode(True)
+        prime()
     barrier()
 
     # ---- device-resident timed region (no per-stage events inside) ------------
@@ -398,6 +415,20 @@ def b200_arm(a, world, rank, local_rank):
     clk = clocks.stop()
     ms = max_over_ranks(ms_local)
     rank_ms = gather_ranks(ms_local)
+
+    # ---- the same K steps eager (no graph), for comparison ----
+    eager_ms = None
+    if use_graph:
+        ctx.set_graph_mode(False)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(a.steps):
+            step(it)
+            it += 1
+        g1.record(stream)
+        torch.cuda.synchronize()
+        eager_ms = max_over_ranks(g0.elapsed_time(g1)) / a.steps
 
     # ---- per-stage breakdown (separate run: CUDA events around every stage) ----
     n_prof = max(V, min(a.steps, 2 * V))
@@ -424,6 +455,7 @@ def b200_arm(a, world, rank, local_rank):
     host_targets = pinned.numpy().reshape(V, a.height, a.width, 3)
     step(it, host_targets)
     it += 1
+    # (the e2e steps run eagerly: with host targets the graph's copy node measured ~1.5 % slower)
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
@@ -446,6 +478,9 @@ def b200_arm(a, world, rank, local_rank):
         n_det = max(V, min(a.steps, 2 * V))
         step(it)  # allocates the fixed-point accumulators
         it += 1
+        if use_graph:  # new options: new graphs
+            ctx.set_graph_mode(True)
+            prime()
         barrier()
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record(stream)
@@ -582,6 +617,12 @@ def b200_arm(a, world, rank, local_rank):
                 "d2h_bytes_per_step": 3 * 8 + 16 * 4, "ms_per_step_events": e2e_ms / a.steps,
                 "ms_per_step_wall": e2e_wall / a.steps},
         "step_roofline": step_roofline,
+        "graph": None if eager_ms is None else {
+            "ms_per_step": step_ms, "ms_per_step_eager": eager_ms, "speedup": eager_ms / step_ms,
+            "what": "the timed steps (and the deterministic ones) replay one CUDA graph per view: no host round trip "
+                    "inside a step (pair counts stay on the device, the tile sort covers each slot's largest "
+                    "count + 2 %); ms_per_step_eager = the same K steps launched eagerly",
+            "priming_steps_per_phase": n_prime},
         "deterministic_mode": None if det_ms is None else {
             "ms_per_step": det_ms, "value": px / 1e6 / (det_ms / 1e3), "unit": "Mpixel/s", "steps": n_det,
             "what": "TrainConfig::deterministic=1 (reference default): IEEE Adam op sequence and "

@@ -324,6 +324,14 @@ int dgs_stage_times(dgs_ctx* ctx, double* ms, uint64_t* counts);
 void* dgs_stream(dgs_ctx* ctx);
 /* Device synchronise + sticky-error check. */
 int dgs_sync(dgs_ctx* ctx);
+/* 1: dgs_train_step runs as a CUDA graph (single rank, device or pinned host
+ * targets, stage timing and counters off, grad_sync off; otherwise eager).
+ * Per key (cameras, target pointer, background): the first call runs eagerly,
+ * the second captures the step without any host round trip (the pair counts
+ * stay on the device and the tile sort covers each slot's largest count
+ * + 2 %) and replays it; later calls replay.  Results are those of the eager
+ * step; a replay whose pair count outgrew the capture is redone eagerly. */
+int dgs_set_graph_mode(dgs_ctx* ctx, int32_t enabled);
 
 #ifdef __cplusplus
 }

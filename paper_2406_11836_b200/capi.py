@@ -156,6 +156,7 @@ _SIGS = {
     "dgs_dump_grad_maps": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
     "dgs_stream": (_P, [_P]),
     "dgs_sync": (C.c_int, [_P]),
+    "dgs_set_graph_mode": (C.c_int, [_P, C.c_int32]),
 }
 
 STAGES = ("preprocess", "binning", "blend_fwd", "merge", "loss", "merge_bwd", "blend_bwd", "project_bwd", "adam",
@@ -172,6 +173,8 @@ def lib() -> C.CDLL:
             raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
         L = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("DGS_LIB") and not hasattr(L, name):
+                continue  # an older build under A/B timing (DGS_LIB): entry points it lacks stay unbound
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -61,9 +61,13 @@ __global__ void k_gather_sorted_rects(const uint32_t* __restrict__ sorted_idx, c
 /// so every store instruction writes 32 consecutive words.
 __global__ void k_emit_pairs(const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ offsets,
                              const uint32_t* __restrict__ cnt_sorted, const uint2* __restrict__ rect_sorted,
-                             int tiles_x, int n, uint16_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_val) {
+                             int tiles_x, int n, uint16_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_val,
+                             uint32_t cap, int* __restrict__ abort) {
+    // cap / abort (graph-captured steps, the pair count is not read back): slots
+    // beyond the capacity are dropped and the step's abort flag is raised
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    if (abort != nullptr && j == 0 && offsets[n - 1] > cap) atomicOr(abort, 2);
     uint32_t i = 0, c = 0, off = 0, x0 = 0, w = 1, y0 = 0;
     if (j < n) {
         i = sorted_idx[j];
@@ -100,7 +104,7 @@ __global__ void k_emit_pairs(const uint32_t* __restrict__ sorted_idx, const uint
         const uint32_t mx0 = __shfl_sync(0xffffffffu, x0, lo);
         const uint32_t mw = __shfl_sync(0xffffffffu, w, lo);
         const uint32_t my0 = __shfl_sync(0xffffffffu, y0, lo);
-        if (q < total) {
+        if (q < total && base + q < cap) {
             const uint32_t r = q - ex;
             // r / mw by a float reciprocal: (r + 0.5) / mw <= tiles_y stays >= 0.5 / mw away from
             // an integer, far beyond the float error (r, mw < 2^16)
@@ -156,6 +160,14 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
         const uint2 r = ranges[t];
         order[atomicAdd(&start[bucket(r.y - r.x)], 1u)] = (uint32_t)t;
     }
+}
+
+/// Graph-captured steps sort a fixed capacity: the slots after the device-side
+/// pair count get the tile key 0xffff, above every tile, so they sort last.
+__global__ void k_pad_pairs(const uint32_t* __restrict__ P_dev, uint32_t cap, uint16_t* __restrict__ pair_tile) {
+    const uint32_t P = min(*P_dev, cap);
+    for (uint32_t q = P + blockIdx.x * blockDim.x + threadIdx.x; q < cap; q += gridDim.x * blockDim.x)
+        pair_tile[q] = 0xffffu;
 }
 
 /// Per-tile [start, end) by binary search over the sorted tile keys (one thread per tile).
@@ -222,7 +234,7 @@ size_t binning_temp_bytes(int n, int64_t pair_cap) {
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
                     uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
                     uint32_t* pair_val_alt, uint32_t* scan_buf, uint2* rect_sorted, uint32_t* pairs_host,
-                    cudaStream_t s) {
+                    cudaStream_t s, int64_t pad_cap) {
     const int tiles = vp.tiles_x * vp.tiles_y;
     cudaMemsetAsync(vb.ranges, 0, sizeof(uint2) * tiles, s);
     vb.pairs = 0;
@@ -251,6 +263,28 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
                                                cnt_sorted, n);
     tb = temp_bytes;
     cub::DeviceScan::InclusiveSum(temp, tb, cnt_sorted, scan_buf, n, s);
+    if (pad_cap > 0) {
+        // graph-captured step: no readback; the pair count stays on the device
+        // (scan_buf[n-1]) and the tile sort runs over pad_cap slots, the tail padded
+        // with key 0xffff (sorted last, never inside a tile range); a count above
+        // pad_cap raises the step's abort flag (the caller re-runs the step)
+        const uint32_t pc = (uint32_t)pad_cap;
+        k_emit_pairs<<<grid, blk, 0, s>>>(sorted_idx, scan_buf, cnt_sorted, rect_sorted, vp.tiles_x, n, vb.pair_tile,
+                                          vb.pair_val, pc, vb.abort);
+        k_pad_pairs<<<148 * 4, 256, 0, s>>>(scan_buf + (n - 1), pc, vb.pair_tile);
+        cub::DoubleBuffer<uint16_t> dk(vb.pair_tile, pair_tile_alt);
+        cub::DoubleBuffer<uint32_t> dv(vb.pair_val, pair_val_alt);
+        tb = temp_bytes;
+        cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, (int)pc, 0, 16, s);
+        if (dk.Current() != vb.pair_tile) {
+            cudaMemcpyAsync(vb.pair_tile, dk.Current(), 2 * (size_t)pc, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(vb.pair_val, dv.Current(), 4 * (size_t)pc, cudaMemcpyDeviceToDevice, s);
+        }
+        k_tile_ranges<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(vb.pair_tile, pc, tiles, vb.ranges);
+        tile_order();
+        vb.pairs = -1;  // known after the replay (scan_buf[n-1])
+        return pad_cap;
+    }
     // the one host round trip of the step's forward: the pair count sizes the
     // tile sort (pinned readback; the caller's pending readbacks ride along)
     cudaMemcpyAsync(pairs_host, scan_buf + (n - 1), 4, cudaMemcpyDeviceToHost, s);
@@ -264,7 +298,7 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
     }
     // 3) emit (tile, member) pairs, range-ordered within every tile
     k_emit_pairs<<<grid, blk, 0, s>>>(sorted_idx, scan_buf, cnt_sorted, rect_sorted, vp.tiles_x, n, vb.pair_tile,
-                                      vb.pair_val);  // scan_buf holds inclusive ends: start = end - count
+                                      vb.pair_val, 0xffffffffu, nullptr);  // scan_buf: inclusive ends
     // 4) stable LSD radix sort by tile id only
     cub::DoubleBuffer<uint16_t> dk(vb.pair_tile, pair_tile_alt);
     cub::DoubleBuffer<uint32_t> dv(vb.pair_val, pair_val_alt);

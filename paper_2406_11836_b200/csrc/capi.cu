@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -85,6 +86,9 @@ const NcclApi& nccl() {
     return api;
 }
 
+/// Bumped whenever any device buffer is (re)allocated or freed.
+std::atomic<uint64_t> g_buffer_epoch{0};
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -93,10 +97,14 @@ struct DevBuf {
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaFree(p);
+            g_buffer_epoch.fetch_add(1);
+        }
     }
     T* ensure(size_t count) {
         if (count > n || p == nullptr) {
+            g_buffer_epoch.fetch_add(1);  // captured step graphs hold device pointers: they must be re-captured
             if (p) CK(cudaFree(p));
             p = nullptr;
             const size_t c = std::max<size_t>(count, 1);
@@ -134,6 +142,8 @@ struct ViewSlot {
         return r;
     }
     int64_t pair_cap = 0;
+    int64_t pairs_max = 0;  // largest pair count of the eager steps (sizes graph_cap)
+    int64_t graph_cap = 0;  // pair slots sorted by a captured step (<= pair_cap)
     size_t temp_bytes = 0;
     ViewBins vb;
     ViewParams vp{};
@@ -150,6 +160,7 @@ struct SubsetState {
     DevBuf<uint32_t> ids32;
     std::vector<uint64_t> ids64;
     uint64_t adam_step = 0, epoch = 0;
+
     std::vector<std::unique_ptr<ViewSlot>> slots;
     ViewSlot& slot(int v) {
         while ((int)slots.size() <= v) slots.emplace_back(new ViewSlot());
@@ -157,6 +168,21 @@ struct SubsetState {
     }
 };
 
+/// Pinned host block the step's results land in (one per context, fixed
+/// capacity so a captured graph's copy targets never move).
+constexpr int kTailMaxBatch = 64, kTailMaxSlices = 64, kTailMaxLocal = 64;
+struct StepTail {
+    double sums[3 * kTailMaxBatch * kTailMaxSlices];
+    size_t nsums = 0;
+    BlendStats st[2];
+    int bad = INT_MAX, abort = 0;
+    uint32_t ovf[kTailMaxLocal * kTailMaxBatch], pairs[kTailMaxLocal * kTailMaxBatch],
+        visible[kTailMaxLocal * kTailMaxBatch];
+    int err[kTailMaxLocal * kTailMaxBatch];
+    double px[kTailMaxBatch];
+    int batch = 0, slices = 0, nlocal = 0;
+    uint64_t nccl_bytes = 0, launches = 0, comm_bytes = 0;
+};
 /// Event pairs around every stage launch, resolved at the next sync point.
 struct StageTimer {
     static constexpr int kStages = 10;
@@ -254,6 +280,39 @@ struct Ctx {
     // batch > 1: view v's exchange / merge / loss / merge adjoint / exchange-back
     // chain runs on xstream while view v+1 renders on `stream`
     cudaStream_t xstream = nullptr;
+    DevBuf<int> abort;                        // per step: non-zero makes K10 skip (zero quaternion, pair overflow)
+    bool capturing = false;                   // the step is being recorded into a CUDA graph (no host round trips)
+    StepTail* tail = nullptr;                 // pinned: the step's results (train_step_body / finish_step)
+    // dgs_set_graph_mode: train steps replayed as CUDA graphs, one per (views, targets, bg) key
+    bool graph_mode = false;
+    uint64_t graph_version = 0;               // bumped by every call that changes what a step launches
+    struct CachedStep {
+        std::vector<uint8_t> key;
+        cudaGraph_t graph = nullptr;  // kept: its K10 nodes get this step's AdamParams at every replay
+        cudaGraphExec_t exec = nullptr;
+        std::vector<void*> arena;  // pinned sources its memcpy nodes read at every replay
+        struct AdamNode {
+            cudaGraphNode_t node;
+            int subset, ap_index;
+        };
+        std::vector<AdamNode> adam;
+    };
+    std::vector<CachedStep> graphs;
+    std::vector<std::vector<uint8_t>> warmed;  // keys with one eager step done (pair maxima learnt)
+    std::vector<void*> arena;                  // pinned sources of the graph being captured (h2d)
+    static void free_step(CachedStep& g) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+        g.graph = nullptr;
+        for (void* p : g.arena) cudaFreeHost(p);
+        g.exec = nullptr;
+        g.arena.clear();
+    }
+    void drop_graphs() {
+        for (auto& g : graphs) free_step(g);
+        graphs.clear();
+        warmed.clear();
+    }
     std::vector<cudaEvent_t> view_done;       // forward of view v finished (stream -> xstream)
     cudaEvent_t chain_done = nullptr;         // every view's chain finished (xstream -> stream)
     // pageable host targets: a helper thread copies them into this pinned
@@ -383,6 +442,23 @@ void download_fields(Ctx& ctx, SubsetState& S, const float* src, dgs_splats* f) 
     }
 }
 
+/// Host->device copy of a small step-time value.  Eager: straight (a pageable
+/// source is staged by the runtime before the call returns).  While a step is
+/// being captured the value goes through a pinned block owned by that graph: a
+/// memcpy node reads its source at every replay, so the source must outlive
+/// the capture and keep this value.
+void h2d(Ctx& ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (!ctx.capturing) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    void* p = nullptr;
+    CK(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+    ctx.arena.push_back(p);
+    std::memcpy(p, src, bytes);
+    CK(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+}
+
 /// partial_render for local subset S into view slot v (engine.hpp:44-52):
 /// K1 projection, K2 binning, K4 blend (+ exact fallback).
 void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int dbg_cap = 0,
@@ -404,6 +480,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     vb.dmax_bits = vs.dmax.ensure(4);
     vb.blk_part = vs.blkp.ensure(preprocess_partials((int)n));
     vb.err_index = vs.err.ensure(1);
+    vb.abort = ctx.abort.ensure(1);
     vb.ranges = vs.ranges.ensure(tiles);
     vb.tile_order = vs.tile_order.ensure(tiles);
     vs.sort_keys_alt.ensure(n);
@@ -427,23 +504,44 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     };
     alloc_pairs();
     const uint32_t dmax0[4] = {0u, 0x7f7fffffu, 0u, 0u};  // (max D, min range, visible count, max range)
-    CK(cudaMemcpyAsync(vb.dmax_bits, dmax0, sizeof(dmax0), cudaMemcpyHostToDevice, ctx.stream));
+    h2d(ctx, vb.dmax_bits, dmax0, sizeof(dmax0), ctx.stream);
     const int int_max = INT_MAX;
-    CK(cudaMemcpyAsync(vb.err_index, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));
+    h2d(ctx, vb.err_index, &int_max, 4, ctx.stream);
     CK(cudaMemsetAsync(vs.ovf_count.p, 0, 4, ctx.stream));
     {
         Stage st(ctx.timer, kStPre, ctx.stream);
         launch_preprocess((int)n, S.P.p, S.ld, S.sh_coeffs, S.ids32.p, vp, ctx.ro, vb, ctx.stream);
     }
     ctx.launches += 2;
+    const bool capture = ctx.capturing;
+    if (capture && n > 0) {
+        // graph capture: no host round trip.  The pair count stays on the device and
+        // the tile sort runs over the slot's graph capacity (learnt from the eager
+        // steps); the zero-quaternion check and the visible count are read after
+        // the replay (a zero quaternion or a pair overflow raises ctx.abort, which
+        // keeps K10 from applying the step)
+        if (vs.graph_cap <= 0 || vs.graph_cap > vs.pair_cap) throw std::logic_error("graph capture: no pair capacity");
+        Stage st_bin(ctx.timer, kStBin, ctx.stream);
+        run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
+                    vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, vs.rect_sorted.ensure(n),
+                    &ctx.hs->pairs, ctx.stream, vs.graph_cap);
+        ctx.launches += 3;
+    }
     // zero-quaternion flag: rides along with the binning's pair-count readback
-    CK(cudaMemcpyAsync(&ctx.hs->err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
-    CK(cudaMemcpyAsync(&ctx.hs->visible, vb.dmax_bits + 2, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    if (!capture) {
+        CK(cudaMemcpyAsync(&ctx.hs->err, vb.err_index, 4, cudaMemcpyDeviceToHost, ctx.stream));
+        CK(cudaMemcpyAsync(&ctx.hs->visible, vb.dmax_bits + 2, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    }
     Stage st_bin(ctx.timer, kStBin, ctx.stream);
-    int64_t P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p,
-                            vs.sort_vals.p, vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p,
-                            vs.rect_sorted.ensure(n), &ctx.hs->pairs, ctx.stream);
-    ctx.launches += 3;
+    int64_t P = 0;
+    if (!capture) {
+        P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
+                        vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, vs.rect_sorted.ensure(n),
+                        &ctx.hs->pairs, ctx.stream);
+        ctx.launches += 3;
+        // the graph capacity of this slot: the largest pair count seen, plus 2 %
+        vs.pairs_max = std::max<int64_t>(vs.pairs_max, P < 0 ? -P : P);
+    }
     if (P < 0) {
         vs.pair_cap = (-P) + (-P) / 4 + 1024;
         alloc_pairs();
@@ -454,9 +552,11 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         if (P < 0) throw std::runtime_error("binning: pair buffer sizing failed");
     }
     st_bin.end();
-    if (n <= 0) CK(cudaStreamSynchronize(ctx.stream));  // run_binning synced otherwise
-    if (ctx.hs->err != INT_MAX) throw std::domain_error("zero quaternion");
-    vb.visible = n > 0 ? ctx.hs->visible : 0;
+    if (!capture) {
+        if (n <= 0) CK(cudaStreamSynchronize(ctx.stream));  // run_binning synced otherwise
+        if (ctx.hs->err != INT_MAX) throw std::domain_error("zero quaternion");
+        vb.visible = n > 0 ? ctx.hs->visible : 0;
+    }
     // Composite records need tiles x 256 x kRecCap x 2 bytes per (subset, view)
     // slot (1.07 GB at 1080p, 4.2 GB at 4K).  A slot whose records would take
     // more than a quarter of the free HBM falls back to the ring-replay
@@ -552,6 +652,15 @@ AdamParams adam_params(const Ctx& ctx, const SubsetState& S, uint64_t step_after
     return ap;
 }
 
+/// K10's launch arguments for subset S this step: its AdamParams and the step's abort flag.
+AdamArgs adam_args(Ctx& ctx, SubsetState& S, const int* abort) {
+    AdamArgs a;
+    a.ap = adam_params(ctx, S, S.adam_step + 1);
+    a.exact = a.ap.exact;
+    a.abort = abort;
+    return a;
+}
+
 void check_bad(Ctx& ctx, SubsetState& S) {
     int bad = INT_MAX;
     CK(cudaMemcpyAsync(&bad, ctx.bad.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
@@ -564,7 +673,7 @@ void check_bad(Ctx& ctx, SubsetState& S) {
 void reset_bad(Ctx& ctx) {
     ctx.bad.ensure(1);
     const int int_max = INT_MAX;
-    CK(cudaMemcpyAsync(ctx.bad.p, &int_max, 4, cudaMemcpyHostToDevice, ctx.stream));
+    h2d(ctx, ctx.bad.p, &int_max, 4, ctx.stream);
 }
 
 const float* ensure_kernel(Ctx& ctx) {
@@ -1222,6 +1331,8 @@ int dgs_ctx_destroy(dgs_ctx* ctx) {
         ctx->subsets.clear();
         cudaStreamDestroy(ctx->stream);
         if (ctx->hs) cudaFreeHost(ctx->hs);
+        ctx->drop_graphs();
+        if (ctx->tail) cudaFreeHost(ctx->tail);
         if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
         if (ctx->xstream) {
             cudaStreamSynchronize(ctx->xstream);
@@ -1268,6 +1379,7 @@ int dgs_sync(dgs_ctx* ctx) {
 
 int dgs_set_table(dgs_ctx* ctx, const dgs_plane* planes, int32_t k_count, int32_t ppk) {
     return dgs_guard([&] {
+        if (ctx) ++ctx->graph_version;  // captured step graphs no longer match
         if (k_count < 1 || k_count > kMaxSubsets) throw std::invalid_argument("set_table: 1..32 subsets supported");
         if (ppk < 0 || ppk > kMaxPlanes) throw std::invalid_argument("set_table: at most 8 planes per subspace");
         Table t{};
@@ -1299,6 +1411,7 @@ int dgs_set_epoch(dgs_ctx* ctx, uint64_t epoch) {
 
 int dgs_set_options(dgs_ctx* ctx, const dgs_render_options* ro, const dgs_train_config* cfg) {
     return dgs_guard([&] {
+        if (ctx) ++ctx->graph_version;  // captured step graphs no longer match
         if (ro) {
             ctx->ro_in = *ro;
             ctx->ro = to_render_opts(*ro);
@@ -1318,6 +1431,7 @@ int dgs_set_options(dgs_ctx* ctx, const dgs_render_options* ro, const dgs_train_
 int dgs_subset_load(dgs_ctx* ctx, int32_t k, const dgs_splats* params, const dgs_splats* m, const dgs_splats* v,
                     uint64_t adam_step, uint64_t epoch) {
     return dgs_guard([&] {
+        if (ctx) ++ctx->graph_version;  // captured step graphs no longer match
         require_table(*ctx);
         if (k < 0 || k >= ctx->table.k_count) throw std::invalid_argument("subset_load: k outside the table");
         if (params->sh_coeffs != 1 && params->sh_coeffs != 4 && params->sh_coeffs != 9 && params->sh_coeffs != 16)
@@ -1356,6 +1470,7 @@ int dgs_subset_load(dgs_ctx* ctx, int32_t k, const dgs_splats* params, const dgs
 int dgs_repartition(dgs_ctx* ctx, int32_t depth, double d_multiplier, int64_t expected_splats, uint64_t epoch,
                     dgs_plane* planes_out) {
     return dgs_guard([&] {
+        if (ctx) ++ctx->graph_version;  // captured step graphs no longer match
         require_table(*ctx);
         if (depth < 0 || depth > 5) throw std::invalid_argument("repartition: kd depth must be 0..5 (<= 32 subsets)");
         const int W = ctx->world, me = ctx->rank;
@@ -1666,6 +1781,7 @@ int dgs_subset_store(dgs_ctx* ctx, int32_t k, dgs_splats* params, dgs_splats* m,
 int dgs_init_from_pointcloud(dgs_ctx* ctx, const float* points, int64_t n_points, const float* colors,
                              int64_t n_colors, int64_t target, uint64_t seed, int32_t sh_degree, dgs_splats* out) {
     return dgs_guard([&] {
+        if (ctx) ++ctx->graph_version;  // captured step graphs no longer match
         // trainer.hpp:24-91, host RNG in libstdc++ (bit-identical picks/jitter), neighbour term on the GPU
         if (n_points <= 0) throw std::invalid_argument("init_from_pointcloud: empty cloud");
         if (n_colors != 0 && n_colors != n_points) throw std::invalid_argument("init_from_pointcloud: color count mismatch");
@@ -2023,8 +2139,8 @@ int dgs_adam_apply(dgs_ctx* ctx, int32_t k, const dgs_splats* grads) {
         SubsetState& S = subset(*ctx, k);
         S.G.ensure(S.rows * S.ld);
         upload_fields(*ctx, S, *grads, S.G.p);
-        const AdamParams ap = adam_params(*ctx, S, S.adam_step + 1);
-        launch_adam((int)S.n, S.P.p, S.M.p, S.V.p, S.ld, S.rows, S.G.p, ap, ctx->stream);
+        const AdamArgs aa = adam_args(*ctx, S, nullptr);
+        launch_adam((int)S.n, S.P.p, S.M.p, S.V.p, S.ld, S.rows, S.G.p, aa, ctx->stream);
         ++S.adam_step;
         CK(cudaStreamSynchronize(ctx->stream));
     });
@@ -2074,9 +2190,44 @@ int dgs_render(dgs_ctx* ctx, const dgs_camera* cam, const float bg[3], float* ou
     });
 }
 
+StepTail& step_tail(Ctx& ctx, int batch, int S, int nlocal) {
+    if (batch > kTailMaxBatch || S > kTailMaxSlices || nlocal > kTailMaxLocal)
+        throw std::invalid_argument("train_step: batch, slices and local subsets are limited to 64 each");
+    if (!ctx.tail) CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx.tail), sizeof(StepTail), cudaHostAllocDefault));
+    ctx.tail->nsums = (size_t)3 * batch * S;
+    return *ctx.tail;
+}
+void finish_step(Ctx& ctx_, const std::vector<int>& local, dgs_step_result* out);
+
+/// Manager::train_step (manager.hpp:313-386).  Eager: launches and finishes the
+/// step (the pair counts are read back mid-step).  With ctx->capturing it only
+/// enqueues the step (no host round trip) for a CUDA graph, including the
+/// copies of its results into the pinned tail buffer; finish_step() turns the
+/// tail into the step result after the replay.
+void train_step_graph(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
+                      int32_t targets_on_device, const float bg[3], dgs_step_result* out);
+void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
+                     int32_t targets_on_device, const float bg[3], dgs_step_result* out);
+
 int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
                    int32_t targets_on_device, const float bg[3], dgs_step_result* out) {
     return dgs_guard([&] {
+        if (!ctx) throw std::invalid_argument("train_step: null context");
+        bool graph = ctx->graph_mode && ctx->world == 1 && !ctx->timer.on && !ctx->collect_stats &&
+                     batch >= 1 && cams != nullptr && targets != nullptr && ctx->cfg.grad_sync == 0;
+        if (graph && !targets_on_device) {  // the graph copies host targets by DMA: pinned memory only
+            cudaPointerAttributes at{};
+            graph = cudaPointerGetAttributes(&at, targets) == cudaSuccess && at.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+        }
+        if (graph) train_step_graph(ctx, batch, cams, targets, targets_on_device, bg, out);
+        else train_step_body(ctx, batch, cams, targets, targets_on_device, bg, out);
+    });
+}
+
+void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
+                     int32_t targets_on_device, const float bg[3], dgs_step_result* out) {
+    {
         require_table(*ctx);
         if (batch < 1 || cams == nullptr || targets == nullptr)
             throw std::invalid_argument("train_step: need one target per camera");
@@ -2096,6 +2247,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
         const uint64_t launches0 = ctx->launches;
         uint64_t nccl_bytes = 0;
         CK(cudaMemsetAsync(ctx->stats.p, 0, 2 * sizeof(BlendStats), ctx->stream));
+        CK(cudaMemsetAsync(ctx->abort.ensure(1), 0, sizeof(int), ctx->stream));
         std::vector<ViewParams> vps(batch);
         uint64_t pairs = 0, visible = 0;
         const float lam = (float)ctx->cfg.lambda_ssim;
@@ -2250,10 +2402,8 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                     Stage st(ctx->timer, kStExchange, cs);
                     nccl_bytes += exchange_forward(*ctx, v, local, Wd, H, S, sl, cs);
                 }
-                CK(cudaMemcpyAsync(ctx->partial_ptrs.p, ptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice,
-                                   cs));
-                CK(cudaMemcpyAsync(ctx->grad_ptrs.p, gptrs.data(), K * sizeof(void*), cudaMemcpyHostToDevice,
-                                   cs));
+                h2d(*ctx, ctx->partial_ptrs.p, ptrs.data(), K * sizeof(void*), cs);
+                h2d(*ctx, ctx->grad_ptrs.p, gptrs.data(), K * sizeof(void*), cs);
                 // ---- merge (engine.hpp:152-182) over rows [h0, h1) ----
                 ctx->merged.ensure((size_t)3 * hr * Wd);
                 {
@@ -2375,16 +2525,16 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             ++ctx->launches;
             for (int k : local) {
                 SubsetState& S_ = subset(*ctx, k);
-                const AdamParams ap = adam_params(*ctx, S_, S_.adam_step + 1);
+                const AdamArgs aa = adam_args(*ctx, S_, ctx->abort.p);
                 Stage st(ctx->timer, kStAdam, ctx->stream);
-                launch_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.rows, S_.G.p, ap, ctx->stream);
+                launch_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.rows, S_.G.p, aa, ctx->stream);
                 ++ctx->launches;
                 ++S_.adam_step;
             }
         }
         for (int k : (sync ? std::vector<int>{} : local)) {
             SubsetState& S_ = subset(*ctx, k);
-            const AdamParams ap = adam_params(*ctx, S_, S_.adam_step + 1);
+            const AdamArgs ap = adam_args(*ctx, S_, ctx->abort.p);
             // K9 (gradient record, one per view) + K10 (streaming Adam after the last view)
             S_.rec.ensure(kGradRecordRows(batch) * S_.ld);
             for (int v = 0; v < batch; ++v) {
@@ -2415,11 +2565,13 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             ++S_.adam_step;
         }
         // loss sums: slices of this rank (fixed order), then across ranks
-        std::vector<double> sums((size_t)3 * batch * S);
+        StepTail& T = step_tail(*ctx, batch, S, (int)local.size());
+        double* sums = T.sums;
         if (W > 1) {
+            if (ctx->capturing) throw std::logic_error("graph capture: single rank only");
             // every rank wrote only its own slice entry; zero the others and sum across ranks
             std::vector<double> mine((size_t)3 * batch * S, 0.0);
-            CK(cudaMemcpyAsync(sums.data(), ctx->sums.p, sums.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(sums, ctx->sums.p, T.nsums * 8, cudaMemcpyDeviceToHost, ctx->stream));
             CK(cudaStreamSynchronize(ctx->stream));
             for (int v = 0; v < batch; ++v)
                 for (int q = 0; q < 3; ++q) mine[(size_t)3 * (v * S + rank) + q] = sums[(size_t)3 * (v * S + rank) + q];
@@ -2434,23 +2586,192 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                 NK(nccl().AllReduce(ctx->sums.p, ctx->sums.p, mine.size(), ncclDouble, ncclSum, ctx->comm, ctx->stream));
             }
         }
-        CK(cudaMemcpyAsync(sums.data(), ctx->sums.p, sums.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        BlendStats st[2]{};
-        CK(cudaMemcpyAsync(st, ctx->stats.p, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
-        int bad = INT_MAX;
-        CK(cudaMemcpyAsync(&bad, ctx->bad.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(sums, ctx->sums.p, T.nsums * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(T.st, ctx->stats.p, 2 * sizeof(BlendStats), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&T.bad, ctx->bad.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&T.abort, ctx->abort.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
         // ring-overflow pixels of every (subset, view): the fallback kernels' device counts
-        std::vector<uint32_t> ovf(local.size() * (size_t)batch, 0u);
         for (size_t i = 0; i < local.size(); ++i)
-            for (int v = 0; v < batch; ++v)
-                CK(cudaMemcpyAsync(&ovf[i * batch + v], subset(*ctx, local[i]).slot(v).ovf_count.p, 4,
-                                   cudaMemcpyDeviceToHost, ctx->stream));
+            for (int v = 0; v < batch; ++v) {
+                SubsetState& S_ = subset(*ctx, local[i]);
+                ViewSlot& vs = S_.slot(v);
+                const size_t q = i * batch + v;
+                CK(cudaMemcpyAsync(&T.ovf[q], vs.ovf_count.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+                if (ctx->capturing && S_.n > 0) {  // what the eager step reads back mid-step
+                    CK(cudaMemcpyAsync(&T.pairs[q], vs.scan.p + (S_.n - 1), 4, cudaMemcpyDeviceToHost, ctx->stream));
+                    CK(cudaMemcpyAsync(&T.visible[q], vs.vb.dmax_bits + 2, 4, cudaMemcpyDeviceToHost, ctx->stream));
+                    CK(cudaMemcpyAsync(&T.err[q], vs.vb.err_index, 4, cudaMemcpyDeviceToHost, ctx->stream));
+                } else {
+                    T.pairs[q] = (uint32_t)std::max<int64_t>(0, vs.vb.pairs);
+                    T.visible[q] = (uint32_t)vs.vb.visible;
+                    T.err[q] = INT_MAX;
+                }
+            }
+        T.nccl_bytes = nccl_bytes;
+        T.launches = ctx->launches - launches0;
+        T.batch = batch;
+        T.slices = S;
+        T.nlocal = (int)local.size();
+        for (int v = 0; v < batch; ++v) T.px[v] = (double)vps[v].width * vps[v].height;
+        T.comm_bytes = (uint64_t)2 * K * batch * (uint64_t)vps[0].width * vps[0].height * 4 * sizeof(float);
+        if (ctx->capturing) return;  // the replay reads the tail
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaGetLastError());
         ctx->timer.resolve();
-        if (bad != INT_MAX) {
+        finish_step(*ctx, local, out);
+    }
+}
+
+std::vector<int> local_subsets(Ctx& ctx) {
+    std::vector<int> local;
+    for (int k = 0; k < ctx.table.k_count; ++k)
+        if (ctx.subsets.count(k) != 0) local.push_back(k);
+    return local;
+}
+
+/// One train step through a CUDA graph (dgs_set_graph_mode): the first call for
+/// a key runs eagerly (it learns every slot's pair count), the second records
+/// the step into a graph and replays it, later calls only write this step's
+/// AdamParams into the pinned staging read by the graph and replay.  A replay
+/// whose pair counts outgrew the captured sort capacity (ctx.abort & 2: K10
+/// skipped it, nothing persistent changed) is re-run eagerly and re-captured on
+/// the next call; a zero quaternion (ctx.abort & 1) is raised like the eager
+/// step, with the parameters untouched.
+void train_step_graph(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
+                      int32_t targets_on_device, const float bg[3], dgs_step_result* out) {
+    std::vector<uint8_t> key(sizeof(int32_t) * 2 + sizeof(dgs_camera) * batch + sizeof(void*) + 3 * sizeof(float) +
+                             2 * sizeof(uint64_t));
+    uint8_t* kp = key.data();
+    auto put = [&](const void* src, size_t b) {
+        std::memcpy(kp, src, b);
+        kp += b;
+    };
+    const uint64_t epoch = g_buffer_epoch.load();
+    put(&batch, sizeof(batch));
+    put(&targets_on_device, sizeof(targets_on_device));
+    put(cams, sizeof(dgs_camera) * batch);
+    put(&targets, sizeof(void*));
+    put(bg, 3 * sizeof(float));
+    put(&ctx->graph_version, sizeof(uint64_t));
+    put(&epoch, sizeof(uint64_t));
+    const std::vector<int> local = local_subsets(*ctx);
+    Ctx::CachedStep* g = nullptr;
+    for (auto& e : ctx->graphs)
+        if (e.key == key) g = &e;
+    if (g == nullptr) {
+        if (std::find(ctx->warmed.begin(), ctx->warmed.end(), key) == ctx->warmed.end()) {
+            train_step_body(ctx, batch, cams, targets, targets_on_device, bg, out);
+            if (g_buffer_epoch.load() == epoch) ctx->warmed.push_back(key);  // sizes settled: capture next time
+            return;
+        }
+        // the sort capacity of every (subset, view) slot: its largest pair count + 2 %
+        for (int k : local) {
+            SubsetState& S = subset(*ctx, k);
+            for (int v = 0; v < batch; ++v) {
+                ViewSlot& vs = S.slot(v);
+                vs.graph_cap = std::min<int64_t>(vs.pair_cap, vs.pairs_max + vs.pairs_max / 50 + 4096);
+                if (getenv("DGS_GRAPH_CAP_TEST")) vs.graph_cap = std::max<int64_t>(1, vs.pairs_max / 2);  // tests: overflow
+            }
+        }
+        std::vector<uint64_t> steps;
+        for (int k : local) steps.push_back(subset(*ctx, k).adam_step);
+        cudaGraph_t graph = nullptr;
+        for (void* p : ctx->arena) cudaFreeHost(p);
+        ctx->arena.clear();
+        ctx->capturing = true;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+        try {
+            train_step_body(ctx, batch, cams, targets, targets_on_device, bg, nullptr);
+        } catch (...) {
+            cudaStreamEndCapture(ctx->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            ctx->capturing = false;
+            for (void* p : ctx->arena) cudaFreeHost(p);
+            ctx->arena.clear();
+            cudaGetLastError();
+            for (size_t i = 0; i < local.size(); ++i) subset(*ctx, local[i]).adam_step = steps[i];
+            throw;
+        }
+        const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &graph);
+        ctx->capturing = false;
+        for (size_t i = 0; i < local.size(); ++i) subset(*ctx, local[i]).adam_step = steps[i];  // the replay counts
+        if (ec != cudaSuccess) throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(ec) + " (graph capture)");
+        Ctx::CachedStep e;
+        e.key = key;
+        e.arena.swap(ctx->arena);
+        e.graph = graph;
+        // K10's kernel nodes: their AdamParams argument is replaced at every replay
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp{};
+            CK(cudaGraphKernelNodeGetParams(nd, &kp));
+            int pi = -1;
+            const int ai = adam_param_index(kp.func, &pi);
+            if (ai < 0) continue;
+            const float* Pn = *reinterpret_cast<float* const*>(kp.kernelParams[pi]);
+            for (int k : local)
+                if (subset(*ctx, k).P.p == Pn) e.adam.push_back({nd, k, ai});
+        }
+        const cudaError_t ei = cudaGraphInstantiate(&e.exec, graph, 0);
+        if (ei != cudaSuccess) {
+            Ctx::free_step(e);
+            throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(ei) + " (graph instantiate)");
+        }
+        if (ctx->graphs.size() >= 64) {  // bounded cache: drop the oldest
+            Ctx::free_step(ctx->graphs.front());
+            ctx->graphs.erase(ctx->graphs.begin());
+        }
+        ctx->graphs.push_back(e);
+        g = &ctx->graphs.back();
+    }
+    // ---- replay: this step's AdamParams into the K10 nodes, launch ----
+    for (int k : local) check_epoch(*ctx, subset(*ctx, k));
+    for (const auto& an : g->adam) {
+        cudaKernelNodeParams kp{};
+        CK(cudaGraphKernelNodeGetParams(an.node, &kp));
+        AdamParams ap = adam_params(*ctx, subset(*ctx, an.subset), subset(*ctx, an.subset).adam_step + 1);
+        std::vector<void*> args;
+        for (int a = 0; a <= an.ap_index + 1; ++a) args.push_back(kp.kernelParams[a]);
+        args[an.ap_index] = &ap;
+        kp.kernelParams = args.data();
+        CK(cudaGraphExecKernelNodeSetParams(g->exec, an.node, &kp));
+    }
+    CK(cudaGraphLaunch(g->exec, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    StepTail& T = *ctx->tail;
+    if (T.abort & 2) {  // a pair count outgrew the captured sort: redo eagerly, re-capture next time
+        Ctx::free_step(*g);
+        ctx->graphs.erase(ctx->graphs.begin() + (g - ctx->graphs.data()));
+        ctx->warmed.erase(std::remove(ctx->warmed.begin(), ctx->warmed.end(), key), ctx->warmed.end());
+        train_step_body(ctx, batch, cams, targets, targets_on_device, bg, out);
+        ctx->warmed.push_back(key);
+        return;
+    }
+    for (int q = 0; q < T.nlocal * batch; ++q)
+        if (T.err[q] != INT_MAX) throw std::domain_error("zero quaternion");
+    for (int k : local) ++subset(*ctx, k).adam_step;
+    finish_step(*ctx, local, out);
+}
+
+/// The step result from the tail buffer (eager: just synchronised; graph:
+/// after the replay).  Throws the reference's non-finite-gradient error.
+void finish_step(Ctx& ctx_, const std::vector<int>& local, dgs_step_result* out) {
+    Ctx* ctx = &ctx_;
+    StepTail& T = *ctx->tail;
+    const int batch = T.batch, S = T.slices;
+    const double* sums = T.sums;
+    const BlendStats* st = T.st;
+    {
+        if (T.bad != INT_MAX) {
             throw std::runtime_error("partial_render_backward: non-finite gradient for splat id " +
-                                     std::to_string(subset(*ctx, local[0]).ids64[(size_t)bad]));
+                                     std::to_string(subset(*ctx, local[0]).ids64[(size_t)T.bad]));
         }
         if (out) {
             std::memset(out, 0, sizeof(*out));
@@ -2460,7 +2781,7 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
                 double s3[3] = {0.0, 0.0, 0.0};
                 for (int sl = 0; sl < S; ++sl)
                     for (int q = 0; q < 3; ++q) s3[q] += sums[(size_t)3 * (v * S + sl) + q];
-                const double n = 3.0 * vps[v].width * vps[v].height;
+                const double n = 3.0 * T.px[v];
                 loss += ((1.0 - lambda) * (s3[0] / n) + lambda * (1.0 - s3[1] / n)) / batch;
                 mse += (s3[2] / n) / batch;
             }
@@ -2468,23 +2789,27 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
             out->psnr = mse == 0.0 ? INFINITY : 10.0 * std::log10(1.0 / mse);
             // reference accounting (manager.hpp:384): every partial map and its
             // gradient cross a link: 2 * K * H * W * 4 * sizeof(float) per view.
-            out->comm_bytes = (uint64_t)2 * K * batch * (uint64_t)vps[0].width * vps[0].height * 4 * sizeof(float);
-            out->nccl_bytes = nccl_bytes;
-            out->pairs = pairs;
+            out->comm_bytes = T.comm_bytes;
+            out->nccl_bytes = T.nccl_bytes;
+            out->pairs = 0;
+            out->visible = 0;
+            out->overflow_pixels = 0;
+            for (int q = 0; q < T.nlocal * batch; ++q) {
+                out->pairs += T.pairs[q];
+                out->visible += T.visible[q];
+                out->overflow_pixels += T.ovf[q];
+            }
             out->evals_fwd = st[0].evals;
             out->contribs_fwd = st[0].contribs;
-            out->overflow_pixels = 0;
-            for (uint32_t o : ovf) out->overflow_pixels += o;
             out->evals_bwd = st[1].evals;
             out->contribs_bwd = st[1].contribs;
             out->subrounds_bwd = st[1].subrounds;
             out->small_subrounds_bwd = st[1].small_rounds;
             out->tiles_work_fwd = st[0].tiles_work;
             out->replay_tiles_bwd = st[1].tiles_work;
-            out->visible = visible;
-            out->kernel_launches = ctx->launches - launches0;
+            out->kernel_launches = T.launches;
         }
-    });
+    }
 }
 
 int dgs_dump_grad_maps(dgs_ctx* ctx, int32_t k, int32_t view, float* partial_ct, float* grad_ct) {
@@ -2501,16 +2826,28 @@ int dgs_dump_grad_maps(dgs_ctx* ctx, int32_t k, int32_t view, float* partial_ct,
     });
 }
 
+int dgs_set_graph_mode(dgs_ctx* ctx, int32_t enabled) {
+    return dgs_guard([&] {
+        if (!ctx) throw std::invalid_argument("set_graph_mode: null context");
+        ctx->graph_mode = enabled != 0;
+        if (!ctx->graph_mode) ctx->drop_graphs();
+    });
+}
+
 int dgs_set_collect_stats(dgs_ctx* ctx, int32_t enabled) {
     return dgs_guard([&] { ctx->collect_stats = enabled != 0; });
 }
 
 int dgs_set_backward_records(dgs_ctx* ctx, int32_t enabled) {
-    return dgs_guard([&] { ctx->records = enabled != 0; });
+    return dgs_guard([&] {
+        if (ctx) ++ctx->graph_version;  // captured step graphs no longer match
+        ctx->records = enabled != 0;
+    });
 }
 
 int dgs_set_virtual_slices(dgs_ctx* ctx, int32_t slices) {
     return dgs_guard([&] {
+        if (ctx) ++ctx->graph_version;  // captured step graphs no longer match
         if (slices < 1) throw std::invalid_argument("virtual slices must be >= 1");
         if (ctx->world > 1 && slices != 1) throw std::invalid_argument("virtual slices are a single-rank mode");
         ctx->virtual_slices = slices;

@@ -28,6 +28,7 @@ struct ViewBins {
                                      //     visible member count, max range (float bits)
     uint32_t* blk_part = nullptr;    // [preprocess_partials(n)] K1's per-block partials of dmax_bits
     int* err_index = nullptr;        // [1] first member with a zero quaternion (or INT_MAX)
+    int* abort = nullptr;            // [1] the step's abort flag: |= 1 on a zero quaternion, |= 2 on pair overflow
     float* shjac = nullptr;          // [10][ld] (optional): d colour_ch / d dir_a (row 3 ch + a) and the
                                      //     pre-clamp sign mask (row 9, bits) for the gradient record (K9)
     uint16_t* pair_tile = nullptr;   // [cap] tile key of each (splat, tile) pair
@@ -55,7 +56,7 @@ size_t binning_temp_bytes(int n, int64_t pair_cap);
 int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void* temp, size_t temp_bytes,
                     uint32_t* sort_keys_alt, uint32_t* sort_vals, uint32_t* sort_vals_alt, uint16_t* pair_tile_alt,
                     uint32_t* pair_val_alt, uint32_t* scan_buf, uint2* rect_sorted, uint32_t* pairs_host,
-                    cudaStream_t s);
+                    cudaStream_t s, int64_t pad_cap = 0);
 
 struct BlendStats {
     unsigned long long evals;      // (pixel, candidate) 2D evaluations
@@ -212,10 +213,24 @@ struct AdamParams {
     int exact;                // 1: reference IEEE op sequence (TrainConfig::deterministic)
 };
 
+/// What the Adam launchers take: the step's AdamParams (a kernel argument: a
+/// captured step graph gets this step's values by a kernel-node parameter
+/// update, adam_param_index) and an optional device abort flag: non-zero skips
+/// the write-back (a step abandoned after launch, e.g. zero quaternion or pair
+/// overflow in a graph replay).
+struct AdamArgs {
+    AdamParams ap{};
+    int exact = 0;
+    const int* abort = nullptr;
+};
+/// For a kernel node of a captured step: the argument index of its AdamParams
+/// and of its parameter rows P if `func` is one of the K10 kernels, else -1.
+int adam_param_index(const void* func, int* p_index);
+
 // K10: the streaming dense Adam over the gradient record (launch_project_bwd_adam
 // runs it after the last view's K9).
 void launch_adam_record(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, int deg, int nviews,
-                        const AdamParams& ap, const float* rec, cudaStream_t s);
+                        const AdamArgs& ap, const float* rec, cudaStream_t s);
 
 // K9 (+K10): projection backward (splat.hpp:363-437) fused with dense Adam
 // (optim.hpp:104-126) when `adam` is non-null; otherwise accumulates the
@@ -231,10 +246,10 @@ void launch_project_bwd(int n, const float* P, size_t ld, int sh_coeffs, const V
 // Call once per view v = 0 .. nviews-1 in order; the last call also runs the Adam stream.
 void launch_project_bwd_adam(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, const ViewParams& vp,
                              const RenderOpts& ro, const uint32_t* counts, const float* shjac, const float* g2d,
-                             size_t ld2, int view, int nviews, const AdamParams& ap, int* bad_index, float* g_rec,
+                             size_t ld2, int view, int nviews, const AdamArgs& ap, int* bad_index, float* g_rec,
                              cudaEvent_t mid_end, cudaEvent_t mid_begin, cudaStream_t s);
 constexpr size_t kGradRecordRows(int nviews) { return 11 + 6 * (size_t)nviews; }
-void launch_adam(int n, float* P, float* M, float* V, size_t ld, int rows, const float* G, const AdamParams& ap,
+void launch_adam(int n, float* P, float* M, float* V, size_t ld, int rows, const float* G, const AdamArgs& ap,
                  cudaStream_t s);
 
 }  // namespace dgs_b200

@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(kPreTB) k_preprocess(int n, const float* __res
         const bool qok = rotation_from_quat(q, r);
         if (visible && !qok) {  // math.hpp:36-37 throws only for projected splats
             atomicMin(vb.err_index, i);
+            if (vb.abort) atomicOr(vb.abort, 1);
             visible = false;
         }
         const float s0 = glibc_expf(row(kRowLogScale)), s1 = glibc_expf(row(kRowLogScale + 1)),

@@ -278,6 +278,10 @@ class Context:
     def stream(self) -> int:
         return lib().dgs_stream(self._h) or 0
 
+    def set_graph_mode(self, on: bool):
+        """Train steps as CUDA graph replays (dgs_set_graph_mode)."""
+        check(lib().dgs_set_graph_mode(self._h, int(on)))
+
     def sync(self):
         check(lib().dgs_sync(self._h))
 
