@@ -6,7 +6,7 @@ OUT=${OUT:-gpurun_out/prof}
 mkdir -p $OUT
 timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; tail -c 3000 $OUT/bench.json
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-deterministic > /dev/null 2>&1
+    --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-deterministic --graph off > /dev/null 2>&1
 # capture the hot kernels of the last (timed) step: skip every matching launch before its preprocess
 RE='k_(preprocess|blend_fwd|blend_bwd_rec|grad_record|adam_stream4|loss|emit_pairs|merge)|Onesweep'
 read SKIP COUNT < <(python - "$OUT/launches.csv" "$RE" <<'PY'
@@ -26,5 +26,5 @@ PY
 )
 echo "ncu full: skip $SKIP, capture $COUNT"
 timeout 1800 ncu --set full --import-source on --clock-control none -k "regex:$RE" \
-    -s $SKIP -c $COUNT -o $OUT/full python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-deterministic > $OUT/ncu.log 2>&1
+    -s $SKIP -c $COUNT -o $OUT/full python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-deterministic --graph off > $OUT/ncu.log 2>&1
 ls -la $OUT
