@@ -388,6 +388,21 @@ def b200_arm(a, world, rank, local_rank):
     use_graph = a.graph == "on" and world == 1 and hasattr(engine.lib(), "dgs_set_graph_mode")
     n_prime = 2 * V if use_graph else 0
 
+    # every measured window below starts from this post-warm-up training state
+    # (parameters, Adam moments and step restored in HBM, same view sequence), so
+    # the windows compare like for like: later windows do not see a later phase
+    # of training (the blends slow down by a few % per hundred steps here)
+    rewindable = hasattr(engine.lib(), "dgs_state_save")
+    if rewindable:
+        ctx.save_state()
+    it0 = it
+
+    def rewind():
+        nonlocal it
+        if rewindable:
+            ctx.restore_state()
+            it = it0
+
     def prime(host=None):
         nonlocal it
         for _ in range(n_prime):
@@ -397,6 +412,7 @@ def b200_arm(a, world, rank, local_rank):
     if use_graph:
         ctx.set_graph_mode(True)
         prime()
+    rewind()
     barrier()
 
     # ---- device-resident timed region (no per-stage events inside) ------------
@@ -420,6 +436,7 @@ def b200_arm(a, world, rank, local_rank):
     eager_ms = None
     if use_graph:
         ctx.set_graph_mode(False)
+        rewind()
         barrier()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
@@ -432,6 +449,7 @@ def b200_arm(a, world, rank, local_rank):
 
     # ---- per-stage breakdown (separate run: CUDA events around every stage) ----
     n_prof = max(V, min(a.steps, 2 * V))
+    rewind()
     ctx.set_profiling(True)
     for _ in range(n_prof):
         step(it)
@@ -442,6 +460,7 @@ def b200_arm(a, world, rank, local_rank):
     rank_members = gather_ranks(float(n_local))
 
     # ---- counters (separate short run over every view: the stats variants are slower) ----
+    rewind()
     ctx.set_collect_stats(True)
     results_stats = []
     for _ in range(V):
@@ -455,20 +474,43 @@ def b200_arm(a, world, rank, local_rank):
     host_targets = pinned.numpy().reshape(V, a.height, a.width, 3)
     step(it, host_targets)
     it += 1
-    # (the e2e steps run eagerly: with host targets the graph's copy node measured ~1.5 % slower)
-    barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    w0 = time.perf_counter()
-    e2e_losses = []
-    for _ in range(a.steps):
-        r = step(it, host_targets)
+
+    def e2e_window():
+        nonlocal it
+        rewind()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        w0 = time.perf_counter()
+        for _ in range(a.steps):
+            step(it, host_targets)
+            it += 1
+        f1.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(f0.elapsed_time(f1)), max_over_ranks((time.perf_counter() - w0) * 1e3)
+
+    # the eager window, then (graph mode) the same calls replayed as graphs; both are
+    # reported, the headline e2e is the faster one (the mode a user would pick)
+    e2e_eager_ms, e2e_eager_wall = e2e_window()
+    e2e_graph_ms = e2e_graph_wall = None
+    if use_graph:
+        ctx.set_graph_mode(True)
+        prime(host_targets)
+        e2e_graph_ms, e2e_graph_wall = e2e_window()
+        ctx.set_graph_mode(False)
+    e2e_modes = {"eager": (e2e_eager_ms, e2e_eager_wall)}
+    if e2e_graph_ms is not None:
+        e2e_modes["graph"] = (e2e_graph_ms, e2e_graph_wall)
+    e2e_mode = min(e2e_modes, key=lambda m: max(e2e_modes[m]))
+    e2e_ms, e2e_wall = e2e_modes[e2e_mode]
+    # stage times of the host-target step (eager, events around every stage)
+    rewind()
+    ctx.set_profiling(True)
+    for _ in range(n_prof):
+        step(it, host_targets)
         it += 1
-        e2e_losses.append(r["loss"])
-    f1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
-    e2e_wall = max_over_ranks((time.perf_counter() - w0) * 1e3)
+    e2e_stages = {k: round(v[0] / n_prof, 4) for k, v in ctx.stage_times().items()}
+    ctx.set_profiling(False)
 
     # ---- deterministic = 1 (the reference default: IEEE Adam, fixed-point backward sums) ----
     det_ms = None
@@ -481,6 +523,7 @@ def b200_arm(a, world, rank, local_rank):
         if use_graph:  # new options: new graphs
             ctx.set_graph_mode(True)
             prime()
+        rewind()
         barrier()
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record(stream)
@@ -615,7 +658,10 @@ def b200_arm(a, world, rank, local_rank):
                   "nccl_bytes_per_step": results[-1].get("nccl_bytes")},
         "e2e": {"value": e2e_value, "unit": "Mpixel/s", "h2d_bytes_per_step": px * 3 * 4,
                 "d2h_bytes_per_step": 3 * 8 + 16 * 4, "ms_per_step_events": e2e_ms / a.steps,
-                "ms_per_step_wall": e2e_wall / a.steps},
+                "ms_per_step_wall": e2e_wall / a.steps,
+                "mode": e2e_mode,
+                "by_mode": {m: a.steps * px / 1e6 / (max(t) / 1e3) for m, t in e2e_modes.items()},
+                "stages_ms_per_step_eager": e2e_stages},
         "step_roofline": step_roofline,
         "graph": None if eager_ms is None else {
             "ms_per_step": step_ms, "ms_per_step_eager": eager_ms, "speedup": eager_ms / step_ms,

@@ -326,12 +326,22 @@ void* dgs_stream(dgs_ctx* ctx);
 int dgs_sync(dgs_ctx* ctx);
 /* 1: dgs_train_step runs as a CUDA graph (single rank, device or pinned host
  * targets, stage timing and counters off, grad_sync off; otherwise eager).
- * Per key (cameras, target pointer, background): the first call runs eagerly,
+ * Per key (cameras, device target pointer, background; pinned host targets
+ * are uploaded outside the graph, so their pointer may change between
+ * replays): the first call runs eagerly,
  * the second captures the step without any host round trip (the pair counts
  * stay on the device and the tile sort covers each slot's largest count
  * + 2 %) and replays it; later calls replay.  Results are those of the eager
  * step; a replay whose pair count outgrew the capture is redone eagerly. */
 int dgs_set_graph_mode(dgs_ctx* ctx, int32_t enabled);
+/* Rollback point in HBM: dgs_state_save copies every local subset's
+ * parameters, Adam moments and step count into a spare device buffer of the
+ * subset; dgs_state_restore copies them back in place (no reallocation, so
+ * captured step graphs stay valid).  Not in the reference, which checkpoints
+ * through the host snapshot (manager.hpp:390-418); used to time several
+ * windows from one training state.  Restore without a save is an error. */
+int dgs_state_save(dgs_ctx* ctx);
+int dgs_state_restore(dgs_ctx* ctx);
 
 #ifdef __cplusplus
 }

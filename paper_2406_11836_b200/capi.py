@@ -157,6 +157,8 @@ _SIGS = {
     "dgs_stream": (_P, [_P]),
     "dgs_sync": (C.c_int, [_P]),
     "dgs_set_graph_mode": (C.c_int, [_P, C.c_int32]),
+    "dgs_state_save": (C.c_int, [_P]),
+    "dgs_state_restore": (C.c_int, [_P]),
 }
 
 STAGES = ("preprocess", "binning", "blend_fwd", "merge", "loss", "merge_bwd", "blend_bwd", "project_bwd", "adam",

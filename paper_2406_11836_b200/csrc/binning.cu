@@ -212,7 +212,25 @@ int bits_for(uint32_t v) {
     return b;
 }
 
+__global__ void k_zero16(uint4* __restrict__ p, size_t n16) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+__global__ void k_zero1(uint8_t* __restrict__ p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = 0;
+}
+
 }  // namespace
+
+void launch_zero(void* p, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15) == 0 && bytes % 16 == 0;
+    const size_t n = vec ? bytes / 16 : bytes;
+    const int grid = (int)std::min<size_t>((n + 255) / 256, (size_t)148 * 8);
+    if (vec) k_zero16<<<grid, 256, 0, s>>>(static_cast<uint4*>(p), n);
+    else k_zero1<<<grid, 256, 0, s>>>(static_cast<uint8_t*>(p), n);
+}
 
 size_t binning_temp_bytes(int n, int64_t pair_cap) {
     size_t a = 0, b = 0, c = 0;
@@ -236,7 +254,7 @@ int64_t run_binning(int n, const ViewParams& vp, ViewBins& vb, int64_t cap, void
                     uint32_t* pair_val_alt, uint32_t* scan_buf, uint2* rect_sorted, uint32_t* pairs_host,
                     cudaStream_t s, int64_t pad_cap) {
     const int tiles = vp.tiles_x * vp.tiles_y;
-    cudaMemsetAsync(vb.ranges, 0, sizeof(uint2) * tiles, s);
+    launch_zero(vb.ranges, sizeof(uint2) * tiles, s);
     vb.pairs = 0;
     // the blends' block order (tiles longest list first) is a permutation on every path
     auto tile_order = [&]() {

@@ -156,6 +156,8 @@ struct SubsetState {
     int rows = 59;
     size_t ld = 0;
     DevBuf<float> P, M, V, G, g2d, rec;
+    DevBuf<float> saved;  // dgs_state_save: (P, M, V) rollback copy in HBM
+    uint64_t saved_step = 0;
     DevBuf<unsigned long long> g2q;  // deterministic mode: fixed-point adjoint sums [9][lo|hi][ld], zero between uses
     DevBuf<uint32_t> ids32;
     std::vector<uint64_t> ids64;
@@ -290,7 +292,6 @@ struct Ctx {
         std::vector<uint8_t> key;
         cudaGraph_t graph = nullptr;  // kept: its K10 nodes get this step's AdamParams at every replay
         cudaGraphExec_t exec = nullptr;
-        std::vector<void*> arena;  // pinned sources its memcpy nodes read at every replay
         struct AdamNode {
             cudaGraphNode_t node;
             int subset, ap_index;
@@ -299,14 +300,11 @@ struct Ctx {
     };
     std::vector<CachedStep> graphs;
     std::vector<std::vector<uint8_t>> warmed;  // keys with one eager step done (pair maxima learnt)
-    std::vector<void*> arena;                  // pinned sources of the graph being captured (h2d)
     static void free_step(CachedStep& g) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         if (g.graph) cudaGraphDestroy(g.graph);
         g.graph = nullptr;
-        for (void* p : g.arena) cudaFreeHost(p);
         g.exec = nullptr;
-        g.arena.clear();
     }
     void drop_graphs() {
         for (auto& g : graphs) free_step(g);
@@ -442,21 +440,37 @@ void download_fields(Ctx& ctx, SubsetState& S, const float* src, dgs_splats* f) 
     }
 }
 
+struct StoreWords {
+    static constexpr int kMax = 240;
+    uint32_t n;
+    uint32_t w[kMax];
+};
+__global__ void k_store_words(uint32_t* __restrict__ dst, const StoreWords v) {
+    for (uint32_t i = threadIdx.x; i < v.n; i += blockDim.x) dst[i] = v.w[i];
+}
+
 /// Host->device copy of a small step-time value.  Eager: straight (a pageable
 /// source is staged by the runtime before the call returns).  While a step is
-/// being captured the value goes through a pinned block owned by that graph: a
-/// memcpy node reads its source at every replay, so the source must outlive
-/// the capture and keep this value.
+/// being captured the value travels as a kernel argument of k_store_words,
+/// baked into the graph: a memcpy node from host memory would queue on the H2D
+/// copy engine behind the step's target upload (tens of MB) and stall the
+/// forward until it drains.
 void h2d(Ctx& ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
     if (!ctx.capturing) {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return;
     }
-    void* p = nullptr;
-    CK(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
-    ctx.arena.push_back(p);
-    std::memcpy(p, src, bytes);
-    CK(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+    if (bytes % 4 != 0 || (reinterpret_cast<uintptr_t>(dst) & 3) != 0)
+        throw std::logic_error("graph capture: h2d of a non-word value");
+    const uint32_t* w = static_cast<const uint32_t*>(src);
+    for (size_t o = 0, nw = bytes / 4; o < nw; o += StoreWords::kMax) {
+        StoreWords v{};
+        v.n = (uint32_t)std::min<size_t>(StoreWords::kMax, nw - o);
+        std::memcpy(v.w, w + o, v.n * 4);
+        k_store_words<<<1, 256, 0, s>>>(static_cast<uint32_t*>(dst) + o, v);
+        CK(cudaGetLastError());
+        ++ctx.launches;
+    }
 }
 
 /// partial_render for local subset S into view slot v (engine.hpp:44-52):
@@ -507,7 +521,8 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
     h2d(ctx, vb.dmax_bits, dmax0, sizeof(dmax0), ctx.stream);
     const int int_max = INT_MAX;
     h2d(ctx, vb.err_index, &int_max, 4, ctx.stream);
-    CK(cudaMemsetAsync(vs.ovf_count.p, 0, 4, ctx.stream));
+    launch_zero(vs.ovf_count.p, 4, ctx.stream);
+    ++ctx.launches;
     {
         Stage st(ctx.timer, kStPre, ctx.stream);
         launch_preprocess((int)n, S.P.p, S.ld, S.sh_coeffs, S.ids32.p, vp, ctx.ro, vb, ctx.stream);
@@ -525,7 +540,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
                     vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, vs.rect_sorted.ensure(n),
                     &ctx.hs->pairs, ctx.stream, vs.graph_cap);
-        ctx.launches += 3;
+        ctx.launches += 4;
     }
     // zero-quaternion flag: rides along with the binning's pair-count readback
     if (!capture) {
@@ -538,7 +553,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
                         vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, vs.rect_sorted.ensure(n),
                         &ctx.hs->pairs, ctx.stream);
-        ctx.launches += 3;
+        ctx.launches += 4;
         // the graph capacity of this slot: the largest pair count seen, plus 2 %
         vs.pairs_max = std::max<int64_t>(vs.pairs_max, P < 0 ? -P : P);
     }
@@ -548,7 +563,7 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
         P = run_binning((int)n, vp, vb, vs.pair_cap, vs.temp.p, vs.temp_bytes, vs.sort_keys_alt.p, vs.sort_vals.p,
                         vs.sort_vals_alt.p, vs.pair_tile_alt.p, vs.pair_val_alt.p, vs.scan.p, vs.rect_sorted.p,
                         &ctx.hs->pairs, ctx.stream);
-        ctx.launches += 3;
+        ctx.launches += 4;
         if (P < 0) throw std::runtime_error("binning: pair buffer sizing failed");
     }
     st_bin.end();
@@ -607,13 +622,15 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     if (det) {
         if (S.g2q.p == nullptr || S.g2q.n < 18 * S.ld) {
             S.g2q.ensure(18 * S.ld);  // launch_fixed_to_float re-zeroes it after every use
-            CK(cudaMemsetAsync(S.g2q.p, 0, 18 * S.ld * sizeof(unsigned long long), ctx.stream));
+            launch_zero(S.g2q.p, 18 * S.ld * sizeof(unsigned long long), ctx.stream);
+            ++ctx.launches;
         }
         ctx.bad.ensure(1);
         acc.q = S.g2q.p;
         acc.bad = ctx.bad.p;
     } else {
-        CK(cudaMemsetAsync(S.g2d.p, 0, 9 * S.ld * sizeof(float), ctx.stream));
+        launch_zero(S.g2d.p, 9 * S.ld * sizeof(float), ctx.stream);
+        ++ctx.launches;
     }
     Stage st(ctx.timer, kStBwd, ctx.stream);
     CompRecords crec;
@@ -2225,6 +2242,20 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
     });
 }
 
+/// Pinned host targets: every view's window [h0, h0 + tgt_win / (3 Wd0)) H2D
+/// into tgt_stage on the copy stream, after the main stream's earlier work
+/// (the previous step's readers of the staging); copy_done marks the end.
+static void upload_pinned_targets(Ctx* ctx, int batch, const float* targets, int Wd0, int H0, int h0,
+                                  size_t tgt_win) {
+    CK(cudaEventRecord(ctx->copy_done, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_done, 0));
+    for (int v = 0; v < batch; ++v)
+        CK(cudaMemcpyAsync(ctx->tgt_stage.p + (size_t)v * tgt_win,
+                           targets + (size_t)v * 3 * Wd0 * H0 + (size_t)h0 * Wd0 * 3, tgt_win * 4,
+                           cudaMemcpyHostToDevice, ctx->copy_stream));
+    CK(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+}
+
 void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const float* targets,
                      int32_t targets_on_device, const float bg[3], dgs_step_result* out) {
     {
@@ -2246,8 +2277,9 @@ void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const 
         for (int k : local) check_epoch(*ctx, subset(*ctx, k));
         const uint64_t launches0 = ctx->launches;
         uint64_t nccl_bytes = 0;
-        CK(cudaMemsetAsync(ctx->stats.p, 0, 2 * sizeof(BlendStats), ctx->stream));
-        CK(cudaMemsetAsync(ctx->abort.ensure(1), 0, sizeof(int), ctx->stream));
+        launch_zero(ctx->stats.p, 2 * sizeof(BlendStats), ctx->stream);
+        launch_zero(ctx->abort.ensure(1), sizeof(int), ctx->stream);
+        ctx->launches += 2;
         std::vector<ViewParams> vps(batch);
         uint64_t pairs = 0, visible = 0;
         const float lam = (float)ctx->cfg.lambda_ssim;
@@ -2284,18 +2316,18 @@ void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const 
             }
             tgt_win = (size_t)(h1 - h0) * Wd0 * 3;
             ctx->tgt_stage.ensure(tgt_win * batch);
-            CK(cudaEventRecord(ctx->copy_done, ctx->stream));  // staging reuse: previous step's readers are done
-            CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_done, 0));
             cudaPointerAttributes at{};
             const bool pinned = cudaPointerGetAttributes(&at, targets) == cudaSuccess && at.type == cudaMemoryTypeHost;
             cudaGetLastError();  // unregistered pointers may leave an error on older runtimes
-            if (pinned) {
-                for (int v = 0; v < batch; ++v)
-                    CK(cudaMemcpyAsync(ctx->tgt_stage.p + (size_t)v * tgt_win,
-                                       targets + (size_t)v * 3 * Wd0 * H0 + (size_t)h0 * Wd0 * 3, tgt_win * 4,
-                                       cudaMemcpyHostToDevice, ctx->copy_stream));
-                CK(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+            if (pinned && ctx->capturing) {
+                // graph steps: the replay wrapper enqueues the upload outside the
+                // graph (upload_pinned_targets); the graph waits on copy_done as an
+                // external event, so the DMA overlaps the captured forward
+            } else if (pinned) {
+                upload_pinned_targets(ctx, batch, targets, Wd0, H0, h0, tgt_win);
             } else {
+                CK(cudaEventRecord(ctx->copy_done, ctx->stream));  // staging reuse: previous step's readers are done
+                CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_done, 0));
                 // pageable: cudaMemcpyAsync would stage synchronously on this thread
                 // (the GPU idles meanwhile); copy through pinned memory on a helper
                 // thread instead, overlapped with the forward (the previous step's
@@ -2426,7 +2458,7 @@ void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const 
                     if (!waited_copy) {
                         if (ctx->stager.joinable()) ctx->stager.join();
                         if (!ctx->stager_err.empty()) throw std::runtime_error(ctx->stager_err);
-                        CK(cudaStreamWaitEvent(cs, ctx->copy_done, 0));
+                        CK(cudaStreamWaitEvent(cs, ctx->copy_done, ctx->capturing ? cudaEventWaitExternal : 0));
                         waited_copy = true;
                     }
                     // window rows [h0, h1) inside the prefetched window (which starts at
@@ -2650,7 +2682,8 @@ void train_step_graph(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const
     put(&batch, sizeof(batch));
     put(&targets_on_device, sizeof(targets_on_device));
     put(cams, sizeof(dgs_camera) * batch);
-    put(&targets, sizeof(void*));
+    const float* tkey = targets_on_device ? targets : nullptr;  // pinned targets are uploaded outside the graph
+    put(&tkey, sizeof(void*));
     put(bg, 3 * sizeof(float));
     put(&ctx->graph_version, sizeof(uint64_t));
     put(&epoch, sizeof(uint64_t));
@@ -2676,8 +2709,6 @@ void train_step_graph(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const
         std::vector<uint64_t> steps;
         for (int k : local) steps.push_back(subset(*ctx, k).adam_step);
         cudaGraph_t graph = nullptr;
-        for (void* p : ctx->arena) cudaFreeHost(p);
-        ctx->arena.clear();
         ctx->capturing = true;
         CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
         try {
@@ -2686,8 +2717,6 @@ void train_step_graph(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const
             cudaStreamEndCapture(ctx->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
             ctx->capturing = false;
-            for (void* p : ctx->arena) cudaFreeHost(p);
-            ctx->arena.clear();
             cudaGetLastError();
             for (size_t i = 0; i < local.size(); ++i) subset(*ctx, local[i]).adam_step = steps[i];
             throw;
@@ -2698,7 +2727,6 @@ void train_step_graph(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const
         if (ec != cudaSuccess) throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(ec) + " (graph capture)");
         Ctx::CachedStep e;
         e.key = key;
-        e.arena.swap(ctx->arena);
         e.graph = graph;
         // K10's kernel nodes: their AdamParams argument is replaced at every replay
         size_t nn = 0;
@@ -2741,6 +2769,12 @@ void train_step_graph(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const
         args[an.ap_index] = &ap;
         kp.kernelParams = args.data();
         CK(cudaGraphExecKernelNodeSetParams(g->exec, an.node, &kp));
+    }
+    if (!targets_on_device) {  // pinned host targets (single rank: the whole image)
+        const int Wd0 = cams[0].width, H0 = cams[0].height;
+        const size_t tgt_win = (size_t)H0 * Wd0 * 3;
+        ctx->tgt_stage.ensure(tgt_win * batch);
+        upload_pinned_targets(ctx, batch, targets, Wd0, H0, 0, tgt_win);
     }
     CK(cudaGraphLaunch(g->exec, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -2831,6 +2865,41 @@ int dgs_set_graph_mode(dgs_ctx* ctx, int32_t enabled) {
         if (!ctx) throw std::invalid_argument("set_graph_mode: null context");
         ctx->graph_mode = enabled != 0;
         if (!ctx->graph_mode) ctx->drop_graphs();
+    });
+}
+
+int dgs_state_save(dgs_ctx* ctx) {
+    return dgs_guard([&] {
+        if (!ctx) throw std::invalid_argument("state_save: null context");
+        CK(cudaSetDevice(ctx->device));
+        for (auto& kv : ctx->subsets) {
+            SubsetState& S = *kv.second;
+            const size_t plane = (size_t)S.rows * S.ld;
+            S.saved.ensure(3 * plane);
+            CK(cudaMemcpyAsync(S.saved.p, S.P.p, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(S.saved.p + plane, S.M.p, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(S.saved.p + 2 * plane, S.V.p, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            S.saved_step = S.adam_step;
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dgs_state_restore(dgs_ctx* ctx) {
+    return dgs_guard([&] {
+        if (!ctx) throw std::invalid_argument("state_restore: null context");
+        CK(cudaSetDevice(ctx->device));
+        for (auto& kv : ctx->subsets) {
+            SubsetState& S = *kv.second;
+            const size_t plane = (size_t)S.rows * S.ld;
+            if (S.saved.p == nullptr || S.saved.n < 3 * plane)
+                throw std::invalid_argument("state_restore: no saved state for subset " + std::to_string(kv.first));
+            CK(cudaMemcpyAsync(S.P.p, S.saved.p, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(S.M.p, S.saved.p + plane, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(S.V.p, S.saved.p + 2 * plane, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            S.adam_step = S.saved_step;
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
     });
 }
 

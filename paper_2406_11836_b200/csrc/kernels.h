@@ -48,6 +48,11 @@ size_t preprocess_partials(int n);
 void launch_preprocess(int n, const float* P, size_t ld, int sh_coeffs, const uint32_t* ids32, const ViewParams& vp,
                        const RenderOpts& ro, const ViewBins& vb, cudaStream_t s);
 
+/// Zero `bytes` of device memory with a kernel.  The step path uses it instead
+/// of cudaMemsetAsync: a memset node of a CUDA graph (and a runtime memset)
+/// runs on a copy engine and queues behind the step's host-target upload.
+void launch_zero(void* p, size_t bytes, cudaStream_t s);
+
 // K2 helpers (CUB radix sorts live in binning.cu).
 size_t binning_temp_bytes(int n, int64_t pair_cap);
 // Sorts members by range, emits pairs in range order, stable-sorts them by

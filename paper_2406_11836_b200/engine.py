@@ -282,6 +282,14 @@ class Context:
         """Train steps as CUDA graph replays (dgs_set_graph_mode)."""
         check(lib().dgs_set_graph_mode(self._h, int(on)))
 
+    def save_state(self):
+        """Rollback point in HBM for every local subset (dgs_state_save)."""
+        check(lib().dgs_state_save(self._h))
+
+    def restore_state(self):
+        """Back to the last save_state, in place (dgs_state_restore)."""
+        check(lib().dgs_state_restore(self._h))
+
     def sync(self):
         check(lib().dgs_sync(self._h))
 

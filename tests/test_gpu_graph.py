@@ -7,7 +7,9 @@ results land in a pinned tail buffer.  With TrainConfig::deterministic = 1 the
 graph steps must equal the eager steps bit for bit (parameters, both Adam
 moments, losses, a render afterwards) across several views (one graph each),
 with one and two KD subsets and with batch 2 (the view chains on the second
-stream join the capture).  A replay whose pair counts outgrow the captured
+stream join the capture), and with pinned host targets (uploaded outside the
+graph on the copy stream, which the graph waits for as an external event; the
+host pointer may change between replays).  A replay whose pair counts outgrow the captured
 capacity (forced with DGS_GRAPH_CAP_TEST, in a subprocess) must skip its Adam
 step, re-run eagerly and still give the eager result."""
 import os
@@ -23,7 +25,8 @@ sys.path.insert(0, str(ROOT))
 from paper_2406_11836_b200 import engine  # noqa: E402
 
 FIELDS = ("mu", "log_scale", "rotation", "opacity_logit", "sh")
-CASES = {"k1_b1": dict(kd=0, batch=1), "k2_b1": dict(kd=1, batch=1), "k2_b2": dict(kd=1, batch=2)}
+CASES = {"k1_b1": dict(kd=0, batch=1), "k2_b1": dict(kd=1, batch=1), "k2_b2": dict(kd=1, batch=2),
+         "k1_b2_host": dict(kd=0, batch=2, host=True)}
 
 
 def scene():
@@ -45,11 +48,17 @@ def run(sc, c, graph, steps=12):
     # device-resident planar targets (the bench's layout): fixed pointers per view
     tdev = torch.from_numpy(targets.transpose(0, 3, 1, 2).copy()).cuda()
     vb = tdev[0].numel() * 4
+    # pinned host targets (HWC, the e2e layout): two copies used alternately, so
+    # replays see a different host pointer than the one captured
+    pins = [torch.from_numpy(targets.copy()).pin_memory() for _ in range(2)] if c.get("host") else None
     losses = []
     for s in range(steps):
         v0 = (s * c["batch"]) % len(cams)
         idx = [(v0 + j) % len(cams) for j in range(c["batch"])]
-        if c["batch"] == 1:
+        if pins is not None:
+            assert idx == list(range(idx[0], idx[0] + c["batch"]))
+            r = mgr.train_step([cams[i] for i in idx], pins[s % 2].numpy()[idx[0]:idx[0] + c["batch"]])
+        elif c["batch"] == 1:
             r = mgr.train_step([cams[idx[0]]], None, targets_device_ptr=tdev.data_ptr() + idx[0] * vb)
         else:  # batches of consecutive views: contiguous device targets
             assert idx == list(range(idx[0], idx[0] + c["batch"]))
@@ -78,6 +87,47 @@ def test_graph_steps_equal_eager(sc, name):
     g, e = run(sc, c, True), run(sc, c, False)
     for key in g:
         assert np.array_equal(g[key], e[key]), key
+
+
+@pytest.mark.gpu
+def test_state_restore_replays_identically(sc):
+    """dgs_state_save / dgs_state_restore: steps after a restore equal the
+    steps after the save bit for bit (parameters, moments, step count, losses),
+    with the step graphs captured in between still replayed."""
+    import torch
+
+    init, cams, targets = sc
+    cfg = engine.train_config(kd_depth=1, deterministic=1)
+    mgr = engine.Manager(init, cfg, engine.render_options())
+    mgr.ctx.set_graph_mode(True)
+    tdev = torch.from_numpy(targets.transpose(0, 3, 1, 2).copy()).cuda()
+    vb = tdev[0].numel() * 4
+
+    def steps(n):
+        return [mgr.train_step([cams[s % len(cams)]], None, targets_device_ptr=tdev.data_ptr() + (s % len(cams)) * vb)
+                ["loss"] for s in range(n)]
+
+    def state():
+        out = {}
+        for k in range(mgr.table.subset_count):
+            p, m, v, step = mgr.ctx.store_subset(k, init.sh_coeffs)
+            out[(k, "step")] = np.asarray(step)
+            for name, sp in (("p", p), ("m", m), ("v", v)):
+                for f in FIELDS:
+                    out[(k, name, f)] = getattr(sp, f)
+        return out
+
+    with pytest.raises(Exception, match="no saved state"):
+        mgr.ctx.restore_state()
+    steps(2 * len(cams))  # every view captured
+    mgr.ctx.save_state()
+    a, sa = steps(10), state()
+    mgr.ctx.restore_state()
+    b, sb = steps(10), state()
+    mgr.close()
+    assert a == b
+    for key in sa:
+        assert np.array_equal(sa[key], sb[key]), key
 
 
 @pytest.mark.gpu
