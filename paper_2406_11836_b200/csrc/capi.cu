@@ -33,18 +33,21 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 void ensure_smem_attr(const void* func, int bytes) {
+    // per (device, kernel): the largest size set so far; a launch asking for
+    // more raises the attribute again (it is a limit, not a reservation)
     static std::mutex mu;
-    static std::set<std::pair<int, const void*>> done;
+    static std::map<std::pair<int, const void*>, int> done;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e) + " (cudaGetDevice)");
     std::lock_guard<std::mutex> lock(mu);
-    if (done.count({dev, func})) return;
+    auto it = done.find({dev, func});
+    if (it != done.end() && it->second >= bytes) return;
     e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess)
         throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e) + " (cudaFuncSetAttribute, " +
                         std::to_string(bytes) + " B dynamic shared memory)");
-    done.insert({dev, func});
+    done[{dev, func}] = bytes;
 }
 
 #define CK(call)                                                                                 \
