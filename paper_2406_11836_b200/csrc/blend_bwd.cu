@@ -493,6 +493,9 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
                                                                  const uint32_t* __restrict__ tile_order) {
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     if (crec.tile_replay[tile]) return;  // handled by the replay kernel
+    __shared__ uint64_t s_exptab[32];  // eval_2d's exp table
+    load_exp_tab(s_exptab);
+    __syncthreads();
     const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
     int px, py;
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
             const float dx = fsub(ps.pxf, A.x), dy = fsub(ps.pyf, A.y);
             const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
                                   fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
-            const float g = gauss_expf(m2, ro.trunc < 13.0f);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
+            const float g = gauss_expf(m2, ro.trunc < 13.0f, s_exptab);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
             const float ag = fmul(A.z, g);
             const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;
             contribution_grad(ps, sigma, g, A, B, D, ro.sigma_clamp, v);

@@ -78,7 +78,7 @@ struct PixelRay {
 __device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewParams& vp, const RenderOpts& ro,
                                                const Subspace& gate, const float4& A, const float4& B,
                                                const float4& C, float zkey, float& t_out, float& sigma_out,
-                                               float& g_out) {
+                                               float& g_out, const uint64_t* exp_tab = nullptr) {
     const float dx = fsub(pr.pxf, A.x), dy = fsub(pr.pyf, A.y);
     // eval_2d (splat.hpp:326-332): m2 = delta . (inv_cov2d * delta)
     const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))), fmul(dy, fadd(fmul(B.z, dx), fmul(B.w, dy))));
@@ -91,7 +91,7 @@ __device__ __forceinline__ bool eval_candidate(const PixelRay& pr, const ViewPar
     const float e0 = fsub(x0, C.x), e1 = fsub(x1, C.y), e2 = fsub(x2, C.z);
     if (dot3(e0, e1, e2, e0, e1, e2) > A.w) return false;
     if (ro.indicator_enabled && !subspace_contains(gate, x0, x1, x2)) return false;
-    const float g = gauss_expf(m2, ro.trunc < 13.0f);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
+    const float g = gauss_expf(m2, ro.trunc < 13.0f, exp_tab);  // eval_2d std::exp in float (splat.hpp:331): sigma bit-exact
     const float ag = fmul(A.z, g);
     const float sigma = (ro.sigma_clamp < ag) ? ro.sigma_clamp : ag;  // std::min(alpha*g, clamp)
     if (!(sigma > 0.0f)) return false;
@@ -149,6 +149,8 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fwd(ViewParams vp, R
     uint16_t* smask = reinterpret_cast<uint16_t*>(bpos + KBUF) + (kBlendThreads / 32) * kBlendThreads;
     __shared__ int s_woff[kBlendThreads / 32];
     __shared__ int s_short;
+    __shared__ uint64_t s_exptab[32];  // eval_2d's exp table (read before the first batch's barrier)
+    load_exp_tab(s_exptab);
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fwd(ViewParams vp, R
             const float4 A = sA[j], B = sB[j], C = sC[j];
             if (STATS) ++n_eval;
             float t, sigma, g;
-            if (!eval_candidate(pr, vp, ro, gate, A, B, C, D.w, t, sigma, g)) continue;
+            if (!eval_candidate(pr, vp, ro, gate, A, B, C, D.w, t, sigma, g, s_exptab)) continue;
             const uint32_t id = __float_as_uint(C.w);
             if (cnt == KBUF) {
                 while (head_t < D.w && !done) emit_head();

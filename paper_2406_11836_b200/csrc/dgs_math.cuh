@@ -82,7 +82,7 @@ static const uint64_t kExp2fTab[32] = {
 /// glibc_expf's evaluation without its special cases: bit-identical to
 /// glibc_expf for |x| < 88 (top12(x) < 0x42b), the range of the blends'
 /// eval_2d argument -m^2/2 whenever truncation_radius < 13.
-DGS_HD float glibc_expf_core(float x) {
+DGS_HD float glibc_expf_core(float x, const uint64_t* tab = nullptr) {
     const double N = 32.0;
     const double InvLn2N = 0x1.71547652b82fep+0 * N;
     const double SHIFT = 0x1.8p+52;
@@ -95,8 +95,10 @@ DGS_HD float glibc_expf_core(float x) {
     kd = kd - SHIFT;
     const double r = dfma(InvLn2N, xd, -kd);
 #if defined(__CUDA_ARCH__)
-    uint64_t t = __ldg(&kExp2fTab[ki % 32]);
+    // tab: a shared-memory copy of kExp2fTab (the blends' hot loops), else the global table
+    uint64_t t = tab != nullptr ? tab[ki % 32] : __ldg(&kExp2fTab[ki % 32]);
 #else
+    (void)tab;
     uint64_t t = kExp2fTab[ki % 32];
 #endif
     t += ki << (52 - 5);
@@ -123,10 +125,17 @@ DGS_HD float glibc_expf(float x) {
 
 /// eval_2d's g = exp(-m^2/2) for 0 <= m^2 <= trunc^2: the special-case-free
 /// core when the whole range stays below |x| < 88 (the flag is uniform).
-DGS_HD float gauss_expf(float m2, bool core_ok) {
+DGS_HD float gauss_expf(float m2, bool core_ok, const uint64_t* tab = nullptr) {
     const float x = fmul(-0.5f, m2);
-    return core_ok ? glibc_expf_core(x) : glibc_expf(x);
+    return core_ok ? glibc_expf_core(x, tab) : glibc_expf(x);
 }
+
+#if defined(__CUDACC__)
+/// kExp2fTab into a CTA's shared copy (threads 0..31); the caller syncs.
+__device__ __forceinline__ void load_exp_tab(uint64_t* s_tab) {
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+}
+#endif
 
 /// math.hpp:21-24: 1/(1+exp(-x)).
 DGS_HD float sigmoidf_exact(float x) { return fdiv(1.0f, fadd(1.0f, glibc_expf(-x))); }
