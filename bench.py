@@ -513,7 +513,7 @@ def b200_arm(a, world, rank, local_rank):
     ctx.set_profiling(False)
 
     # ---- deterministic = 1 (the reference default: IEEE Adam, fixed-point backward sums) ----
-    det_ms = None
+    det_ms = det_stages = None
     if not a.no_deterministic:
         cfg_det = engine.train_config(kd_depth=int(math.log2(world)), iterations=a.iterations, deterministic=1)
         ctx.set_options(ro, cfg_det)
@@ -533,6 +533,16 @@ def b200_arm(a, world, rank, local_rank):
         d1.record(stream)
         torch.cuda.synchronize()
         det_ms = max_over_ranks(d0.elapsed_time(d1)) / n_det
+        # its stage times (eager, events around every stage), from the same state
+        if use_graph:
+            ctx.set_graph_mode(False)
+        rewind()
+        ctx.set_profiling(True)
+        for _ in range(n_prof):
+            step(it)
+            it += 1
+        det_stages = {k: round(v[0] / n_prof, 4) for k, v in ctx.stage_times().items()}
+        ctx.set_profiling(False)
         ctx.set_options(ro, cfg)
 
     px = a.width * a.height
@@ -671,6 +681,7 @@ def b200_arm(a, world, rank, local_rank):
             "priming_steps_per_phase": n_prime},
         "deterministic_mode": None if det_ms is None else {
             "ms_per_step": det_ms, "value": px / 1e6 / (det_ms / 1e3), "unit": "Mpixel/s", "steps": n_det,
+            "stages_ms_per_step_eager": det_stages,
             "what": "TrainConfig::deterministic=1 (reference default): IEEE Adam op sequence and "
                     "fixed-point (2^-72) backward sums in one pass (bitwise reproducible); the headline "
                     "uses deterministic=0 (fast Adam, float RED atomics)"},
