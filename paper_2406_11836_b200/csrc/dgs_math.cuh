@@ -111,7 +111,7 @@ DGS_HD float glibc_expf_core(float x, const uint64_t* tab = nullptr) {
     return (float)y;
 }
 
-DGS_HD float glibc_expf(float x) {
+DGS_HD float glibc_expf(float x, const uint64_t* tab = nullptr) {
     const uint32_t ux = f2u(x);
     const uint32_t abstop = (ux >> 20) & 0x7ff;
     if (abstop >= 0x42b) {  // top12(88.0f)
@@ -120,7 +120,7 @@ DGS_HD float glibc_expf(float x) {
         if (x > 0x1.62e42ep6f) return u2f(0x7f800000u);  // x > log(0x1p128): overflow
         if (x < -0x1.9fe368p6f) return 0.0f;            // x < log(0x1p-150): underflow
     }
-    return glibc_expf_core(x);
+    return glibc_expf_core(x, tab);
 }
 
 /// eval_2d's g = exp(-m^2/2) for 0 <= m^2 <= trunc^2: the special-case-free
@@ -138,7 +138,9 @@ __device__ __forceinline__ void load_exp_tab(uint64_t* s_tab) {
 #endif
 
 /// math.hpp:21-24: 1/(1+exp(-x)).
-DGS_HD float sigmoidf_exact(float x) { return fdiv(1.0f, fadd(1.0f, glibc_expf(-x))); }
+DGS_HD float sigmoidf_exact(float x, const uint64_t* tab = nullptr) {
+    return fdiv(1.0f, fadd(1.0f, glibc_expf(-x, tab)));
+}
 
 /// math.hpp:33-45 rotation_from_quat (the quaternion norm is a contiguous
 /// Vec4 reduction).  Row-major r[9].  Returns false for a zero quaternion
