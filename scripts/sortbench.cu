@@ -6,18 +6,18 @@
 #include <cstdio>
 #include <vector>
 
-template <typename K, typename V, int THREADS, int ITEMS>
+template <typename K, typename V, int THREADS, int ITEMS, int RB = 8>
 struct Hub {
     using Base = typename cub::detail::radix::policy_hub<K, V, int>::Policy1000;
     struct Policy : cub::ChainedPolicy<1000, Policy, Policy> {
         static constexpr bool ONESWEEP = true;
-        static constexpr int ONESWEEP_RADIX_BITS = 8;
+        static constexpr int ONESWEEP_RADIX_BITS = RB;
         using HistogramPolicy = typename Base::HistogramPolicy;
         using ExclusiveSumPolicy = typename Base::ExclusiveSumPolicy;
         using DominantT = typename cub::detail::radix::policy_hub<K, V, int>::DominantT;
         using OnesweepPolicy =
             cub::AgentRadixSortOnesweepPolicy<THREADS, ITEMS, DominantT, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
-                                              cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+                                              cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, RB>;
         using ScanPolicy = typename Base::ScanPolicy;
         using DownsweepPolicy = typename Base::DownsweepPolicy;
         using AltDownsweepPolicy = typename Base::AltDownsweepPolicy;
@@ -30,9 +30,9 @@ struct Hub {
     using MaxPolicy = Policy;
 };
 
-template <typename K, typename V, int THREADS, int ITEMS>
+template <typename K, typename V, int THREADS, int ITEMS, int RB = 8>
 float run(K* k0, K* k1, V* v0, V* v1, int n, int bits, void* tmp, size_t tmpb, int reps) {
-    using D = cub::DispatchRadixSort<false, K, V, int, Hub<K, V, THREADS, ITEMS>>;
+    using D = cub::DispatchRadixSort<false, K, V, int, Hub<K, V, THREADS, ITEMS, RB>>;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -79,6 +79,7 @@ float run_default(K* k0, K* k1, uint32_t* v0, uint32_t* v1, int n, int bits, voi
 
 #define RUN32(T, I) printf("u32 %3d x %2d : %.3f ms\n", T, I, run<uint32_t, uint32_t, T, I>(k32a, k32b, va, vb, n1, 24, tmp, tmpb, 5))
 #define RUN16(T, I) printf("u16 %3d x %2d : %.3f ms\n", T, I, run<uint16_t, uint32_t, T, I>(k16a, k16b, va, vb, n2, 13, tmp, tmpb, 5))
+#define RUN16B(T, I, B) printf("u16 %3d x %2d rb %d : %.3f ms\n", T, I, B, run<uint16_t, uint32_t, T, I, B>(k16a, k16b, va, vb, n2, 13, tmp, tmpb, 5))
 
 int main() {
     const int n1 = 10000000, n2 = 42800000;
@@ -105,5 +106,12 @@ int main() {
     RUN32(128, 16); RUN32(256, 8); RUN32(384, 12); RUN32(192, 16);
     RUN16(512, 20); RUN16(256, 20); RUN16(256, 16); RUN16(256, 12); RUN16(512, 12); RUN16(384, 16);
     RUN16(128, 16); RUN16(256, 8); RUN16(512, 8); RUN16(192, 20);
+    RUN16B(256, 16, 7); RUN16B(512, 16, 7); RUN16B(384, 16, 7); RUN16B(256, 24, 7); RUN16B(256, 20, 7);
+    RUN16B(512, 12, 7); RUN16B(256, 16, 6); RUN16B(512, 16, 6); RUN16B(384, 20, 7); RUN16B(256, 32, 7);
+    printf("-- repeat\n");
+    printf("default u16: %.3f ms\n", run_default<uint16_t>(k16a, k16b, va, vb, n2, 13, tmp, tmpb, 5));
+    RUN16B(384, 20, 7); RUN16B(384, 24, 7); RUN16B(512, 20, 7); RUN16B(320, 24, 7); RUN16B(384, 18, 7);
+    RUN16B(256, 28, 7); RUN16B(384, 20, 8); RUN16B(384, 24, 8); RUN16B(448, 20, 7); RUN16B(384, 28, 7);
+    printf("default u16: %.3f ms\n", run_default<uint16_t>(k16a, k16b, va, vb, n2, 13, tmp, tmpb, 5));
     return 0;
 }
