@@ -2248,10 +2248,19 @@ int dgs_train_step(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const fl
 /// Pinned host targets: every view's window [h0, h0 + tgt_win / (3 Wd0)) H2D
 /// into tgt_stage on the copy stream, after the main stream's earlier work
 /// (the previous step's readers of the staging); copy_done marks the end.
+__global__ void k_spin_ns(unsigned long long ns) {
+    const unsigned long long t0 = clock64();
+    // ~ns at >= 1 GHz; only for the upload-ordering test (DGS_TEST_UPLOAD_DELAY_US)
+    while ((unsigned long long)(clock64() - t0) < ns) __nanosleep(1000);
+}
+
 static void upload_pinned_targets(Ctx* ctx, int batch, const float* targets, int Wd0, int H0, int h0,
                                   size_t tgt_win) {
     CK(cudaEventRecord(ctx->copy_done, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_done, 0));
+    // tests: hold the upload back so that a consumer which did not wait for it would read stale data
+    static const long delay_us = getenv("DGS_TEST_UPLOAD_DELAY_US") ? atol(getenv("DGS_TEST_UPLOAD_DELAY_US")) : 0;
+    if (delay_us > 0) k_spin_ns<<<1, 1, 0, ctx->copy_stream>>>((unsigned long long)delay_us * 2000ull);
     for (int v = 0; v < batch; ++v)
         CK(cudaMemcpyAsync(ctx->tgt_stage.p + (size_t)v * tgt_win,
                            targets + (size_t)v * 3 * Wd0 * H0 + (size_t)h0 * Wd0 * 3, tgt_win * 4,

@@ -141,6 +141,23 @@ def test_graph_capacity_overflow_reruns_eagerly(sc, tmp_path):
         assert np.array_equal(g[key], e[key]), key
 
 
+@pytest.mark.gpu
+def test_graph_waits_for_the_host_target_upload(sc, tmp_path):
+    """Pinned host targets are uploaded outside the graph; the graph waits for
+    the upload through an external event node.  With the upload held back by
+    20 ms (DGS_TEST_UPLOAD_DELAY_US, a spin kernel ahead of it on the copy
+    stream) a replay that did not wait would blend against the previous
+    step's targets; it must still equal the eager steps."""
+    out = tmp_path / "delayed.npz"
+    env = dict(os.environ, DGS_TEST_UPLOAD_DELAY_US="20000")
+    subprocess.run([sys.executable, __file__, str(out), "k1_b2_host"], check=True, env=env, cwd=ROOT, timeout=600)
+    g = np.load(out)
+    e = run(sc, CASES["k1_b2_host"], False)
+    for key in e:
+        assert np.array_equal(g[key], e[key]), key
+
+
 if __name__ == "__main__":
-    res = run(scene(), CASES["k1_b1"], True)
+    case = sys.argv[2] if len(sys.argv) > 2 else "k1_b1"
+    res = run(scene(), CASES[case], True)
     np.savez(sys.argv[1], **res)
