@@ -33,6 +33,9 @@ namespace {
 
 constexpr int KBUF = 8;  // must equal blend_fwd.cu (identical overflow decisions)
 constexpr float kInf = __builtin_huge_valf();
+#ifndef DGS_K8_DIRECT
+#define DGS_K8_DIRECT 8  // sub-rounds of up to this many lanes add their adjoints directly (vector REDs)
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 // staged records (4 float4) + ring (t, id, sigma, list position)
 constexpr size_t kBwdSmem = 4 * kBlendThreads * sizeof(float4) + 4 * KBUF * kBlendThreads * sizeof(float) +
@@ -89,14 +92,24 @@ __device__ __forceinline__ void load_rec(const SplatRec* __restrict__ recs, uint
 /// Per-pixel backward state.
 struct PixState {
     float T;                 // replayed transmittance (bitwise the forward's sequence)
-    // suffix_i = sum_{j>i} c_j sigma_j A_j, kept as the forward's double total C minus the
-    // running prefix (raster.hpp:212-224 accumulates it backwards in float): double keeps
-    // its relative accuracy however much of C is already spent
-    double r0, r1, r2;
+    // gc . suffix_i, suffix_i = sum_{j>i} c_j sigma_j A_j (raster.hpp:212-224 accumulates
+    // it backwards in float): only its dot with gc enters the adjoint, so one double carries
+    // gc . (C - prefix), C the forward's double total, each term gc . c_j sigma_j A_j formed
+    // in double (a float gc . c_j would add its rounding over the whole prefix); double
+    // keeps the relative accuracy however much of C is already spent
+    double q, gd0, gd1, gd2;
     float gc0, gc1, gc2, gT;
     float Tf;
     float pxf, pyf;
 };
+
+/// The suffix state from the forward's double colour total (gc set first).
+__device__ __forceinline__ void init_suffix(PixState& ps, const double* __restrict__ cd) {
+    ps.gd0 = ps.gc0;
+    ps.gd1 = ps.gc1;
+    ps.gd2 = ps.gc2;
+    ps.q = ps.gd0 * cd[0] + ps.gd1 * cd[1] + ps.gd2 * cd[2];
+}
 
 /// One emitted contribution's 9 pixel-space adjoints:
 /// [d_mean.x, d_mean.y, d_cov00, d_cov01(=d_cov10), d_cov11, d_col.r, d_col.g, d_col.b, d_alpha].
@@ -106,15 +119,15 @@ __device__ __forceinline__ void contribution_grad(PixState& ps, float sigma, flo
     const float a_i = ps.T;
     const float w = fmul(sigma, a_i);
     const double wd = (double)sigma * (double)a_i;
-    ps.r0 -= (double)D.x * wd;
-    ps.r1 -= (double)D.y * wd;
-    ps.r2 -= (double)D.z * wd;
+    ps.q -= (ps.gd0 * (double)D.x + ps.gd1 * (double)D.y + ps.gd2 * (double)D.z) * wd;
     ps.T = fmul(ps.T, fsub(1.0f, sigma));
     // the rest in float, as in the reference
-    const float s0 = (float)ps.r0, s1 = (float)ps.r1, s2 = (float)ps.r2;
     const float gdc = ps.gc0 * D.x + ps.gc1 * D.y + ps.gc2 * D.z;
-    const float num = ps.gc0 * s0 + ps.gc1 * s1 + ps.gc2 * s2 + ps.gT * ps.Tf;
-    const float inv_om = __frcp_rn(1.0f - sigma);  // 1/(1-sigma), sigma <= 0.99
+    const float num = (float)ps.q + ps.gT * ps.Tf;
+    // 1/(1-sigma), 1-sigma in [0.01, 1]: MUFU reciprocal (1 ulp; the adjoint's tolerance
+    // is 1e-3, and the value is still a deterministic function of sigma)
+    float inv_om;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_om) : "f"(1.0f - sigma));
     const float d_sigma = gdc * a_i - num * inv_om;
     v[5] = ps.gc0 * w;
     v[6] = ps.gc1 * w;
@@ -175,7 +188,7 @@ __device__ __forceinline__ void to_fixed(float v, unsigned long long& lo32, long
 template <int MODE>
 __device__ __forceinline__ void acc_add(const GradAcc& a, int f, uint32_t mem, float v, float) {
     if constexpr (MODE == kAccFloat) {
-        if (v != 0.0f) atomicAdd(a.f + (size_t)f * a.ld + mem, v);
+        if (v != 0.0f) atomicAdd(a.f + g2d_index(f, mem, a.ld), v);
     } else {
         if (v == 0.0f) return;
         if (!(fabsf(v) < kFixedMax)) {  // non-finite (or beyond the fixed-point range): reported
@@ -192,7 +205,10 @@ __device__ __forceinline__ void acc_add(const GradAcc& a, int f, uint32_t mem, f
 }
 
 /// One emission sub-round's accumulation: all `go` lanes hold adjoints of the
-/// same member `mem`.  One or two lanes: direct atomics.  Otherwise a
+/// same member `mem`.  Up to DGS_K8_DIRECT lanes (float mode; two in
+/// deterministic mode): direct atomics, for the float mode two vector REDs +
+/// one scalar RED per lane, i.e. three instructions for the warp, cheaper than
+/// the ~45-instruction butterfly while the same-sector REDs stay few.  Otherwise a
 /// transposed butterfly (every exchange halves the values a lane still
 /// carries: 4 + 2 + 1 + 1 + 1 shuffles for fields 0-7 instead of 8 x 5)
 /// leaves the full sum of field (lane >> 2) & 7 in every lane; lanes 0, 4,
@@ -204,10 +220,18 @@ template <int MODE>
 __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint32_t mem, const float v[9],
                                             const GradAcc& acc, float scale) {
     const int n = __popc(gm);
-    if (n <= 2) {
+    if (n <= (MODE == kAccFloat ? DGS_K8_DIRECT : 2)) {
         if (go) {
+            if constexpr (MODE == kAccFloat) {
+                // fields 0-7 are one 32-byte sector of g2d: two vector REDs
+                float4* p = reinterpret_cast<float4*>(acc.f + 8 * (size_t)mem);
+                atomicAdd(p, make_float4(v[0], v[1], v[2], v[3]));
+                atomicAdd(p + 1, make_float4(v[4], v[5], v[6], v[7]));
+                acc_add<MODE>(acc, 8, mem, v[8], scale);
+            } else {
 #pragma unroll
-            for (int f = 0; f < 9; ++f) acc_add<MODE>(acc, f, mem, v[f], scale);
+                for (int f = 0; f < 9; ++f) acc_add<MODE>(acc, f, mem, v[f], scale);
+            }
         }
         return;
     }
@@ -238,7 +262,12 @@ __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint
     float a8 = v[8];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) a8 += __shfl_xor_sync(kFull, a8, off);
-    if ((lane & 3) == 0) acc_add<MODE>(acc, (lane >> 2) & 7, mem_w, a0, scale);
+    if constexpr (MODE == kAccFloat) {
+        // the 8 lanes' REDs land in one 32-byte sector (fields 0-7 of mem_w)
+        if ((lane & 3) == 0) atomicAdd(acc.f + 8 * (size_t)mem_w + ((lane >> 2) & 7), a0);
+    } else {
+        if ((lane & 3) == 0) acc_add<MODE>(acc, (lane >> 2) & 7, mem_w, a0, scale);
+    }
     if (lane == 0) acc_add<MODE>(acc, 8, mem_w, a8, scale);
 }
 
@@ -301,9 +330,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_bwd(ViewParams vp, R
         ps.gc1 = g.y;
         ps.gc2 = g.z;
         ps.gT = g.w;
-        ps.r0 = fwd_cd[3 * pix];
-        ps.r1 = fwd_cd[3 * pix + 1];
-        ps.r2 = fwd_cd[3 * pix + 2];
+        init_suffix(ps, fwd_cd + 3 * pix);
         ps.Tf = f.w;
         const float e = ro.grad_skip_eps;
         const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
@@ -514,9 +541,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
         ps.gc1 = g.y;
         ps.gc2 = g.z;
         ps.gT = g.w;
-        ps.r0 = fwd_cd[3 * pix];
-        ps.r1 = fwd_cd[3 * pix + 1];
-        ps.r2 = fwd_cd[3 * pix + 2];
+        init_suffix(ps, fwd_cd + 3 * pix);
         ps.Tf = f.w;
         const float e = ro.grad_skip_eps;
         const bool gc_zero = fabsf(g.x) <= e && fabsf(g.y) <= e && fabsf(g.z) <= e;
@@ -563,6 +588,10 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
         uint32_t mem = 0;
         float msc = 1.0f;
         if (go) {
+            // A.w and D.w are not needed, but a dead lane of the in-flight 128-bit record
+            // loads must not be reallocated (e.g. to the ballot's result): the write would
+            // wait on the load (WAW) right after the prefetch.  Both are finite (the D gate
+            // and the range), so this test never fires; it keeps their registers live here.
             // sigma and g exactly as the forward computed them (eval_candidate)
             const float dx = fsub(ps.pxf, A.x), dy = fsub(ps.pyf, A.y);
             const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),
@@ -628,9 +657,7 @@ __global__ void __launch_bounds__(64) k_blend_bwd_fallback(ViewParams vp, Render
         ps.gc1 = gg.y;
         ps.gc2 = gg.z;
         ps.gT = gg.w;
-        ps.r0 = fwd_cd[3 * (size_t)pix];
-        ps.r1 = fwd_cd[3 * (size_t)pix + 1];
-        ps.r2 = fwd_cd[3 * (size_t)pix + 2];
+        init_suffix(ps, fwd_cd + 3 * (size_t)pix);
         ps.Tf = ff.w;
         const float e = ro.grad_skip_eps;
         if (fabsf(gg.x) <= e && fabsf(gg.y) <= e && fabsf(gg.z) <= e && gg.w == 0.0f) continue;
@@ -707,28 +734,18 @@ void blend_bwd_fallback_impl(const ViewParams& vp, const RenderOpts& ro, const S
 
 /// Deterministic mode: g2d = (hi 2^32 + lo) 2^-72 (acc.q [9][lo | hi][ld]),
 /// then the accumulators are zeroed for the next backward (they stay zero
-/// between uses).  Two members per thread (16-byte words, ld is a multiple of
-/// 32), all 9 fields' loads issued before any store: HBM-bound.
+/// between uses).  One member per thread, coalesced 8-byte row reads, all
+/// loads issued before any store: HBM-bound.  The training step fuses this
+/// into K9 instead (k_grad_record's fixed-point input).
 __global__ void __launch_bounds__(256) k_fixed_to_float(GradAcc acc, int n) {
     const size_t ld = acc.ld;
-    const int pairs = (n + 1) >> 1;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < pairs; p += gridDim.x * blockDim.x) {
-        const size_t i = 2 * (size_t)p;
-        ulonglong2 lo[9], hi[9];
-#pragma unroll
-        for (int f = 0; f < 9; ++f) {
-            lo[f] = *reinterpret_cast<const ulonglong2*>(acc.q + (2 * f) * ld + i);
-            hi[f] = *reinterpret_cast<const ulonglong2*>(acc.q + (2 * f + 1) * ld + i);
-        }
-        const ulonglong2 z = make_ulonglong2(0ull, 0ull);
-#pragma unroll
-        for (int f = 0; f < 9; ++f) {
-            *reinterpret_cast<ulonglong2*>(acc.q + (2 * f) * ld + i) = z;
-            *reinterpret_cast<ulonglong2*>(acc.q + (2 * f + 1) * ld + i) = z;
-            const float a = (float)(fma((double)(long long)hi[f].x, 0x1p32, (double)lo[f].x) * 0x1p-72);
-            const float b = (float)(fma((double)(long long)hi[f].y, 0x1p32, (double)lo[f].y) * 0x1p-72);
-            *reinterpret_cast<float2*>(acc.f + f * ld + i) = make_float2(a, b);
-        }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        float a[9];
+        fixed_to_float9(acc.q, ld, i, a);
+        float4* o = reinterpret_cast<float4*>(acc.f + 8 * (size_t)i);
+        o[0] = make_float4(a[0], a[1], a[2], a[3]);
+        o[1] = make_float4(a[4], a[5], a[6], a[7]);
+        acc.f[8 * ld + i] = a[8];
     }
 }
 
@@ -753,8 +770,7 @@ void launch_fixed_to_float(const GradAcc& acc, int n, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int pairs = (n + 1) / 2;
-    k_fixed_to_float<<<std::min((pairs + 255) / 256, sms * 8), 256, 0, s>>>(acc, n);
+    k_fixed_to_float<<<std::min((n + 255) / 256, sms * 8), 256, 0, s>>>(acc, n);  // a warp per 32 members
 }
 
 }  // namespace dgs_b200

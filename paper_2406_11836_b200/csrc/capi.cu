@@ -615,7 +615,9 @@ void forward_subset(Ctx& ctx, SubsetState& S, int v, const ViewParams& vp, int d
 /// adjoints are summed as fixed point (2^-72 units) in one pass (kernels.h GradAcc),
 /// then converted; a non-finite contribution is reported through ctx.bad like
 /// K9's check.
-void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
+/// fuse_convert: in deterministic mode leave the fixed-point sums in S.g2q for
+/// K9 to convert (launch_project_bwd_adam's g2q) instead of a separate pass.
+void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats, bool fuse_convert = false) {
     ViewSlot& vs = S.slot(v);
     S.g2d.ensure(9 * S.ld);
     const bool det = ctx.cfg.deterministic != 0;
@@ -641,7 +643,7 @@ void backward_blend(Ctx& ctx, SubsetState& S, int v, BlendStats* stats) {
     launch_blend_bwd(vs.vp, ctx.ro, ctx.table.sub[S.k], vs.vb, vs.ct.p, vs.cd.p, vs.grad_ct.p, vs.ovf_flag.p, crec,
                      acc, vs.ovf_list.p, vs.ovf_count.p, stats, ctx.stream);
     ctx.launches += det ? 6 : 3;
-    if (det) {
+    if (det && !fuse_convert) {
         launch_fixed_to_float(acc, (int)S.n, ctx.stream);
         ++ctx.launches;
     }
@@ -2150,7 +2152,7 @@ int dgs_dump_pixel_grads(dgs_ctx* ctx, int32_t k, float* out) {
         std::vector<float> h(9 * S.ld);
         CK(cudaMemcpy(h.data(), S.g2d.p, h.size() * 4, cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < S.n; ++i)
-            for (int f = 0; f < 9; ++f) out[i * 9 + f] = h[(size_t)f * S.ld + i];
+            for (int f = 0; f < 9; ++f) out[i * 9 + f] = h[g2d_index(f, (size_t)i, S.ld)];
     });
 }
 
@@ -2583,7 +2585,7 @@ void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const 
             S_.rec.ensure(kGradRecordRows(batch) * S_.ld);
             for (int v = 0; v < batch; ++v) {
                 ViewSlot& vs = S_.slot(v);
-                backward_blend(*ctx, S_, v, ctx->collect_stats ? ctx->stats.p + 1 : nullptr);
+                backward_blend(*ctx, S_, v, ctx->collect_stats ? ctx->stats.p + 1 : nullptr, true);
                 const bool last = v + 1 == batch;
                 cudaEvent_t a = nullptr, m1 = nullptr, m2 = nullptr, b = nullptr;
                 if (ctx->timer.on) {
@@ -2593,7 +2595,8 @@ void train_step_body(dgs_ctx* ctx, int32_t batch, const dgs_camera* cams, const 
                     CK(cudaEventRecord(a, ctx->stream));
                 }
                 launch_project_bwd_adam((int)S_.n, S_.P.p, S_.M.p, S_.V.p, S_.ld, S_.sh_coeffs, vs.vp, ctx->ro,
-                                        vs.vb.counts, vs.vb.shjac, S_.g2d.p, S_.ld, v, batch, ap, ctx->bad.p,
+                                        vs.vb.counts, vs.vb.shjac, S_.g2d.p, S_.ld,
+                                        ctx->cfg.deterministic ? S_.g2q.p : nullptr, v, batch, ap, ctx->bad.p,
                                         S_.rec.p, last ? m1 : nullptr, m2, ctx->stream);
                 if (ctx->timer.on) {
                     if (!last) CK(cudaEventRecord(m1, ctx->stream));

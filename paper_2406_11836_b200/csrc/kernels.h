@@ -104,15 +104,42 @@ void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
 /// whatever order the atomics land in; launch_fixed_to_float converts them
 /// into f and re-zeroes q.  A non-finite value (or |value| >= 2^22) sets
 /// bad = min(member index).  q must be zero on the first use.
+/// Layout of the 9 pixel-space adjoints per member (g2d, acc.f): fields 0-7
+/// of member i are the 32-byte sector at 8 i (one vector RED / one L2 sector
+/// per warp reduction), field 8 (d_alpha) is a row at 8 ld + i.  9 ld floats.
+__host__ __device__ inline size_t g2d_index(int f, size_t i, size_t ld) {
+    return f < 8 ? 8 * i + (size_t)f : 8 * ld + i;
+}
+
+#ifdef __CUDACC__
+/// Deterministic mode's fixed-point sums (acc.q, [9][lo | hi][ld] words):
+/// member i's 9 totals (hi 2^32 + lo) 2^-72 as floats; the words are zeroed
+/// for the next backward (they stay zero between uses).
+__device__ __forceinline__ void fixed_to_float9(unsigned long long* __restrict__ q, size_t ld, size_t i, float a[9]) {
+    unsigned long long lo[9], hi[9];
+#pragma unroll
+    for (int f = 0; f < 9; ++f) {
+        lo[f] = __ldcs(q + (2 * f) * ld + i);
+        hi[f] = __ldcs(q + (2 * f + 1) * ld + i);
+    }
+#pragma unroll
+    for (int f = 0; f < 9; ++f) {
+        __stcs(q + (2 * f) * ld + i, 0ull);
+        __stcs(q + (2 * f + 1) * ld + i, 0ull);
+        a[f] = (float)(fma((double)(long long)hi[f], 0x1p32, (double)lo[f]) * 0x1p-72);
+    }
+}
+#endif
+
 struct GradAcc {
-    float* f = nullptr;
-    unsigned long long* q = nullptr;  // [9][2][ld]
+    float* f = nullptr;  // g2d_index layout
+    unsigned long long* q = nullptr;  // [9][lo | hi][ld]
     int* bad = nullptr;
     size_t ld = 0;
 };
 
 // K8: backward blend (+ the exact fallback for ring-overflow pixels);
-// accumulates 9 pixel-space adjoints per member into acc (SoA [9][ld]).
+// accumulates 9 pixel-space adjoints per member into acc (g2d_index layout).
 // fwd_cd: the forward's double-precision colour sums (suffix = C - prefix without cancellation loss).
 // With records (rec.pos != nullptr): the record walk for unflagged tiles plus
 // the ordered-ring replay for flagged tiles; without: replay everywhere.
@@ -248,11 +275,14 @@ void launch_project_bwd(int n, const float* P, size_t ld, int sh_coeffs, const V
 // g_rec: scratch of kGradRecordRows(nviews) rows x ld floats (the per-member gradient record:
 // 11 non-SH gradient rows summed over the views, then colour adjoint + direction per view).
 // shjac: the preprocess's SH colour Jacobian rows ([10][ld], ViewBins::shjac) or nullptr (read the SH rows).
+// g2q: deterministic mode's fixed-point sums (GradAcc::q) not yet converted, or nullptr (read g2d):
+// K9 converts and re-zeroes them and writes g2d.
 // Call once per view v = 0 .. nviews-1 in order; the last call also runs the Adam stream.
 void launch_project_bwd_adam(int n, float* P, float* M, float* V, size_t ld, int sh_coeffs, const ViewParams& vp,
-                             const RenderOpts& ro, const uint32_t* counts, const float* shjac, const float* g2d,
-                             size_t ld2, int view, int nviews, const AdamArgs& ap, int* bad_index, float* g_rec,
-                             cudaEvent_t mid_end, cudaEvent_t mid_begin, cudaStream_t s);
+                             const RenderOpts& ro, const uint32_t* counts, const float* shjac, float* g2d,
+                             size_t ld2, unsigned long long* g2q, int view, int nviews, const AdamArgs& ap,
+                             int* bad_index, float* g_rec, cudaEvent_t mid_end, cudaEvent_t mid_begin,
+                             cudaStream_t s);
 constexpr size_t kGradRecordRows(int nviews) { return 11 + 6 * (size_t)nviews; }
 void launch_adam(int n, float* P, float* M, float* V, size_t ld, int rows, const float* G, const AdamArgs& ap,
                  cudaStream_t s);
