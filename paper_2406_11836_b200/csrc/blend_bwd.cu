@@ -34,7 +34,7 @@ namespace {
 constexpr int KBUF = 8;  // must equal blend_fwd.cu (identical overflow decisions)
 constexpr float kInf = __builtin_huge_valf();
 #ifndef DGS_K8_DIRECT
-#define DGS_K8_DIRECT 8  // sub-rounds of up to this many lanes add their adjoints directly (vector REDs)
+#define DGS_K8_DIRECT 24  // sub-rounds of up to this many lanes add their adjoints directly (vector REDs)
 #endif
 constexpr unsigned kFull = 0xffffffffu;
 // staged records (4 float4) + ring (t, id, sigma, list position)
@@ -588,10 +588,6 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_bwd_rec(ViewParams v
         uint32_t mem = 0;
         float msc = 1.0f;
         if (go) {
-            // A.w and D.w are not needed, but a dead lane of the in-flight 128-bit record
-            // loads must not be reallocated (e.g. to the ballot's result): the write would
-            // wait on the load (WAW) right after the prefetch.  Both are finite (the D gate
-            // and the range), so this test never fires; it keeps their registers live here.
             // sigma and g exactly as the forward computed them (eval_candidate)
             const float dx = fsub(ps.pxf, A.x), dy = fsub(ps.pyf, A.y);
             const float m2 = fadd(fmul(dx, fadd(fmul(B.x, dx), fmul(B.y, dy))),

@@ -95,7 +95,7 @@ void launch_blend_fwd_fallback(const ViewParams& vp, const RenderOpts& ro, const
                                float4* out_ct, const uint32_t* ovf_list, const uint32_t* n_ovf_dev, uint32_t* dbg_ids,
                                uint32_t* dbg_cnt, int dbg_cap, double* out_cd, cudaStream_t s);
 
-/// Where K8 accumulates the 9 pixel-space adjoints of each member (SoA [9][ld]).
+/// Where K8 accumulates the 9 pixel-space adjoints of each member (g2d_index layout).
 /// q == nullptr: float RED atomics into f (order-dependent rounding).
 /// q != nullptr (TrainConfig::deterministic, "fixed-order reductions",
 /// optim.hpp:33): one pass; every sub-round sum is rounded to an integer
