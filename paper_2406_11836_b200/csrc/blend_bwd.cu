@@ -227,7 +227,7 @@ __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint
                 float4* p = reinterpret_cast<float4*>(acc.f + 8 * (size_t)mem);
                 atomicAdd(p, make_float4(v[0], v[1], v[2], v[3]));
                 atomicAdd(p + 1, make_float4(v[4], v[5], v[6], v[7]));
-                acc_add<MODE>(acc, 8, mem, v[8], scale);
+                atomicAdd(acc.f + 8 * acc.ld + mem, v[8]);  // d_alpha row (g2d_index(8, ..))
             } else {
 #pragma unroll
                 for (int f = 0; f < 9; ++f) acc_add<MODE>(acc, f, mem, v[f], scale);
@@ -268,7 +268,11 @@ __device__ __forceinline__ void reduce_emit(unsigned gm, bool go, int lane, uint
     } else {
         if ((lane & 3) == 0) acc_add<MODE>(acc, (lane >> 2) & 7, mem_w, a0, scale);
     }
-    if (lane == 0) acc_add<MODE>(acc, 8, mem_w, a8, scale);
+    if constexpr (MODE == kAccFloat) {
+        if (lane == 0) atomicAdd(acc.f + 8 * acc.ld + mem_w, a8);
+    } else {
+        if (lane == 0) acc_add<MODE>(acc, 8, mem_w, a8, scale);
+    }
 }
 
 template <bool STATS, int MODE>
